@@ -1,0 +1,148 @@
+/*
+ * adattn_b200.h -- C-ABI of the B200-native alpha-entmax attention library
+ * (libadattn_b200.so).  Plain pointers and sizes only; no CUDA or torch types
+ * cross this boundary (streams travel as void*).
+ *
+ * Each entry point replaces one reference interface (paths relative to
+ * /root/reference/proj):
+ *
+ *   adattn_b200_forward        <- adattn::forward        include/adattn/attention.hpp:72-76
+ *                                                         (src/attention.cpp:157-361)
+ *   adattn_b200_compute_delta  <- adattn::compute_delta  attention.hpp:82-85 (attention.cpp:411-446)
+ *   adattn_b200_backward       <- adattn::backward       attention.hpp:87-92 (attention.cpp:448-539)
+ *   adattn_b200_stats          <- AttentionStats fill + adattn::block_sparsity
+ *                                                         attention.hpp:38-43, 94-97 (attention.cpp:355-359, 541-551)
+ *   adattn_b200_validate       <- validate() + PackedHistogramAcc ctor checks
+ *                                                         attention.cpp:42-63, 160; bitpack.cpp:55-65
+ *   adattn_b200_last_error     <- the what() string of the reference's std::invalid_argument
+ *
+ * The reference is single-head; this ABI batches B x H independent heads
+ * ("harness loops over heads").  Tensors are dense row-major:
+ *   q    [B][H][n][d]     k [B][H][m][d]     v [B][H][m][dv]     dout [B][H][n][dv]
+ *   out  [B][H][n][dv]    dq [B][H][n][d]    dk [B][H][m][d]     dv   [B][H][m][dv]
+ *   tau, row_max, delta [B][H][n] (double; tau on the centred z scale, attention.hpp:46-49)
+ *   row_steps [B][H][n] (int32, nullable; the reference's private RowSolve.steps)
+ *   mask [B][H][t_r][ceil(t_c/32)] u32 -- the reference PackedBlockMask word layout
+ *        (bitpack.hpp:72-110), byte-identical to PackedBlockMask::serialize() payload.
+ * All device pointers must be 16-byte aligned.
+ *
+ * Return codes replace exceptions: 0 ok; ADATTN_ERR_INVALID where the
+ * reference throws std::invalid_argument (same message via last_error);
+ * ADATTN_ERR_UNSUPPORTED for a valid problem outside this build's GPU
+ * envelope; ADATTN_ERR_CUDA for a CUDA failure; ADATTN_ERR_WORKSPACE for a
+ * short workspace.  There is no CPU fallback.
+ */
+#ifndef ADATTN_B200_H
+#define ADATTN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADATTN_B200_ABI_VERSION 1
+
+enum {
+  ADATTN_OK = 0,
+  ADATTN_ERR_INVALID = 1,
+  ADATTN_ERR_UNSUPPORTED = 4,
+  ADATTN_ERR_CUDA = 5,
+  ADATTN_ERR_WORKSPACE = 6
+};
+
+/* element types */
+enum { ADATTN_F32 = 0, ADATTN_BF16 = 1, ADATTN_F64 = 2 };
+
+/* compute paths:
+ *   EXACT -- fp64 SIMT kernels; reproduce the reference's operation order
+ *            (bit-identical results for fp32/bf16-representable inputs).
+ *            The "fp32 path" of the north star.
+ *   TC    -- bf16 tcgen05/TMEM tensor-core kernels, fp32 epilogue math.
+ *   AUTO  -- TC for bf16 inputs when the shape is in its envelope, else EXACT. */
+enum { ADATTN_PATH_AUTO = 0, ADATTN_PATH_EXACT = 1, ADATTN_PATH_TC = 2 };
+
+/* Mirrors AttentionProblem (attention.hpp:24-36) plus batching and dtypes. */
+typedef struct {
+  int32_t batch, heads;
+  int32_t n, m, d, dv;
+  double alpha;
+  double scale; /* 0 => 1/sqrt(d) */
+  int32_t causal;
+  int32_t block_r, block_c;
+  int32_t bins;
+  int32_t refine_iters;
+  double refine_tol;
+  int32_t in_dtype;  /* q, k, v, dout: ADATTN_F32 | ADATTN_BF16 | ADATTN_F64 */
+  int32_t out_dtype; /* out, dq, dk, dv: ADATTN_F32 | ADATTN_F64 */
+  int32_t path;      /* ADATTN_PATH_* */
+  int32_t reserved;
+} adattn_problem;
+
+/* Mirrors AttentionStats (attention.hpp:38-43), aggregated over heads. */
+typedef struct {
+  double block_sparsity;
+  uint64_t blocks_visited_fwd;
+  uint64_t blocks_visited_bwd;
+  uint64_t flushes;
+  uint64_t addressable_blocks;
+  uint64_t active_blocks;
+} adattn_stats;
+
+int adattn_b200_abi_version(void);
+const char* adattn_b200_last_error(void);
+
+/* Same checks and messages as the reference's validate(); returns
+ * ADATTN_ERR_INVALID or ADATTN_ERR_UNSUPPORTED accordingly. */
+int adattn_b200_validate(const adattn_problem* p);
+
+/* The path AUTO resolves to (ADATTN_PATH_EXACT or ADATTN_PATH_TC), or <0. */
+int adattn_b200_resolved_path(const adattn_problem* p);
+
+size_t adattn_b200_forward_workspace(const adattn_problem* p);
+size_t adattn_b200_backward_workspace(const adattn_problem* p);
+
+/* Device pointers; all work is enqueued on `stream` (cudaStream_t or NULL). */
+int adattn_b200_forward(const adattn_problem* p, const void* q, const void* k, const void* v,
+                        void* out, double* tau, double* row_max, uint32_t* mask,
+                        int32_t* row_steps, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+int adattn_b200_compute_delta(const adattn_problem* p, const void* q, const void* k,
+                              const void* v, const double* tau, const double* row_max,
+                              const uint32_t* mask, const void* dout, double* delta,
+                              void* workspace, size_t workspace_bytes, void* stream);
+
+int adattn_b200_backward(const adattn_problem* p, const void* q, const void* k,
+                         const void* v, const double* tau, const double* row_max,
+                         const uint32_t* mask, const void* dout, void* dq, void* dk,
+                         void* dv, double* delta, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
+/* Mask statistics (synchronises `stream`): popcounts, block sparsity over the
+ * addressable blocks, visits (fwd = nnz, bwd = 2 nnz) and the flush count of
+ * the reference's packed histogram stream. */
+int adattn_b200_stats(const adattn_problem* p, const uint32_t* mask, adattn_stats* out,
+                      void* stream);
+
+/* block_sparsity (attention.cpp:541-551) of a device mask of `heads` x t_r x
+ * ceil(t_c/32) words, aggregated over heads; synchronises `stream`. */
+int adattn_b200_mask_sparsity(const uint32_t* mask, int32_t heads, int32_t t_r, int32_t t_c,
+                              int32_t causal, adattn_stats* out, void* stream);
+
+/* End-to-end call on HOST buffers (the reference's value-semantics calling
+ * convention): uploads inputs, runs forward (+ backward when dout != NULL),
+ * downloads results.  Device buffers are cached between calls. */
+int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, const void* v,
+                         const void* dout, void* out, double* tau, double* row_max,
+                         uint32_t* mask, void* dq, void* dk, void* dv, double* delta,
+                         adattn_stats* stats);
+
+/* Number of kernels this library has launched in this process (profiling aid). */
+uint64_t adattn_b200_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

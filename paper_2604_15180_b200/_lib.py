@@ -1,0 +1,108 @@
+"""ctypes binding of libadattn_b200.so (include/adattn_b200.h).
+
+The library is built in-tree by ``paper_2604_15180_b200/Makefile`` (see
+``__graft_entry__.build``).  There is no fallback: if the shared object is
+missing or fails to load, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libadattn_b200.so")
+
+ADATTN_OK = 0
+ADATTN_ERR_INVALID = 1
+ADATTN_ERR_UNSUPPORTED = 4
+ADATTN_ERR_CUDA = 5
+ADATTN_ERR_WORKSPACE = 6
+
+F32, BF16, F64 = 0, 1, 2
+PATH_AUTO, PATH_EXACT, PATH_TC = 0, 1, 2
+
+# every symbol include/adattn_b200.h declares
+EXPORTS = (
+    "adattn_b200_abi_version", "adattn_b200_last_error", "adattn_b200_validate",
+    "adattn_b200_resolved_path", "adattn_b200_forward_workspace",
+    "adattn_b200_backward_workspace", "adattn_b200_forward", "adattn_b200_compute_delta",
+    "adattn_b200_backward", "adattn_b200_stats", "adattn_b200_mask_sparsity",
+    "adattn_b200_run_host",
+    "adattn_b200_launch_count",
+)
+
+
+class Problem(C.Structure):
+    _fields_ = [
+        ("batch", C.c_int32), ("heads", C.c_int32),
+        ("n", C.c_int32), ("m", C.c_int32), ("d", C.c_int32), ("dv", C.c_int32),
+        ("alpha", C.c_double), ("scale", C.c_double),
+        ("causal", C.c_int32), ("block_r", C.c_int32), ("block_c", C.c_int32),
+        ("bins", C.c_int32), ("refine_iters", C.c_int32), ("refine_tol", C.c_double),
+        ("in_dtype", C.c_int32), ("out_dtype", C.c_int32), ("path", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [("block_sparsity", C.c_double), ("blocks_visited_fwd", C.c_uint64),
+                ("blocks_visited_bwd", C.c_uint64), ("flushes", C.c_uint64),
+                ("addressable_blocks", C.c_uint64), ("active_blocks", C.c_uint64)]
+
+
+class AdattnError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load the in-tree shared object; raise loudly when it is absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(
+                f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(no CPU fallback exists)")
+        lib = C.CDLL(LIB_PATH)
+        vp, P, S = C.c_void_p, C.POINTER(Problem), C.POINTER(Stats)
+        lib.adattn_b200_abi_version.restype = C.c_int
+        lib.adattn_b200_last_error.restype = C.c_char_p
+        lib.adattn_b200_validate.argtypes = [P]
+        lib.adattn_b200_resolved_path.argtypes = [P]
+        lib.adattn_b200_forward_workspace.argtypes = [P]
+        lib.adattn_b200_forward_workspace.restype = C.c_size_t
+        lib.adattn_b200_backward_workspace.argtypes = [P]
+        lib.adattn_b200_backward_workspace.restype = C.c_size_t
+        lib.adattn_b200_forward.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+        lib.adattn_b200_compute_delta.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                                  C.c_size_t, vp]
+        lib.adattn_b200_backward.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                             C.c_size_t, vp]
+        lib.adattn_b200_stats.argtypes = [P, vp, S, vp]
+        lib.adattn_b200_mask_sparsity.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                  S, vp]
+        lib.adattn_b200_run_host.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, S]
+        lib.adattn_b200_launch_count.restype = C.c_uint64
+        if lib.adattn_b200_abi_version() != 1:
+            raise RuntimeError("libadattn_b200.so ABI mismatch")
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc == ADATTN_OK:
+        return
+    msg = load().adattn_b200_last_error().decode()
+    if rc == ADATTN_ERR_INVALID:
+        raise ValueError(msg)  # the reference's std::invalid_argument
+    if rc == ADATTN_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise AdattnError(rc, msg)

@@ -1,0 +1,424 @@
+// capi.cu -- the C-ABI (include/adattn_b200.h): validation with the
+// reference's messages, path dispatch, mask statistics and the host-buffer
+// end-to-end entry.  No CPU compute fallback: every numeric result comes from
+// a CUDA kernel; a problem outside the GPU envelope is refused.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "adattn_b200.h"
+#include "common.cuh"
+#include "exact.cuh"
+#include "tc.cuh"
+
+namespace adattn_b200 {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(ADATTN_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// validate (attention.cpp:42-63) + PackedHistogramAcc ctor (bitpack.cpp:55-65,
+// attention.cpp:35, 160), same order and messages; then this build's envelope.
+int check(const adattn_problem* p, Geom* out) {
+  if (!p) return fail(ADATTN_ERR_INVALID, "adattn_b200: null problem");
+  if (p->batch < 1 || p->heads < 1)
+    return fail(ADATTN_ERR_INVALID, "adattn_b200: batch and heads must be positive");
+  if (p->n < 1 || p->m < 1 || p->d < 1 || p->dv < 1)
+    return fail(ADATTN_ERR_INVALID, "attention: empty operand");
+  if (p->causal && p->m != p->n)
+    return fail(ADATTN_ERR_INVALID, "attention: causal needs square score matrix");
+  if (!(p->alpha > 1.0)) return fail(ADATTN_ERR_INVALID, "attention: alpha must exceed 1");
+  if (p->block_r < 1 || p->block_c < 1)
+    return fail(ADATTN_ERR_INVALID, "attention: bad tile size");
+  if (p->refine_iters < 0 || !(p->refine_tol > 0.0))
+    return fail(ADATTN_ERR_INVALID, "attention: bad refinement config");
+  const int word_bits = p->bins <= 16 ? 64 : 128;
+  if (p->bins <= 0 || word_bits % p->bins != 0)
+    return fail(ADATTN_ERR_INVALID, "PackedHistogramAcc: bins must divide word_bits");
+  if (word_bits / p->bins < 4)
+    return fail(ADATTN_ERR_INVALID, "PackedHistogramAcc: needs at least 4 bits per bin");
+  if (p->in_dtype != ADATTN_F32 && p->in_dtype != ADATTN_BF16 && p->in_dtype != ADATTN_F64)
+    return fail(ADATTN_ERR_INVALID, "adattn_b200: bad in_dtype");
+  if (p->out_dtype != ADATTN_F32 && p->out_dtype != ADATTN_F64)
+    return fail(ADATTN_ERR_INVALID, "adattn_b200: bad out_dtype");
+  if (p->path < ADATTN_PATH_AUTO || p->path > ADATTN_PATH_TC)
+    return fail(ADATTN_ERR_INVALID, "adattn_b200: bad path");
+  Geom g;
+  g.bh = p->batch * p->heads;
+  g.n = p->n;
+  g.m = p->m;
+  g.d = p->d;
+  g.dv = p->dv;
+  g.block_r = p->block_r;
+  g.block_c = p->block_c;
+  g.t_r = (p->n + p->block_r - 1) / p->block_r;
+  g.t_c = (p->m + p->block_c - 1) / p->block_c;
+  g.wpr = (g.t_c + 31) / 32;
+  g.bins = p->bins;
+  g.causal = p->causal ? 1 : 0;
+  g.refine_iters = p->refine_iters;
+  g.in_dtype = p->in_dtype;
+  g.out_dtype = p->out_dtype;
+  g.alpha = p->alpha;
+  g.scale = p->scale != 0.0 ? p->scale : 1.0 / std::sqrt((double)p->d);
+  g.refine_tol = p->refine_tol;
+  g.e0 = 1.0 / (p->alpha - 1.0);
+  if (out) *out = g;
+  return ADATTN_OK;
+}
+
+int resolve(const adattn_problem* p, const Geom& g) {
+  const bool tc_ok = p->in_dtype == ADATTN_BF16 && tc_supported(g);
+  if (p->path == ADATTN_PATH_TC) {
+    if (!tc_ok)
+      return -fail(ADATTN_ERR_UNSUPPORTED,
+                   "adattn_b200: tensor-core path needs bf16 inputs, block 64x64, d=dv in "
+                   "{64,128}, bins<=32 (" + tc_envelope() + ")");
+    return ADATTN_PATH_TC;
+  }
+  if (p->path == ADATTN_PATH_AUTO && tc_ok) return ADATTN_PATH_TC;
+  if (!exact_supported(g))
+    return -fail(ADATTN_ERR_UNSUPPORTED,
+                 "adattn_b200: exact path supports block_r, block_c <= 64 and d, dv <= 128");
+  return ADATTN_PATH_EXACT;
+}
+
+// ------------------------------------------------------------- stats kernel
+__global__ void mask_stats_kernel(Geom g, const uint32_t* __restrict__ mask,
+                                  unsigned long long* __restrict__ acc) {
+  unsigned long long nnz = 0, active = 0;
+  const size_t words = (size_t)g.bh * g.t_r * g.wpr;
+  for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < words;
+       w += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t bits = mask[w];
+    if (!bits) continue;
+    const int wi = (int)(w % g.wpr);
+    const int i = (int)((w / g.wpr) % g.t_r);
+    nnz += __popc(bits);
+    uint32_t addr = 0;
+    for (int b = 0; b < 32; ++b) {
+      const long long j = (long long)wi * 32 + b;
+      if (j >= g.t_c) break;
+      if (!g.causal || j * g.t_r < (long long)(i + 1) * g.t_c) addr |= 1u << b;
+    }
+    active += __popc(bits & addr);
+  }
+  for (int off = 16; off; off >>= 1) {
+    nnz += __shfl_xor_sync(0xffffffffu, nnz, off);
+    active += __shfl_xor_sync(0xffffffffu, active, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (nnz) atomicAdd(&acc[0], nnz);
+    if (active) atomicAdd(&acc[1], active);
+  }
+}
+
+// Host buffers for adattn_b200_run_host (kept across calls).
+struct HostCtx {
+  std::mutex mu;
+  void* buf[16] = {};
+  size_t cap[16] = {};
+  cudaStream_t stream = nullptr;
+  void* get(int slot, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (cap[slot] < bytes) {
+      if (buf[slot]) cudaFree(buf[slot]);
+      buf[slot] = nullptr;
+      if (cudaMalloc(&buf[slot], bytes) != cudaSuccess) {
+        cap[slot] = 0;
+        return nullptr;
+      }
+      cap[slot] = bytes;
+    }
+    return buf[slot];
+  }
+};
+HostCtx& host_ctx() {
+  static HostCtx* c = new HostCtx();
+  return *c;
+}
+
+size_t elem_size(int dtype) { return dtype == ADATTN_BF16 ? 2 : dtype == ADATTN_F32 ? 4 : 8; }
+
+}  // namespace
+
+uint64_t flushes_of(const Geom& g) {
+  const int word_bits = g.bins <= 16 ? 64 : 128;
+  const int bits = word_bits / g.bins;
+  const unsigned long long L = bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
+  uint64_t per_head = 0;
+  for (int it = 0; it < g.t_r; ++it) {
+    const int r1 = std::min(g.n, (it + 1) * g.block_r);
+    const int jlim = g.causal ? (r1 - 1) / g.block_c : g.t_c - 1;
+    const unsigned long long J = (unsigned long long)jlim + 1;
+    per_head += (J + L - 1) / L;
+  }
+  return per_head * (uint64_t)g.bh;
+}
+
+uint64_t addressable_of(const Geom& g) {
+  uint64_t per_head = 0;
+  for (int i = 0; i < g.t_r; ++i) {
+    if (!g.causal) {
+      per_head += (uint64_t)g.t_c;
+      continue;
+    }
+    // count j in [0, t_c) with j * t_r < (i + 1) * t_c
+    const long long lim = ((long long)(i + 1) * g.t_c + g.t_r - 1) / g.t_r;
+    per_head += (uint64_t)std::min<long long>(lim, g.t_c);
+  }
+  return per_head * (uint64_t)g.bh;
+}
+
+}  // namespace adattn_b200
+
+using namespace adattn_b200;
+
+extern "C" {
+
+int adattn_b200_abi_version(void) { return ADATTN_B200_ABI_VERSION; }
+
+const char* adattn_b200_last_error(void) { return g_err.c_str(); }
+
+uint64_t adattn_b200_launch_count(void) { return g_launches.load(); }
+
+int adattn_b200_validate(const adattn_problem* p) {
+  Geom g;
+  int rc = check(p, &g);
+  if (rc) return rc;
+  const int path = resolve(p, g);
+  return path < 0 ? -path : ADATTN_OK;
+}
+
+int adattn_b200_resolved_path(const adattn_problem* p) {
+  Geom g;
+  int rc = check(p, &g);
+  if (rc) return -rc;
+  return resolve(p, g);
+}
+
+size_t adattn_b200_forward_workspace(const adattn_problem* p) {
+  Geom g;
+  if (check(p, &g)) return 0;
+  return resolve(p, g) == ADATTN_PATH_TC ? tc_forward_workspace(g) : 0;
+}
+
+size_t adattn_b200_backward_workspace(const adattn_problem* p) {
+  Geom g;
+  if (check(p, &g)) return 0;
+  return resolve(p, g) == ADATTN_PATH_TC ? tc_backward_workspace(g) : 16;
+}
+
+int adattn_b200_forward(const adattn_problem* p, const void* q, const void* k, const void* v,
+                        void* out, double* tau, double* row_max, uint32_t* mask,
+                        int32_t* row_steps, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  Geom g;
+  int rc = check(p, &g);
+  if (rc) return rc;
+  const int path = resolve(p, g);
+  if (path < 0) return -path;
+  if (!q || !k || !v || !out || !tau || !row_max || !mask)
+    return fail(ADATTN_ERR_INVALID, "adattn_b200_forward: null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (path == ADATTN_PATH_TC) {
+    if (workspace_bytes < tc_forward_workspace(g))
+      return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_forward: workspace too small");
+    e = tc_forward(g, q, k, v, out, tau, row_max, mask, row_steps, workspace, st);
+  } else {
+    e = exact_forward(g, q, k, v, out, tau, row_max, mask, row_steps, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "adattn_b200_forward");
+  return ADATTN_OK;
+}
+
+int adattn_b200_compute_delta(const adattn_problem* p, const void* q, const void* k,
+                              const void* v, const double* tau, const double* row_max,
+                              const uint32_t* mask, const void* dout, double* delta,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  Geom g;
+  int rc = check(p, &g);
+  if (rc) return rc;
+  const int path = resolve(p, g);
+  if (path < 0) return -path;
+  if (!q || !k || !v || !tau || !row_max || !mask || !dout || !delta)
+    return fail(ADATTN_ERR_INVALID, "compute_delta: null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (path == ADATTN_PATH_TC) {
+    if (workspace_bytes < tc_backward_workspace(g))
+      return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_compute_delta: workspace too small");
+    e = tc_delta(g, q, k, v, tau, row_max, mask, dout, delta, workspace, st);
+  } else {
+    e = exact_delta(g, q, k, v, tau, row_max, mask, dout, delta, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "adattn_b200_compute_delta");
+  return ADATTN_OK;
+}
+
+int adattn_b200_backward(const adattn_problem* p, const void* q, const void* k,
+                         const void* v, const double* tau, const double* row_max,
+                         const uint32_t* mask, const void* dout, void* dq, void* dk,
+                         void* dv, double* delta, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  Geom g;
+  int rc = check(p, &g);
+  if (rc) return rc;
+  const int path = resolve(p, g);
+  if (path < 0) return -path;
+  if (!q || !k || !v || !tau || !row_max || !mask || !dout || !dq || !dk || !dv || !delta)
+    return fail(ADATTN_ERR_INVALID, "backward: null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (path == ADATTN_PATH_TC) {
+    if (workspace_bytes < tc_backward_workspace(g))
+      return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_backward: workspace too small");
+    e = tc_backward(g, q, k, v, tau, row_max, mask, dout, dq, dk, dv, delta, workspace, st);
+  } else {
+    if (workspace_bytes < 8 || !workspace)
+      return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_backward: workspace too small");
+    unsigned long long* visited = reinterpret_cast<unsigned long long*>(workspace);
+    cudaMemsetAsync(visited, 0, sizeof(unsigned long long), st);
+    e = exact_backward(g, q, k, v, tau, row_max, mask, dout, dq, dk, dv, delta, visited, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "adattn_b200_backward");
+  return ADATTN_OK;
+}
+
+static int stats_impl(const Geom& g, const uint32_t* mask, adattn_stats* out,
+                      cudaStream_t st) {
+  if (!mask || !out) return fail(ADATTN_ERR_INVALID, "adattn_b200_stats: null buffer");
+  unsigned long long* acc = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&acc, 2 * sizeof(unsigned long long), st);
+  if (e) return cuda_fail(e, "adattn_b200_stats");
+  cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), st);
+  const size_t words = (size_t)g.bh * g.t_r * g.wpr;
+  const int blocks = (int)std::min<size_t>((words + 255) / 256, 4096);
+  mask_stats_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(g, mask, acc);
+  note_launch();
+  unsigned long long h[2] = {0, 0};
+  cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(acc, st);
+  e = cudaStreamSynchronize(st);
+  if (e) return cuda_fail(e, "adattn_b200_stats");
+  out->blocks_visited_fwd = h[0];
+  out->blocks_visited_bwd = 2 * h[0];
+  out->active_blocks = h[1];
+  out->addressable_blocks = addressable_of(g);
+  out->flushes = flushes_of(g);
+  out->block_sparsity =
+      out->addressable_blocks == 0
+          ? 0.0
+          : double(out->addressable_blocks - out->active_blocks) / double(out->addressable_blocks);
+  return ADATTN_OK;
+}
+
+int adattn_b200_stats(const adattn_problem* p, const uint32_t* mask, adattn_stats* out,
+                      void* stream) {
+  Geom g;
+  int rc = check(p, &g);
+  if (rc) return rc;
+  return stats_impl(g, mask, out, (cudaStream_t)stream);
+}
+
+int adattn_b200_mask_sparsity(const uint32_t* mask, int32_t heads, int32_t t_r, int32_t t_c,
+                              int32_t causal, adattn_stats* out, void* stream) {
+  if (heads < 1 || t_r < 1 || t_c < 1)
+    return fail(ADATTN_ERR_INVALID, "PackedBlockMask: bad dimensions");
+  Geom g{};
+  g.bh = heads;
+  g.n = t_r;
+  g.m = t_c;
+  g.block_r = g.block_c = 1;
+  g.t_r = t_r;
+  g.t_c = t_c;
+  g.wpr = (t_c + 31) / 32;
+  g.bins = 8;
+  g.causal = causal ? 1 : 0;
+  return stats_impl(g, mask, out, (cudaStream_t)stream);
+}
+
+int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, const void* v,
+                         const void* dout, void* out, double* tau, double* row_max,
+                         uint32_t* mask, void* dq, void* dk, void* dv, double* delta,
+                         adattn_stats* stats) {
+  Geom g;
+  int rc = check(p, &g);
+  if (rc) return rc;
+  const int path = resolve(p, g);
+  if (path < 0) return -path;
+  HostCtx& c = host_ctx();
+  std::lock_guard<std::mutex> lock(c.mu);
+  if (!c.stream && cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: stream create failed");
+  const size_t ei = elem_size(p->in_dtype), eo = elem_size(p->out_dtype);
+  const size_t BH = (size_t)g.bh;
+  const size_t nq = BH * g.n * g.d, nk = BH * g.m * g.d, nv = BH * g.m * g.dv;
+  const size_t no = BH * g.n * g.dv, nrow = BH * g.n;
+  const size_t mwords = BH * g.t_r * g.wpr;
+  void* dQ = c.get(0, nq * ei);
+  void* dK = c.get(1, nk * ei);
+  void* dV = c.get(2, nv * ei);
+  void* dO = c.get(3, no * eo);
+  double* dTau = (double*)c.get(4, nrow * 8);
+  double* dRm = (double*)c.get(5, nrow * 8);
+  uint32_t* dMask = (uint32_t*)c.get(6, mwords * 4);
+  const size_t wsf = adattn_b200_forward_workspace(p);
+  const size_t wsb = adattn_b200_backward_workspace(p);
+  void* ws = c.get(7, std::max(wsf, wsb));
+  if (!dQ || !dK || !dV || !dO || !dTau || !dRm || !dMask || !ws)
+    return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: device allocation failed");
+  cudaStream_t st = c.stream;
+  cudaMemcpyAsync(dQ, q, nq * ei, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dK, k, nk * ei, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(dV, v, nv * ei, cudaMemcpyHostToDevice, st);
+  rc = adattn_b200_forward(p, dQ, dK, dV, dO, dTau, dRm, dMask, nullptr, ws, std::max(wsf, wsb),
+                           st);
+  if (rc) return rc;
+  if (dout) {
+    void* dDO = c.get(8, no * ei);
+    void* dDQ = c.get(9, nq * eo);
+    void* dDK = c.get(10, nk * eo);
+    void* dDV = c.get(11, nv * eo);
+    double* dDl = (double*)c.get(12, nrow * 8);
+    if (!dDO || !dDQ || !dDK || !dDV || !dDl)
+      return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: device allocation failed");
+    cudaMemcpyAsync(dDO, dout, no * ei, cudaMemcpyHostToDevice, st);
+    rc = adattn_b200_backward(p, dQ, dK, dV, dTau, dRm, dMask, dDO, dDQ, dDK, dDV, dDl, ws,
+                              std::max(wsf, wsb), st);
+    if (rc) return rc;
+    if (dq) cudaMemcpyAsync(dq, dDQ, nq * eo, cudaMemcpyDeviceToHost, st);
+    if (dk) cudaMemcpyAsync(dk, dDK, nk * eo, cudaMemcpyDeviceToHost, st);
+    if (dv) cudaMemcpyAsync(dv, dDV, nv * eo, cudaMemcpyDeviceToHost, st);
+    if (delta) cudaMemcpyAsync(delta, dDl, nrow * 8, cudaMemcpyDeviceToHost, st);
+  }
+  if (out) cudaMemcpyAsync(out, dO, no * eo, cudaMemcpyDeviceToHost, st);
+  if (tau) cudaMemcpyAsync(tau, dTau, nrow * 8, cudaMemcpyDeviceToHost, st);
+  if (row_max) cudaMemcpyAsync(row_max, dRm, nrow * 8, cudaMemcpyDeviceToHost, st);
+  if (mask) cudaMemcpyAsync(mask, dMask, mwords * 4, cudaMemcpyDeviceToHost, st);
+  if (stats) {
+    rc = adattn_b200_stats(p, dMask, stats, st);
+    if (rc) return rc;
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e) return cuda_fail(e, "adattn_b200_run_host");
+  return ADATTN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol
+include/adattn_b200.h declares, and host-side validation mirrors the
+reference's validate() messages (attention.cpp:42-63, bitpack.cpp:55-65)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2604_15180_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "adattn_b200.h")).read()
+    return sorted(set(re.findall(r"\b(adattn_b200_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(_lib.EXPORTS) == syms
+    assert lib.adattn_b200_abi_version() == 1
+
+
+def prob(**kw):
+    base = dict(batch=1, heads=1, n=8, m=8, d=4, dv=4, alpha=1.5, scale=0.0, causal=0,
+                block_r=4, block_c=4, bins=8, refine_iters=2, refine_tol=1e-6,
+                in_dtype=_lib.F32, out_dtype=_lib.F64, path=_lib.PATH_AUTO, reserved=0)
+    base.update(kw)
+    return _lib.Problem(**base)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(n=0), "attention: empty operand"),
+    (dict(causal=1, m=6), "attention: causal needs square score matrix"),
+    (dict(alpha=1.0), "attention: alpha must exceed 1"),
+    (dict(block_r=0), "attention: bad tile size"),
+    (dict(refine_iters=-1), "attention: bad refinement config"),
+    (dict(refine_tol=0.0), "attention: bad refinement config"),
+    (dict(bins=5), "PackedHistogramAcc: bins must divide word_bits"),
+    (dict(bins=64), "PackedHistogramAcc: needs at least 4 bits per bin"),
+])
+def test_validate_messages(kw, msg):
+    lib = _lib.load()
+    p = prob(**kw)
+    assert lib.adattn_b200_validate(C.byref(p)) == _lib.ADATTN_ERR_INVALID
+    assert lib.adattn_b200_last_error().decode() == msg
+    with pytest.raises(ValueError, match=re.escape(msg)):
+        _lib.check(_lib.ADATTN_ERR_INVALID)
+
+
+def test_valid_and_envelope():
+    lib = _lib.load()
+    assert lib.adattn_b200_validate(C.byref(prob(bins=32))) == 0  # 128-bit words
+    assert lib.adattn_b200_validate(C.byref(prob(bins=2))) == 0
+    assert lib.adattn_b200_resolved_path(C.byref(prob())) == _lib.PATH_EXACT
+    # exact path envelope: d <= 128, tiles <= 64
+    assert lib.adattn_b200_validate(C.byref(prob(d=256))) == _lib.ADATTN_ERR_UNSUPPORTED
+    assert lib.adattn_b200_validate(C.byref(prob(block_r=128))) == _lib.ADATTN_ERR_UNSUPPORTED
+    # fp32 inputs never take the tensor-core path
+    assert lib.adattn_b200_validate(C.byref(prob(path=_lib.PATH_TC))) == _lib.ADATTN_ERR_UNSUPPORTED
