@@ -1,0 +1,24 @@
+// tc_host.cuh -- host helpers for the tensor-core path: TMA tensor maps.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace adattn_b200 {
+namespace tc {
+
+// 2-D bf16 tensor map over a row-major [rows][cols] matrix, box = 64 columns
+// (128 B, SWIZZLE_128B) x box_rows rows.
+cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                         uint32_t box_rows);
+
+int alpha_kind(double alpha);
+
+cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
+                    double* tau, double* row_max, uint32_t* mask, int32_t* steps,
+                    cudaStream_t st);
+
+}  // namespace tc
+}  // namespace adattn_b200
