@@ -50,21 +50,24 @@ std::string tc_envelope() {
   return "bf16 inputs, block_r=block_c=64, d=dv in {64,128}, n%256==0, m%64==0, 2<=bins<=32";
 }
 size_t tc_forward_workspace(const Geom&) { return 0; }
-size_t tc_backward_workspace(const Geom&) { return 16; }
+size_t tc_backward_workspace(const Geom& g) { return tc::backward_workspace(g); }
 
 cudaError_t tc_forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                        double* tau, double* row_max, uint32_t* mask, int32_t* steps, void*,
                        cudaStream_t st) {
   return tc::forward(g, q, k, v, out, tau, row_max, mask, steps, st);
 }
-cudaError_t tc_delta(const Geom&, const void*, const void*, const void*, const double*,
-                     const double*, const uint32_t*, const void*, double*, void*, cudaStream_t) {
-  return cudaErrorNotSupported;
+cudaError_t tc_delta(const Geom& g, const void* q, const void* k, const void* v,
+                     const double* tau, const double* row_max, const uint32_t* mask,
+                     const void* dout, double* delta, void* ws, cudaStream_t st) {
+  return tc::backward(g, q, k, v, tau, row_max, mask, dout, nullptr, nullptr, nullptr, delta, ws,
+                      true, st);
 }
-cudaError_t tc_backward(const Geom&, const void*, const void*, const void*, const double*,
-                        const double*, const uint32_t*, const void*, void*, void*, void*,
-                        double*, void*, cudaStream_t) {
-  return cudaErrorNotSupported;
+cudaError_t tc_backward(const Geom& g, const void* q, const void* k, const void* v,
+                        const double* tau, const double* row_max, const uint32_t* mask,
+                        const void* dout, void* dq, void* dk, void* dv, double* delta, void* ws,
+                        cudaStream_t st) {
+  return tc::backward(g, q, k, v, tau, row_max, mask, dout, dq, dk, dv, delta, ws, false, st);
 }
 
 }  // namespace adattn_b200

@@ -18,6 +18,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -143,6 +144,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool a_mn, b
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
          ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// A operand fp16 (probabilities / score gradients), B operand bf16 (inputs).
+__host__ __device__ constexpr uint32_t idesc_f16a_bf16b_f32(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (0u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 
 // Byte offset of bf16 element (r, k) (k < 64) inside a SWIZZLE_128B tile of 128 B rows.
 __device__ __forceinline__ uint32_t sw128_offset(int r, int k) {
@@ -152,6 +158,19 @@ __device__ __forceinline__ uint32_t sw128_offset(int r, int k) {
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Split (x0, x1) into bf16 pairs hi + lo with x ~= hi + lo to 2^-16 relative:
+// the second bf16 operand of a two-pass MMA recovers the bits bf16 drops.
+__device__ __forceinline__ void split_bf16x2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  hi = pack_bf16x2(x0, x1);
+  const float h0 = __uint_as_float(hi << 16), h1 = __uint_as_float(hi & 0xFFFF0000u);
+  lo = pack_bf16x2(x0 - h0, x1 - h1);
+}
+
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
 

@@ -59,7 +59,7 @@ template <int D>
 struct FwdSmem {
   static constexpr int QBYTES = BM * D * 2;
   static constexpr int TILE = BN * D * 2;
-  static constexpr int PBYTES = BM * BN * 2;
+  static constexpr int PBYTES = 2 * BM * BN * 2;  // P_hi, P_lo
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_RING = OFF_Q + QBYTES;
   static constexpr int OFF_P = OFF_RING + NST * TILE;
@@ -261,9 +261,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d_t = tmem + 256 + rg * D;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            umma_bf16(d_t, desc_kmajor(p_addr + rg * 128 * 128 + k * 32),
-                      desc_mnmajor(ring_addr + st * L::TILE + k * 16 * 128, BN * 128), IDESC_PV,
+            const uint64_t bd = desc_mnmajor(ring_addr + st * L::TILE + k * 16 * 128, BN * 128);
+            umma_bf16(d_t, desc_kmajor(p_addr + rg * 128 * 128 + k * 32), bd, IDESC_PV,
                       (o_init[rg] || k > 0) ? 1u : 0u);
+            umma_bf16(d_t, desc_kmajor(p_addr + BM * BN * 2 + rg * 128 * 128 + k * 32), bd,
+                      IDESC_PV, 1u);
           }
           o_init[rg] = true;
         }
@@ -463,19 +465,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool need = out_active(rg, j);
         any_out |= need;
         fetch(j, need);
-        uint32_t pk[32];
+        uint32_t ph[32], pl[32];
         if (need) {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            pk[i] = pack_bf16x2(p_of<AK>(fmaf(A1, v[2 * i], C), a.e0f),
-                                p_of<AK>(fmaf(A1, v[2 * i + 1], C), a.e0f));
+            split_bf16x2(p_of<AK>(fmaf(A1, v[2 * i], C), a.e0f),
+                         p_of<AK>(fmaf(A1, v[2 * i + 1], C), a.e0f), ph[i], pl[i]);
         }
         mbar_wait(p_empty, (pi & 1) ^ 1);
         if (need) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            st_shared_v4(p_row + ((q ^ (e & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
-                         pk[4 * q + 3]);
+          for (int q = 0; q < 8; ++q) {
+            const uint32_t off = (q ^ (e & 7)) << 4;
+            st_shared_v4(p_row + off, ph[4 * q], ph[4 * q + 1], ph[4 * q + 2], ph[4 * q + 3]);
+            st_shared_v4(p_row + BM * BN * 2 + off, pl[4 * q], pl[4 * q + 1], pl[4 * q + 2],
+                         pl[4 * q + 3]);
+          }
         }
         fence_proxy_async_smem();
         __syncwarp();

@@ -20,5 +20,12 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
                     double* tau, double* row_max, uint32_t* mask, int32_t* steps,
                     cudaStream_t st);
 
+size_t backward_workspace(const Geom& g);
+
+cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v, const double* tau,
+                     const double* row_max, const uint32_t* mask, const void* dout, void* dq,
+                     void* dk, void* dv, double* delta, void* workspace, bool delta_only,
+                     cudaStream_t st);
+
 }  // namespace tc
 }  // namespace adattn_b200

@@ -94,3 +94,38 @@ def test_tc_forward_matches_exact(case):
     if diff.any():
         margin = block_margin(q, k, rx, alpha, causal).cpu().numpy()
         assert np.all(np.abs(margin[diff] + 1e-9) <= 1e-5), margin[diff]
+
+
+BWD_CASES = [
+    (1, 2, 256, 64, 1.5, True, 1.0),
+    (1, 2, 512, 128, 1.5, True, 1.0),
+    (1, 1, 512, 128, 1.5, False, 1.0),
+    (2, 1, 768, 64, 2.0, True, 1.0),
+    (1, 2, 512, 128, 1.25, True, 1.0),
+    (1, 1, 1024, 128, 1.5, True, 8.0),
+    (1, 1, 512, 64, 1.75, False, 2.0),
+]
+
+
+@pytest.mark.parametrize("case", BWD_CASES, ids=[str(c) for c in BWD_CASES])
+def test_tc_backward_matches_exact(case):
+    B, H, N, D, alpha, causal, qs = case
+    q, k, v, do = inputs(hash(case) % 997 + 1, B, H, N, D, qs)
+    _, rx, gx = run(q, k, v, do, "exact", alpha=alpha, causal=causal)
+    # backward on the TC path from the exact forward state: isolates the backward
+    prob_t = pa.AttentionProblem(q, k, v, path="tc", out_dtype=torch.float64, alpha=alpha,
+                                 causal=causal)
+    gt = pa.backward(prob_t, rx, do)
+    torch.cuda.synchronize()
+    errs = {n: (getattr(gt, n) - getattr(gx, n)).abs().max().item()
+            for n in ("delta", "dq", "dk", "dv")}
+    mags = {n: getattr(gx, n).abs().max().item() for n in ("delta", "dq", "dk", "dv")}
+    print(case, {n: f"{errs[n]:.2e}/{mags[n]:.1f}" for n in errs})
+    for n in errs:
+        assert errs[n] <= 2e-2, (n, errs[n])
+    # full TC round trip (TC forward state feeding the TC backward)
+    _, rt, gt2 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    e2 = {n: (getattr(gt2, n) - getattr(gx, n)).abs().max().item() for n in ("dq", "dk", "dv")}
+    print("  round trip", {n: f"{e2[n]:.2e}" for n in e2})
+    for n in e2:
+        assert e2[n] <= 2e-2, (n, e2[n])
