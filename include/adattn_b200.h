@@ -142,6 +142,13 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
 /* Number of kernels this library has launched in this process (profiling aid). */
 uint64_t adattn_b200_launch_count(void);
 
+/* Per-kernel CUDA-event timing (off by default).  While enabled every kernel
+ * launch is bracketed by events on its own stream.  profile_read synchronises,
+ * writes up to `max` durations (ms) and '\n'-separated kernel names, returns
+ * the number recorded and clears the log. */
+void adattn_b200_profile_enable(int on);
+int adattn_b200_profile_read(char* names, size_t names_len, double* ms, int max);
+
 #ifdef __cplusplus
 }
 #endif

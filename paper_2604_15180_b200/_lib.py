@@ -29,7 +29,7 @@ EXPORTS = (
     "adattn_b200_backward_workspace", "adattn_b200_forward", "adattn_b200_compute_delta",
     "adattn_b200_backward", "adattn_b200_stats", "adattn_b200_mask_sparsity",
     "adattn_b200_run_host",
-    "adattn_b200_launch_count",
+    "adattn_b200_launch_count", "adattn_b200_profile_enable", "adattn_b200_profile_read",
 )
 
 
@@ -91,6 +91,10 @@ def load() -> C.CDLL:
                                                   S, vp]
         lib.adattn_b200_run_host.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, S]
         lib.adattn_b200_launch_count.restype = C.c_uint64
+        lib.adattn_b200_profile_enable.argtypes = [C.c_int]
+        lib.adattn_b200_profile_enable.restype = None
+        lib.adattn_b200_profile_read.argtypes = [C.c_char_p, C.c_size_t,
+                                                 C.POINTER(C.c_double), C.c_int]
         if lib.adattn_b200_abi_version() != 1:
             raise RuntimeError("libadattn_b200.so ABI mismatch")
         _lib = lib
@@ -106,3 +110,17 @@ def check(rc: int) -> None:
     if rc == ADATTN_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
     raise AdattnError(rc, msg)
+
+
+def profile_enable(on: bool = True) -> None:
+    load().adattn_b200_profile_enable(1 if on else 0)
+
+
+def profile_read(max_n: int = 4096):
+    """[(kernel name, ms)] of the launches recorded since the last read."""
+    lib = load()
+    names = C.create_string_buffer(64 * max_n)
+    ms = (C.c_double * max_n)()
+    n = lib.adattn_b200_profile_read(names, len(names), ms, max_n)
+    keys = names.value.decode().split("\n")[:n]
+    return list(zip(keys, [ms[i] for i in range(n)]))

@@ -186,13 +186,16 @@ class AttentionResult:
     row_steps: torch.Tensor
     _problem: _lib.Problem = field(repr=False, default=None)
     _stats: Optional[AttentionStats] = field(repr=False, default=None)
+    _bwd_done: bool = field(repr=False, default=False)
 
     @property
     def stats(self) -> AttentionStats:
+        """Lazily computed (one popcount kernel + a stream sync) on first access."""
         if self._stats is None:
             st = _mask_stats(self._problem, self.mask.words)
             self._stats = AttentionStats(st.block_sparsity, int(st.blocks_visited_fwd), 0,
                                          int(st.flushes))
+        self._stats.blocks_visited_bwd = 2 * self._stats.blocks_visited_fwd if self._bwd_done else 0
         return self._stats
 
 
@@ -309,8 +312,7 @@ def backward(p: AttentionProblem, res: AttentionResult, dout: torch.Tensor,
         C.byref(pb), _ptr(p.q), _ptr(p.k), _ptr(p.v), _ptr(res.tau), _ptr(res.row_max),
         _ptr(res.mask.words), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(delta), _ptr(ws),
         ws_bytes, _stream()))
-    if res._stats is not None or res._problem is not None:
-        res.stats.blocks_visited_bwd = 2 * res.stats.blocks_visited_fwd
+    res._bwd_done = True  # stats report blocks_visited_bwd = 2 * nnz (attention.cpp:537)
     return AttentionGradients(dq, dk, dv, delta)
 
 

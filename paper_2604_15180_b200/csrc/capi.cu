@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "adattn_b200.h"
 #include "common.cuh"
@@ -18,6 +19,32 @@ namespace adattn_b200 {
 
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+}  // namespace
+
+void prof_begin(const char* name, cudaStream_t st) {
+  std::lock_guard<std::mutex> l(g_prof_mu);
+  if (!g_prof_on) return;
+  ProfRec r;
+  r.name = name;
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, st);
+  g_prof.push_back(r);
+}
+void prof_end(cudaStream_t st) {
+  std::lock_guard<std::mutex> l(g_prof_mu);
+  if (!g_prof_on || g_prof.empty()) return;
+  cudaEventRecord(g_prof.back().b, st);
+}
 
 namespace {
 
@@ -197,6 +224,37 @@ const char* adattn_b200_last_error(void) { return g_err.c_str(); }
 
 uint64_t adattn_b200_launch_count(void) { return g_launches.load(); }
 
+void adattn_b200_profile_enable(int on) {
+  std::lock_guard<std::mutex> l(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+int adattn_b200_profile_read(char* names, size_t names_len, double* ms, int max) {
+  std::lock_guard<std::mutex> l(g_prof_mu);
+  int n = 0;
+  std::string all;
+  for (auto& r : g_prof) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (n < max && ms) ms[n] = t;
+    if (n < max) {
+      all += r.name;
+      all += '\n';
+    }
+    ++n;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  if (names && names_len) {
+    const size_t k = std::min(all.size(), names_len - 1);
+    std::memcpy(names, all.data(), k);
+    names[k] = 0;
+  }
+  return std::min(n, max);
+}
+
 int adattn_b200_validate(const adattn_problem* p) {
   Geom g;
   int rc = check(p, &g);
@@ -310,7 +368,9 @@ static int stats_impl(const Geom& g, const uint32_t* mask, adattn_stats* out,
   cudaMemsetAsync(acc, 0, 2 * sizeof(unsigned long long), st);
   const size_t words = (size_t)g.bh * g.t_r * g.wpr;
   const int blocks = (int)std::min<size_t>((words + 255) / 256, 4096);
+  prof_begin("mask_stats", st);
   mask_stats_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(g, mask, acc);
+  prof_end(st);
   note_launch();
   unsigned long long h[2] = {0, 0};
   cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, st);

@@ -193,4 +193,8 @@ __device__ __forceinline__ bool row_step(RowSolve& rs, double alpha, double refi
 // Launch accounting (exported through adattn_b200_launch_count).
 void note_launch();
 
+// Optional per-kernel event timing (adattn_b200_profile_enable).
+void prof_begin(const char* name, cudaStream_t st);
+void prof_end(cudaStream_t st);
+
 }  // namespace adattn_b200

@@ -621,13 +621,16 @@ cudaError_t exact_forward(const Geom& g, const void* q, const void* k, const voi
   cudaError_t e;
   if (g.in_dtype == ADATTN_F64) {
     if ((e = prep(exact_forward_kernel<false>, smem))) return e;
+    prof_begin("exact_fwd", st);
     exact_forward_kernel<false><<<grid, kThreads, smem, st>>>(g, q, k, v, out, tau, row_max,
                                                              mask, steps);
   } else {
     if ((e = prep(exact_forward_kernel<true>, smem))) return e;
+    prof_begin("exact_fwd", st);
     exact_forward_kernel<true><<<grid, kThreads, smem, st>>>(g, q, k, v, out, tau, row_max,
                                                             mask, steps);
   }
+  prof_end(st);
   note_launch();
   return cudaGetLastError();
 }

@@ -168,20 +168,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
+      const bool leader = elect_one_sync();
       const int qrow = G.bh * g.n + G.row0;
-      mbar_expect_tx(q_full, 2 * L::QB);
+      if (leader) mbar_expect_tx(q_full, 2 * L::QB);
       for (int c = 0; c < NCH; ++c) {
-        tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
-        tma_load_2d(sDO + c * BM * 128, &tm_do, q_full, c * 64, qrow);
+        if (leader) tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
+        if (leader) tma_load_2d(sDO + c * BM * 128, &tm_do, q_full, c * 64, qrow);
       }
       uint32_t r = 0;
       auto load = [&](const CUtensorMap* tm, int row) {
         const uint32_t st = r % NST, ph = (r / NST) & 1;
         mbar_wait(&empty[st], ph ^ 1);
-        mbar_expect_tx(&full[st], L::TILE);
+        if (leader) mbar_expect_tx(&full[st], L::TILE);
         for (int c = 0; c < NCH; ++c)
-          tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
+          if (leader) tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
         ++r;
       };
       const int krow0 = G.bh * g.m;
@@ -191,7 +192,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
+      const bool leader = elect_one_sync();
       constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, false, false);
       const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ring_addr = smem_u32(sRing);
       mbar_wait(q_full, 0);
@@ -210,17 +212,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < NCH; ++c)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              umma_bf16(sc, desc_kmajor(q_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
+              if (leader) umma_bf16(sc, desc_kmajor(q_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
                         desc_kmajor(ring_addr + kst * L::TILE + c * BN * 128 + k * 32), IDESC_S,
                         (c | k) != 0);
-              umma_bf16(sc + 128, desc_kmajor(do_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
+              if (leader) umma_bf16(sc + 128, desc_kmajor(do_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
                         desc_kmajor(ring_addr + vst * L::TILE + c * BN * 128 + k * 32), IDESC_S,
                         (c | k) != 0);
             }
         }
-        umma_commit(&empty[kst]);
-        umma_commit(&empty[vst]);
-        umma_commit(&s_full[b]);
+        if (leader) umma_commit(&empty[kst]);
+        if (leader) umma_commit(&empty[vst]);
+        if (leader) umma_commit(&s_full[b]);
         ++item;
         r += 2;
       }
@@ -370,20 +372,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
+      const bool leader = elect_one_sync();
       const int qrow = bh * g.n + row0;
-      mbar_expect_tx(q_full, 2 * L::QB);
+      if (leader) mbar_expect_tx(q_full, 2 * L::QB);
       for (int c = 0; c < NCH; ++c) {
-        tma_load_2d(sQ + c * QB_DQ * 128, &tm_q, q_full, c * 64, qrow);
-        tma_load_2d(sDO + c * QB_DQ * 128, &tm_do, q_full, c * 64, qrow);
+        if (leader) tma_load_2d(sQ + c * QB_DQ * 128, &tm_q, q_full, c * 64, qrow);
+        if (leader) tma_load_2d(sDO + c * QB_DQ * 128, &tm_do, q_full, c * 64, qrow);
       }
       uint32_t r = 0;
       auto load = [&](const CUtensorMap* tm, int row) {
         const uint32_t st = r % NST, ph = (r / NST) & 1;
         mbar_wait(&empty[st], ph ^ 1);
-        mbar_expect_tx(&full[st], L::TILE);
+        if (leader) mbar_expect_tx(&full[st], L::TILE);
         for (int c = 0; c < NCH; ++c)
-          tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
+          if (leader) tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
         ++r;
       };
       const int krow0 = bh * g.m;
@@ -393,7 +396,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
+      const bool leader = elect_one_sync();
       constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, false, false);
       constexpr uint32_t IDESC_DQ = idesc_bf16_f32(128, D, false, true);
       const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO);
@@ -410,13 +414,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint64_t bd = desc_mnmajor(ring_addr + kst * L::TILE + k * 16 * 128, BN * 128);
-          umma_bf16(tmem + 256, desc_kmajor(ds_addr + k * 32), bd, IDESC_DQ,
+          if (leader) umma_bf16(tmem + 256, desc_kmajor(ds_addr + k * 32), bd, IDESC_DQ,
                     (acc_init || k > 0) ? 1u : 0u);
-          umma_bf16(tmem + 256, desc_kmajor(ds_addr + L::DSB + k * 32), bd, IDESC_DQ, 1u);
+          if (leader) umma_bf16(tmem + 256, desc_kmajor(ds_addr + L::DSB + k * 32), bd, IDESC_DQ, 1u);
         }
         acc_init = true;
-        umma_commit(&empty[kst]);
-        umma_commit(ds_empty);
+        if (leader) umma_commit(&empty[kst]);
+        if (leader) umma_commit(ds_empty);
       };
       for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
         const uint32_t b = item & 1;
@@ -429,15 +433,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            umma_bf16(sc, desc_kmajor(q_addr + c * QB_DQ * 128 + k * 32),
+            if (leader) umma_bf16(sc, desc_kmajor(q_addr + c * QB_DQ * 128 + k * 32),
                       desc_kmajor(ring_addr + kst * L::TILE + c * BN * 128 + k * 32), IDESC_S,
                       (c | k) != 0);
-            umma_bf16(sc + 64, desc_kmajor(do_addr + c * QB_DQ * 128 + k * 32),
+            if (leader) umma_bf16(sc + 64, desc_kmajor(do_addr + c * QB_DQ * 128 + k * 32),
                       desc_kmajor(ring_addr + vst * L::TILE + c * BN * 128 + k * 32), IDESC_S,
                       (c | k) != 0);
           }
-        umma_commit(&empty[vst]);
-        umma_commit(&s_full[b]);
+        if (leader) umma_commit(&empty[vst]);
+        if (leader) umma_commit(&s_full[b]);
         if (prev >= 0) dq_mma(prev_kst, item - 1);
         prev = j;
         prev_kst = kst;
@@ -445,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         r += 2;
       }
       if (prev >= 0) dq_mma(prev_kst, item - 1);
-      umma_commit(acc_full);
+      if (leader) umma_commit(acc_full);
     }
   } else if (warp >= 4) {
     const int half = (warp - 4) >> 2;  // key columns 32*half .. +31 of each tile
@@ -651,30 +655,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
+      const bool leader = elect_one_sync();
       const int krow = bh * g.m + key0;
-      mbar_expect_tx(kv_full, 2 * L::KVB);
+      if (leader) mbar_expect_tx(kv_full, 2 * L::KVB);
       for (int c = 0; c < NCH; ++c) {
-        tma_load_2d(sK + c * KB * 128, &tm_kb, kv_full, c * 64, krow);
-        tma_load_2d(sV + c * KB * 128, &tm_vb, kv_full, c * 64, krow);
+        if (leader) tma_load_2d(sK + c * KB * 128, &tm_kb, kv_full, c * 64, krow);
+        if (leader) tma_load_2d(sV + c * KB * 128, &tm_vb, kv_full, c * 64, krow);
       }
       uint32_t r = 0;
       for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1)) {
         const uint32_t st = r % KST, ph = (r / KST) & 1;
         mbar_wait(&empty[st], ph ^ 1);
-        mbar_expect_tx(&full[st], 2 * L::QTB + QT * 8);
+        if (leader) mbar_expect_tx(&full[st], 2 * L::QTB + QT * 8);
         uint8_t* base = sSt + st * L::STAGE;
         const int qrow = bh * g.n + i * QT;
         for (int c = 0; c < NCH; ++c) {
-          tma_load_2d(base + c * QT * 128, &tm_qt, &full[st], c * 64, qrow);
-          tma_load_2d(base + L::QTB + c * QT * 128, &tm_dot, &full[st], c * 64, qrow);
+          if (leader) tma_load_2d(base + c * QT * 128, &tm_qt, &full[st], c * 64, qrow);
+          if (leader) tma_load_2d(base + L::QTB + c * QT * 128, &tm_dot, &full[st], c * 64, qrow);
         }
-        bulk_load(base + 2 * L::QTB, a.rowc + qrow, QT * 8, &full[st]);
+        if (leader) bulk_load(base + 2 * L::QTB, a.rowc + qrow, QT * 8, &full[st]);
         ++r;
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
+      const bool leader = elect_one_sync();
       constexpr uint32_t IDESC_S = idesc_bf16_f32(128, QT, false, false);
       constexpr uint32_t IDESC_G = idesc_bf16_f32(128, D, false, true);
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), st_addr = smem_u32(sSt);
@@ -697,13 +703,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bdo = desc_mnmajor(qb + L::QTB + k * 16 * 128, QT * 128);
           const uint64_t bq = desc_mnmajor(qb + k * 16 * 128, QT * 128);
           const uint32_t acc = (init || k > 0) ? 1u : 0u;
-          umma_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G, acc);
-          umma_bf16_ts(tmem + 256, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
-          umma_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol, bq, IDESC_G, acc);
-          umma_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol + 16, bq, IDESC_G, 1u);
+          if (leader) umma_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G, acc);
+          if (leader) umma_bf16_ts(tmem + 256, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
+          if (leader) umma_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol, bq, IDESC_G, acc);
+          if (leader) umma_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol + 16, bq, IDESC_G, 1u);
         }
         init = true;
-        umma_commit(&empty[st]);
+        if (leader) umma_commit(&empty[st]);
       };
       for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1)) {
         const uint32_t st = u % KST;
@@ -714,19 +720,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            umma_bf16(tmem + b * 128, desc_kmajor(k_addr + c * KB * 128 + k * 32),
+            if (leader) umma_bf16(tmem + b * 128, desc_kmajor(k_addr + c * KB * 128 + k * 32),
                       desc_kmajor(qb + c * QT * 128 + k * 32), IDESC_S, (c | k) != 0);
-            umma_bf16(tmem + b * 128 + 64, desc_kmajor(v_addr + c * KB * 128 + k * 32),
+            if (leader) umma_bf16(tmem + b * 128 + 64, desc_kmajor(v_addr + c * KB * 128 + k * 32),
                       desc_kmajor(qb + L::QTB + c * QT * 128 + k * 32), IDESC_S, (c | k) != 0);
           }
-        umma_commit(&s_full[b]);
+        if (leader) umma_commit(&s_full[b]);
         if (prev >= 0) grad_mma(u - 1, prev_st);
         prev = i;
         prev_st = st;
         ++u;
       }
       if (prev >= 0) grad_mma(u - 1, prev_st);
-      umma_commit(acc_full);
+      if (leader) umma_commit(acc_full);
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
@@ -828,7 +834,9 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     auto k0 = tc_delta_kernel<D, AK>;
     const size_t sm = DeltaSmem<D>::bytes(g.wpr);
     if ((e = set_smem(k0, sm))) return e;
+    prof_begin("tc_delta", st);
     k0<<<dim3((unsigned)(a.ncta_rows * g.bh)), kThreads, sm, st>>>(m[0], m[1], m[2], m[3], a);
+    prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
   }
@@ -837,7 +845,9 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     auto k2 = tc_dkdv_kernel<D, AK>;
     const size_t sm = KvSmem<D>::bytes(g.t_r);
     if ((e = set_smem(k2, sm))) return e;
+    prof_begin("tc_dkdv", st);
     k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kThreads, sm, st>>>(m[4], m[5], m[6], m[7], a);
+    prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
   }
@@ -845,7 +855,9 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     auto k1 = tc_dq_kernel<D, AK>;
     const size_t sm = DqSmem<D>::bytes(g.wpr);
     if ((e = set_smem(k1, sm))) return e;
+    prof_begin("tc_dq", st);
     k1<<<dim3((unsigned)((g.n / QB_DQ) * g.bh)), kThreads, sm, st>>>(m[8], m[1], m[2], m[9], a);
+    prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
   }

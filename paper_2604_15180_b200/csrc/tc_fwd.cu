@@ -2,27 +2,32 @@
 // sm_100a (reference: /root/reference/proj/src/attention.cpp:157-361).
 //
 // One CTA = 256 query rows (four 64-row reference tiles, two M=128 UMMA row
-// groups) of one head; keys stream in 64-key tiles (one reference key tile).
-// Warp roles (384 threads):
+// groups RG0/RG1) of one head; keys stream in 64-key tiles (one reference key
+// tile), so every K tile fetched from L2 feeds two M=128 MMAs.
+// Warp roles (640 threads):
 //   warp 0      TMA producer: Q once, then K (and V in the output pass) tiles
 //               into a 4-stage SWIZZLE_128B ring
-//   warp 1      MMA issuer: S_g = Q_g K_j^T (M=128, N=64) into TMEM (double
-//               buffered), O_g += P_g V_j (M=128, N=dv) in the output pass
+//   warp 1      MMA issuer: S_g = Q_g K_j^T (M=128, N=64) into TMEM, double
+//               buffered per row group; O_g += P_g V_j (M=128, N=dv) in the
+//               output pass, with P split into bf16 hi + lo (two MMAs) so the
+//               bf16 rounding of P drops out of O
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4-11  epilogue, one thread per query row (tcgen05.ld 32x32b):
+//   warps 4-19  epilogue: 8 warps per row group, one thread per (row, 32-key
+//               half) -> 4 epilogue warps per SM sub-partition; each row group
+//               has its own S full/empty barriers, so the two groups drift
+//               apart and hide each other's TMEM-load latency.
 //               pass MAX  -> row max
 //               pass HIST -> bin counts of z >= 0 -> solve_histogram -> tau_h
 //               pass REF  -> f, f', f'' partial sums + 64x64 activity bits;
 //                            safeguarded step per row (repeats until no row moves)
-//               pass OUT  -> P = [z - tau]_+^(1/(alpha-1)) (bf16) into smem for
-//                            the P*V MMA, over the set mask bits only
+//               pass OUT  -> P = [z - tau]_+^(1/(alpha-1)) over the set mask bits
 // Per-row refinement state and the step rules run in fp64 exactly as the
-// reference; score-element math is fp32 (z = A1*acc + B, one FFMA).
+// reference; score-element math is fp32 (z = A1*acc + B, one FFMA), packed
+// f32x2 where it pays.
 #include <cuda.h>
 #include <math_constants.h>
 
-#include <cstdio>
-#include <mutex>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "tc.cuh"
@@ -33,14 +38,36 @@ namespace adattn_b200 {
 namespace tc {
 namespace {
 
-constexpr int BM = 256;       // query rows per CTA
-constexpr int BN = 64;        // keys per tile
-constexpr int NST = 4;        // ring stages
-constexpr int kThreads = 384;
-constexpr int kEpi = 256;     // epilogue threads
+constexpr int BM = 256;        // query rows per CTA
+constexpr int BN = 64;         // keys per tile
+constexpr int NST = 4;         // ring stages
+constexpr int kEpiWarps = 16;
+constexpr int kEpi = kEpiWarps * 32;
+constexpr int kThreads = 128 + kEpi;
 constexpr int DEC_REF = 0, DEC_OUT = 1;
 
 enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
+
+// Optional wait-cycle accounting (build with -DADATTN_PIPE_STATS): per CTA,
+// [0] MMA waits on TMA-full, [1] MMA waits on S-empty, [2] MMA waits on P-full,
+// [3] producer waits on ring-empty, [4] epilogue (warp 4 lane 0) waits on S-full,
+// [5] epilogue busy cycles, [6] MMA total cycles, [7] S tiles issued.
+}  // namespace
+#ifdef ADATTN_PIPE_STATS
+__device__ unsigned long long g_pipe_stats[8];
+#endif
+namespace {
+#ifdef ADATTN_PIPE_STATS
+#define PSTAT_T0() const long long _t0 = clock64()
+#define PSTAT_ADD(i) atomicAdd(&g_pipe_stats[i], (unsigned long long)(clock64() - _t0))
+#else
+#define PSTAT_T0() \
+  do {             \
+  } while (0)
+#define PSTAT_ADD(i) \
+  do {               \
+  } while (0)
+#endif
 
 struct FwdArgs {
   Geom g;
@@ -53,49 +80,24 @@ struct FwdArgs {
   double* row_max;
   uint32_t* mask;
   int32_t* steps;
+  int dbg;  // ADATTN_PIPE_STATS builds only: 1 = epilogue skips tcgen05.ld, 2 = skips math
 };
 
 template <int D>
 struct FwdSmem {
   static constexpr int QBYTES = BM * D * 2;
   static constexpr int TILE = BN * D * 2;
-  static constexpr int PBYTES = 2 * BM * BN * 2;  // P_hi, P_lo
+  static constexpr int PB = BM * BN * 2;  // one of P_hi / P_lo
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_RING = OFF_Q + QBYTES;
-  static constexpr int OFF_P = OFF_RING + NST * TILE;
-  static constexpr int OFF_BAR = OFF_P + PBYTES;
-  static constexpr int NBAR = 2 * NST + 10;
+  static constexpr int OFF_P = OFF_RING + NST * TILE;  // also the HIST/REF combine scratch
+  static constexpr int OFF_BAR = OFF_P + 2 * PB;
+  static constexpr int NBAR = 2 * NST + 16;
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
-  static constexpr int OFF_MASK = OFF_MISC + 64;
+  static constexpr int OFF_ROW = OFF_MISC + 64;  // [256][4] f32 per-row scratch
+  static constexpr int OFF_MASK = OFF_ROW + BM * 4 * 4;
   static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
 };
-
-template <int AK>
-__device__ __forceinline__ void ref_accumulate(float t, float e0f, float e1f, float e2f,
-                                               float& s0, float& s1, float& s2) {
-  const float tp = fmaxf(t, 0.f);
-  if constexpr (AK == AK15) {  // e0=2, e1=1, e2=0
-    s0 = fmaf(tp, tp, s0);
-    s1 += tp;
-    s2 += (t > 0.f) ? 1.f : 0.f;
-  } else if constexpr (AK == AK2) {  // e0=1, e1=0 (e2 unused by Newton)
-    s0 += tp;
-    s1 += (t > 0.f) ? 1.f : 0.f;
-  } else if constexpr (AK == AK125) {  // e0=4, e1=3, e2=2
-    const float t2 = tp * tp;
-    s0 = fmaf(t2, t2, s0);
-    s1 = fmaf(t2, tp, s1);
-    s2 += t2;
-  } else {
-    if (t > 0.f) {
-      const float lt = __log2f(t);
-      s0 += exp2f(e0f * lt);
-      const float l1 = e1f < 0.f ? __log2f(fmaxf(t, 1e-12f)) : lt;
-      s1 += (e1f == 0.f) ? 1.f : exp2f(e1f * l1);
-      s2 += (e2f == 0.f) ? 1.f : exp2f(e2f * (e2f < 0.f ? __log2f(fmaxf(t, 1e-12f)) : lt));
-    }
-  }
-}
 
 template <int AK>
 __device__ __forceinline__ float p_of(float t, float e0f) {
@@ -108,6 +110,65 @@ __device__ __forceinline__ float p_of(float t, float e0f) {
   } else {
     return tp > 0.f ? exp2f(e0f * __log2f(tp)) : 0.f;
   }
+}
+
+// Partial sums of one 32-element slice for the refinement pass: two
+// independent accumulator sets of packed f32x2 for ILP.
+template <int AK>
+__device__ __forceinline__ void ref_slice(const float* v, float A1, float C, float e0f, float e1f,
+                                          float e2f, float& s0o, float& s1o, float& s2o,
+                                          float& mxo) {
+  const float2 A2 = make_float2(A1, A1), C2 = make_float2(C, C);
+  float2 s0a = make_float2(0.f, 0.f), s1a = s0a, s2a = s0a, s0b = s0a, s1b = s0a, s2b = s0a;
+  float mxa = -CUDART_INF_F, mxb = -CUDART_INF_F;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 t = __ffma2_rn(A2, make_float2(v[2 * i], v[2 * i + 1]), C2);
+    float2& s0 = (i & 1) ? s0b : s0a;
+    float2& s1 = (i & 1) ? s1b : s1a;
+    float2& s2 = (i & 1) ? s2b : s2a;
+    float& mx = (i & 1) ? mxb : mxa;
+    mx = fmaxf(mx, fmaxf(t.x, t.y));
+    const float2 tp = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
+    if constexpr (AK == AK15) {  // e0=2, e1=1, e2=0
+      s0 = __ffma2_rn(tp, tp, s0);
+      s1 = __fadd2_rn(s1, tp);
+      s2 = __fadd2_rn(s2, make_float2(__saturatef(tp.x * 0x1p126f), __saturatef(tp.y * 0x1p126f)));
+    } else if constexpr (AK == AK2) {  // e0=1, e1=0; f2 is unused by Newton
+      s0 = __fadd2_rn(s0, tp);
+      s1 = __fadd2_rn(s1, make_float2(__saturatef(tp.x * 0x1p126f), __saturatef(tp.y * 0x1p126f)));
+    } else if constexpr (AK == AK125) {  // e0=4, e1=3, e2=2
+      const float2 t2 = __fmul2_rn(tp, tp);
+      s0 = __ffma2_rn(t2, t2, s0);
+      s1 = __ffma2_rn(t2, tp, s1);
+      s2 = __fadd2_rn(s2, t2);
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float x = h ? tp.y : tp.x;
+        if (x > 0.f) {
+          const float lt = __log2f(x);
+          const float l1 = e1f < 0.f ? __log2f(fmaxf(x, 1e-12f)) : lt;
+          const float l2 = e2f < 0.f ? __log2f(fmaxf(x, 1e-12f)) : lt;
+          const float a0 = exp2f(e0f * lt), a1 = (e1f == 0.f) ? 1.f : exp2f(e1f * l1);
+          const float a2 = (e2f == 0.f) ? 1.f : exp2f(e2f * l2);
+          if (h) {
+            s0.y += a0;
+            s1.y += a1;
+            s2.y += a2;
+          } else {
+            s0.x += a0;
+            s1.x += a1;
+            s2.x += a2;
+          }
+        }
+      }
+    }
+  }
+  s0o = (s0a.x + s0a.y) + (s0b.x + s0b.y);
+  s1o = (s1a.x + s1a.y) + (s1b.x + s1b.y);
+  s2o = (s2a.x + s2a.y) + (s2b.x + s2b.y);
+  mxo = fmaxf(mxa, mxb);
 }
 
 template <int D, int AK>
@@ -124,18 +185,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sRing = smem + L::OFF_RING;
   uint8_t* sP = smem + L::OFF_P;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + NST;
-  uint64_t* s_full = bars + 2 * NST;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
+  uint64_t* full = bars;               // [NST]
+  uint64_t* empty = bars + NST;        // [NST]
+  uint64_t* s_full = bars + 2 * NST;   // [2 buffers][2 row groups]
+  uint64_t* s_empty = s_full + 4;      // [2][2]
+  uint64_t* p_full = s_empty + 4;
   uint64_t* p_empty = p_full + 1;
   uint64_t* o_full = p_empty + 1;
   uint64_t* q_full = o_full + 1;
   uint64_t* dec_bar = q_full + 1;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
-  volatile uint32_t* s_tmem = misc;         // TMEM base
+  volatile uint32_t* s_tmem = misc;  // TMEM base
   volatile uint32_t* s_decision = misc + 1;
+  // Combine scratch of the two key halves of a row.  The count and partial-sum
+  // arrays overlay the P buffers, which stay unused until the output pass.
+  uint32_t* sCnt = reinterpret_cast<uint32_t*>(sP);                // [2][256][32] u32
+  double* sPart = reinterpret_cast<double*>(sP + BM * 32 * 4);     // [256][4] f64 (REF only)
+  float* sRow = reinterpret_cast<float*>(smem + L::OFF_ROW);      // [256][4] f32
   uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [4][wpr]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -153,11 +219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 8);
     }
-    mbar_init(p_full, 8);
+    mbar_init(p_full, kEpiWarps);
     mbar_init(p_empty, 1);
     mbar_init(o_full, 1);
     mbar_init(q_full, 1);
@@ -189,17 +255,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
+    {
+      const bool leader = elect_one_sync();
       const int qrow = bh * g.n + row0;
-      mbar_expect_tx(q_full, L::QBYTES);
-      for (int c = 0; c < NCH; ++c) tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
+      if (leader) mbar_expect_tx(q_full, L::QBYTES);
+      for (int c = 0; c < NCH; ++c)
+        if (leader) tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
       uint32_t r = 0;
       auto load = [&](const CUtensorMap* tm, int row) {
         const uint32_t st = r % NST, ph = (r / NST) & 1;
-        mbar_wait(&empty[st], ph ^ 1);
-        mbar_expect_tx(&full[st], L::TILE);
+        {
+          PSTAT_T0();
+          mbar_wait(&empty[st], ph ^ 1);
+          PSTAT_ADD(3);
+        }
+        if (leader) mbar_expect_tx(&full[st], L::TILE);
         for (int c = 0; c < NCH; ++c)
-          tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
+          if (leader) tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
         ++r;
       };
       const int krow0 = bh * g.m;
@@ -220,33 +292,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    {
+      const bool leader = elect_one_sync();
       constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, false, false);
       constexpr uint32_t IDESC_PV = idesc_bf16_f32(128, D, false, true);
       const uint32_t q_addr = smem_u32(sQ), ring_addr = smem_u32(sRing), p_addr = smem_u32(sP);
       mbar_wait(q_full, 0);
       tc_fence_after();
-      uint32_t item = 0, r = 0;
+#ifdef ADATTN_PIPE_STATS
+      const long long t_mma0 = clock64();
+#endif
+      uint32_t it[2] = {0, 0}, r = 0;
       auto s_tile = [&](int j, bool out_pass) {
-        const uint32_t b = item & 1;
-        mbar_wait(&s_empty[b], ((item >> 1) & 1) ^ 1);
         const uint32_t st = r % NST;
-        mbar_wait(&full[st], (r / NST) & 1);
+        {
+          PSTAT_T0();
+          mbar_wait(&full[st], (r / NST) & 1);
+          PSTAT_ADD(0);
+        }
         tc_fence_after();
         for (int rg = 0; rg < 2; ++rg) {
           const bool need = out_pass ? out_active(rg, j) : (j <= rg_jlim[rg]);
           if (!need) continue;
+          const uint32_t b = it[rg] & 1;
+          {
+            PSTAT_T0();
+            mbar_wait(&s_empty[b * 2 + rg], ((it[rg] >> 1) & 1) ^ 1);
+            PSTAT_ADD(1);
+          }
+          tc_fence_after();
           const uint32_t d_t = tmem + b * 128 + rg * 64;
           for (int c = 0; c < NCH; ++c)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              umma_bf16(d_t, desc_kmajor(q_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
+              if (leader) umma_bf16(d_t, desc_kmajor(q_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
                         desc_kmajor(ring_addr + st * L::TILE + c * BN * 128 + k * 32), IDESC_S,
                         (c | k) != 0);
+          if (leader) umma_commit(&s_full[b * 2 + rg]);
+          ++it[rg];
         }
-        umma_commit(&empty[st]);
-        umma_commit(&s_full[b]);
-        ++item;
+        if (leader) umma_commit(&empty[st]);
         ++r;
       };
       bool o_init[2] = {false, false};
@@ -254,7 +339,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto pv_tile = [&](int j) {
         const uint32_t st = r % NST;
         mbar_wait(&full[st], (r / NST) & 1);
-        mbar_wait(p_full, pi & 1);
+        {
+          PSTAT_T0();
+          mbar_wait(p_full, pi & 1);
+          PSTAT_ADD(2);
+        }
         tc_fence_after();
         for (int rg = 0; rg < 2; ++rg) {
           if (!out_active(rg, j)) continue;
@@ -262,15 +351,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t bd = desc_mnmajor(ring_addr + st * L::TILE + k * 16 * 128, BN * 128);
-            umma_bf16(d_t, desc_kmajor(p_addr + rg * 128 * 128 + k * 32), bd, IDESC_PV,
+            if (leader) umma_bf16(d_t, desc_kmajor(p_addr + rg * 128 * 128 + k * 32), bd, IDESC_PV,
                       (o_init[rg] || k > 0) ? 1u : 0u);
-            umma_bf16(d_t, desc_kmajor(p_addr + BM * BN * 2 + rg * 128 * 128 + k * 32), bd,
-                      IDESC_PV, 1u);
+            if (leader) umma_bf16(d_t, desc_kmajor(p_addr + L::PB + rg * 128 * 128 + k * 32), bd, IDESC_PV,
+                      1u);
           }
           o_init[rg] = true;
         }
-        umma_commit(&empty[st]);
-        umma_commit(p_empty);
+        if (leader) umma_commit(&empty[st]);
+        if (leader) umma_commit(p_empty);
         ++r;
         ++pi;
       };
@@ -288,79 +377,97 @@ __global__ void __launch_bounds__(kThreads, 1)
         prev = j;
       }
       if (prev >= 0) pv_tile(prev);
-      umma_commit(o_full);
+      if (leader) umma_commit(o_full);
+#ifdef ADATTN_PIPE_STATS
+      atomicAdd(&g_pipe_stats[6], (unsigned long long)(clock64() - t_mma0));
+      atomicAdd(&g_pipe_stats[7], (unsigned long long)r);
+#endif
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    const int e = tid - 128;          // 0..255 == local query row
-    const int rg = e >> 7;            // row group
+    const int ew = warp - 4;          // 0..15
+    const int rg = ew >> 3;           // row group
+    const int half = (ew >> 2) & 1;   // key columns 32*half .. +31 of each tile
     const int lq = warp & 3;          // TMEM lane quarter
+    const int e = rg * 128 + lq * 32 + lane;  // local query row 0..255
     const int grow = row0 + e;        // query row within the head
     const int rb = e >> 6;            // 64-row reference tile within the CTA
-    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16);
+    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + rg * 64 + half * 32;
     const int jl = rg_jlim[rg];
+    const int bar_rg = 1 + rg;        // named barrier of this row group (256 threads)
     const float A1 = a.A1;
     uint32_t item = 0;
 
-    // Fetch S for (item, key tile j) into v[64]; release the TMEM buffer.
-    float v[64];
-    auto fetch = [&](int j, bool need) {
+    // S slice (32 keys) of key tile j into v[32]; release the TMEM buffer.
+    float v[32];
+    auto fetch = [&](int j) {
       const uint32_t b = item & 1;
-      mbar_wait(&s_full[b], (item >> 1) & 1);
+#ifdef ADATTN_PIPE_STATS
+      const long long _tw = clock64();
+#endif
+      mbar_wait(&s_full[b * 2 + rg], (item >> 1) & 1);
+#ifdef ADATTN_PIPE_STATS
+      if (warp == 4 && lane == 0) atomicAdd(&g_pipe_stats[4], (unsigned long long)(clock64() - _tw));
+#endif
       tc_fence_after();
-      if (need) {
-        tmem_ld32(tl + b * 128 + rg * 64, v);
-        tmem_ld32(tl + b * 128 + rg * 64 + 32, v + 32);
+#ifdef ADATTN_PIPE_STATS
+      if (a.dbg & 1) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = (float)(i - 40);
+      } else
+#endif
+      {
+        tmem_ld32(tl + b * 128, v);
         tmem_wait_ld();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[b]);
+      if (lane == 0) mbar_arrive(&s_empty[b * 2 + rg]);
       ++item;
-      if (need && g.causal && j * BN + BN - 1 > grow) {
+      const int c0 = j * BN + half * 32;
+      if (g.causal && c0 + 31 > grow) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (j * BN + i > grow) v[i] = -CUDART_INF_F;
+        for (int i = 0; i < 32; ++i)
+          if (c0 + i > grow) v[i] = -CUDART_INF_F;
       }
     };
 
-    // pass MAX (attention.cpp:182-195): max of raw dot products, scaled once
+    // ---- pass MAX (attention.cpp:182-195): max of raw dot products, scaled once
     float mraw = -CUDART_INF_F;
-    for (int j = 0; j <= jmax; ++j) {
-      const bool need = j <= jl;
-      fetch(j, need);
-      if (need) {
+    for (int j = 0; j <= jl; ++j) {
+      fetch(j);
 #pragma unroll
-        for (int i = 0; i < 64; ++i) mraw = fmaxf(mraw, v[i]);
-      }
+      for (int i = 0; i < 32; i += 2) mraw = fmaxf(mraw, fmaxf(v[i], v[i + 1]));
     }
+    sRow[e * 4 + half] = mraw;
+    bar_sync(bar_rg, 256);
+    mraw = fmaxf(sRow[e * 4], sRow[e * 4 + 1]);
     const float m_f = a.scale_f * mraw;  // == max(scale * s): rounding is monotone
     const double B = 1.0 - (g.alpha - 1.0) * (double)m_f;  // z = A1*acc + B
     const float Bf = (float)B;
 
-    // pass HIST (attention.cpp:201-232): counts of bin min(floor(B*z), B-1), z >= 0
+    // ---- pass HIST (attention.cpp:201-232): counts of min(floor(B z), B-1), z >= 0
     const int nb = g.bins;
-    uint32_t cnt[32];
+    uint32_t cnt[8];  // bins <= 8 in registers; larger bin counts go to shared memory
 #pragma unroll
-    for (int k = 0; k < 32; ++k) cnt[k] = 0;
+    for (int k = 0; k < 8; ++k) cnt[k] = 0;
+    uint32_t* my_cnt = sCnt + (half * BM + e) * 32;  // [2][256][32] over the P buffers
+    if (nb > 8)
+      for (int k = 0; k < nb; ++k) my_cnt[k] = 0;
     {
       const float An = A1 * (float)nb, Bn = Bf * (float)nb;  // exact: nb is a power of 2
-      for (int j = 0; j <= jmax; ++j) {
-        const bool need = j <= jl;
-        fetch(j, need);
-        if (!need) continue;
+      for (int j = 0; j <= jl; ++j) {
+        fetch(j);
         if (nb <= 8) {
-          uint32_t lo = 0, hi = 0;  // 8-bit fields, <= 64 per tile
+          uint32_t lo = 0, hi = 0;  // 8-bit fields, <= 32 per tile
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
+          for (int i = 0; i < 32; ++i) {
             const float y = fmaf(An, v[i], Bn);
-            if (y >= 0.f) {
-              int b = (int)(__float_as_uint(__fadd_rd(y, 8388608.f)) & 0x3Fu);
-              b = min(b, nb - 1);
-              const uint32_t inc = 1u << ((b & 3) << 3);
-              if (b < 4) lo += inc;
-              else hi += inc;
-            }
+            int b = (int)(__float_as_uint(__fadd_rd(fmaxf(y, 0.f), 8388608.f)) & 0x3Fu);
+            b = min(b, nb - 1);
+            const uint32_t inc = (y >= 0.f) ? (1u << ((b & 3) << 3)) : 0u;
+            lo += (b < 4) ? inc : 0u;
+            hi += (b >= 4) ? inc : 0u;
           }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -369,24 +476,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
+          for (int i = 0; i < 32; ++i) {
             const float y = fmaf(An, v[i], Bn);
             if (y >= 0.f) {
               int b = (int)(__float_as_uint(__fadd_rd(y, 8388608.f)) & 0x3Fu);
-              b = min(b, nb - 1);
-#pragma unroll
-              for (int k = 0; k < 32; ++k)
-                if (k == b) cnt[k] += 1;
+              my_cnt[min(b, nb - 1)] += 1;
             }
           }
         }
       }
     }
+    // combine the two key halves; the half-0 thread owns the row's solver state
     RowSolve rs;
-    {
-      uint32_t c32[32];
+    rs.tau = 0.0;
+    rs.lo = rs.hi = 0.0;
+    rs.steps = 0;
+    rs.done = true;
+    if (half == 1 && nb <= 8) {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) c32[k] = cnt[k];
+      for (int k = 0; k < 8; ++k) my_cnt[k] = cnt[k];
+    }
+    bar_sync(bar_rg, 256);
+    if (half == 0) {
+      uint32_t c32[32];
+      const uint32_t* other = sCnt + (BM + e) * 32;
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        c32[k] = k < nb ? (nb <= 8 ? cnt[k & 7] : my_cnt[k]) + other[k] : 0u;
       double th, lo, hi;
       solve_histogram_dev(c32, nb, g.alpha, th, lo, hi);
       rs.tau = th;
@@ -398,87 +514,90 @@ __global__ void __launch_bounds__(kThreads, 1)
       rs.steps = 0;
       rs.sec_seeded = false;
       rs.done = false;
+      sRow[e * 4 + 2] = (float)(B - rs.tau);
+      sRow[e * 4 + 3] = (float)(B - rs.hi);
     }
 
-    // passes REF (attention.cpp:234-332)
+    // ---- passes REF (attention.cpp:234-332)
     const bool need_sec = g.alpha > 2.0;
     const double e0 = g.e0;
     bool first_pass = true;
     for (uint32_t ref = 0;; ++ref) {
-      for (int i = e; i < 4 * wpr; i += kEpi) smask[i] = 0u;
-      bar_sync(1, kEpi);
-      double f = -1.0, f1 = 0.0, f2 = 0.0, fhi = -1.0;
-      const float C = (float)(B - rs.tau);
-      const float Chi = (float)(B - rs.hi);
-      for (int j = 0; j <= jmax; ++j) {
-        const bool need = j <= jl;
-        fetch(j, need);
-        bool act = false;
-        if (need) {
-          float s0 = 0.f, s1 = 0.f, s2 = 0.f, shi = 0.f, mx = -CUDART_INF_F;
+      for (int i = tid - 128; i < 4 * wpr; i += kEpi) smask[i] = 0u;
+      bar_sync(3, kEpi);  // C/Chi published, masks cleared, sCnt consumed
+      const float C = sRow[e * 4 + 2];
+      const float Chi = sRow[e * 4 + 3];
+      double f = 0.0, f1 = 0.0, f2 = 0.0, fhi = 0.0;
+      for (int j = 0; j <= jl; ++j) {
+        fetch(j);
+        float s0, s1, s2, mx;
+        ref_slice<AK>(v, A1, C, a.e0f, a.e1f, a.e2f, s0, s1, s2, mx);
+        if (first_pass && need_sec) {
+          float shi = 0.f;
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
-            const float t = fmaf(A1, v[i], C);
-            mx = fmaxf(mx, t);
-            ref_accumulate<AK>(t, a.e0f, a.e1f, a.e2f, s0, s1, s2);
+          for (int i = 0; i < 32; ++i) {
+            const float th = fmaf(A1, v[i], Chi);
+            if (th > 0.f) shi += exp2f(a.e0f * __log2f(th));
           }
-          if (first_pass && need_sec) {
-#pragma unroll
-            for (int i = 0; i < 64; ++i) {
-              const float th = fmaf(A1, v[i], Chi);
-              if (th > 0.f) shi += exp2f(a.e0f * __log2f(th));
-            }
-          }
-          f += (double)s0;
-          f1 -= e0 * (double)s1;
-          f2 += e0 * (e0 - 1.0) * (double)s2;
-          if (first_pass && need_sec) fhi += (double)shi;
-          act = mx > -1e-9f;
+          fhi += (double)shi;
         }
-        if (__any_sync(0xffffffffu, act) && lane == 0)
+        f += (double)s0;
+        f1 += (double)s1;
+        f2 += (double)s2;
+        if (__any_sync(0xffffffffu, mx > -1e-9f) && lane == 0)
           atomicOr(&smask[rb * wpr + (j >> 5)], 1u << (j & 31));
       }
+      if (half == 1) {
+        sPart[e * 4 + 0] = f;
+        sPart[e * 4 + 1] = f1;
+        sPart[e * 4 + 2] = f2;
+        sPart[e * 4 + 3] = fhi;
+      }
+      bar_sync(bar_rg, 256);
       bool stepped = false;
-      if (!rs.done) {
-        rs.f = f;
-        rs.f1 = f1;
-        rs.f2 = f2;
-        if (first_pass) rs.f_hi = fhi;
+      if (half == 0 && !rs.done) {
+        rs.f = -1.0 + (f + sPart[e * 4 + 0]);
+        rs.f1 = -e0 * (f1 + sPart[e * 4 + 1]);
+        rs.f2 = e0 * (e0 - 1.0) * (f2 + sPart[e * 4 + 2]);
+        if (first_pass) rs.f_hi = -1.0 + (fhi + sPart[e * 4 + 3]);
         stepped = row_step(rs, g.alpha, g.refine_tol, g.refine_iters, need_sec);
+        sRow[e * 4 + 2] = (float)(B - rs.tau);
       }
       first_pass = false;
-      const bool any = bar_red_or(2, kEpi, stepped);
-      if (e == 0) {
+      const bool any = bar_red_or(4, kEpi, stepped);
+      if (tid == 128) {
         *s_decision = any ? DEC_REF : DEC_OUT;
         mbar_arrive(dec_bar);
       }
       if (!any) break;
     }
 
-    // pass OUT (attention.cpp:334-352): P over the active 64x64 blocks
+    // ---- pass OUT (attention.cpp:334-352): P over the active 64x64 blocks
     {
-      const float C = (float)(B - rs.tau);
+      const float C = sRow[e * 4 + 2];
+      const float2 A2 = make_float2(A1, A1), C2 = make_float2(C, C);
       uint32_t pi = 0;
       const uint32_t p_row = smem_u32(sP) + (uint32_t)e * 128u;
       bool any_out = false;
       for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
         const bool need = out_active(rg, j);
-        any_out |= need;
-        fetch(j, need);
-        uint32_t ph[32], pl[32];
+        uint32_t ph[16], pl[16];
         if (need) {
+          any_out = true;
+          fetch(j);
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            split_bf16x2(p_of<AK>(fmaf(A1, v[2 * i], C), a.e0f),
-                         p_of<AK>(fmaf(A1, v[2 * i + 1], C), a.e0f), ph[i], pl[i]);
+          for (int i = 0; i < 16; ++i) {
+            const float2 t = __ffma2_rn(A2, make_float2(v[2 * i], v[2 * i + 1]), C2);
+            split_bf16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f), ph[i], pl[i]);
+          }
         }
         mbar_wait(p_empty, (pi & 1) ^ 1);
         if (need) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const uint32_t off = (q ^ (e & 7)) << 4;
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t off = (((uint32_t)(half * 4 + q)) ^ (uint32_t)(e & 7)) << 4;
             st_shared_v4(p_row + off, ph[4 * q], ph[4 * q + 1], ph[4 * q + 2], ph[4 * q + 3]);
-            st_shared_v4(p_row + BM * BN * 2 + off, pl[4 * q], pl[4 * q + 1], pl[4 * q + 2],
+            st_shared_v4(p_row + L::PB + off, pl[4 * q], pl[4 * q + 1], pl[4 * q + 2],
                          pl[4 * q + 3]);
           }
         }
@@ -487,33 +606,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(p_full);
         ++pi;
       }
-      // write O (fp32 or fp64), tau, row_max, steps
+      // write O (fp32 or fp64): this thread's half of the row's dv columns
       const size_t orow = (size_t)bh * g.n + grow;
       mbar_wait(o_full, 0);
       tc_fence_after();
+      const bool written = __any_sync(0xffffffffu, any_out);
+      const uint32_t to = tmem + ((uint32_t)(lq * 32) << 16) + 256 + rg * D + half * (D / 2);
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / 64; ++c) {
         float o[32];
-        tmem_ld32(tl + 256 + rg * D + c * 32, o);
+        tmem_ld32(to + c * 32, o);
         tmem_wait_ld();
-        if (!__any_sync(0xffffffffu, any_out)) {
+        if (!written) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = 0.f;
         }
+        const int x0 = half * (D / 2) + c * 32;
         if (g.out_dtype == ADATTN_F64) {
-          double* dst = reinterpret_cast<double*>(a.out) + orow * D + c * 32;
+          double* dst = reinterpret_cast<double*>(a.out) + orow * D + x0;
 #pragma unroll
           for (int i = 0; i < 32; ++i) dst[i] = (double)o[i];
         } else {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + orow * D + c * 32);
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + orow * D + x0);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
         }
       }
-      a.tau[orow] = rs.tau;
-      a.row_max[orow] = (double)m_f;
-      if (a.steps) a.steps[orow] = rs.steps;
-      for (int i = e; i < 4 * wpr; i += kEpi) {
+      if (half == 0) {
+        a.tau[orow] = rs.tau;
+        a.row_max[orow] = (double)m_f;
+        if (a.steps) a.steps[orow] = rs.steps;
+      }
+      for (int i = tid - 128; i < 4 * wpr; i += kEpi) {
         const int rbi = i / wpr, w = i - rbi * wpr;
         a.mask[((size_t)bh * g.t_r + (row0 / 64 + rbi)) * wpr + w] = smask[i];
       }
@@ -532,7 +657,9 @@ cudaError_t launch_fwd(const Geom& g, const CUtensorMap& tq, const CUtensorMap& 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
   const dim3 grid((unsigned)(a.ncta_rows * g.bh));
+  prof_begin("tc_fwd", st);
   kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, a);
+  prof_end(st);
   note_launch();
   return cudaGetLastError();
 }
@@ -578,6 +705,10 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.row_max = row_max;
   a.mask = mask;
   a.steps = steps;
+  a.dbg = 0;
+#ifdef ADATTN_PIPE_STATS
+  if (const char* dv = getenv("ADATTN_DBG")) a.dbg = atoi(dv);
+#endif
   const int ak = alpha_kind(g.alpha);
   if (g.d == 64) return launch_fwd_d<64>(g, ak, tq, tk, tv, a, st);
   return launch_fwd_d<128>(g, ak, tq, tk, tv, a, st);
@@ -585,3 +716,13 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
 
 }  // namespace tc
 }  // namespace adattn_b200
+
+#ifdef ADATTN_PIPE_STATS
+extern "C" void adattn_b200_pipe_stats(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, adattn_b200::tc::g_pipe_stats, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(adattn_b200::tc::g_pipe_stats, z, sizeof z);
+  }
+}
+#endif

@@ -1,0 +1,64 @@
+"""Synthetic inputs for the measurement harness (BASELINE.json configs).
+
+* ``gaussian``  -- cmd_attn's distribution (atn_main.cpp:227-232): Q = qscale*N(0,1),
+  K, V, dO ~ N(0,1), drawn on the GPU with torch (bf16).
+* ``anchored``  -- SURVEY.md section 7 item 7: each 64-row query tile picks G=2 anchor
+  key tiles (its diagonal tile and one random earlier tile); every row picks a
+  random anchor key c <= r inside them and sets q_r = beta * k_c + N(0,1).
+  beta is the temperature knob that sweeps 64x64 block sparsity from ~0 to the
+  1 - G*T/A ceiling; the harness reports the sparsity it measures.
+"""
+from __future__ import annotations
+
+import torch
+
+# BASELINE.json "configs" (index -> shape); C3 is the headline (metric quoted at N=32K)
+CONFIGS = {
+    "c1": dict(B=1, H=4, N=1024, D=64, alpha=1.5, causal=True, dtype=torch.float32),
+    "c2": dict(B=4, H=16, N=8192, D=128, alpha=1.5, causal=True, dtype=torch.bfloat16),
+    "c3": dict(B=2, H=32, N=32768, D=128, alpha=1.5, causal=True, dtype=torch.bfloat16),
+    "c4": dict(B=8, H=32, N=16384, D=64, alpha=1.5, causal=False, dtype=torch.bfloat16),
+    "c5": dict(B=1, H=32, N=131072, D=128, alpha=1.5, causal=True, dtype=torch.bfloat16),
+}
+
+
+def gaussian(B, H, N, D, qscale=1.0, seed=0, device="cuda", dtype=torch.bfloat16):
+    g = torch.Generator(device=device).manual_seed(seed)
+    mk = lambda s: (s * torch.randn(B, H, N, D, generator=g, device=device)).to(dtype)
+    q = mk(qscale)
+    k, v, do = mk(1.0), mk(1.0), mk(1.0)
+    return q, k, v, do
+
+
+def anchored(B, H, N, D, beta, causal=True, seed=0, device="cuda", dtype=torch.bfloat16):
+    g = torch.Generator(device=device).manual_seed(seed)
+    k = torch.randn(B, H, N, D, generator=g, device=device)
+    v = torch.randn(B, H, N, D, generator=g, device=device)
+    do = torch.randn(B, H, N, D, generator=g, device=device)
+    noise = torch.randn(B, H, N, D, generator=g, device=device)
+    T = N // 64
+    tiles = torch.arange(T, device=device)
+    hi = tiles + 1 if causal else torch.full_like(tiles, T)
+    other = (torch.rand(B, H, T, generator=g, device=device) * hi).long()  # random tile
+    other = torch.minimum(other, hi - 1)
+    r = torch.arange(N, device=device)
+    rt = r // 64
+    pick = torch.rand(B, H, N, generator=g, device=device) < 0.5
+    tile = torch.where(pick, other[:, :, rt], rt.expand(B, H, N))
+    # key inside the tile; in the diagonal tile stay at or below the row (causal)
+    width = torch.where((tile == rt) & causal, (r % 64) + 1, torch.full_like(r, 64))
+    off = (torch.rand(B, H, N, generator=g, device=device) * width).long()
+    c = tile * 64 + torch.minimum(off, width - 1)
+    kc = torch.gather(k, 2, c.unsqueeze(-1).expand(B, H, N, D))
+    q = beta * kc + noise
+    return q.to(dtype), k.to(dtype), v.to(dtype), do.to(dtype)
+
+
+def flops(D: int, nnz: int, addressable: int, ref_passes: int = 3) -> dict:
+    """F_eff = 14 d 4096 nnz (fwd QK^T+PV, bwd S, dP, dV, dK, dQ
+    over active 64x64 blocks); F_alg = F_eff + 2 d 4096 (2 + R) A (max, histogram and
+    R refinement QK^T passes over every addressable block)."""
+    f_eff = 14.0 * D * 4096 * nnz
+    f_alg = f_eff + 2.0 * D * 4096 * (2 + ref_passes) * addressable
+    f_fwd = 4.0 * D * 4096 * nnz + 2.0 * D * 4096 * (2 + ref_passes) * addressable
+    return dict(f_eff=f_eff, f_alg=f_alg, f_fwd=f_fwd)

@@ -1,0 +1,103 @@
+// mma_bench.cu -- microbenchmark of tcgen05.mma issue throughput per SM for the
+// operand sources / shapes the attention kernels use (dev tool, not product).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2604_15180_b200/csrc
+//        -I../include tools/mma_bench.cu -o mma_bench -lcuda
+#include <cstdio>
+#include <cstdlib>
+
+#include "tc_common.cuh"
+
+using namespace adattn_b200::tc;
+
+// MODE bit0: commit to a side barrier every 8 MMAs; bit1: tcgen05 fence::after
+// every 8; bit2: mbarrier try_wait on an already-complete barrier every 8
+template <int N, bool TS, int NMMA, int MODE = 0>
+__global__ void __launch_bounds__(128, 1) bench(unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, side, done;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&side, 1);
+    mbar_init(&done, 1);
+    mbar_arrive(&done);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (warp == 1) {
+    const bool leader = elect_one_sync();
+    const uint32_t a_addr = smem_u32(smem), b_addr = smem_u32(smem + 32768);
+    constexpr uint32_t IDESC = idesc_bf16_f32(128, N, false, false);
+    const long long t0 = clock64();
+    for (int i = 0; i < NMMA; ++i) {
+      const int k = i & 3;
+      if ((i & 7) == 0 && i) {
+        if (MODE & 1)
+          if (leader) umma_commit(&side);
+        if (MODE & 4) mbar_wait(&done, 0);
+        if (MODE & 2) tc_fence_after();
+      }
+      if (leader) {
+        if constexpr (TS) {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256),
+              "r"(tmem + 8 * k), "l"(desc_kmajor(b_addr + k * 32)), "r"(IDESC), "r"(1u));
+        } else {
+          umma_bf16(tmem + 256, desc_kmajor(a_addr + k * 32), desc_kmajor(b_addr + k * 32), IDESC,
+                    1u);
+        }
+      }
+    }
+    if (leader) umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (leader) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int N, bool TS, int MODE = 0>
+void run(const char* name) {
+  constexpr int NMMA = 4096;
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  auto k = bench<N, TS, NMMA, MODE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k<<<148, 128, 100 * 1024>>>(d);
+  k<<<148, 128, 100 * 1024>>>(d);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += (double)h[i] / 148.0;
+  const double cyc = avg / NMMA;
+  const double macs = 128.0 * N * 16;
+  printf("%-18s %s  cycles/MMA %7.1f  MAC/cycle/SM %7.0f  (%.0f%% of 4096)\n", name,
+         e ? cudaGetErrorString(e) : "ok", cyc, macs / cyc, 100.0 * macs / cyc / 4096.0);
+  cudaFree(d);
+}
+
+int main() {
+  run<64, false>("SS M128 N64");
+  run<128, false>("SS M128 N128");
+  run<256, false>("SS M128 N256");
+  run<64, true>("TS M128 N64");
+  run<128, true>("TS M128 N128");
+  run<256, true>("TS M128 N256");
+  run<64, false, 1>("SS N64 +commit/8");
+  run<64, false, 2>("SS N64 +fence/8");
+  run<64, false, 4>("SS N64 +wait/8");
+  run<64, false, 7>("SS N64 +all/8");
+  run<64, true, 7>("TS N64 +all/8");
+  return 0;
+}

@@ -1,0 +1,29 @@
+"""Loads the ADATTN_PIPE_STATS build and prints per-role wait fractions of the forward."""
+import ctypes as C, os, sys
+sys.path.insert(0, ".")
+import paper_2604_15180_b200._lib as L
+L.LIB_PATH = os.path.abspath("paper_2604_15180_b200/libadattn_b200_stats.so")
+import torch
+import paper_2604_15180_b200 as pa
+from paper_2604_15180_b200 import workloads
+lib = L.load()
+fn = lib.adattn_b200_pipe_stats
+fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+B, H, N = (int(x) for x in sys.argv[1:4])
+beta = float(sys.argv[4]) if len(sys.argv) > 4 else None
+q, k, v, do = (workloads.gaussian(B, H, N, 128, 1.0, seed=1) if beta is None
+               else workloads.anchored(B, H, N, 128, beta, True, seed=1))
+p = pa.AttentionProblem(q, k, v, alpha=1.5, causal=True)
+r = pa.forward(p); torch.cuda.synchronize()
+buf = (C.c_ulonglong * 8)()
+fn(buf, 1)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); r = pa.forward(p); e1.record(); e1.synchronize()
+fn(buf, 1)
+st = list(buf)
+mma = st[6]
+names = ["mma_wait_full(TMA)", "mma_wait_s_empty(epi)", "mma_wait_p_full", "prod_wait_empty", "epi_w4_wait_s_full"]
+print("fwd ms", e0.elapsed_time(e1), "sparsity", r.stats.block_sparsity, "tiles", st[7])
+for i, n in enumerate(names):
+    print(f"{n:26s} {st[i] / mma:6.3f} of MMA-warp cycles")
+print("MMA cycles per tile", mma / st[7])
