@@ -43,11 +43,11 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint
 // reference tiles, d == dv in {64, 128}, n a multiple of 256, m of 64.
 bool tc_supported(const Geom& g) {
   return g.in_dtype == ADATTN_BF16 && g.block_r == 64 && g.block_c == 64 && g.d == g.dv &&
-         (g.d == 64 || g.d == 128) && g.n % 256 == 0 && g.m % 64 == 0 && g.bins <= 32 &&
+         (g.d == 64 || g.d == 128) && g.n % 256 == 0 && g.m % 128 == 0 && g.bins <= 32 &&
          g.bins >= 2;
 }
 std::string tc_envelope() {
-  return "bf16 inputs, block_r=block_c=64, d=dv in {64,128}, n%256==0, m%64==0, 2<=bins<=32";
+  return "bf16 inputs, block_r=block_c=64, d=dv in {64,128}, n%256==0, m%128==0, 2<=bins<=32";
 }
 size_t tc_forward_workspace(const Geom&) { return 0; }
 size_t tc_backward_workspace(const Geom& g) { return tc::backward_workspace(g); }

@@ -2,28 +2,32 @@
 // sm_100a (reference: /root/reference/proj/src/attention.cpp:157-361).
 //
 // One CTA = 256 query rows (four 64-row reference tiles, two M=128 UMMA row
-// groups RG0/RG1) of one head; keys stream in 64-key tiles (one reference key
-// tile), so every K tile fetched from L2 feeds two M=128 MMAs.
+// groups RG0/RG1) of one head.  Keys stream in 128-key tiles (two reference
+// key tiles): S_g = Q_g K_J^T is an SS MMA with N=128, which is the smallest N
+// that runs at the full tensor rate from shared memory (tools/mma_bench.cu:
+// SMEM operand bandwidth is 128 B/cycle), and every K tile fetched from L2
+// feeds both row groups.
+//
 // Warp roles (640 threads):
 //   warp 0      TMA producer: Q once, then K (and V in the output pass) tiles
-//               into a 4-stage SWIZZLE_128B ring
-//   warp 1      MMA issuer: S_g = Q_g K_j^T (M=128, N=64) into TMEM, double
-//               buffered per row group; O_g += P_g V_j (M=128, N=dv) in the
-//               output pass, with P split into bf16 hi + lo (two MMAs) so the
-//               bf16 rounding of P drops out of O
+//               into a 3-stage SWIZZLE_128B ring
+//   warp 1      MMA issuer (converged warp, one elected lane issues)
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4-19  epilogue: 8 warps per row group, one thread per (row, 32-key
-//               half) -> 4 epilogue warps per SM sub-partition; each row group
-//               has its own S full/empty barriers, so the two groups drift
-//               apart and hide each other's TMEM-load latency.
-//               pass MAX  -> row max
-//               pass HIST -> bin counts of z >= 0 -> solve_histogram -> tau_h
-//               pass REF  -> f, f', f'' partial sums + 64x64 activity bits;
-//                            safeguarded step per row (repeats until no row moves)
-//               pass OUT  -> P = [z - tau]_+^(1/(alpha-1)) over the set mask bits
+//   warps 4-19  epilogue: 8 warps per row group, one thread per (row, 64-key
+//               half of the tile); each row group has its own S barriers so
+//               the two groups drift apart and hide each other's latency.
+// TMEM: threshold passes: S[b][g] at b*256 + g*128 (double buffered);
+//       output pass:      S[g] at g*128, O[g] at 256 + g*128.  P (bf16) is
+//       written back over the thread's own S columns (tcgen05.st) and read as
+//       the TMEM A operand of O_g += P_g V_J (TS MMA, no shared-memory trip).
+// Passes (per CTA, in order):
+//   MAX  -> row max; HIST -> bin counts of z >= 0 -> solve_histogram -> tau_h;
+//   REF  -> f, f', f'' partial sums + 64x64 activity bits, one safeguarded step
+//           per row, repeated until no row moves (the last pass's bits are the
+//           mask); OUT -> P over the set mask bits, O = P V.
 // Per-row refinement state and the step rules run in fp64 exactly as the
-// reference; score-element math is fp32 (z = A1*acc + B, one FFMA), packed
-// f32x2 where it pays.
+// reference; score-element math is fp32 (z = A1*acc + B, one FFMA) with packed
+// f32x2 arithmetic.
 #include <cuda.h>
 #include <math_constants.h>
 
@@ -39,8 +43,8 @@ namespace tc {
 namespace {
 
 constexpr int BM = 256;        // query rows per CTA
-constexpr int BN = 64;         // keys per tile
-constexpr int NST = 4;         // ring stages
+constexpr int BN = 128;        // keys per S tile (two 64-key reference tiles)
+constexpr int NST = 3;         // ring stages
 constexpr int kEpiWarps = 16;
 constexpr int kEpi = kEpiWarps * 32;
 constexpr int kThreads = 128 + kEpi;
@@ -48,18 +52,19 @@ constexpr int DEC_REF = 0, DEC_OUT = 1;
 
 enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 
-// Optional wait-cycle accounting (build with -DADATTN_PIPE_STATS): per CTA,
-// [0] MMA waits on TMA-full, [1] MMA waits on S-empty, [2] MMA waits on P-full,
-// [3] producer waits on ring-empty, [4] epilogue (warp 4 lane 0) waits on S-full,
-// [5] epilogue busy cycles, [6] MMA total cycles, [7] S tiles issued.
 }  // namespace
+// Optional wait-cycle accounting (build with -DADATTN_PIPE_STATS): [0] MMA waits
+// on TMA-full, [1] MMA waits on S-empty, [2] MMA waits on P-full, [3] producer
+// waits on ring-empty, [4] epilogue warp 4 waits on S-full, [6] MMA-warp cycles,
+// [7] ring items.
 #ifdef ADATTN_PIPE_STATS
 __device__ unsigned long long g_pipe_stats[8];
 #endif
 namespace {
 #ifdef ADATTN_PIPE_STATS
 #define PSTAT_T0() const long long _t0 = clock64()
-#define PSTAT_ADD(i) atomicAdd(&g_pipe_stats[i], (unsigned long long)(clock64() - _t0))
+#define PSTAT_ADD(i) \
+  if (leader) atomicAdd(&g_pipe_stats[i], (unsigned long long)(clock64() - _t0))
 #else
 #define PSTAT_T0() \
   do {             \
@@ -80,18 +85,17 @@ struct FwdArgs {
   double* row_max;
   uint32_t* mask;
   int32_t* steps;
-  int dbg;  // ADATTN_PIPE_STATS builds only: 1 = epilogue skips tcgen05.ld, 2 = skips math
 };
 
 template <int D>
 struct FwdSmem {
   static constexpr int QBYTES = BM * D * 2;
   static constexpr int TILE = BN * D * 2;
-  static constexpr int PB = BM * BN * 2;  // one of P_hi / P_lo
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_RING = OFF_Q + QBYTES;
-  static constexpr int OFF_P = OFF_RING + NST * TILE;  // also the HIST/REF combine scratch
-  static constexpr int OFF_BAR = OFF_P + 2 * PB;
+  static constexpr int OFF_CNT = OFF_RING + NST * TILE;   // [256][32] u32 (HIST combine)
+  static constexpr int OFF_PART = OFF_CNT;                // [256][4] f64 (REF combine, reuses)
+  static constexpr int OFF_BAR = OFF_CNT + BM * 32 * 4;
   static constexpr int NBAR = 2 * NST + 16;
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
   static constexpr int OFF_ROW = OFF_MISC + 64;  // [256][4] f32 per-row scratch
@@ -171,6 +175,26 @@ __device__ __forceinline__ void ref_slice(const float* v, float A1, float C, flo
   mxo = fmaxf(mxa, mxb);
 }
 
+// HIST binning of a 32-element slice into packed 8-bit fields (<= 32 per slice).
+__device__ __forceinline__ void hist_slice8(const float* v, float An, float Bn, int nb,
+                                            uint32_t* cnt) {
+  uint32_t lo = 0, hi = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float y = fmaf(An, v[i], Bn);
+    int b = (int)(__float_as_uint(__fadd_rd(fmaxf(y, 0.f), 8388608.f)) & 0x3Fu);
+    b = min(b, nb - 1);
+    const uint32_t inc = (y >= 0.f) ? (1u << ((b & 3) << 3)) : 0u;
+    lo += (b < 4) ? inc : 0u;
+    hi += (b >= 4) ? inc : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    cnt[k] += (lo >> (8 * k)) & 0xFFu;
+    cnt[k + 4] += (hi >> (8 * k)) & 0xFFu;
+  }
+}
+
 template <int D, int AK>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -183,36 +207,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem + L::OFF_Q;
   uint8_t* sRing = smem + L::OFF_RING;
-  uint8_t* sP = smem + L::OFF_P;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* full = bars;               // [NST]
   uint64_t* empty = bars + NST;        // [NST]
   uint64_t* s_full = bars + 2 * NST;   // [2 buffers][2 row groups]
   uint64_t* s_empty = s_full + 4;      // [2][2]
-  uint64_t* p_full = s_empty + 4;
-  uint64_t* p_empty = p_full + 1;
-  uint64_t* o_full = p_empty + 1;
+  uint64_t* p_full = s_empty + 4;      // [2 row groups]
+  uint64_t* o_full = p_full + 2;
   uint64_t* q_full = o_full + 1;
   uint64_t* dec_bar = q_full + 1;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
   volatile uint32_t* s_tmem = misc;  // TMEM base
   volatile uint32_t* s_decision = misc + 1;
-  // Combine scratch of the two key halves of a row.  The count and partial-sum
-  // arrays overlay the P buffers, which stay unused until the output pass.
-  uint32_t* sCnt = reinterpret_cast<uint32_t*>(sP);                // [2][256][32] u32
-  double* sPart = reinterpret_cast<double*>(sP + BM * 32 * 4);     // [256][4] f64 (REF only)
-  float* sRow = reinterpret_cast<float*>(smem + L::OFF_ROW);      // [256][4] f32
+  uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + L::OFF_CNT);
+  double* sPart = reinterpret_cast<double*>(smem + L::OFF_PART);
+  float* sRow = reinterpret_cast<float*>(smem + L::OFF_ROW);
   uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [4][wpr]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bh = blockIdx.x % g.bh;
   const int crow = a.ncta_rows - 1 - blockIdx.x / g.bh;  // heaviest causal tiles first
   const int row0 = crow * BM;
-  const int jmax = g.causal ? (row0 + BM - 1) / BN : g.t_c - 1;
+  const int nkt = g.m / BN;                              // 128-key tiles
+  const int Jmax = g.causal ? (row0 + BM - 1) / BN : nkt - 1;
   const int wpr = g.wpr;
   int rg_jlim[2];
-  rg_jlim[0] = g.causal ? (row0 + 127) / BN : g.t_c - 1;
-  rg_jlim[1] = jmax;
+  rg_jlim[0] = g.causal ? (row0 + 127) / BN : nkt - 1;
+  rg_jlim[1] = Jmax;
 
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
@@ -223,8 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 8);
     }
-    mbar_init(p_full, kEpiWarps);
-    mbar_init(p_empty, 1);
+    mbar_init(&p_full[0], 8);
+    mbar_init(&p_full[1], 8);
     mbar_init(o_full, 1);
     mbar_init(q_full, 1);
     mbar_init(dec_bar, 1);
@@ -241,204 +262,241 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
-  // activity of row group rg for key tile j in the output pass
-  auto out_active = [&](int rg, int j) -> bool {
-    const uint32_t bit = 1u << (j & 31);
-    return ((smask[(2 * rg) * wpr + (j >> 5)] | smask[(2 * rg + 1) * wpr + (j >> 5)]) & bit) != 0;
+  // output-pass activity of row group rg for 128-key tile J (reference blocks
+  // (2rg, 2J), (2rg, 2J+1), (2rg+1, 2J), (2rg+1, 2J+1))
+  auto out_active = [&](int rg, int J) -> bool {
+    const uint32_t bits = 3u << ((2 * J) & 31);
+    const int w = (2 * J) >> 5;
+    return ((smask[(2 * rg) * wpr + w] | smask[(2 * rg + 1) * wpr + w]) & bits) != 0;
   };
-  auto any_active = [&](int j) -> bool { return out_active(0, j) || out_active(1, j); };
-  auto next_active = [&](int j) -> int {  // first active key tile >= j, or -1
-    for (; j <= jmax; ++j)
-      if (any_active(j)) return j;
+  auto next_active = [&](int J) -> int {  // first active key tile >= J, or -1
+    for (; J <= Jmax; ++J)
+      if (out_active(0, J) || out_active(1, J)) return J;
     return -1;
   };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    {
-      const bool leader = elect_one_sync();
-      const int qrow = bh * g.n + row0;
-      if (leader) mbar_expect_tx(q_full, L::QBYTES);
+    const bool leader = elect_one_sync();
+    const int qrow = bh * g.n + row0;
+    if (leader) mbar_expect_tx(q_full, L::QBYTES);
+    for (int c = 0; c < NCH; ++c)
+      if (leader) tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
+    uint32_t r = 0;
+    auto load = [&](const CUtensorMap* tm, int row) {
+      const uint32_t st = r % NST, ph = (r / NST) & 1;
+      {
+        PSTAT_T0();
+        mbar_wait(&empty[st], ph ^ 1);
+        PSTAT_ADD(3);
+      }
+      if (leader) mbar_expect_tx(&full[st], L::TILE);
       for (int c = 0; c < NCH; ++c)
-        if (leader) tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
-      uint32_t r = 0;
-      auto load = [&](const CUtensorMap* tm, int row) {
-        const uint32_t st = r % NST, ph = (r / NST) & 1;
-        {
-          PSTAT_T0();
-          mbar_wait(&empty[st], ph ^ 1);
-          PSTAT_ADD(3);
-        }
-        if (leader) mbar_expect_tx(&full[st], L::TILE);
-        for (int c = 0; c < NCH; ++c)
-          if (leader) tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
-        ++r;
-      };
-      const int krow0 = bh * g.m;
-      for (int pass = 0; pass < 2; ++pass)
-        for (int j = 0; j <= jmax; ++j) load(&tm_k, krow0 + j * BN);
-      for (uint32_t ref = 0;; ++ref) {
-        for (int j = 0; j <= jmax; ++j) load(&tm_k, krow0 + j * BN);
-        mbar_wait(dec_bar, ref & 1);
-        if (*s_decision == DEC_OUT) break;
-      }
-      int prev = -1;
-      for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
-        load(&tm_k, krow0 + j * BN);
-        if (prev >= 0) load(&tm_v, krow0 + prev * BN);
-        prev = j;
-      }
-      if (prev >= 0) load(&tm_v, krow0 + prev * BN);
+        if (leader) tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
+      ++r;
+    };
+    const int krow0 = bh * g.m;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);
+    for (uint32_t ref = 0;; ++ref) {
+      for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);
+      mbar_wait(dec_bar, ref & 1);
+      if (*s_decision == DEC_OUT) break;
     }
+    int prev = -1;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      load(&tm_k, krow0 + J * BN);
+      if (prev >= 0) load(&tm_v, krow0 + prev * BN);
+      prev = J;
+    }
+    if (prev >= 0) load(&tm_v, krow0 + prev * BN);
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    {
-      const bool leader = elect_one_sync();
-      constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, false, false);
-      constexpr uint32_t IDESC_PV = idesc_bf16_f32(128, D, false, true);
-      const uint32_t q_addr = smem_u32(sQ), ring_addr = smem_u32(sRing), p_addr = smem_u32(sP);
-      mbar_wait(q_full, 0);
-      tc_fence_after();
+    const bool leader = elect_one_sync();
+    constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, false, false);
+    constexpr uint32_t IDESC_PV = idesc_bf16_f32(128, D, false, true);
+    const uint32_t q_addr = smem_u32(sQ), ring_addr = smem_u32(sRing);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
 #ifdef ADATTN_PIPE_STATS
-      const long long t_mma0 = clock64();
+    const long long t_mma0 = clock64();
 #endif
-      uint32_t it[2] = {0, 0}, r = 0;
-      auto s_tile = [&](int j, bool out_pass) {
-        const uint32_t st = r % NST;
+    uint32_t uses[4] = {0, 0, 0, 0};  // completed uses of S buffer (b, rg)
+    uint32_t it[2] = {0, 0}, r = 0;
+    auto wait_ring = [&]() -> uint32_t {
+      const uint32_t st = r % NST;
+      PSTAT_T0();
+      mbar_wait(&full[st], (r / NST) & 1);
+      PSTAT_ADD(0);
+      tc_fence_after();
+      return st;
+    };
+    auto issue_s = [&](uint32_t d_t, int rg, uint32_t st) {
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (leader)
+            umma_bf16(d_t, desc_kmajor(q_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
+                      desc_kmajor(ring_addr + st * L::TILE + c * BN * 128 + k * 32), IDESC_S,
+                      (c | k) != 0);
+    };
+    // threshold passes: S double buffered per row group
+    auto s_tile = [&](int J) {
+      const uint32_t st = wait_ring();
+      for (int rg = 0; rg < 2; ++rg) {
+        if (J > rg_jlim[rg]) continue;
+        const uint32_t b = it[rg] & 1;
         {
           PSTAT_T0();
-          mbar_wait(&full[st], (r / NST) & 1);
-          PSTAT_ADD(0);
+          mbar_wait(&s_empty[b * 2 + rg], (uses[b * 2 + rg] & 1) ^ 1);
+          PSTAT_ADD(1);
         }
         tc_fence_after();
-        for (int rg = 0; rg < 2; ++rg) {
-          const bool need = out_pass ? out_active(rg, j) : (j <= rg_jlim[rg]);
-          if (!need) continue;
-          const uint32_t b = it[rg] & 1;
-          {
-            PSTAT_T0();
-            mbar_wait(&s_empty[b * 2 + rg], ((it[rg] >> 1) & 1) ^ 1);
-            PSTAT_ADD(1);
-          }
-          tc_fence_after();
-          const uint32_t d_t = tmem + b * 128 + rg * 64;
-          for (int c = 0; c < NCH; ++c)
+        issue_s(tmem + b * 256 + rg * 128, rg, st);
+        if (leader) umma_commit(&s_full[b * 2 + rg]);
+        ++uses[b * 2 + rg];
+        ++it[rg];
+      }
+      if (leader) umma_commit(&empty[st]);
+      ++r;
+    };
+    for (int pass = 0; pass < 2; ++pass)
+      for (int J = 0; J <= Jmax; ++J) s_tile(J);
+    for (uint32_t ref = 0;; ++ref) {
+      for (int J = 0; J <= Jmax; ++J) s_tile(J);
+      mbar_wait(dec_bar, ref & 1);
+      if (*s_decision == DEC_OUT) break;
+    }
+    // output pass: S[g] at g*128 (buffer 0 of each group), O[g] at 256 + g*128.
+    // Per active tile J, per group g: PV_g(prev) then S_g(J) -- in tensor-pipe
+    // order, so S_g(J) overwrites P_g(prev) only after PV_g(prev) has read it,
+    // and one group's P computation overlaps the other group's MMAs.
+    bool o_init[2] = {false, false};
+    uint32_t pcnt[2] = {0, 0};
+    auto pv = [&](int rg, uint32_t vst) {
+      {
+        PSTAT_T0();
+        mbar_wait(&p_full[rg], pcnt[rg] & 1);
+        PSTAT_ADD(2);
+      }
+      ++pcnt[rg];
+      tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (leader) umma_bf16(d_t, desc_kmajor(q_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
-                        desc_kmajor(ring_addr + st * L::TILE + c * BN * 128 + k * 32), IDESC_S,
-                        (c | k) != 0);
-          if (leader) umma_commit(&s_full[b * 2 + rg]);
-          ++it[rg];
-        }
-        if (leader) umma_commit(&empty[st]);
-        ++r;
-      };
-      bool o_init[2] = {false, false};
-      uint32_t pi = 0;
-      auto pv_tile = [&](int j) {
-        const uint32_t st = r % NST;
-        mbar_wait(&full[st], (r / NST) & 1);
-        {
-          PSTAT_T0();
-          mbar_wait(p_full, pi & 1);
-          PSTAT_ADD(2);
-        }
+      for (int k = 0; k < 8; ++k) {
+        // keys 16k..16k+15: packed P pairs at TMEM cols rg*128 + 64*(k>>2) + 8*(k&3)
+        const uint32_t acol = rg * 128 + 64 * (k >> 2) + 8 * (k & 3);
+        if (leader)
+          umma_bf16_ts(tmem + 256 + rg * D, tmem + acol,
+                       desc_mnmajor(ring_addr + vst * L::TILE + k * 16 * 128, BN * 128), IDESC_PV,
+                       (o_init[rg] || k > 0) ? 1u : 0u);
+      }
+      o_init[rg] = true;
+    };
+    int prev = -1;
+    bool prev_act[2] = {false, false};
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      const uint32_t kst = wait_ring();  // K(J) is ring item r
+      uint32_t vst = 0;
+      if (prev >= 0) {
+        vst = (r + 1) % NST;  // V(prev) follows K(J) in the producer's order
+        PSTAT_T0();
+        mbar_wait(&full[vst], ((r + 1) / NST) & 1);
+        PSTAT_ADD(0);
         tc_fence_after();
-        for (int rg = 0; rg < 2; ++rg) {
-          if (!out_active(rg, j)) continue;
-          const uint32_t d_t = tmem + 256 + rg * D;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t bd = desc_mnmajor(ring_addr + st * L::TILE + k * 16 * 128, BN * 128);
-            if (leader) umma_bf16(d_t, desc_kmajor(p_addr + rg * 128 * 128 + k * 32), bd, IDESC_PV,
-                      (o_init[rg] || k > 0) ? 1u : 0u);
-            if (leader) umma_bf16(d_t, desc_kmajor(p_addr + L::PB + rg * 128 * 128 + k * 32), bd, IDESC_PV,
-                      1u);
-          }
-          o_init[rg] = true;
+      }
+      bool act[2];
+      for (int rg = 0; rg < 2; ++rg) {
+        if (prev >= 0 && prev_act[rg]) pv(rg, vst);
+        act[rg] = out_active(rg, J);
+        if (act[rg]) {
+          issue_s(tmem + rg * 128, rg, kst);
+          if (leader) umma_commit(&s_full[rg]);
+          ++uses[rg];
         }
-        if (leader) umma_commit(&empty[st]);
-        if (leader) umma_commit(p_empty);
+      }
+      if (leader) umma_commit(&empty[kst]);
+      ++r;
+      if (prev >= 0) {
+        if (leader) umma_commit(&empty[vst]);
         ++r;
-        ++pi;
-      };
-      for (int pass = 0; pass < 2; ++pass)
-        for (int j = 0; j <= jmax; ++j) s_tile(j, false);
-      for (uint32_t ref = 0;; ++ref) {
-        for (int j = 0; j <= jmax; ++j) s_tile(j, false);
-        mbar_wait(dec_bar, ref & 1);
-        if (*s_decision == DEC_OUT) break;
       }
-      int prev = -1;
-      for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
-        s_tile(j, true);
-        if (prev >= 0) pv_tile(prev);
-        prev = j;
-      }
-      if (prev >= 0) pv_tile(prev);
-      if (leader) umma_commit(o_full);
+      prev = J;
+      prev_act[0] = act[0];
+      prev_act[1] = act[1];
+    }
+    if (prev >= 0) {
+      const uint32_t vst = wait_ring();
+      for (int rg = 0; rg < 2; ++rg)
+        if (prev_act[rg]) pv(rg, vst);
+      if (leader) umma_commit(&empty[vst]);
+      ++r;
+    }
+    if (leader) umma_commit(o_full);
 #ifdef ADATTN_PIPE_STATS
+    if (leader) {
       atomicAdd(&g_pipe_stats[6], (unsigned long long)(clock64() - t_mma0));
       atomicAdd(&g_pipe_stats[7], (unsigned long long)r);
-#endif
     }
+#endif
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;          // 0..15
     const int rg = ew >> 3;           // row group
-    const int half = (ew >> 2) & 1;   // key columns 32*half .. +31 of each tile
+    const int half = (ew >> 2) & 1;   // keys 64*half .. +63 of each 128-key tile
     const int lq = warp & 3;          // TMEM lane quarter
     const int e = rg * 128 + lq * 32 + lane;  // local query row 0..255
     const int grow = row0 + e;        // query row within the head
     const int rb = e >> 6;            // 64-row reference tile within the CTA
-    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + rg * 64 + half * 32;
+    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + rg * 128 + half * 64;
     const int jl = rg_jlim[rg];
     const int bar_rg = 1 + rg;        // named barrier of this row group (256 threads)
     const float A1 = a.A1;
-    uint32_t item = 0;
+    uint32_t cnt_b[2] = {0, 0};       // completed uses of S buffer b by this group
+    uint32_t it = 0;
 
-    // S slice (32 keys) of key tile j into v[32]; release the TMEM buffer.
     float v[32];
-    auto fetch = [&](int j) {
-      const uint32_t b = item & 1;
-#ifdef ADATTN_PIPE_STATS
-      const long long _tw = clock64();
-#endif
-      mbar_wait(&s_full[b * 2 + rg], (item >> 1) & 1);
-#ifdef ADATTN_PIPE_STATS
-      if (warp == 4 && lane == 0) atomicAdd(&g_pipe_stats[4], (unsigned long long)(clock64() - _tw));
-#endif
-      tc_fence_after();
-#ifdef ADATTN_PIPE_STATS
-      if (a.dbg & 1) {
+    // 32-key chunk c (0/1) of this thread's 64 keys of tile J, from buffer column base
+    auto load_chunk = [&](uint32_t col, int J, int c) {
+      tmem_ld32(tl + col + c * 32, v);
+      tmem_wait_ld();
+      const int k0 = J * BN + half * 64 + c * 32;
+      if (g.causal && k0 + 31 > grow) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = (float)(i - 40);
-      } else
-#endif
-      {
-        tmem_ld32(tl + b * 128, v);
-        tmem_wait_ld();
+        for (int i = 0; i < 32; ++i)
+          if (k0 + i > grow) v[i] = -CUDART_INF_F;
       }
+    };
+    // threshold-pass tile: wait, run body(c) on chunks 0 and 1, release the buffer
+    auto tau_tile = [&](int J, auto&& body) {
+      const uint32_t b = it & 1;
+      {
+#ifdef ADATTN_PIPE_STATS
+        const long long _tw = clock64();
+#endif
+        mbar_wait(&s_full[b * 2 + rg], cnt_b[b] & 1);
+#ifdef ADATTN_PIPE_STATS
+        if (warp == 4 && lane == 0) atomicAdd(&g_pipe_stats[4], (unsigned long long)(clock64() - _tw));
+#endif
+      }
+      ++cnt_b[b];
+      ++it;
+      tc_fence_after();
+      load_chunk(b * 256, J, 0);
+      body(0);
+      load_chunk(b * 256, J, 1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[b * 2 + rg]);
-      ++item;
-      const int c0 = j * BN + half * 32;
-      if (g.causal && c0 + 31 > grow) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i > grow) v[i] = -CUDART_INF_F;
-      }
+      body(1);
     };
 
     // ---- pass MAX (attention.cpp:182-195): max of raw dot products, scaled once
     float mraw = -CUDART_INF_F;
-    for (int j = 0; j <= jl; ++j) {
-      fetch(j);
+    for (int J = 0; J <= jl; ++J)
+      tau_tile(J, [&](int) {
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) mraw = fmaxf(mraw, fmaxf(v[i], v[i + 1]));
-    }
+        for (int i = 0; i < 32; i += 2) mraw = fmaxf(mraw, fmaxf(v[i], v[i + 1]));
+      });
     sRow[e * 4 + half] = mraw;
     bar_sync(bar_rg, 256);
     mraw = fmaxf(sRow[e * 4], sRow[e * 4 + 1]);
@@ -448,43 +506,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // ---- pass HIST (attention.cpp:201-232): counts of min(floor(B z), B-1), z >= 0
     const int nb = g.bins;
-    uint32_t cnt[8];  // bins <= 8 in registers; larger bin counts go to shared memory
+    uint32_t cnt[8];  // bins <= 8 in registers; more bins count into shared memory
 #pragma unroll
     for (int k = 0; k < 8; ++k) cnt[k] = 0;
-    uint32_t* my_cnt = sCnt + (half * BM + e) * 32;  // [2][256][32] over the P buffers
-    if (nb > 8)
-      for (int k = 0; k < nb; ++k) my_cnt[k] = 0;
+    uint32_t* row_cnt = sCnt + e * 32;
+    if (nb > 8 && half == 0)
+      for (int k = 0; k < nb; ++k) row_cnt[k] = 0;
+    if (nb > 8) bar_sync(bar_rg, 256);
     {
       const float An = A1 * (float)nb, Bn = Bf * (float)nb;  // exact: nb is a power of 2
-      for (int j = 0; j <= jl; ++j) {
-        fetch(j);
-        if (nb <= 8) {
-          uint32_t lo = 0, hi = 0;  // 8-bit fields, <= 32 per tile
+      for (int J = 0; J <= jl; ++J)
+        tau_tile(J, [&](int) {
+          if (nb <= 8) {
+            hist_slice8(v, An, Bn, nb, cnt);
+          } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float y = fmaf(An, v[i], Bn);
-            int b = (int)(__float_as_uint(__fadd_rd(fmaxf(y, 0.f), 8388608.f)) & 0x3Fu);
-            b = min(b, nb - 1);
-            const uint32_t inc = (y >= 0.f) ? (1u << ((b & 3) << 3)) : 0u;
-            lo += (b < 4) ? inc : 0u;
-            hi += (b >= 4) ? inc : 0u;
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            cnt[k] += (lo >> (8 * k)) & 0xFFu;
-            cnt[k + 4] += (hi >> (8 * k)) & 0xFFu;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float y = fmaf(An, v[i], Bn);
-            if (y >= 0.f) {
-              int b = (int)(__float_as_uint(__fadd_rd(y, 8388608.f)) & 0x3Fu);
-              my_cnt[min(b, nb - 1)] += 1;
+            for (int i = 0; i < 32; ++i) {
+              const float y = fmaf(An, v[i], Bn);
+              if (y >= 0.f) {
+                const int b = (int)(__float_as_uint(__fadd_rd(y, 8388608.f)) & 0x3Fu);
+                atomicAdd(&row_cnt[min(b, nb - 1)], 1u);
+              }
             }
           }
-        }
-      }
+        });
     }
     // combine the two key halves; the half-0 thread owns the row's solver state
     RowSolve rs;
@@ -494,15 +539,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     rs.done = true;
     if (half == 1 && nb <= 8) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) my_cnt[k] = cnt[k];
+      for (int k = 0; k < 8; ++k) row_cnt[k] = cnt[k];
     }
     bar_sync(bar_rg, 256);
     if (half == 0) {
       uint32_t c32[32];
-      const uint32_t* other = sCnt + (BM + e) * 32;
 #pragma unroll
       for (int k = 0; k < 32; ++k)
-        c32[k] = k < nb ? (nb <= 8 ? cnt[k & 7] : my_cnt[k]) + other[k] : 0u;
+        c32[k] = k < nb ? (nb <= 8 ? cnt[k & 7] + row_cnt[k] : row_cnt[k]) : 0u;
       double th, lo, hi;
       solve_histogram_dev(c32, nb, g.alpha, th, lo, hi);
       rs.tau = th;
@@ -524,28 +568,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool first_pass = true;
     for (uint32_t ref = 0;; ++ref) {
       for (int i = tid - 128; i < 4 * wpr; i += kEpi) smask[i] = 0u;
-      bar_sync(3, kEpi);  // C/Chi published, masks cleared, sCnt consumed
+      bar_sync(3, kEpi);  // C/Chi published, masks cleared, counts consumed
       const float C = sRow[e * 4 + 2];
       const float Chi = sRow[e * 4 + 3];
       double f = 0.0, f1 = 0.0, f2 = 0.0, fhi = 0.0;
-      for (int j = 0; j <= jl; ++j) {
-        fetch(j);
-        float s0, s1, s2, mx;
-        ref_slice<AK>(v, A1, C, a.e0f, a.e1f, a.e2f, s0, s1, s2, mx);
-        if (first_pass && need_sec) {
-          float shi = 0.f;
+      for (int J = 0; J <= jl; ++J) {
+        float mx_t = -CUDART_INF_F;
+        tau_tile(J, [&](int) {
+          float s0, s1, s2, mx;
+          ref_slice<AK>(v, A1, C, a.e0f, a.e1f, a.e2f, s0, s1, s2, mx);
+          if (first_pass && need_sec) {
+            float shi = 0.f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float th = fmaf(A1, v[i], Chi);
-            if (th > 0.f) shi += exp2f(a.e0f * __log2f(th));
+            for (int i = 0; i < 32; ++i) {
+              const float th = fmaf(A1, v[i], Chi);
+              if (th > 0.f) shi += exp2f(a.e0f * __log2f(th));
+            }
+            fhi += (double)shi;
           }
-          fhi += (double)shi;
-        }
-        f += (double)s0;
-        f1 += (double)s1;
-        f2 += (double)s2;
-        if (__any_sync(0xffffffffu, mx > -1e-9f) && lane == 0)
-          atomicOr(&smask[rb * wpr + (j >> 5)], 1u << (j & 31));
+          f += (double)s0;
+          f1 += (double)s1;
+          f2 += (double)s2;
+          mx_t = fmaxf(mx_t, mx);
+        });
+        const int jt = 2 * J + half;  // reference key tile of this thread's half
+        if (__any_sync(0xffffffffu, mx_t > -1e-9f) && lane == 0)
+          atomicOr(&smask[rb * wpr + (jt >> 5)], 1u << (jt & 31));
       }
       if (half == 1) {
         sPart[e * 4 + 0] = f;
@@ -572,39 +620,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!any) break;
     }
 
-    // ---- pass OUT (attention.cpp:334-352): P over the active 64x64 blocks
+    // ---- pass OUT (attention.cpp:334-352): P over the active blocks, O = P V
     {
       const float C = sRow[e * 4 + 2];
       const float2 A2 = make_float2(A1, A1), C2 = make_float2(C, C);
-      uint32_t pi = 0;
-      const uint32_t p_row = smem_u32(sP) + (uint32_t)e * 128u;
       bool any_out = false;
-      for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
-        const bool need = out_active(rg, j);
-        uint32_t ph[16], pl[16];
-        if (need) {
-          any_out = true;
-          fetch(j);
+      for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+        if (!out_active(rg, J)) continue;
+        any_out = true;
+        mbar_wait(&s_full[rg], cnt_b[0] & 1);  // output-pass S lives in buffer 0
+        ++cnt_b[0];
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          load_chunk(0, J, c);
+          uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float2 t = __ffma2_rn(A2, make_float2(v[2 * i], v[2 * i + 1]), C2);
-            split_bf16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f), ph[i], pl[i]);
+            pk[i] = pack_bf16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f));
           }
+          // packed P of keys 64*half + 32c .. +31 -> TMEM cols 64*half + 16c .. +15
+          tmem_st16(tl + c * 16, pk);
         }
-        mbar_wait(p_empty, (pi & 1) ^ 1);
-        if (need) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t off = (((uint32_t)(half * 4 + q)) ^ (uint32_t)(e & 7)) << 4;
-            st_shared_v4(p_row + off, ph[4 * q], ph[4 * q + 1], ph[4 * q + 2], ph[4 * q + 3]);
-            st_shared_v4(p_row + L::PB + off, pl[4 * q], pl[4 * q + 1], pl[4 * q + 2],
-                         pl[4 * q + 3]);
-          }
-        }
-        fence_proxy_async_smem();
+        tmem_wait_st();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
-        ++pi;
+        if (lane == 0) mbar_arrive(&p_full[rg]);
       }
       // write O (fp32 or fp64): this thread's half of the row's dv columns
       const size_t orow = (size_t)bh * g.n + grow;
@@ -705,10 +747,6 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.row_max = row_max;
   a.mask = mask;
   a.steps = steps;
-  a.dbg = 0;
-#ifdef ADATTN_PIPE_STATS
-  if (const char* dv = getenv("ADATTN_DBG")) a.dbg = atoi(dv);
-#endif
   const int ak = alpha_kind(g.alpha);
   if (g.d == 64) return launch_fwd_d<64>(g, ak, tq, tk, tv, a, st);
   return launch_fwd_d<128>(g, ak, tq, tk, tv, a, st);
