@@ -158,7 +158,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2604_15180_b200 as pa
-    from paper_2604_15180_b200 import _lib, workloads
+    from paper_2604_15180_b200 import _lib, parallel, workloads
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -204,11 +204,7 @@ def main():
         if profile:
             _lib.profile_enable(False)
             kt = _lib.profile_read()
-        ms = e0.elapsed_time(e1) / steps
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = t.item()
+        ms = parallel.max_over_ranks(e0.elapsed_time(e1) / steps, device=dev)
         return ms, res, launches, kt
 
     clk = ClockSampler(local)
@@ -216,6 +212,17 @@ def main():
     ms, res, launches, ktimes = timed(prob, do, args.warmup, args.steps, profile=True)
     clocks = clk.stop()
 
+    # one validation gather over NVLink, outside the timed region: per-rank checksums
+    chk = torch.stack([res.tau.double().sum(), res.out.double().abs().sum(),
+                       torch.tensor(float(torch.isfinite(res.out).all()), device=dev,
+                                    dtype=torch.float64)])
+    gathered = parallel.gather_to_rank0(chk.unsqueeze(0))
+    validation = None
+    if rank == 0:
+        gathered = gathered.cpu()
+        validation = {"ranks": int(gathered.shape[0]),
+                      "all_finite": bool((gathered[:, 2] == 1).all()),
+                      "tau_sums": [round(float(x), 3) for x in gathered[:, 0]]}
     st = res.stats
     T = N // 64
     A_head = T * (T + 1) // 2 if causal else T * T
@@ -286,11 +293,8 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             e2e_call()
-        e_ms = 1000.0 * (time.perf_counter() - t0) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = t.item()
+        e_ms = parallel.max_over_ranks(1000.0 * (time.perf_counter() - t0) / args.e2e_steps,
+                                       device=dev)
         h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv, hdo))
         d2h = sum(x.numel() * x.element_size() for x in (hout, hdq, hdk, hdv, htau, hrm, hdl, hmask))
         e2e = {"value": fl["f_eff"] / (e_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": e_ms,
@@ -341,6 +345,7 @@ def main():
             "tau_iters_avg": tau_iters, "tflops_alg": tflops_alg,
             "gpu_launches": int(launches), "kernels": kern, "roofline": roofline,
             "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu, "sweep": sweep,
+            "validation_gather": validation,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
