@@ -75,45 +75,135 @@ __device__ __forceinline__ void pu_of(float t, float e0f, float e1f, float& p, f
   }
 }
 
-// Shared geometry of the query-major kernels.
-struct QmGeom {
-  int bh, row0, jmax;
-  int rg_jlim[2];
-};
+// dS = u (dp - delta) of one 32-key chunk, split into bf16 hi + lo pairs.
+// MASKED: keys i > lim (causal diagonal) are outside the row's support.
+template <int AK, bool MASKED>
+__device__ __forceinline__ void ds_chunk(const float* s, const float* dp, float A1, float C,
+                                         float dl, float e0f, float e1f, int lim, uint32_t* hi,
+                                         uint32_t* lo) {
+  const float2 A2 = make_float2(A1, A1), C2 = make_float2(C, C), D2 = make_float2(-dl, -dl);
+#pragma unroll
+  for (int x = 0; x < 16; ++x) {
+    float2 t = __ffma2_rn(A2, make_float2(s[2 * x], s[2 * x + 1]), C2);
+    if (MASKED) {
+      if (2 * x > lim) t.x = -1.f;
+      if (2 * x + 1 > lim) t.y = -1.f;
+    }
+    float2 u;
+    if constexpr (AK == AK15) {
+      u = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
+    } else {
+      float p;
+      pu_of<AK>(t.x, e0f, e1f, p, u.x);
+      pu_of<AK>(t.y, e0f, e1f, p, u.y);
+    }
+    const float2 d = __fadd2_rn(make_float2(dp[2 * x], dp[2 * x + 1]), D2);
+    const float2 ds = __fmul2_rn(u, d);
+    split_bf16x2(ds.x, ds.y, hi[x], lo[x]);
+  }
+}
 
-__device__ __forceinline__ QmGeom qm_geom(const Geom& g, int ncta_rows) {
-  QmGeom q;
-  q.bh = blockIdx.x % g.bh;
-  const int crow = ncta_rows - 1 - blockIdx.x / g.bh;
-  q.row0 = crow * BM;
-  q.jmax = g.causal ? (q.row0 + BM - 1) / BN : g.t_c - 1;
-  q.rg_jlim[0] = g.causal ? (q.row0 + 127) / BN : g.t_c - 1;
-  q.rg_jlim[1] = q.jmax;
-  return q;
+// sum u dp and sum u of one 32-key chunk (delta numerator / denominator).
+template <int AK, bool MASKED>
+__device__ __forceinline__ void delta_chunk(const float* s, const float* dp, float A1, float C,
+                                            float e0f, float e1f, int lim, float& n_out,
+                                            float& d_out) {
+  const float2 A2 = make_float2(A1, A1), C2 = make_float2(C, C);
+  float2 n2a = make_float2(0.f, 0.f), d2a = n2a, n2b = n2a, d2b = n2a;
+#pragma unroll
+  for (int x = 0; x < 16; ++x) {
+    float2 t = __ffma2_rn(A2, make_float2(s[2 * x], s[2 * x + 1]), C2);
+    if (MASKED) {
+      if (2 * x > lim) t.x = -1.f;
+      if (2 * x + 1 > lim) t.y = -1.f;
+    }
+    float2 u;
+    if constexpr (AK == AK15) {
+      u = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
+    } else {
+      float p;
+      pu_of<AK>(t.x, e0f, e1f, p, u.x);
+      pu_of<AK>(t.y, e0f, e1f, p, u.y);
+    }
+    const float2 d = make_float2(dp[2 * x], dp[2 * x + 1]);
+    if (x & 1) {
+      n2b = __ffma2_rn(u, d, n2b);
+      d2b = __fadd2_rn(d2b, u);
+    } else {
+      n2a = __ffma2_rn(u, d, n2a);
+      d2a = __fadd2_rn(d2a, u);
+    }
+  }
+  n_out = (n2a.x + n2a.y) + (n2b.x + n2b.y);
+  d_out = (d2a.x + d2a.y) + (d2b.x + d2b.y);
+}
+
+// Key-major (dK/dV) chunk: 32 queries of one key.  P^T = t^e0 and
+// dS^T = u (dp - delta_q), both split into bf16 hi + lo pairs.  rc[q] =
+// (C_q, delta_q) from shared memory.  MASKED: queries q < lim (above the causal
+// diagonal for this key) are outside the support.
+template <int AK, bool MASKED>
+__device__ __forceinline__ void pds_chunk(const float* s, const float* dp, const float2* rc,
+                                          float A1, float e0f, float e1f, int lim, uint32_t* ph,
+                                          uint32_t* pl, uint32_t* dh, uint32_t* dl) {
+  const float2 A2 = make_float2(A1, A1);
+#pragma unroll
+  for (int x = 0; x < 16; ++x) {
+    const float4 c = reinterpret_cast<const float4*>(rc)[x];  // (C, delta) of queries 2x, 2x+1
+    float2 t = __ffma2_rn(A2, make_float2(s[2 * x], s[2 * x + 1]), make_float2(c.x, c.z));
+    if (MASKED) {
+      if (2 * x < lim) t.x = -1.f;
+      if (2 * x + 1 < lim) t.y = -1.f;
+    }
+    float2 p, u;
+    if constexpr (AK == AK15) {
+      u = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
+      p = __fmul2_rn(u, u);
+    } else {
+      pu_of<AK>(t.x, e0f, e1f, p.x, u.x);
+      pu_of<AK>(t.y, e0f, e1f, p.y, u.y);
+    }
+    const float2 d = __fadd2_rn(make_float2(dp[2 * x], dp[2 * x + 1]), make_float2(-c.y, -c.w));
+    const float2 ds = __fmul2_rn(u, d);
+    split_bf16x2(p.x, p.y, ph[x], pl[x]);
+    split_bf16x2(ds.x, ds.y, dh[x], dl[x]);
+  }
 }
 
 // ================================================================== delta
-// Query-major delta kernel: 256 rows per CTA (two M=128 row groups), S and dP
-// double-buffered in TMEM (4 x 128 columns).
+// Query-major delta kernel: 256 rows per CTA (two M=128 row groups), keys in
+// 128-key tiles so S = Q K^T and dP = dO V^T are SS MMAs with N=128 (full
+// tensor rate from shared memory).  TMEM: row group g owns S_g (cols 256g ..)
+// and dP_g (cols 256g + 128 ..), single-buffered; the two groups ping-pong so
+// one group's epilogue overlaps the other group's MMAs.  Each 64-key half of a
+// tile is one reference block: only set mask blocks contribute (the
+// reference's for_each_set, attention.cpp:420-444).
+constexpr int DBN = 128;  // keys per tile (delta, dQ)
+
 template <int D>
 struct DeltaSmem {
   static constexpr int QB = BM * D * 2;
-  static constexpr int TILE = BN * D * 2;
+  static constexpr int TILE = DBN * D * 2;
+  static constexpr int NST = D == 128 ? 3 : 6;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_DO = OFF_Q + QB;
   static constexpr int OFF_RING = OFF_DO + QB;
   static constexpr int OFF_BAR = OFF_RING + NST * TILE;
   static constexpr int OFF_MISC = OFF_BAR + 32 * 8;
+  static constexpr int OFF_RED = OFF_RING;  // [256] x 2 f64 half-1 partials (ring drained)
   static constexpr int OFF_MASK = OFF_MISC + 64;
   static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
 };
 
+constexpr int kDeltaThreads = 128 + 512;
+
 template <int D, int AK>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kDeltaThreads, 1)
     tc_delta_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
                     const BwdArgs a) {
   using L = DeltaSmem<D>;
+  constexpr int NST = L::NST;
   constexpr int NCH = D / 64;
   const Geom& g = a.g;
   extern __shared__ uint8_t smem_raw[];
@@ -125,219 +215,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* full = bars;              // [NST]
   uint64_t* empty = bars + NST;       // [NST]
-  uint64_t* s_full = bars + 2 * NST;  // [2]
-  uint64_t* s_empty = s_full + 2;     // [2]
-  uint64_t* q_full = s_empty + 2;
+  uint64_t* s_full = bars + 2 * NST;  // [2 row groups]
+  uint64_t* s_free = s_full + 2;      // [2]
+  uint64_t* q_full = s_free + 2;
   volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
+  double* sRed = reinterpret_cast<double*>(smem + L::OFF_RED);
   uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const QmGeom G = qm_geom(g, a.ncta_rows);
   const int wpr = g.wpr;
-
-  for (int i = tid; i < 4 * wpr; i += kThreads) {
-    const int rbi = i / wpr, w = i - rbi * wpr;
-    smask[i] = a.mask[((size_t)G.bh * g.t_r + (G.row0 / 64 + rbi)) * wpr + w];
-  }
-  if (tid == 0) {
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);
-    }
-    mbar_init(q_full, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *s_tmem;
-
-  auto rb_active = [&](int rb, int j) -> bool {
-    return (smask[rb * wpr + (j >> 5)] >> (j & 31)) & 1u;
-  };
-  auto rg_active = [&](int rg, int j) -> bool { return rb_active(2 * rg, j) || rb_active(2 * rg + 1, j); };
-  auto next_active = [&](int j) -> int {
-    for (; j <= G.jmax; ++j)
-      if (rg_active(0, j) || rg_active(1, j)) return j;
-    return -1;
-  };
-
-  if (warp == 0) {
-    {
-      const bool leader = elect_one_sync();
-      const int qrow = G.bh * g.n + G.row0;
-      if (leader) mbar_expect_tx(q_full, 2 * L::QB);
-      for (int c = 0; c < NCH; ++c) {
-        if (leader) tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
-        if (leader) tma_load_2d(sDO + c * BM * 128, &tm_do, q_full, c * 64, qrow);
-      }
-      uint32_t r = 0;
-      auto load = [&](const CUtensorMap* tm, int row) {
-        const uint32_t st = r % NST, ph = (r / NST) & 1;
-        mbar_wait(&empty[st], ph ^ 1);
-        if (leader) mbar_expect_tx(&full[st], L::TILE);
-        for (int c = 0; c < NCH; ++c)
-          if (leader) tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
-        ++r;
-      };
-      const int krow0 = G.bh * g.m;
-      for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
-        load(&tm_k, krow0 + j * BN);
-        load(&tm_v, krow0 + j * BN);
-      }
-    }
-  } else if (warp == 1) {
-    {
-      const bool leader = elect_one_sync();
-      constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, false, false);
-      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ring_addr = smem_u32(sRing);
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      uint32_t item = 0, r = 0;
-      for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
-        const uint32_t b = item & 1;
-        mbar_wait(&s_empty[b], ((item >> 1) & 1) ^ 1);
-        const uint32_t kst = r % NST, vst = (r + 1) % NST;
-        mbar_wait(&full[kst], (r / NST) & 1);
-        mbar_wait(&full[vst], ((r + 1) / NST) & 1);
-        tc_fence_after();
-        for (int rg = 0; rg < 2; ++rg) {
-          if (!rg_active(rg, j)) continue;
-          const uint32_t sc = tmem + b * 256 + rg * 64;
-          for (int c = 0; c < NCH; ++c)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (leader) umma_bf16(sc, desc_kmajor(q_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
-                        desc_kmajor(ring_addr + kst * L::TILE + c * BN * 128 + k * 32), IDESC_S,
-                        (c | k) != 0);
-              if (leader) umma_bf16(sc + 128, desc_kmajor(do_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
-                        desc_kmajor(ring_addr + vst * L::TILE + c * BN * 128 + k * 32), IDESC_S,
-                        (c | k) != 0);
-            }
-        }
-        if (leader) umma_commit(&empty[kst]);
-        if (leader) umma_commit(&empty[vst]);
-        if (leader) umma_commit(&s_full[b]);
-        ++item;
-        r += 2;
-      }
-    }
-  } else if (warp >= 4) {
-    const int e = tid - 128;
-    const int rg = e >> 7, lq = warp & 3, rb = e >> 6;
-    const int grow = G.row0 + e;
-    const size_t orow = (size_t)G.bh * g.n + grow;
-    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16);
-    const float A1 = a.A1;
-    const double B = 1.0 - (g.alpha - 1.0) * a.row_max[orow];
-    const float C = (float)(B - a.tau[orow]);
-    double num = 0.0, den = 0.0;
-    uint32_t item = 0;
-    for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
-      const bool need = rg_active(rg, j);
-      const bool mine = rb_active(rb, j);  // the reference visits set blocks only
-      const uint32_t b = item & 1;
-      mbar_wait(&s_full[b], (item >> 1) & 1);
-      tc_fence_after();
-      float s[64], dp[64];
-      if (need) {
-        tmem_ld32(tl + b * 256 + rg * 64, s);
-        tmem_ld32(tl + b * 256 + rg * 64 + 32, s + 32);
-        tmem_ld32(tl + b * 256 + 128 + rg * 64, dp);
-        tmem_ld32(tl + b * 256 + 128 + rg * 64 + 32, dp + 32);
-        tmem_wait_ld();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[b]);
-      if (need && mine) {
-        const bool diag = g.causal && j * BN + BN - 1 > grow;
-        float n32 = 0.f, d32 = 0.f;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          float t = fmaf(A1, s[i], C);
-          if (diag && j * BN + i > grow) t = -1.f;
-          float p, u;
-          pu_of<AK>(t, a.e0f, a.e1f, p, u);
-          n32 = fmaf(u, dp[i], n32);
-          d32 += u;
-        }
-        num += (double)n32;
-        den += (double)d32;
-      }
-      ++item;
-    }
-    const double dlt = den > 0.0 ? num / den : 0.0;
-    a.delta[orow] = dlt;
-    a.rowc[orow] = make_float2(C, (float)dlt);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) tmem_dealloc(tmem, 512);
-}
-
-// ===================================================================== dQ
-// Query-major dQ kernel: 128 rows per CTA (one M=128 row group); the 8
-// epilogue warps split each 64-key tile into two 32-column halves.
-// dS = u (dp - delta) is split into bf16 hi + lo and both halves feed the
-// dQ += dS K_j MMA (K_j read MN-major), so the bf16 rounding of dS drops out.
-constexpr int QB_DQ = 128;
-
-template <int D>
-struct DqSmem {
-  static constexpr int QB = QB_DQ * D * 2;
-  static constexpr int TILE = BN * D * 2;
-  static constexpr int DSB = QB_DQ * BN * 2;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_DO = OFF_Q + QB;
-  static constexpr int OFF_RING = OFF_DO + QB;
-  static constexpr int OFF_DS = OFF_RING + NST * TILE;  // hi, lo
-  static constexpr int OFF_BAR = OFF_DS + 2 * DSB;
-  static constexpr int OFF_MISC = OFF_BAR + 32 * 8;
-  static constexpr int OFF_MASK = OFF_MISC + 64;
-  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 2 * wpr * 4 + 64; }
-};
-
-template <int D, int AK>
-__global__ void __launch_bounds__(kThreads, 1)
-    tc_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
-                 const BwdArgs a) {
-  using L = DqSmem<D>;
-  constexpr int NCH = D / 64;
-  const Geom& g = a.g;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sQ = smem + L::OFF_Q;
-  uint8_t* sDO = smem + L::OFF_DO;
-  uint8_t* sRing = smem + L::OFF_RING;
-  uint8_t* sDS = smem + L::OFF_DS;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* full = bars;              // [NST]
-  uint64_t* empty = bars + NST;       // [NST]
-  uint64_t* s_full = bars + 2 * NST;  // [2]
-  uint64_t* s_empty = s_full + 2;     // [2]
-  uint64_t* ds_full = s_empty + 2;
-  uint64_t* ds_empty = ds_full + 1;
-  uint64_t* acc_full = ds_empty + 1;
-  uint64_t* q_full = acc_full + 1;
-  volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
-  uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [2][wpr]
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ncta = g.n / QB_DQ;
   const int bh = blockIdx.x % g.bh;
-  const int row0 = (ncta - 1 - blockIdx.x / g.bh) * QB_DQ;
-  const int jmax = g.causal ? (row0 + QB_DQ - 1) / BN : g.t_c - 1;
-  const int wpr = g.wpr;
+  const int row0 = (a.ncta_rows - 1 - (int)(blockIdx.x / g.bh)) * BM;  // heaviest first
+  const int nkt = g.m / DBN;
+  const int jmax = g.causal ? (row0 + BM - 1) / DBN : nkt - 1;
 
-  for (int i = tid; i < 2 * wpr; i += kThreads) {
+  for (int i = tid; i < 4 * wpr; i += kDeltaThreads) {
     const int rbi = i / wpr, w = i - rbi * wpr;
     smask[i] = a.mask[((size_t)bh * g.t_r + (row0 / 64 + rbi)) * wpr + w];
   }
@@ -348,10 +240,240 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);
+      mbar_init(&s_free[i], 8);
     }
-    mbar_init(ds_full, 8);
-    mbar_init(ds_empty, 1);
+    mbar_init(q_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  // bits of reference blocks (row block rb of this CTA, key blocks 2J, 2J+1)
+  auto bits2 = [&](int rb, int J) -> uint32_t {
+    return (smask[rb * wpr + ((2 * J) >> 5)] >> ((2 * J) & 31)) & 3u;
+  };
+  auto rg_active = [&](int rg, int J) -> bool { return (bits2(2 * rg, J) | bits2(2 * rg + 1, J)) != 0; };
+  auto next_active = [&](int J) -> int {
+    for (; J <= jmax; ++J)
+      if (rg_active(0, J) || rg_active(1, J)) return J;
+    return -1;
+  };
+
+  if (warp == 0) {
+    const bool leader = elect_one_sync();
+    const int qrow = bh * g.n + row0;
+    if (leader) mbar_expect_tx(q_full, 2 * L::QB);
+    for (int c = 0; c < NCH; ++c) {
+      if (leader) tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
+      if (leader) tma_load_2d(sDO + c * BM * 128, &tm_do, q_full, c * 64, qrow);
+    }
+    uint32_t r = 0;
+    auto load = [&](const CUtensorMap* tm, int row) {
+      const uint32_t st = r % NST, ph = (r / NST) & 1;
+      mbar_wait(&empty[st], ph ^ 1);
+      if (leader) mbar_expect_tx(&full[st], L::TILE);
+      for (int c = 0; c < NCH; ++c)
+        if (leader) tma_load_2d(sRing + st * L::TILE + c * DBN * 128, tm, &full[st], c * 64, row);
+      ++r;
+    };
+    const int krow0 = bh * g.m;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      load(&tm_k, krow0 + J * DBN);
+      load(&tm_v, krow0 + J * DBN);
+    }
+  } else if (warp == 1) {
+    const bool leader = elect_one_sync();
+    constexpr uint32_t IDESC_S = idesc_bf16_f32(128, DBN, false, false);
+    const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ring_addr = smem_u32(sRing);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    uint32_t r = 0, uses[2] = {0, 0};
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      const uint32_t kst = r % NST, vst = (r + 1) % NST;
+      mbar_wait(&full[kst], (r / NST) & 1);
+      mbar_wait(&full[vst], ((r + 1) / NST) & 1);
+      tc_fence_after();
+      const bool act1 = rg_active(1, J);
+      for (int rg = 0; rg < 2; ++rg) {
+        if (!rg_active(rg, J)) continue;
+        mbar_wait(&s_free[rg], (uses[rg] & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t sc = tmem + rg * 256;
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (leader)
+              umma_bf16(sc, desc_kmajor(q_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
+                        desc_kmajor(ring_addr + kst * L::TILE + c * DBN * 128 + k * 32), IDESC_S,
+                        (c | k) != 0);
+        // K_J's last reader issued: free its slot early (the next item, V_{J+1}, refills it)
+        if (rg == 1 || !act1)
+          if (leader) umma_commit(&empty[kst]);
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (leader)
+              umma_bf16(sc + 128, desc_kmajor(do_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
+                        desc_kmajor(ring_addr + vst * L::TILE + c * DBN * 128 + k * 32), IDESC_S,
+                        (c | k) != 0);
+        if (leader) umma_commit(&s_full[rg]);
+        ++uses[rg];
+      }
+      if (leader) umma_commit(&empty[vst]);
+      r += 2;
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;             // 0..15
+    const int rg = ew >> 3;              // row group
+    const int half = (ew >> 2) & 1;      // keys 64*half .. +63 of each tile
+    const int lq = warp & 3;             // TMEM lane quarter
+    const int e = rg * 128 + lq * 32 + lane;
+    const int rb = e >> 6;
+    const int grow = row0 + e;
+    const size_t orow = (size_t)bh * g.n + grow;
+    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + rg * 256 + half * 64;
+    const float A1 = a.A1;
+    const double B = 1.0 - (g.alpha - 1.0) * a.row_max[orow];
+    const float C = (float)(B - a.tau[orow]);
+    double num = 0.0, den = 0.0;
+    uint32_t uses = 0;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      if (!rg_active(rg, J)) continue;
+      mbar_wait(&s_full[rg], uses & 1);
+      ++uses;
+      tc_fence_after();
+      const bool mine = (bits2(rb, J) >> half) & 1u;  // the reference visits set blocks only
+      const int k0 = J * DBN + half * 64;
+      float s[32], dp[32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tmem_ld32(tl + c * 32, s);
+        tmem_ld32(tl + 128 + c * 32, dp);
+        tmem_wait_ld();
+        if (c == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_free[rg]);
+        }
+        if (mine) {
+          const int c0 = k0 + 32 * c;
+          float n32, d32;
+          if (g.causal && c0 + 31 > grow)
+            delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, grow - c0, n32, d32);
+          else
+            delta_chunk<AK, false>(s, dp, A1, C, a.e0f, a.e1f, 0, n32, d32);
+          num += (double)n32;
+          den += (double)d32;
+        }
+      }
+    }
+    // every epilogue thread has passed its last s_full wait: all MMAs (and ring
+    // reads) are complete, so the ring can hold the half-1 partials
+    bar_sync(1, 512);
+    if (half == 1) {
+      sRed[2 * e] = num;
+      sRed[2 * e + 1] = den;
+    }
+    bar_sync(1, 512);
+    if (half == 0) {
+      num += sRed[2 * e];
+      den += sRed[2 * e + 1];
+      const double dlt = den > 0.0 ? num / den : 0.0;
+      a.delta[orow] = dlt;
+      a.rowc[orow] = make_float2(C, (float)dlt);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+// ===================================================================== dQ
+// Query-major dQ kernel: 128 rows per CTA, 128-key tiles.  Per tile J:
+//   S_J = Q K_J^T (SS, N=128) into S[J&1], dP_J = dO V_J^T into dP,
+//   dS = u (dp - delta) split into bf16 hi + lo and written back over S[J&1]
+//   (tcgen05.st), then dQ += dS_hi K_J + dS_lo K_J as TS MMAs (A from TMEM, K_J
+//   read MN-major from the ring) -- no shared-memory round trip for dS.
+// TMEM: S[0] 0..127, S[1] 128..255, dP 256..383, dQ 384..384+D.  The pipe
+// order S_J, dP_J, dQ_{J-1} keeps the tensor core busy while the epilogue
+// turns tile J into dS (attention.cpp:508-535; one writer per dQ row).
+constexpr int QB_DQ = 128;
+
+template <int D>
+struct DqSmem {
+  static constexpr int QB = QB_DQ * D * 2;
+  static constexpr int TILE = DBN * D * 2;
+  // K_J stays resident until dQ_J (issued after dP_{J+1}); V_J only until dP_J
+  static constexpr int NSK = D == 128 ? 3 : 4;
+  static constexpr int NSV = D == 128 ? 2 : 3;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_DO = OFF_Q + QB;
+  static constexpr int OFF_KR = OFF_DO + QB;
+  static constexpr int OFF_VR = OFF_KR + NSK * TILE;
+  static constexpr int OFF_BAR = OFF_VR + NSV * TILE;
+  static constexpr int OFF_MISC = OFF_BAR + 40 * 8;
+  static constexpr int OFF_MASK = OFF_MISC + 64;
+  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 2 * wpr * 4 + 64; }
+};
+
+template <int D, int AK>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                 const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_do,
+                 const BwdArgs a) {
+  using L = DqSmem<D>;
+  constexpr int NSK = L::NSK, NSV = L::NSV;
+  constexpr int NCH = D / 64;
+  const Geom& g = a.g;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem + L::OFF_Q;
+  uint8_t* sDO = smem + L::OFF_DO;
+  uint8_t* sK = smem + L::OFF_KR;
+  uint8_t* sV = smem + L::OFF_VR;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* kfull = bars;              // [NSK]
+  uint64_t* kempty = kfull + NSK;      // [NSK]
+  uint64_t* vfull = kempty + NSK;      // [NSV]
+  uint64_t* vempty = vfull + NSV;      // [NSV]
+  uint64_t* s_full = vempty + NSV;     // [2] S_J and dP_J in TMEM
+  uint64_t* ds_full = s_full + 2;      // [2] dS_J written over S[J&1]
+  uint64_t* dp_free = ds_full + 2;     // dP consumed
+  uint64_t* acc_full = dp_free + 1;
+  uint64_t* q_full = acc_full + 1;
+  volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
+  uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [2][wpr]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ncta = g.n / QB_DQ;
+  const int bh = blockIdx.x % g.bh;
+  const int row0 = (ncta - 1 - (int)(blockIdx.x / g.bh)) * QB_DQ;
+  const int nkt = g.m / DBN;
+  const int jmax = g.causal ? (row0 + QB_DQ - 1) / DBN : nkt - 1;
+  const int wpr = g.wpr;
+
+  for (int i = tid; i < 2 * wpr; i += kThreads) {
+    const int rbi = i / wpr, w = i - rbi * wpr;
+    smask[i] = a.mask[((size_t)bh * g.t_r + (row0 / 64 + rbi)) * wpr + w];
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NSK; ++i) {
+      mbar_init(&kfull[i], 1);
+      mbar_init(&kempty[i], 1);
+    }
+    for (int i = 0; i < NSV; ++i) {
+      mbar_init(&vfull[i], 1);
+      mbar_init(&vempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&ds_full[i], 8);
+    }
+    mbar_init(dp_free, 8);
     mbar_init(acc_full, 1);
     mbar_init(q_full, 1);
     fence_barrier_init();
@@ -362,97 +484,91 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
-  auto rb_active = [&](int rb, int j) -> bool {
-    return (smask[rb * wpr + (j >> 5)] >> (j & 31)) & 1u;
+  auto bits2 = [&](int rb, int J) -> uint32_t {
+    return (smask[rb * wpr + ((2 * J) >> 5)] >> ((2 * J) & 31)) & 3u;
   };
-  auto next_active = [&](int j) -> int {
-    for (; j <= jmax; ++j)
-      if (rb_active(0, j) || rb_active(1, j)) return j;
+  auto next_active = [&](int J) -> int {
+    for (; J <= jmax; ++J)
+      if (bits2(0, J) | bits2(1, J)) return J;
     return -1;
   };
 
   if (warp == 0) {
-    {
-      const bool leader = elect_one_sync();
-      const int qrow = bh * g.n + row0;
-      if (leader) mbar_expect_tx(q_full, 2 * L::QB);
-      for (int c = 0; c < NCH; ++c) {
-        if (leader) tma_load_2d(sQ + c * QB_DQ * 128, &tm_q, q_full, c * 64, qrow);
-        if (leader) tma_load_2d(sDO + c * QB_DQ * 128, &tm_do, q_full, c * 64, qrow);
-      }
-      uint32_t r = 0;
-      auto load = [&](const CUtensorMap* tm, int row) {
-        const uint32_t st = r % NST, ph = (r / NST) & 1;
-        mbar_wait(&empty[st], ph ^ 1);
-        if (leader) mbar_expect_tx(&full[st], L::TILE);
-        for (int c = 0; c < NCH; ++c)
-          if (leader) tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
-        ++r;
-      };
-      const int krow0 = bh * g.m;
-      for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
-        load(&tm_k, krow0 + j * BN);
-        load(&tm_v, krow0 + j * BN);
-      }
+    const bool leader = elect_one_sync();
+    const int qrow = bh * g.n + row0;
+    if (leader) mbar_expect_tx(q_full, 2 * L::QB);
+    for (int c = 0; c < NCH; ++c) {
+      if (leader) tma_load_2d(sQ + c * QB_DQ * 128, &tm_q, q_full, c * 64, qrow);
+      if (leader) tma_load_2d(sDO + c * QB_DQ * 128, &tm_do, q_full, c * 64, qrow);
+    }
+    uint32_t t = 0;
+    const int krow0 = bh * g.m;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1), ++t) {
+      const uint32_t ks = t % NSK, vs = t % NSV;
+      mbar_wait(&kempty[ks], ((t / NSK) & 1) ^ 1);
+      if (leader) mbar_expect_tx(&kfull[ks], L::TILE);
+      for (int c = 0; c < NCH; ++c)
+        if (leader) tma_load_2d(sK + ks * L::TILE + c * DBN * 128, &tm_k, &kfull[ks], c * 64, krow0 + J * DBN);
+      mbar_wait(&vempty[vs], ((t / NSV) & 1) ^ 1);
+      if (leader) mbar_expect_tx(&vfull[vs], L::TILE);
+      for (int c = 0; c < NCH; ++c)
+        if (leader) tma_load_2d(sV + vs * L::TILE + c * DBN * 128, &tm_v, &vfull[vs], c * 64, krow0 + J * DBN);
     }
   } else if (warp == 1) {
-    {
-      const bool leader = elect_one_sync();
-      constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, false, false);
-      constexpr uint32_t IDESC_DQ = idesc_bf16_f32(128, D, false, true);
-      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO);
-      const uint32_t ring_addr = smem_u32(sRing), ds_addr = smem_u32(sDS);
-      mbar_wait(q_full, 0);
+    const bool leader = elect_one_sync();
+    constexpr uint32_t IDESC_S = idesc_bf16_f32(128, DBN, false, false);
+    constexpr uint32_t IDESC_DQ = idesc_bf16_f32(128, D, false, true);
+    const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO);
+    const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    uint32_t t = 0;
+    bool acc_init = false;
+    auto dq_mma = [&](uint32_t tt) {  // dQ += dS_tt K_tt (dS in S[tt&1], K in slot tt % NSK)
+      const uint32_t b = tt & 1, ks = tt % NSK;
+      mbar_wait(&ds_full[b], (tt >> 1) & 1);
       tc_fence_after();
-      uint32_t item = 0, r = 0;
-      bool acc_init = false;
-      int prev = -1;
-      uint32_t prev_kst = 0;
-      auto dq_mma = [&](uint32_t kst, uint32_t it) {
-        mbar_wait(ds_full, it & 1);
-        tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint64_t bd = desc_mnmajor(ring_addr + kst * L::TILE + k * 16 * 128, BN * 128);
-          if (leader) umma_bf16(tmem + 256, desc_kmajor(ds_addr + k * 32), bd, IDESC_DQ,
-                    (acc_init || k > 0) ? 1u : 0u);
-          if (leader) umma_bf16(tmem + 256, desc_kmajor(ds_addr + L::DSB + k * 32), bd, IDESC_DQ, 1u);
-        }
-        acc_init = true;
-        if (leader) umma_commit(&empty[kst]);
-        if (leader) umma_commit(ds_empty);
-      };
-      for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
-        const uint32_t b = item & 1;
-        mbar_wait(&s_empty[b], ((item >> 1) & 1) ^ 1);
-        const uint32_t kst = r % NST, vst = (r + 1) % NST;
-        mbar_wait(&full[kst], (r / NST) & 1);
-        mbar_wait(&full[vst], ((r + 1) / NST) & 1);
-        tc_fence_after();
-        const uint32_t sc = tmem + b * 128;
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (leader) umma_bf16(sc, desc_kmajor(q_addr + c * QB_DQ * 128 + k * 32),
-                      desc_kmajor(ring_addr + kst * L::TILE + c * BN * 128 + k * 32), IDESC_S,
-                      (c | k) != 0);
-            if (leader) umma_bf16(sc + 64, desc_kmajor(do_addr + c * QB_DQ * 128 + k * 32),
-                      desc_kmajor(ring_addr + vst * L::TILE + c * BN * 128 + k * 32), IDESC_S,
-                      (c | k) != 0);
-          }
-        if (leader) umma_commit(&empty[vst]);
-        if (leader) umma_commit(&s_full[b]);
-        if (prev >= 0) dq_mma(prev_kst, item - 1);
-        prev = j;
-        prev_kst = kst;
-        ++item;
-        r += 2;
+      for (int k = 0; k < 8; ++k) {
+        // keys 16k..16k+15: chunk k>>1 (32 keys) at cols 32(k>>1): hi +8(k&1), lo +16+8(k&1)
+        const uint32_t acol = b * 128 + 32 * (k >> 1) + 8 * (k & 1);
+        const uint64_t bd = desc_mnmajor(k_addr + ks * L::TILE + k * 16 * 128, DBN * 128);
+        if (leader) umma_bf16_ts(tmem + 384, tmem + acol, bd, IDESC_DQ, (acc_init || k > 0) ? 1u : 0u);
+        if (leader) umma_bf16_ts(tmem + 384, tmem + acol + 16, bd, IDESC_DQ, 1u);
       }
-      if (prev >= 0) dq_mma(prev_kst, item - 1);
-      if (leader) umma_commit(acc_full);
+      acc_init = true;
+      if (leader) umma_commit(&kempty[ks]);
+    };
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1), ++t) {
+      const uint32_t ks = t % NSK, vs = t % NSV, b = t & 1;
+      mbar_wait(&kfull[ks], (t / NSK) & 1);
+      tc_fence_after();
+      // S[b] was last read by dQ_{t-2}, issued earlier (in-order tensor pipe)
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (leader)
+            umma_bf16(tmem + b * 128, desc_kmajor(q_addr + c * QB_DQ * 128 + k * 32),
+                      desc_kmajor(k_addr + ks * L::TILE + c * DBN * 128 + k * 32), IDESC_S,
+                      (c | k) != 0);
+      mbar_wait(&vfull[vs], (t / NSV) & 1);
+      if (t > 0) mbar_wait(dp_free, (t - 1) & 1);
+      tc_fence_after();
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (leader)
+            umma_bf16(tmem + 256, desc_kmajor(do_addr + c * QB_DQ * 128 + k * 32),
+                      desc_kmajor(v_addr + vs * L::TILE + c * DBN * 128 + k * 32), IDESC_S,
+                      (c | k) != 0);
+      if (leader) umma_commit(&s_full[b]);
+      if (leader) umma_commit(&vempty[vs]);
+      if (t > 0) dq_mma(t - 1);
     }
+    if (t > 0) dq_mma(t - 1);
+    if (leader) umma_commit(acc_full);
   } else if (warp >= 4) {
-    const int half = (warp - 4) >> 2;  // key columns 32*half .. +31 of each tile
+    const int half = (warp - 4) >> 2;  // keys 64*half .. +63 of each tile
     const int lq = warp & 3;
     const int e = lq * 32 + lane;      // local query row 0..127
     const int rb = e >> 6;
@@ -461,71 +577,70 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16);
     const float A1 = a.A1;
     const float2 rc = a.rowc[orow];  // {C, delta} from the delta kernel
-    uint32_t item = 0;
-    const uint32_t ds_row = smem_u32(sDS) + (uint32_t)e * 128u;
-    for (int j = next_active(0); j >= 0; j = next_active(j + 1)) {
-      const bool mine = rb_active(rb, j);
-      const uint32_t b = item & 1;
-      mbar_wait(&s_full[b], (item >> 1) & 1);
+    uint32_t t = 0;
+    bool any = false;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      const uint32_t b = t & 1;
+      const bool mine = (bits2(rb, J) >> half) & 1u;
+      any |= mine;
+      mbar_wait(&s_full[b], (t >> 1) & 1);
       tc_fence_after();
-      float s[32], dp[32];
-      tmem_ld32(tl + b * 128 + half * 32, s);
-      tmem_ld32(tl + b * 128 + 64 + half * 32, dp);
-      tmem_wait_ld();
+      const int k0 = J * DBN + half * 64;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float s[32], dp[32];
+        const uint32_t scol = tl + b * 128 + half * 64 + c * 32;
+        tmem_ld32(tl + 256 + half * 64 + c * 32, dp);
+        tmem_ld32(scol, s);
+        tmem_wait_ld();
+        if (c == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dp_free);
+        }
+        const int c0 = k0 + 32 * c;
+        uint32_t hi[16], lo[16];
+        if (!mine) {
+#pragma unroll
+          for (int x = 0; x < 16; ++x) hi[x] = lo[x] = 0u;
+        } else if (g.causal && c0 + 31 > grow) {
+          ds_chunk<AK, true>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, grow - c0, hi, lo);
+        } else {
+          ds_chunk<AK, false>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, 0, hi, lo);
+        }
+        // chunk c (keys 32c..32c+31 of this half) keeps its own 32 columns:
+        // packed hi at +0..15, lo at +16..31
+        tmem_st16(scol, hi);
+        tmem_st16(scol + 16, lo);
+      }
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[b]);
-      const int c0 = j * BN + half * 32;
-      const bool diag = g.causal && c0 + 31 > grow;
-      uint32_t hi[16], lo[16];
-#pragma unroll
-      for (int x = 0; x < 16; ++x) {
-        float ds2[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int i = 2 * x + h;
-          float t = fmaf(A1, s[i], rc.x);
-          if (!mine || (diag && c0 + i > grow)) t = -1.f;
-          float p, u;
-          pu_of<AK>(t, a.e0f, a.e1f, p, u);
-          ds2[h] = u * (dp[i] - rc.y);
-        }
-        split_bf16x2(ds2[0], ds2[1], hi[x], lo[x]);
-      }
-      mbar_wait(ds_empty, (item & 1) ^ 1);
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const uint32_t off = (((uint32_t)(half * 4 + qq)) ^ (uint32_t)(e & 7)) << 4;
-        st_shared_v4(ds_row + off, hi[4 * qq], hi[4 * qq + 1], hi[4 * qq + 2], hi[4 * qq + 3]);
-        st_shared_v4(ds_row + L::DSB + off, lo[4 * qq], lo[4 * qq + 1], lo[4 * qq + 2],
-                     lo[4 * qq + 3]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
-      ++item;
+      if (lane == 0) mbar_arrive(&ds_full[b]);
+      ++t;
     }
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    bool any = false;
-    for (int j = 0; j <= jmax; ++j) any |= rb_active(rb, j);
+    (void)any;
+    bool rany = false;  // the row's tile has any set block (padding bits are 0)
+    for (int w = 0; w < wpr; ++w) rany |= smask[rb * wpr + w] != 0u;
 #pragma unroll
     for (int c = 0; c < D / 64; ++c) {
       float o[32];
-      tmem_ld32(tl + 256 + half * (D / 2) + c * 32, o);
+      tmem_ld32(tl + 384 + half * (D / 2) + c * 32, o);
       tmem_wait_ld();
       const int x0 = half * (D / 2) + c * 32;
       if (g.out_dtype == ADATTN_F64) {
         double* dst = reinterpret_cast<double*>(a.dq) + orow * D + x0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) dst[i] = any ? (double)(a.scale_f * o[i]) : 0.0;
+        for (int i = 0; i < 32; ++i) dst[i] = rany ? (double)(a.scale_f * o[i]) : 0.0;
       } else {
         float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dq) + orow * D + x0);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          dst[i] = any ? make_float4(a.scale_f * o[4 * i], a.scale_f * o[4 * i + 1],
-                                     a.scale_f * o[4 * i + 2], a.scale_f * o[4 * i + 3])
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+          dst[i] = rany ? make_float4(a.scale_f * o[4 * i], a.scale_f * o[4 * i + 1],
+                                      a.scale_f * o[4 * i + 2], a.scale_f * o[4 * i + 3])
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
   }
@@ -537,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ================================================================= dK / dV
 constexpr int KB = 128;      // keys per CTA
 constexpr int QT = 64;       // query rows per unit (one reference tile)
-constexpr int KST = 3;       // Q/dO stages
+constexpr int KST = 4;       // Q/dO stages
 
 template <int D>
 struct KvSmem {
@@ -728,22 +843,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2* rc = reinterpret_cast<const float2*>(sSt + st * L::STAGE + 2 * L::QTB);
       uint32_t ph[16], pl[16], dh[16], dl[16];
       const int q0 = i * QT + half * 32;
+      if (!mine) {
 #pragma unroll
-      for (int x = 0; x < 16; ++x) {
-        float pp[2], dd[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int qi = 2 * x + h;
-          const float2 c = rc[half * 32 + qi];
-          float t = fmaf(A1, s[qi], c.x);
-          if (!mine || (g.causal && gkey > q0 + qi)) t = -1.f;
-          float p, uu;
-          pu_of<AK>(t, a.e0f, a.e1f, p, uu);
-          pp[h] = p;
-          dd[h] = uu * (dp[qi] - c.y);
-        }
-        split_bf16x2(pp[0], pp[1], ph[x], pl[x]);
-        split_bf16x2(dd[0], dd[1], dh[x], dl[x]);
+        for (int x = 0; x < 16; ++x) ph[x] = pl[x] = dh[x] = dl[x] = 0u;
+      } else if (g.causal && q0 < key0 + lq * 32 + 31) {  // warp-uniform: diagonal tiles
+        pds_chunk<AK, true>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, gkey - q0, ph, pl, dh, dl);
+      } else {
+        pds_chunk<AK, false>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, 0, ph, pl, dh, dl);
       }
       // half h owns TMEM columns 32h..32h+31 of the S^T / dP^T regions it just read:
       // packed hi at +0..15, lo at +16..31
@@ -805,7 +911,7 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     const size_t sm = DeltaSmem<D>::bytes(g.wpr);
     if ((e = set_smem(k0, sm))) return e;
     prof_begin("tc_delta", st);
-    k0<<<dim3((unsigned)(a.ncta_rows * g.bh)), kThreads, sm, st>>>(m[0], m[1], m[2], m[3], a);
+    k0<<<dim3((unsigned)(a.ncta_rows * g.bh)), kDeltaThreads, sm, st>>>(m[0], m[1], m[2], m[3], a);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
@@ -857,8 +963,8 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   cudaError_t e;
   const uint64_t nq = (uint64_t)g.bh * g.n, nk = (uint64_t)g.bh * g.m;
   if ((e = make_tmap_2d(&m[0], q, nq, g.d, BM))) return e;
-  if ((e = make_tmap_2d(&m[1], k, nk, g.d, BN))) return e;
-  if ((e = make_tmap_2d(&m[2], v, nk, g.dv, BN))) return e;
+  if ((e = make_tmap_2d(&m[1], k, nk, g.d, DBN))) return e;
+  if ((e = make_tmap_2d(&m[2], v, nk, g.dv, DBN))) return e;
   if ((e = make_tmap_2d(&m[3], dout, nq, g.dv, BM))) return e;
   if ((e = make_tmap_2d(&m[4], q, nq, g.d, QT))) return e;
   if ((e = make_tmap_2d(&m[5], k, nk, g.d, KB))) return e;
