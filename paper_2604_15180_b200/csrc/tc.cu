@@ -1,6 +1,7 @@
 // tc.cu -- dispatch for the bf16 tensor-core path and its TMA descriptor helper.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "tc.cuh"
@@ -37,6 +38,54 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+namespace {
+__global__ void nsmid_probe(int* out) {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%nsmid;" : "=r"(v));
+  *out = (int)v;
+}
+}  // namespace
+
+// Number of %smid values of the current device (one list slot per resident CTA).
+static int nsmid_slots() {
+  static int cache[64];
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+  std::call_once(once[dev], [dev] {
+    int* d = nullptr;
+    int h = 0;
+    if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
+      nsmid_probe<<<1, 1>>>(d);
+      if (cudaMemcpy(&h, d, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) h = 0;
+      cudaFree(d);
+    }
+    cudaGetLastError();
+    cache[dev] = h;
+  });
+  return cache[dev];
+}
+
+// Lists pay off when few scores fall in the refinement window; alpha < 1.4
+// (e.g. 1.25: thousands of candidates per row at N=32K) keeps the sweeps.
+// ADATTN_CAND_CAP overrides the per-thread capacity (0 disables the lists).
+CandPlan cand_plan(const Geom& g) {
+  CandPlan p{0, 0};
+  int cap = 256;
+  if (const char* s = std::getenv("ADATTN_CAND_CAP")) cap = std::atoi(s);
+  if (cap < 64 || g.alpha < 1.4) return p;
+  cap = (cap + 63) / 64 * 64;
+  p.slots = nsmid_slots();
+  if (p.slots <= 0) return p;
+  p.cap = cap;
+  return p;
+}
+
+size_t forward_workspace(const Geom& g) {
+  const CandPlan p = cand_plan(g);
+  return p.cap > 0 ? (size_t)p.slots * 512 * (size_t)p.cap * 8 : 0;
+}
+
 }  // namespace tc
 
 // Envelope of the tensor-core kernels: bf16 inputs, 64x64
@@ -49,13 +98,13 @@ bool tc_supported(const Geom& g) {
 std::string tc_envelope() {
   return "bf16 inputs, block_r=block_c=64, d=dv in {64,128}, n%256==0, m%128==0, 2<=bins<=32";
 }
-size_t tc_forward_workspace(const Geom&) { return 0; }
+size_t tc_forward_workspace(const Geom& g) { return tc::forward_workspace(g); }
 size_t tc_backward_workspace(const Geom& g) { return tc::backward_workspace(g); }
 
 cudaError_t tc_forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
-                       double* tau, double* row_max, uint32_t* mask, int32_t* steps, void*,
+                       double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,
                        cudaStream_t st) {
-  return tc::forward(g, q, k, v, out, tau, row_max, mask, steps, st);
+  return tc::forward(g, q, k, v, out, tau, row_max, mask, steps, ws, st);
 }
 cudaError_t tc_delta(const Geom& g, const void* q, const void* k, const void* v,
                      const double* tau, const double* row_max, const uint32_t* mask,

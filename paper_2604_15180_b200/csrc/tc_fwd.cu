@@ -85,6 +85,11 @@ struct FwdArgs {
   double* row_max;
   uint32_t* mask;
   int32_t* steps;
+  // candidate lists (REF from lists instead of sweeps): per resident CTA slot
+  // (%smid) and epilogue thread, `cand_cap` entries of (raw score, block)
+  uint2* cand;
+  int cand_cap;
+  int cand_slots;
 };
 
 template <int D>
@@ -173,6 +178,39 @@ __device__ __forceinline__ void ref_slice(const float* v, float A1, float C, flo
   s1o = (s1a.x + s1a.y) + (s1b.x + s1b.y);
   s2o = (s2a.x + s2a.y) + (s2b.x + s2b.y);
   mxo = fmaxf(mxa, mxb);
+}
+
+// 1 << s with PTX clamp semantics (s >= 32 -> 0).
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t s) {
+  uint32_t r;
+  asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(s));
+  return r;
+}
+
+// HIST binning of a 32-element slice, nibble-packed.  w = nb c (z + 1) with
+// c = 1 - 2^-20 maps bin k of z (k/nb <= z < (k+1)/nb) to floor(w) = nb + k and
+// z < 0 below nb; fadd.rd(w, 2^23) puts floor(w) in the mantissa, so
+// sh = 4 (bits - (2^23 + nb)) is 4k for counted bins and a huge (clamped)
+// shift for z < 0: one FFMA2 + FADD2 + IMAD + SHF + IADD per element.
+// Three nibble accumulators (<= 11 elements each) fold into the 8-bit
+// even/odd-bin fields hE (bins 0,2,4,6) / hO (1,3,5,7).
+__device__ __forceinline__ void hist_nib(const float* v, float2 Aw, float2 Bw, uint32_t K,
+                                         uint32_t& hE, uint32_t& hO) {
+  uint32_t n0 = 0, n1 = 0, n2 = 0;
+  const float2 M = make_float2(8388608.f, 8388608.f);
+#pragma unroll
+  for (int x = 0; x < 16; ++x) {
+    const float2 w = __ffma2_rn(Aw, make_float2(v[2 * x], v[2 * x + 1]), Bw);
+    const float2 F = __fadd2_rd(w, M);
+    const uint32_t i0 = shl_clamp(1u, __float_as_uint(F.x) * 4u + K);
+    const uint32_t i1 = shl_clamp(1u, __float_as_uint(F.y) * 4u + K);
+    uint32_t& na = (2 * x) < 11 ? n0 : ((2 * x) < 22 ? n1 : n2);
+    na += i0;
+    uint32_t& nb_ = (2 * x + 1) < 11 ? n0 : ((2 * x + 1) < 22 ? n1 : n2);
+    nb_ += i1;
+  }
+  hE += (n0 & 0x0F0F0F0Fu) + (n1 & 0x0F0F0F0Fu) + (n2 & 0x0F0F0F0Fu);
+  hO += ((n0 >> 4) & 0x0F0F0F0Fu) + ((n1 >> 4) & 0x0F0F0F0Fu) + ((n2 >> 4) & 0x0F0F0F0Fu);
 }
 
 // HIST binning of a 32-element slice into packed 8-bit fields (<= 32 per slice).
@@ -298,11 +336,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int krow0 = bh * g.m;
     for (int pass = 0; pass < 2; ++pass)
       for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);
-    for (uint32_t ref = 0;; ++ref) {
+    uint32_t dround = 0;
+    bool out_now = false;
+    if (a.cand) {  // CAND sweep
       for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);
-      mbar_wait(dec_bar, ref & 1);
-      if (*s_decision == DEC_OUT) break;
+      mbar_wait(dec_bar, 0);
+      dround = 1;
+      out_now = *s_decision == DEC_OUT;
     }
+    if (!out_now)
+      for (uint32_t ref = 0;; ++ref) {
+        for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);
+        mbar_wait(dec_bar, (dround + ref) & 1);
+        if (*s_decision == DEC_OUT) break;
+      }
     int prev = -1;
     for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
       load(&tm_k, krow0 + J * BN);
@@ -362,11 +409,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     for (int pass = 0; pass < 2; ++pass)
       for (int J = 0; J <= Jmax; ++J) s_tile(J);
-    for (uint32_t ref = 0;; ++ref) {
+    uint32_t dround = 0;
+    bool out_now = false;
+    if (a.cand) {  // CAND sweep
       for (int J = 0; J <= Jmax; ++J) s_tile(J);
-      mbar_wait(dec_bar, ref & 1);
-      if (*s_decision == DEC_OUT) break;
+      mbar_wait(dec_bar, 0);
+      dround = 1;
+      out_now = *s_decision == DEC_OUT;
     }
+    if (!out_now)
+      for (uint32_t ref = 0;; ++ref) {
+        for (int J = 0; J <= Jmax; ++J) s_tile(J);
+        mbar_wait(dec_bar, (dround + ref) & 1);
+        if (*s_decision == DEC_OUT) break;
+      }
     // output pass: S[g] at g*128 (buffer 0 of each group), O[g] at 256 + g*128.
     // Per active tile J, per group g: PV_g(prev) then S_g(J) -- in tensor-pipe
     // order, so S_g(J) overwrites P_g(prev) only after PV_g(prev) has read it,
@@ -513,20 +569,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (nb > 8 && half == 0)
       for (int k = 0; k < nb; ++k) row_cnt[k] = 0;
     if (nb > 8) bar_sync(bar_rg, 256);
-    {
+    if (nb <= 8) {
+      const float cw = 1.0f - 0x1p-20f;  // keeps z = 1 (the row max) inside bin nb-1
+      const float2 Aw = make_float2(A1 * (float)nb * cw, A1 * (float)nb * cw);
+      const float bw = (float)((B + 1.0) * (double)nb * (double)cw);
+      const float2 Bw = make_float2(bw, bw);
+      const uint32_t K = 0u - 4u * (0x4B000000u + (uint32_t)nb);
+      uint32_t W0 = 0, W1 = 0, W2 = 0, W3 = 0;  // 16-bit fields: (0,4) (2,6) (1,5) (3,7)
+      auto drain = [&]() {
+        cnt[0] += W0 & 0xFFFFu; cnt[4] += W0 >> 16;
+        cnt[2] += W1 & 0xFFFFu; cnt[6] += W1 >> 16;
+        cnt[1] += W2 & 0xFFFFu; cnt[5] += W2 >> 16;
+        cnt[3] += W3 & 0xFFFFu; cnt[7] += W3 >> 16;
+        W0 = W1 = W2 = W3 = 0;
+      };
+      for (int J = 0; J <= jl; ++J) {
+        uint32_t hE = 0, hO = 0;  // 8-bit fields, <= 64 per tile
+        tau_tile(J, [&](int) { hist_nib(v, Aw, Bw, K, hE, hO); });
+        W0 += hE & 0x00FF00FFu;
+        W1 += (hE >> 8) & 0x00FF00FFu;
+        W2 += hO & 0x00FF00FFu;
+        W3 += (hO >> 8) & 0x00FF00FFu;
+        if ((J & 511) == 511) drain();  // 16-bit fields hold < 1024 tiles of 64
+      }
+      drain();
+    } else {
       const float An = A1 * (float)nb, Bn = Bf * (float)nb;  // exact: nb is a power of 2
       for (int J = 0; J <= jl; ++J)
         tau_tile(J, [&](int) {
-          if (nb <= 8) {
-            hist_slice8(v, An, Bn, nb, cnt);
-          } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float y = fmaf(An, v[i], Bn);
-              if (y >= 0.f) {
-                const int b = (int)(__float_as_uint(__fadd_rd(y, 8388608.f)) & 0x3Fu);
-                atomicAdd(&row_cnt[min(b, nb - 1)], 1u);
-              }
+          for (int i = 0; i < 32; ++i) {
+            const float y = fmaf(An, v[i], Bn);
+            if (y >= 0.f) {
+              const int b = (int)(__float_as_uint(__fadd_rd(y, 8388608.f)) & 0x3Fu);
+              atomicAdd(&row_cnt[min(b, nb - 1)], 1u);
             }
           }
         });
@@ -562,11 +638,127 @@ __global__ void __launch_bounds__(kThreads, 1)
       sRow[e * 4 + 3] = (float)(B - rs.hi);
     }
 
-    // ---- passes REF (attention.cpp:234-332)
     const bool need_sec = g.alpha > 2.0;
     const double e0 = g.e0;
     bool first_pass = true;
-    for (uint32_t ref = 0;; ++ref) {
+    uint32_t dround = 0;
+    bool list_ok = false;
+
+    // ---- pass CAND: every score that can matter for tau in [lo, hi] or for
+    // the mask (z > lo - eps) is appended to a per-thread list as (raw score,
+    // 64-key block); the refinement (attention.cpp:234-332) then runs on the
+    // lists with no further sweeps.  Exact: f, f', f'' and the mask only see
+    // z > tau - 1e-9 >= lo - 1e-9, and each listed term is evaluated with the
+    // sweep's own formula t = A1*acc + (B - tau).  Overflow -> REF sweeps.
+    if (a.cand) {
+      if (half == 0) {
+        const float eps_t = 1e-6f * (2.f + fabsf(Bf));  // fp32 slack of z (|B| scale)
+        sRow[e * 4 + 0] = (float)(B - rs.lo) + eps_t;
+      }
+      bar_sync(bar_rg, 256);
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      const int cap = a.cand_cap;
+      uint2* lst = a.cand + ((size_t)smid * kEpi + (size_t)(tid - 128)) * (size_t)cap;
+      bool ovf = (int)smid >= a.cand_slots;
+      int cnt = 0;
+      {
+        const float Cc = sRow[e * 4 + 0];
+        const float2 A2 = make_float2(A1, A1), C2 = make_float2(Cc, Cc);
+        for (int J = 0; J <= jl; ++J) {
+          const uint32_t blk = (uint32_t)(2 * J + half);
+          if (cnt > cap - 64) ovf = true;  // a tile appends <= 64 entries
+          tau_tile(J, [&](int) {
+            if (ovf) return;
+#pragma unroll
+            for (int x = 0; x < 16; ++x) {
+              const float2 t = __ffma2_rn(A2, make_float2(v[2 * x], v[2 * x + 1]), C2);
+              if (t.x > 0.f) lst[cnt++] = make_uint2(__float_as_uint(v[2 * x]), blk);
+              if (t.y > 0.f) lst[cnt++] = make_uint2(__float_as_uint(v[2 * x + 1]), blk);
+            }
+          });
+        }
+      }
+      const bool ovf_any = bar_red_or(4, kEpi, ovf);
+      if (!ovf_any) {
+        // refinement rounds on the lists (same RowSolve / row_step as the sweeps)
+        for (;;) {
+          bar_sync(bar_rg, 256);  // C / Chi published
+          const float C = sRow[e * 4 + 2];
+          const float Chi = sRow[e * 4 + 3];
+          double f = 0.0, f1 = 0.0, f2 = 0.0, fhi = 0.0;
+          for (int i = 0; i < cnt; ++i) {
+            const float acc = __uint_as_float(lst[i].x);
+            const float t = fmaf(A1, acc, C);
+            if (t > 0.f) {
+              if constexpr (AK == AK15) {
+                f += (double)(t * t);
+                f1 += (double)t;
+                f2 += 1.0;
+              } else if constexpr (AK == AK2) {
+                f += (double)t;
+                f1 += 1.0;
+              } else if constexpr (AK == AK125) {
+                const float t2 = t * t;
+                f += (double)(t2 * t2);
+                f1 += (double)(t2 * t);
+                f2 += (double)t2;
+              } else {
+                const float lt = __log2f(t);
+                const float l1 = a.e1f < 0.f ? __log2f(fmaxf(t, 1e-12f)) : lt;
+                const float l2 = a.e2f < 0.f ? __log2f(fmaxf(t, 1e-12f)) : lt;
+                f += (double)exp2f(a.e0f * lt);
+                f1 += a.e1f == 0.f ? 1.0 : (double)exp2f(a.e1f * l1);
+                f2 += a.e2f == 0.f ? 1.0 : (double)exp2f(a.e2f * l2);
+              }
+            }
+            if (first_pass && need_sec) {
+              const float th = fmaf(A1, acc, Chi);
+              if (th > 0.f) fhi += (double)exp2f(a.e0f * __log2f(th));
+            }
+          }
+          if (half == 1) {
+            sPart[e * 4 + 0] = f;
+            sPart[e * 4 + 1] = f1;
+            sPart[e * 4 + 2] = f2;
+            sPart[e * 4 + 3] = fhi;
+          }
+          bar_sync(bar_rg, 256);
+          bool stepped = false;
+          if (half == 0 && !rs.done) {
+            rs.f = -1.0 + (f + sPart[e * 4 + 0]);
+            rs.f1 = -e0 * (f1 + sPart[e * 4 + 1]);
+            rs.f2 = e0 * (e0 - 1.0) * (f2 + sPart[e * 4 + 2]);
+            if (first_pass) rs.f_hi = -1.0 + (fhi + sPart[e * 4 + 3]);
+            stepped = row_step(rs, g.alpha, g.refine_tol, g.refine_iters, need_sec);
+            sRow[e * 4 + 2] = (float)(B - rs.tau);
+          }
+          first_pass = false;
+          if (!bar_red_or(4, kEpi, stepped)) break;
+        }
+        // mask at the final tau: block active iff any z > tau - 1e-9 (attention.cpp:254-266)
+        for (int i = tid - 128; i < 4 * wpr; i += kEpi) smask[i] = 0u;
+        bar_sync(3, kEpi);
+        {
+          const float C = sRow[e * 4 + 2];
+          for (int i = 0; i < cnt; ++i) {
+            const uint2 en = lst[i];
+            if (fmaf(A1, __uint_as_float(en.x), C) > -1e-9f)
+              atomicOr(&smask[rb * wpr + (en.y >> 5)], 1u << (en.y & 31));
+          }
+        }
+        list_ok = true;
+      }
+      bar_sync(3, kEpi);
+      if (tid == 128) {
+        *s_decision = list_ok ? DEC_OUT : DEC_REF;
+        mbar_arrive(dec_bar);
+      }
+      dround = 1;
+    }
+
+    // ---- passes REF (attention.cpp:234-332): sweeps (no lists, or a list overflowed)
+    for (uint32_t ref = 0; !list_ok; ++ref) {
       for (int i = tid - 128; i < 4 * wpr; i += kEpi) smask[i] = 0u;
       bar_sync(3, kEpi);  // C/Chi published, masks cleared, counts consumed
       const float C = sRow[e * 4 + 2];
@@ -727,7 +919,7 @@ int alpha_kind(double alpha) {
 }
 
 cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
-                    double* tau, double* row_max, uint32_t* mask, int32_t* steps,
+                    double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,
                     cudaStream_t st) {
   CUtensorMap tq, tk, tv;
   cudaError_t e;
@@ -747,6 +939,10 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.row_max = row_max;
   a.mask = mask;
   a.steps = steps;
+  const CandPlan cp = cand_plan(g);
+  a.cand = (cp.cap > 0 && ws) ? reinterpret_cast<uint2*>(ws) : nullptr;
+  a.cand_cap = cp.cap;
+  a.cand_slots = cp.slots;
   const int ak = alpha_kind(g.alpha);
   if (g.d == 64) return launch_fwd_d<64>(g, ak, tq, tk, tv, a, st);
   return launch_fwd_d<128>(g, ak, tq, tk, tv, a, st);

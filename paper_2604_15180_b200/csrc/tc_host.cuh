@@ -16,8 +16,16 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint
 
 int alpha_kind(double alpha);
 
+// Candidate-list plan of the forward: `cap` entries per epilogue thread (0 =
+// refinement by sweeps only), `slots` resident-CTA slots (%nsmid).
+struct CandPlan {
+  int cap, slots;
+};
+CandPlan cand_plan(const Geom& g);
+size_t forward_workspace(const Geom& g);
+
 cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
-                    double* tau, double* row_max, uint32_t* mask, int32_t* steps,
+                    double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,
                     cudaStream_t st);
 
 size_t backward_workspace(const Geom& g);

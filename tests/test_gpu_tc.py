@@ -129,3 +129,39 @@ def test_tc_backward_matches_exact(case):
     print("  round trip", {n: f"{e2[n]:.2e}" for n in e2})
     for n in e2:
         assert e2[n] <= 2e-2, (n, e2[n])
+
+
+LIST_CASES = [
+    # (B, H, N, D, alpha, causal, qscale): refinement from candidate lists
+    (1, 2, 2048, 128, 1.5, True, 1.0),
+    (1, 1, 2048, 64, 2.0, False, 1.0),
+    (1, 1, 1024, 128, 1.75, True, 4.0),
+    (1, 1, 1024, 128, 2.5, True, 1.0),
+]
+
+
+@pytest.mark.parametrize("case", LIST_CASES, ids=[str(c) for c in LIST_CASES])
+def test_tc_candidate_lists_and_sweep_fallback(case, monkeypatch):
+    """The list refinement (default) and the sweep refinement (forced by a
+    list capacity too small to hold the candidates -> per-CTA overflow ->
+    fallback) give the same thresholds, masks and outputs, and both match the
+    exact path."""
+    B, H, N, D, alpha, causal, qs = case
+    q, k, v, do = inputs(hash(case) % 991 + 7, B, H, N, D, qs)
+    _, rx, _ = run(q, k, v, None, "exact", alpha=alpha, causal=causal)
+    monkeypatch.delenv("ADATTN_CAND_CAP", raising=False)
+    _, rl, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_CAND_CAP", "64")
+    _, rs, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_CAND_CAP", "0")
+    _, r0, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
+    for name, r in (("list", rl), ("fallback", rs), ("sweeps", r0)):
+        tau_err = (r.tau - rx.tau).abs().max().item()
+        out_err = (r.out - rx.out).abs().max().item()
+        print(case, name, f"tau {tau_err:.2e} out {out_err:.2e} steps {r.row_steps.float().mean().item():.3f}")
+        assert tau_err <= 1e-3 and out_err <= 2e-2
+    # list vs sweeps: same steps, tau equal up to fp32 summation order
+    assert torch.equal(rl.row_steps, r0.row_steps)
+    assert (rl.tau - r0.tau).abs().max().item() <= 1e-6
+    assert torch.equal(rs.tau, r0.tau) and torch.equal(rs.out, r0.out)
+    assert torch.equal(rl.mask.words, r0.mask.words)
