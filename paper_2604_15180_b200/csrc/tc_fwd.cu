@@ -660,24 +660,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       const int cap = a.cand_cap;
       uint2* lst = a.cand + ((size_t)smid * kEpi + (size_t)(tid - 128)) * (size_t)cap;
-      bool ovf = (int)smid >= a.cand_slots;
+      bool ovf = (int)smid >= a.cand_slots;  // (uniform: one CTA per SM)
       int cnt = 0;
       {
+        // z > lo - eps  <=>  acc > theta (A1 > 0): one compare per score, the
+        // threshold lowered by a few ulps so the raw test is a superset
         const float Cc = sRow[e * 4 + 0];
-        const float2 A2 = make_float2(A1, A1), C2 = make_float2(Cc, Cc);
+        float theta = -Cc / A1;
+        theta -= 4e-7f * fabsf(theta) + 1e-30f;
+        uint32_t ucnt = 0;
         for (int J = 0; J <= jl; ++J) {
           const uint32_t blk = (uint32_t)(2 * J + half);
-          if (cnt > cap - 64) ovf = true;  // a tile appends <= 64 entries
+          // a tile appends <= 64 entries; warp-uniform (the append votes are warp-collective)
+          ovf = __any_sync(0xffffffffu, ovf || (int)ucnt > cap - 64);
           tau_tile(J, [&](int) {
             if (ovf) return;
+            // candidates are rare (~0.3% of scores): a warp vote per column
+            // keeps the common path at compare + vote + branch
 #pragma unroll
-            for (int x = 0; x < 16; ++x) {
-              const float2 t = __ffma2_rn(A2, make_float2(v[2 * x], v[2 * x + 1]), C2);
-              if (t.x > 0.f) lst[cnt++] = make_uint2(__float_as_uint(v[2 * x]), blk);
-              if (t.y > 0.f) lst[cnt++] = make_uint2(__float_as_uint(v[2 * x + 1]), blk);
-            }
+            for (int i = 0; i < 32; i += 2)
+              asm volatile(
+                  "{\n\t.reg .pred p0, p1, pa, q;\n\t.reg .u64 ad;\n\t"
+                  "setp.gt.f32 p0, %1, %3;\n\t"
+                  "setp.gt.f32 p1, %2, %3;\n\t"
+                  "or.pred pa, p0, p1;\n\t"
+                  "vote.sync.any.pred q, pa, 0xffffffff;\n\t"
+                  "@!q bra.uni CAND_SKIP_%=;\n\t"
+                  "mad.wide.u32 ad, %0, 8, %4;\n\t"
+                  "@p0 st.global.v2.b32 [ad], {%5, %7};\n\t"
+                  "@p0 add.u32 %0, %0, 1;\n\t"
+                  "mad.wide.u32 ad, %0, 8, %4;\n\t"
+                  "@p1 st.global.v2.b32 [ad], {%6, %7};\n\t"
+                  "@p1 add.u32 %0, %0, 1;\n\t"
+                  "CAND_SKIP_%=:\n\t}"
+                  : "+r"(ucnt)
+                  : "f"(v[i]), "f"(v[i + 1]), "f"(theta), "l"(lst), "r"(__float_as_uint(v[i])),
+                    "r"(__float_as_uint(v[i + 1])), "r"(blk)
+                  : "memory");
           });
         }
+        cnt = (int)ucnt;
       }
       const bool ovf_any = bar_red_or(4, kEpi, ovf);
       if (!ovf_any) {
