@@ -224,8 +224,9 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wpr = g.wpr;
-  const int bh = blockIdx.x % g.bh;
-  const int row0 = (a.ncta_rows - 1 - (int)(blockIdx.x / g.bh)) * BM;  // heaviest first
+  // head-major (K/V L2-resident), heaviest causal row blocks first within a head
+  const int bh = blockIdx.x / a.ncta_rows;
+  const int row0 = (a.ncta_rows - 1 - (int)(blockIdx.x % a.ncta_rows)) * BM;
   const int nkt = g.m / DBN;
   const int jmax = g.causal ? (row0 + BM - 1) / DBN : nkt - 1;
 
@@ -450,8 +451,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ncta = g.n / QB_DQ;
-  const int bh = blockIdx.x % g.bh;
-  const int row0 = (ncta - 1 - (int)(blockIdx.x / g.bh)) * QB_DQ;
+  const int bh = blockIdx.x / ncta;  // head-major, heaviest first
+  const int row0 = (ncta - 1 - (int)(blockIdx.x % ncta)) * QB_DQ;
   const int nkt = g.m / DBN;
   const int jmax = g.causal ? (row0 + QB_DQ - 1) / DBN : nkt - 1;
   const int wpr = g.wpr;
@@ -694,16 +695,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nkb = g.m / KB;
-  const int bh = blockIdx.x % g.bh;
-  const int kb = blockIdx.x / g.bh;  // causal: low key blocks have the most query tiles
+  const int bh = blockIdx.x / nkb;   // head-major (Q/dO L2-resident)
+  const int kb = blockIdx.x % nkb;   // causal: low key blocks have the most query tiles
   const int key0 = kb * KB;
   const int j0 = key0 / 64;          // first of the two reference key tiles
   const int wpr = g.wpr;
   const int i_first = g.causal ? key0 / QT : 0;
 
   {
-    const int jw = (blockIdx.x / g.bh) * KB / 64;
-    const int bhh = blockIdx.x % g.bh;
+    const int jw = kb * KB / 64;
+    const int bhh = bh;
     for (int i = threadIdx.x; i < g.t_r; i += kThreads) {
       const uint32_t w = a.mask[((size_t)bhh * g.t_r + i) * g.wpr + (jw >> 5)];
       ubits[i] = (uint8_t)((w >> (jw & 31)) & 3u);

@@ -58,14 +58,24 @@ enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 // waits on ring-empty, [4] epilogue warp 4 waits on S-full, [6] MMA-warp cycles,
 // [7] ring items.
 #ifdef ADATTN_PIPE_STATS
-__device__ unsigned long long g_pipe_stats[8];
+__device__ unsigned long long g_pipe_stats[16];
 #endif
 namespace {
 #ifdef ADATTN_PIPE_STATS
 #define PSTAT_T0() const long long _t0 = clock64()
 #define PSTAT_ADD(i) \
   if (leader) atomicAdd(&g_pipe_stats[i], (unsigned long long)(clock64() - _t0))
+// epilogue phase marks (thread 128): [8+k] = cycles spent before mark k since the previous one
+#define PASS_MARK(k)                                                                  \
+  if (tid == 128) {                                                                   \
+    const long long _n = clock64();                                                   \
+    atomicAdd(&g_pipe_stats[8 + (k)], (unsigned long long)(_n - _pm));                \
+    _pm = _n;                                                                         \
+  }
 #else
+#define PASS_MARK(k) \
+  do {               \
+  } while (0)
 #define PSTAT_T0() \
   do {             \
   } while (0)
@@ -263,8 +273,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [4][wpr]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int bh = blockIdx.x % g.bh;
-  const int crow = a.ncta_rows - 1 - blockIdx.x / g.bh;  // heaviest causal tiles first
+  // head-major (the head's K/V stay L2-resident across its CTAs' sweeps),
+  // heaviest causal row blocks first within a head
+  const int bh = blockIdx.x / a.ncta_rows;
+  const int crow = a.ncta_rows - 1 - (int)(blockIdx.x % a.ncta_rows);
   const int row0 = crow * BM;
   const int nkt = g.m / BN;                              // 128-key tiles
   const int Jmax = g.causal ? (row0 + BM - 1) / BN : nkt - 1;
@@ -546,6 +558,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       body(1);
     };
 
+#ifdef ADATTN_PIPE_STATS
+    long long _pm = clock64();
+#endif
     // ---- pass MAX (attention.cpp:182-195): max of raw dot products, scaled once
     float mraw = -CUDART_INF_F;
     for (int J = 0; J <= jl; ++J)
@@ -556,6 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sRow[e * 4 + half] = mraw;
     bar_sync(bar_rg, 256);
     mraw = fmaxf(sRow[e * 4], sRow[e * 4 + 1]);
+    PASS_MARK(0);
     const float m_f = a.scale_f * mraw;  // == max(scale * s): rounding is monotone
     const double B = 1.0 - (g.alpha - 1.0) * (double)m_f;  // z = A1*acc + B
     const float Bf = (float)B;
@@ -607,6 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         });
     }
+    PASS_MARK(1);
     // combine the two key halves; the half-0 thread owns the row's solver state
     RowSolve rs;
     rs.tau = 0.0;
@@ -701,6 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         cnt = (int)ucnt;
       }
+      PASS_MARK(2);
       const bool ovf_any = bar_red_or(4, kEpi, ovf);
       if (!ovf_any) {
         // refinement rounds on the lists (same RowSolve / row_step as the sweeps)
@@ -771,6 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         list_ok = true;
       }
+      PASS_MARK(3);
       bar_sync(3, kEpi);
       if (tid == 128) {
         *s_decision = list_ok ? DEC_OUT : DEC_REF;
@@ -834,6 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!any) break;
     }
 
+    PASS_MARK(4);
     // ---- pass OUT (attention.cpp:334-352): P over the active blocks, O = P V
     {
       const float C = sRow[e * 4 + 2];
@@ -865,6 +885,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // write O (fp32 or fp64): this thread's half of the row's dv columns
       const size_t orow = (size_t)bh * g.n + grow;
       mbar_wait(o_full, 0);
+      PASS_MARK(5);
       tc_fence_after();
       const bool written = __any_sync(0xffffffffu, any_out);
       const uint32_t to = tmem + ((uint32_t)(lq * 32) << 16) + 256 + rg * D + half * (D / 2);
@@ -899,6 +920,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         a.mask[((size_t)bh * g.t_r + (row0 / 64 + rbi)) * wpr + w] = smask[i];
       }
     }
+    PASS_MARK(6);
   }
   tc_fence_before();
   __syncthreads();
@@ -975,9 +997,9 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
 
 #ifdef ADATTN_PIPE_STATS
 extern "C" void adattn_b200_pipe_stats(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, adattn_b200::tc::g_pipe_stats, sizeof(unsigned long long) * 8);
+  cudaMemcpyFromSymbol(out, adattn_b200::tc::g_pipe_stats, sizeof(unsigned long long) * 16);
   if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[16] = {};
     cudaMemcpyToSymbol(adattn_b200::tc::g_pipe_stats, z, sizeof z);
   }
 }

@@ -1,4 +1,6 @@
-"""Loads the ADATTN_PIPE_STATS build and prints per-role wait fractions of the forward."""
+"""Loads the ADATTN_PIPE_STATS build (make -C paper_2604_15180_b200 stats) and
+prints per-role wait fractions and per-phase cycle shares of the forward.
+    python tools/pipe_stats.py B H N [beta]"""
 import ctypes as C, os, sys
 sys.path.insert(0, ".")
 import paper_2604_15180_b200._lib as L
@@ -11,19 +13,23 @@ fn = lib.adattn_b200_pipe_stats
 fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 B, H, N = (int(x) for x in sys.argv[1:4])
 beta = float(sys.argv[4]) if len(sys.argv) > 4 else None
+alpha = float(os.environ.get("ALPHA", "1.5"))
 q, k, v, do = (workloads.gaussian(B, H, N, 128, 1.0, seed=1) if beta is None
                else workloads.anchored(B, H, N, 128, beta, True, seed=1))
-p = pa.AttentionProblem(q, k, v, alpha=1.5, causal=True)
+p = pa.AttentionProblem(q, k, v, alpha=alpha, causal=True)
 r = pa.forward(p); torch.cuda.synchronize()
-buf = (C.c_ulonglong * 8)()
+buf = (C.c_ulonglong * 16)()
 fn(buf, 1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); r = pa.forward(p); e1.record(); e1.synchronize()
 fn(buf, 1)
 st = list(buf)
-mma = st[6]
+mma = max(st[6], 1)
 names = ["mma_wait_full(TMA)", "mma_wait_s_empty(epi)", "mma_wait_p_full", "prod_wait_empty", "epi_w4_wait_s_full"]
-print("fwd ms", e0.elapsed_time(e1), "sparsity", r.stats.block_sparsity, "tiles", st[7])
+print("fwd ms", e0.elapsed_time(e1), "sparsity", r.stats.block_sparsity, "ring items", st[7])
 for i, n in enumerate(names):
     print(f"{n:26s} {st[i] / mma:6.3f} of MMA-warp cycles")
-print("MMA cycles per tile", mma / st[7])
+ph = ["MAX", "HIST", "CAND sweep", "list REF+mask", "REF sweeps", "OUT (S+PV)", "O/tau store"]
+tot = sum(st[8:15]) or 1
+for i, n in enumerate(ph):
+    print(f"phase {n:16s} {100.0 * st[8 + i] / tot:5.1f}%")
