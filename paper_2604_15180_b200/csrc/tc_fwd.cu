@@ -44,7 +44,7 @@ namespace {
 
 constexpr int BM = 256;        // query rows per CTA
 constexpr int BN = 128;        // keys per S tile (two 64-key reference tiles)
-constexpr int NST = 3;         // ring stages
+constexpr int NST = 4;         // ring stages
 constexpr int kEpiWarps = 16;
 constexpr int kEpi = kEpiWarps * 32;
 constexpr int kThreads = 128 + kEpi;
@@ -108,9 +108,9 @@ struct FwdSmem {
   static constexpr int TILE = BN * D * 2;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_RING = OFF_Q + QBYTES;
-  static constexpr int OFF_CNT = OFF_RING + NST * TILE;   // [256][32] u32 (HIST combine)
+  static constexpr int OFF_CNT = OFF_RING + NST * TILE;   // [256][16] u32 (HIST combine)
   static constexpr int OFF_PART = OFF_CNT;                // [256][4] f64 (REF combine, reuses)
-  static constexpr int OFF_BAR = OFF_CNT + BM * 32 * 4;
+  static constexpr int OFF_BAR = OFF_CNT + BM * 16 * 4;
   static constexpr int NBAR = 2 * NST + 16;
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
   static constexpr int OFF_ROW = OFF_MISC + 64;  // [256][4] f32 per-row scratch
@@ -204,43 +204,71 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t s) {
 // shift for z < 0: one FFMA2 + FADD2 + IMAD + SHF + IADD per element.
 // Three nibble accumulators (<= 11 elements each) fold into the 8-bit
 // even/odd-bin fields hE (bins 0,2,4,6) / hO (1,3,5,7).
+template <int NW>  // nibble words: bins <= 8 (1) or <= 16 (2)
 __device__ __forceinline__ void hist_nib(const float* v, float2 Aw, float2 Bw, uint32_t K,
-                                         uint32_t& hE, uint32_t& hO) {
-  uint32_t n0 = 0, n1 = 0, n2 = 0;
+                                         uint32_t* hE, uint32_t* hO) {
+  uint32_t n[3][NW];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int w = 0; w < NW; ++w) n[a][w] = 0;
   const float2 M = make_float2(8388608.f, 8388608.f);
 #pragma unroll
   for (int x = 0; x < 16; ++x) {
-    const float2 w = __ffma2_rn(Aw, make_float2(v[2 * x], v[2 * x + 1]), Bw);
-    const float2 F = __fadd2_rd(w, M);
-    const uint32_t i0 = shl_clamp(1u, __float_as_uint(F.x) * 4u + K);
-    const uint32_t i1 = shl_clamp(1u, __float_as_uint(F.y) * 4u + K);
-    uint32_t& na = (2 * x) < 11 ? n0 : ((2 * x) < 22 ? n1 : n2);
-    na += i0;
-    uint32_t& nb_ = (2 * x + 1) < 11 ? n0 : ((2 * x + 1) < 22 ? n1 : n2);
-    nb_ += i1;
+    const float2 wv = __ffma2_rn(Aw, make_float2(v[2 * x], v[2 * x + 1]), Bw);
+    const float2 F = __fadd2_rd(wv, M);
+    const uint32_t s0 = __float_as_uint(F.x) * 4u + K;
+    const uint32_t s1 = __float_as_uint(F.y) * 4u + K;
+    const int a0 = (2 * x) < 11 ? 0 : ((2 * x) < 22 ? 1 : 2);
+    const int a1 = (2 * x + 1) < 11 ? 0 : ((2 * x + 1) < 22 ? 1 : 2);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {  // word w holds bins 8w .. 8w+7
+      n[a0][w] += shl_clamp(1u, s0 - 32u * w);
+      n[a1][w] += shl_clamp(1u, s1 - 32u * w);
+    }
   }
-  hE += (n0 & 0x0F0F0F0Fu) + (n1 & 0x0F0F0F0Fu) + (n2 & 0x0F0F0F0Fu);
-  hO += ((n0 >> 4) & 0x0F0F0F0Fu) + ((n1 >> 4) & 0x0F0F0F0Fu) + ((n2 >> 4) & 0x0F0F0F0Fu);
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    hE[w] += (n[0][w] & 0x0F0F0F0Fu) + (n[1][w] & 0x0F0F0F0Fu) + (n[2][w] & 0x0F0F0F0Fu);
+    hO[w] += ((n[0][w] >> 4) & 0x0F0F0F0Fu) + ((n[1][w] >> 4) & 0x0F0F0F0Fu) +
+             ((n[2][w] >> 4) & 0x0F0F0F0Fu);
+  }
 }
 
-// HIST binning of a 32-element slice into packed 8-bit fields (<= 32 per slice).
-__device__ __forceinline__ void hist_slice8(const float* v, float An, float Bn, int nb,
-                                            uint32_t* cnt) {
-  uint32_t lo = 0, hi = 0;
+// Whole HIST sweep of one thread (64 keys per tile) for nb <= 8 NW: counts of
+// bins 0..8NW-1 into cnt[].  Per tile the 8-bit fields (<= 64) fold into
+// 16-bit fields, drained to cnt every 512 tiles.
+template <int NW, typename TileFn>
+__device__ __forceinline__ void hist_sweep(int jl, float2 Aw, float2 Bw, uint32_t K, uint32_t* cnt,
+                                           TileFn&& tile) {
+  uint32_t W[NW][4];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const float y = fmaf(An, v[i], Bn);
-    int b = (int)(__float_as_uint(__fadd_rd(fmaxf(y, 0.f), 8388608.f)) & 0x3Fu);
-    b = min(b, nb - 1);
-    const uint32_t inc = (y >= 0.f) ? (1u << ((b & 3) << 3)) : 0u;
-    lo += (b < 4) ? inc : 0u;
-    hi += (b >= 4) ? inc : 0u;
-  }
+  for (int w = 0; w < NW; ++w) W[w][0] = W[w][1] = W[w][2] = W[w][3] = 0;
+  auto drain = [&]() {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    cnt[k] += (lo >> (8 * k)) & 0xFFu;
-    cnt[k + 4] += (hi >> (8 * k)) & 0xFFu;
+    for (int w = 0; w < NW; ++w) {  // fields: W0 (0,4) W1 (2,6) W2 (1,5) W3 (3,7)
+      cnt[8 * w + 0] += W[w][0] & 0xFFFFu; cnt[8 * w + 4] += W[w][0] >> 16;
+      cnt[8 * w + 2] += W[w][1] & 0xFFFFu; cnt[8 * w + 6] += W[w][1] >> 16;
+      cnt[8 * w + 1] += W[w][2] & 0xFFFFu; cnt[8 * w + 5] += W[w][2] >> 16;
+      cnt[8 * w + 3] += W[w][3] & 0xFFFFu; cnt[8 * w + 7] += W[w][3] >> 16;
+      W[w][0] = W[w][1] = W[w][2] = W[w][3] = 0;
+    }
+  };
+  for (int J = 0; J <= jl; ++J) {
+    uint32_t hE[NW], hO[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) hE[w] = hO[w] = 0;
+    tile(J, hE, hO);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      W[w][0] += hE[w] & 0x00FF00FFu;
+      W[w][1] += (hE[w] >> 8) & 0x00FF00FFu;
+      W[w][2] += hO[w] & 0x00FF00FFu;
+      W[w][3] += (hO[w] >> 8) & 0x00FF00FFu;
+    }
+    if ((J & 511) == 511) drain();  // 16-bit fields hold < 1024 tiles of 64
   }
+  drain();
 }
 
 template <int D, int AK>
@@ -577,50 +605,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float Bf = (float)B;
 
     // ---- pass HIST (attention.cpp:201-232): counts of min(floor(B z), B-1), z >= 0
-    const int nb = g.bins;
-    uint32_t cnt[8];  // bins <= 8 in registers; more bins count into shared memory
+    const int nb = g.bins;  // 2..16 on this path (tc_supported)
+    uint32_t cnt[16];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) cnt[k] = 0;
-    uint32_t* row_cnt = sCnt + e * 32;
-    if (nb > 8 && half == 0)
-      for (int k = 0; k < nb; ++k) row_cnt[k] = 0;
-    if (nb > 8) bar_sync(bar_rg, 256);
-    if (nb <= 8) {
+    for (int k = 0; k < 16; ++k) cnt[k] = 0;
+    uint32_t* row_cnt = sCnt + e * 16;
+    {
       const float cw = 1.0f - 0x1p-20f;  // keeps z = 1 (the row max) inside bin nb-1
       const float2 Aw = make_float2(A1 * (float)nb * cw, A1 * (float)nb * cw);
       const float bw = (float)((B + 1.0) * (double)nb * (double)cw);
       const float2 Bw = make_float2(bw, bw);
       const uint32_t K = 0u - 4u * (0x4B000000u + (uint32_t)nb);
-      uint32_t W0 = 0, W1 = 0, W2 = 0, W3 = 0;  // 16-bit fields: (0,4) (2,6) (1,5) (3,7)
-      auto drain = [&]() {
-        cnt[0] += W0 & 0xFFFFu; cnt[4] += W0 >> 16;
-        cnt[2] += W1 & 0xFFFFu; cnt[6] += W1 >> 16;
-        cnt[1] += W2 & 0xFFFFu; cnt[5] += W2 >> 16;
-        cnt[3] += W3 & 0xFFFFu; cnt[7] += W3 >> 16;
-        W0 = W1 = W2 = W3 = 0;
-      };
-      for (int J = 0; J <= jl; ++J) {
-        uint32_t hE = 0, hO = 0;  // 8-bit fields, <= 64 per tile
-        tau_tile(J, [&](int) { hist_nib(v, Aw, Bw, K, hE, hO); });
-        W0 += hE & 0x00FF00FFu;
-        W1 += (hE >> 8) & 0x00FF00FFu;
-        W2 += hO & 0x00FF00FFu;
-        W3 += (hO >> 8) & 0x00FF00FFu;
-        if ((J & 511) == 511) drain();  // 16-bit fields hold < 1024 tiles of 64
-      }
-      drain();
-    } else {
-      const float An = A1 * (float)nb, Bn = Bf * (float)nb;  // exact: nb is a power of 2
-      for (int J = 0; J <= jl; ++J)
-        tau_tile(J, [&](int) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float y = fmaf(An, v[i], Bn);
-            if (y >= 0.f) {
-              const int b = (int)(__float_as_uint(__fadd_rd(y, 8388608.f)) & 0x3Fu);
-              atomicAdd(&row_cnt[min(b, nb - 1)], 1u);
-            }
-          }
+      if (nb <= 8)
+        hist_sweep<1>(jl, Aw, Bw, K, cnt, [&](int J, uint32_t* hE, uint32_t* hO) {
+          tau_tile(J, [&](int) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
+        });
+      else
+        hist_sweep<2>(jl, Aw, Bw, K, cnt, [&](int J, uint32_t* hE, uint32_t* hO) {
+          tau_tile(J, [&](int) { hist_nib<2>(v, Aw, Bw, K, hE, hO); });
         });
     }
     PASS_MARK(1);
@@ -630,16 +632,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     rs.lo = rs.hi = 0.0;
     rs.steps = 0;
     rs.done = true;
-    if (half == 1 && nb <= 8) {
+    if (half == 1) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) row_cnt[k] = cnt[k];
+      for (int k = 0; k < 16; ++k) row_cnt[k] = cnt[k];
     }
     bar_sync(bar_rg, 256);
     if (half == 0) {
       uint32_t c32[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k)
-        c32[k] = k < nb ? (nb <= 8 ? cnt[k & 7] + row_cnt[k] : row_cnt[k]) : 0u;
+        c32[k] = k < nb ? cnt[k & 15] + row_cnt[k & 15] : 0u;
       double th, lo, hi;
       solve_histogram_dev(c32, nb, g.alpha, th, lo, hi);
       rs.tau = th;

@@ -165,3 +165,19 @@ def test_tc_candidate_lists_and_sweep_fallback(case, monkeypatch):
     assert (rl.tau - r0.tau).abs().max().item() <= 1e-6
     assert torch.equal(rs.tau, r0.tau) and torch.equal(rs.out, r0.out)
     assert torch.equal(rl.mask.words, r0.mask.words)
+
+
+@pytest.mark.parametrize("bins", [2, 4, 16])
+def test_tc_bins(bins):
+    """Histogram widths other than the default 8 (nibble counters in one or two
+    words) against the exact path; bins=32 is outside the TC envelope and runs
+    on the exact path."""
+    q, k, v, do = inputs(100 + bins, 1, 2, 1024, 128, 1.0)
+    _, rx, _ = run(q, k, v, None, "exact", alpha=1.5, causal=True, bins=bins)
+    _, rt, _ = run(q, k, v, None, "tc", alpha=1.5, causal=True, bins=bins)
+    tau_err = (rt.tau - rx.tau).abs().max().item()
+    out_err = (rt.out - rx.out).abs().max().item()
+    print(bins, tau_err, out_err)
+    assert tau_err <= 1e-3 and out_err <= 2e-2
+    with pytest.raises(Exception):
+        run(q, k, v, None, "tc", alpha=1.5, causal=True, bins=32)
