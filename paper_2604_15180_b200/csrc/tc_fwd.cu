@@ -111,12 +111,38 @@ struct FwdSmem {
   static constexpr int OFF_CNT = OFF_RING + NST * TILE;   // [256][16] u32 (HIST combine)
   static constexpr int OFF_PART = OFF_CNT;                // [256][4] f64 (REF combine, reuses)
   static constexpr int OFF_BAR = OFF_CNT + BM * 16 * 4;
-  static constexpr int NBAR = 2 * NST + 16;
+  static constexpr int NBAR = 2 * NST + 18;
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
   static constexpr int OFF_ROW = OFF_MISC + 64;  // [256][4] f32 per-row scratch
   static constexpr int OFF_MASK = OFF_ROW + BM * 4 * 4;
-  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
+  // after the mask ([4][wpr] u32): tile maxima [2][nkt] u32 (ordered encoding),
+  // thresholds [4] u32, activity sets [2 sets][2 row groups][aw] u32
+  __host__ __device__ static int off_tmax(int wpr) { return OFF_MASK + 4 * wpr * 4; }
+  __host__ __device__ static int off_thr(int wpr, int nkt) { return off_tmax(wpr) + 2 * nkt * 4; }
+  __host__ __device__ static int off_act(int wpr, int nkt) { return off_thr(wpr, nkt) + 16; }
+  static size_t bytes(int wpr, int nkt) {
+    return 1024 + off_act(wpr, nkt) + 4 * ((nkt + 31) / 32) * 4 + 64;
+  }
 };
+
+// Order-preserving float <-> u32 (atomicMax / atomicMin on floats in smem).
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+__device__ __forceinline__ float warp_max(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+__device__ __forceinline__ float warp_min(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fminf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
 
 template <int AK>
 __device__ __forceinline__ float p_of(float t, float e0f) {
@@ -238,9 +264,9 @@ __device__ __forceinline__ void hist_nib(const float* v, float2 Aw, float2 Bw, u
 // Whole HIST sweep of one thread (64 keys per tile) for nb <= 8 NW: counts of
 // bins 0..8NW-1 into cnt[].  Per tile the 8-bit fields (<= 64) fold into
 // 16-bit fields, drained to cnt every 512 tiles.
-template <int NW, typename TileFn>
+template <int NW, typename ActFn, typename TileFn>
 __device__ __forceinline__ void hist_sweep(int jl, float2 Aw, float2 Bw, uint32_t K, uint32_t* cnt,
-                                           TileFn&& tile) {
+                                           ActFn&& active, TileFn&& tile) {
   uint32_t W[NW][4];
 #pragma unroll
   for (int w = 0; w < NW; ++w) W[w][0] = W[w][1] = W[w][2] = W[w][3] = 0;
@@ -255,6 +281,7 @@ __device__ __forceinline__ void hist_sweep(int jl, float2 Aw, float2 Bw, uint32_
     }
   };
   for (int J = 0; J <= jl; ++J) {
+    if (!active(J)) continue;
     uint32_t hE[NW], hO[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) hE[w] = hO[w] = 0;
@@ -292,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* o_full = p_full + 2;
   uint64_t* q_full = o_full + 1;
   uint64_t* dec_bar = q_full + 1;
+  uint64_t* plan_bar = dec_bar + 1;  // activity set published (phase 0: HIST, 1: CAND)
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
   volatile uint32_t* s_tmem = misc;  // TMEM base
   volatile uint32_t* s_decision = misc + 1;
@@ -299,6 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* sPart = reinterpret_cast<double*>(smem + L::OFF_PART);
   float* sRow = reinterpret_cast<float*>(smem + L::OFF_ROW);
   uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [4][wpr]
+  const int nkt_ = g.m / BN, aw = (nkt_ + 31) / 32;
+  uint32_t* sTmax = reinterpret_cast<uint32_t*>(smem + L::off_tmax(g.wpr));   // [2][nkt]
+  uint32_t* sThr = reinterpret_cast<uint32_t*>(smem + L::off_thr(g.wpr, nkt_));  // [2 sets][2 rg]
+  uint32_t* sAct = reinterpret_cast<uint32_t*>(smem + L::off_act(g.wpr, nkt_));  // [2][2][aw]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // head-major (the head's K/V stay L2-resident across its CTAs' sweeps),
@@ -327,8 +359,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(o_full, 1);
     mbar_init(q_full, 1);
     mbar_init(dec_bar, 1);
+    mbar_init(plan_bar, 1);
     fence_barrier_init();
   }
+  for (int i = tid; i < 2 * nkt_; i += kThreads) sTmax[i] = 0u;  // < every encoded float
+  if (tid < 4) sThr[tid] = 0xFFFFFFFFu;
   if (warp == 2) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_q);
@@ -339,6 +374,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+
+  // threshold-sweep activity: set s (0: HIST, 1: CAND / REF), row group rg, tile J
+  auto act = [&](int s, int rg, int J) -> bool {
+    return (sAct[(s * 2 + rg) * aw + (J >> 5)] >> (J & 31)) & 1u;
+  };
+  auto act_any = [&](int s, int J) -> bool { return act(s, 0, J) || act(s, 1, J); };
 
   // output-pass activity of row group rg for 128-key tile J (reference blocks
   // (2rg, 2J), (2rg, 2J+1), (2rg+1, 2J), (2rg+1, 2J+1))
@@ -374,19 +415,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++r;
     };
     const int krow0 = bh * g.m;
-    for (int pass = 0; pass < 2; ++pass)
-      for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);
+    for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);  // MAX
+    mbar_wait(plan_bar, 0);
+    for (int J = 0; J <= Jmax; ++J)  // HIST: tiles that can hold z >= 0
+      if (act_any(0, J)) load(&tm_k, krow0 + J * BN);
+    mbar_wait(plan_bar, 1);
     uint32_t dround = 0;
     bool out_now = false;
-    if (a.cand) {  // CAND sweep
-      for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);
+    if (a.cand) {  // CAND sweep: tiles that can hold z > lo - eps
+      for (int J = 0; J <= Jmax; ++J)
+        if (act_any(1, J)) load(&tm_k, krow0 + J * BN);
       mbar_wait(dec_bar, 0);
       dround = 1;
       out_now = *s_decision == DEC_OUT;
     }
     if (!out_now)
       for (uint32_t ref = 0;; ++ref) {
-        for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);
+        for (int J = 0; J <= Jmax; ++J)
+          if (act_any(1, J)) load(&tm_k, krow0 + J * BN);
         mbar_wait(dec_bar, (dround + ref) & 1);
         if (*s_decision == DEC_OUT) break;
       }
@@ -428,10 +474,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                       (c | k) != 0);
     };
     // threshold passes: S double buffered per row group
-    auto s_tile = [&](int J) {
+    auto s_tile = [&](int J, int set) {  // set < 0: every tile (MAX)
       const uint32_t st = wait_ring();
       for (int rg = 0; rg < 2; ++rg) {
-        if (J > rg_jlim[rg]) continue;
+        if (J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J))) continue;
         const uint32_t b = it[rg] & 1;
         {
           PSTAT_T0();
@@ -447,19 +493,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (leader) umma_commit(&empty[st]);
       ++r;
     };
-    for (int pass = 0; pass < 2; ++pass)
-      for (int J = 0; J <= Jmax; ++J) s_tile(J);
+    for (int J = 0; J <= Jmax; ++J) s_tile(J, -1);  // MAX
+    mbar_wait(plan_bar, 0);
+    for (int J = 0; J <= Jmax; ++J)
+      if (act_any(0, J)) s_tile(J, 0);  // HIST
+    mbar_wait(plan_bar, 1);
     uint32_t dround = 0;
     bool out_now = false;
     if (a.cand) {  // CAND sweep
-      for (int J = 0; J <= Jmax; ++J) s_tile(J);
+      for (int J = 0; J <= Jmax; ++J)
+        if (act_any(1, J)) s_tile(J, 1);
       mbar_wait(dec_bar, 0);
       dround = 1;
       out_now = *s_decision == DEC_OUT;
     }
     if (!out_now)
       for (uint32_t ref = 0;; ++ref) {
-        for (int J = 0; J <= Jmax; ++J) s_tile(J);
+        for (int J = 0; J <= Jmax; ++J)
+          if (act_any(1, J)) s_tile(J, 1);
         mbar_wait(dec_bar, (dround + ref) & 1);
         if (*s_decision == DEC_OUT) break;
       }
@@ -590,12 +641,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     long long _pm = clock64();
 #endif
     // ---- pass MAX (attention.cpp:182-195): max of raw dot products, scaled once
+    // Also the per-(row group, tile) maximum raw score, for the activity sets
+    // of the later sweeps (tiles whose every score is below every row's
+    // threshold are skipped there).
     float mraw = -CUDART_INF_F;
-    for (int J = 0; J <= jl; ++J)
+    for (int J = 0; J <= jl; ++J) {
+      float tmx = -CUDART_INF_F;
       tau_tile(J, [&](int) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) mraw = fmaxf(mraw, fmaxf(v[i], v[i + 1]));
+        for (int i = 0; i < 32; i += 2) tmx = fmaxf(tmx, fmaxf(v[i], v[i + 1]));
       });
+      mraw = fmaxf(mraw, tmx);
+      tmx = warp_max(tmx);
+      if (lane == 0) atomicMax(&sTmax[rg * nkt_ + J], f2ord(tmx));
+    }
     sRow[e * 4 + half] = mraw;
     bar_sync(bar_rg, 256);
     mraw = fmaxf(sRow[e * 4], sRow[e * 4 + 1]);
@@ -603,6 +662,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float m_f = a.scale_f * mraw;  // == max(scale * s): rounding is monotone
     const double B = 1.0 - (g.alpha - 1.0) * (double)m_f;  // z = A1*acc + B
     const float Bf = (float)B;
+
+    // activity set 0 (HIST): tile J of row group rg can hold a binned score
+    // (z >= 0 <=> acc >= -B/A1) only if its max reaches the group's lowest
+    // row threshold (lowered by a few ulps: a superset)
+    auto publish_set = [&](int s, float thr) {
+      thr = warp_min(thr);
+      if (lane == 0) atomicMin(&sThr[s * 2 + rg], f2ord(thr));
+      bar_sync(3, kEpi);
+      for (int i = tid - 128; i < 2 * aw; i += kEpi) {
+        const int r = i / aw, w = i - r * aw;
+        const uint32_t th = sThr[s * 2 + r];
+        uint32_t bits = 0;
+        for (int b = 0; b < 32; ++b) {
+          const int J = 32 * w + b;
+          if (J <= rg_jlim[r] && sTmax[r * nkt_ + J] >= th) bits |= 1u << b;
+        }
+        sAct[(s * 2 + r) * aw + w] = bits;
+      }
+      bar_sync(3, kEpi);
+      if (tid == 128) mbar_arrive(plan_bar);
+    };
+    {
+      float th = (float)(-B / (double)A1);
+      th -= 4e-7f * fabsf(th) + 1e-30f;
+      publish_set(0, th);
+    }
 
     // ---- pass HIST (attention.cpp:201-232): counts of min(floor(B z), B-1), z >= 0
     const int nb = g.bins;  // 2..16 on this path (tc_supported)
@@ -617,11 +702,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 Bw = make_float2(bw, bw);
       const uint32_t K = 0u - 4u * (0x4B000000u + (uint32_t)nb);
       if (nb <= 8)
-        hist_sweep<1>(jl, Aw, Bw, K, cnt, [&](int J, uint32_t* hE, uint32_t* hO) {
+        hist_sweep<1>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
+                      [&](int J, uint32_t* hE, uint32_t* hO) {
           tau_tile(J, [&](int) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
         });
       else
-        hist_sweep<2>(jl, Aw, Bw, K, cnt, [&](int J, uint32_t* hE, uint32_t* hO) {
+        hist_sweep<2>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
+                      [&](int J, uint32_t* hE, uint32_t* hO) {
           tau_tile(J, [&](int) { hist_nib<2>(v, Aw, Bw, K, hE, hO); });
         });
     }
@@ -669,12 +756,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     // lists with no further sweeps.  Exact: f, f', f'' and the mask only see
     // z > tau - 1e-9 >= lo - 1e-9, and each listed term is evaluated with the
     // sweep's own formula t = A1*acc + (B - tau).  Overflow -> REF sweeps.
+    // activity set 1 (CAND / REF sweeps): scores below lo - eps contribute to
+    // neither f, f', f'' (tau >= lo) nor the mask (z > tau - 1e-9)
+    if (half == 0) {
+      const float eps_t = 1e-6f * (2.f + fabsf(Bf));  // fp32 slack of z (|B| scale)
+      sRow[e * 4 + 0] = (float)(B - rs.lo) + eps_t;
+    }
+    bar_sync(bar_rg, 256);
+    // z > lo - eps  <=>  acc > theta (A1 > 0), lowered by a few ulps (superset)
+    float theta = -sRow[e * 4 + 0] / A1;
+    theta -= 4e-7f * fabsf(theta) + 1e-30f;
+    publish_set(1, theta);
+
     if (a.cand) {
-      if (half == 0) {
-        const float eps_t = 1e-6f * (2.f + fabsf(Bf));  // fp32 slack of z (|B| scale)
-        sRow[e * 4 + 0] = (float)(B - rs.lo) + eps_t;
-      }
-      bar_sync(bar_rg, 256);
       uint32_t smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       const int cap = a.cand_cap;
@@ -682,13 +776,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool ovf = (int)smid >= a.cand_slots;  // (uniform: one CTA per SM)
       int cnt = 0;
       {
-        // z > lo - eps  <=>  acc > theta (A1 > 0): one compare per score, the
-        // threshold lowered by a few ulps so the raw test is a superset
-        const float Cc = sRow[e * 4 + 0];
-        float theta = -Cc / A1;
-        theta -= 4e-7f * fabsf(theta) + 1e-30f;
         uint32_t ucnt = 0;
         for (int J = 0; J <= jl; ++J) {
+          if (!act(1, rg, J)) continue;
           const uint32_t blk = (uint32_t)(2 * J + half);
           // a tile appends <= 64 entries; warp-uniform (the append votes are warp-collective)
           ovf = __any_sync(0xffffffffu, ovf || (int)ucnt > cap - 64);
@@ -808,6 +898,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float Chi = sRow[e * 4 + 3];
       double f = 0.0, f1 = 0.0, f2 = 0.0, fhi = 0.0;
       for (int J = 0; J <= jl; ++J) {
+        if (!act(1, rg, J)) continue;
         float mx_t = -CUDART_INF_F;
         tau_tile(J, [&](int) {
           float s0, s1, s2, mx;
@@ -932,7 +1023,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D, int AK>
 cudaError_t launch_fwd(const Geom& g, const CUtensorMap& tq, const CUtensorMap& tk,
                        const CUtensorMap& tv, const FwdArgs& a, cudaStream_t st) {
-  const size_t smem = FwdSmem<D>::bytes(g.wpr);
+  const size_t smem = FwdSmem<D>::bytes(g.wpr, g.m / BN);
   auto kern = tc_fwd_kernel<D, AK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
