@@ -23,6 +23,21 @@
 
 namespace adattn_b200 {
 namespace tc {
+#ifdef ADATTN_PIPE_STATS
+// dK/dV kernel: [0] MMA waits on Q/dO stage, [1] MMA waits on p_full, [2]
+// epilogue warp 4 waits on s_full, [3] MMA-warp cycles, [4] units
+__device__ unsigned long long g_bwd_stats[8];
+#define BSTAT_T0() const long long _t0 = clock64()
+#define BSTAT_ADD(i, cond) \
+  if (cond) atomicAdd(&g_bwd_stats[i], (unsigned long long)(clock64() - _t0))
+#else
+#define BSTAT_T0() \
+  do {             \
+  } while (0)
+#define BSTAT_ADD(i, cond) \
+  do {                     \
+  } while (0)
+#endif
 namespace {
 
 constexpr int BM = 256;  // query rows per CTA (delta, dQ)
@@ -772,13 +787,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), st_addr = smem_u32(sSt);
       mbar_wait(kv_full, 0);
       tc_fence_after();
+#ifdef ADATTN_PIPE_STATS
+      const long long t_m0 = clock64();
+#endif
       uint32_t u = 0;
       bool init = false;
       int prev = -1;
       uint32_t prev_st = 0;
       auto grad_mma = [&](uint32_t uu, uint32_t st) {
         const uint32_t b = uu & 1;
-        mbar_wait(&p_full[b], (uu >> 1) & 1);
+        {
+          BSTAT_T0();
+          mbar_wait(&p_full[b], (uu >> 1) & 1);
+          BSTAT_ADD(1, leader);
+        }
         tc_fence_after();
         const uint32_t qb = st_addr + st * L::STAGE;
 #pragma unroll
@@ -799,7 +821,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1)) {
         const uint32_t st = u % KST;
-        mbar_wait(&full[st], (u / KST) & 1);
+        {
+          BSTAT_T0();
+          mbar_wait(&full[st], (u / KST) & 1);
+          BSTAT_ADD(0, leader);
+        }
         tc_fence_after();
         const uint32_t b = u & 1;
         const uint32_t qb = st_addr + st * L::STAGE;
@@ -819,6 +845,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (prev >= 0) grad_mma(u - 1, prev_st);
       if (leader) umma_commit(acc_full);
+#ifdef ADATTN_PIPE_STATS
+      if (leader) {
+        atomicAdd(&g_bwd_stats[3], (unsigned long long)(clock64() - t_m0));
+        atomicAdd(&g_bwd_stats[4], (unsigned long long)u);
+      }
+#endif
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
@@ -835,7 +867,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t st = u % KST, b = u & 1;
       const bool mine = (unit_bits(i) >> ksub) & 1u;
       any |= mine;
-      mbar_wait(&s_full[b], (u >> 1) & 1);
+      {
+        BSTAT_T0();
+        mbar_wait(&s_full[b], (u >> 1) & 1);
+        BSTAT_ADD(2, warp == 4 && lane == 0);
+      }
       tc_fence_after();
       float s[32], dp[32];
       tmem_ld32(tl + b * 128 + half * 32, s);
@@ -995,3 +1031,13 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
 
 }  // namespace tc
 }  // namespace adattn_b200
+
+#ifdef ADATTN_PIPE_STATS
+extern "C" void adattn_b200_bwd_stats(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, adattn_b200::tc::g_bwd_stats, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(adattn_b200::tc::g_bwd_stats, z, sizeof z);
+  }
+}
+#endif

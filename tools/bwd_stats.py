@@ -1,0 +1,24 @@
+"""dK/dV kernel wait fractions (ADATTN_PIPE_STATS build).  python tools/bwd_stats.py B H N"""
+import ctypes as C, os, sys
+sys.path.insert(0, ".")
+import paper_2604_15180_b200._lib as L
+L.LIB_PATH = os.path.abspath("paper_2604_15180_b200/libadattn_b200_stats.so")
+import torch
+import paper_2604_15180_b200 as pa
+from paper_2604_15180_b200 import workloads
+lib = L.load()
+fn = lib.adattn_b200_bwd_stats
+fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+B, H, N = (int(x) for x in sys.argv[1:4])
+q, k, v, do = workloads.gaussian(B, H, N, 128, 1.0, seed=1)
+p = pa.AttentionProblem(q, k, v, alpha=1.5, causal=True)
+r = pa.forward(p); g = pa.backward(p, r, do); torch.cuda.synchronize()
+buf = (C.c_ulonglong * 8)()
+fn(buf, 1)
+g = pa.backward(p, r, do); torch.cuda.synchronize()
+fn(buf, 1)
+st = list(buf)
+mma = max(st[3], 1)
+print("units", st[4], "MMA cycles/unit", mma / max(st[4], 1))
+for i, n in enumerate(["mma_wait_stage(TMA)", "mma_wait_p_full(epi)", "epi_w4_wait_s_full"]):
+    print(f"{n:24s} {st[i] / mma:6.3f} of MMA-warp cycles")

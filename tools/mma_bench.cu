@@ -10,7 +10,9 @@
 using namespace adattn_b200::tc;
 
 // MODE bit0: commit to a side barrier every 8 MMAs; bit1: tcgen05 fence::after
-// every 8; bit2: mbarrier try_wait on an already-complete barrier every 8
+// every 8; bit2: mbarrier try_wait on an already-complete barrier every 8;
+// bit3: B operand MN-major (SW128, 64-element MN chunks 16 KB apart); bit4:
+// alternate two accumulators every 2 MMAs (hi/lo pairs into dV then dK)
 template <int N, bool TS, int NMMA, int MODE = 0>
 __global__ void __launch_bounds__(128, 1) bench(unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -34,7 +36,8 @@ __global__ void __launch_bounds__(128, 1) bench(unsigned long long* out) {
   if (warp == 1) {
     const bool leader = elect_one_sync();
     const uint32_t a_addr = smem_u32(smem), b_addr = smem_u32(smem + 32768);
-    constexpr uint32_t IDESC = idesc_bf16_f32(128, N, false, false);
+    constexpr bool BMN = (MODE & 8) != 0;
+    constexpr uint32_t IDESC = idesc_bf16_f32(128, N, false, BMN);
     const long long t0 = clock64();
     for (int i = 0; i < NMMA; ++i) {
       const int k = i & 3;
@@ -44,15 +47,17 @@ __global__ void __launch_bounds__(128, 1) bench(unsigned long long* out) {
         if (MODE & 4) mbar_wait(&done, 0);
         if (MODE & 2) tc_fence_after();
       }
+      const uint64_t bdesc = BMN ? desc_mnmajor(b_addr + k * 2048, 16384)
+                                 : desc_kmajor(b_addr + k * 32);
+      const uint32_t dt = (MODE & 16) ? tmem + 256 + ((i >> 1) & 1) * 128 : tmem + 256;
       if (leader) {
         if constexpr (TS) {
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256),
-              "r"(tmem + 8 * k), "l"(desc_kmajor(b_addr + k * 32)), "r"(IDESC), "r"(1u));
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dt),
+              "r"(tmem + 8 * k), "l"(bdesc), "r"(IDESC), "r"(1u));
         } else {
-          umma_bf16(tmem + 256, desc_kmajor(a_addr + k * 32), desc_kmajor(b_addr + k * 32), IDESC,
-                    1u);
+          umma_bf16(dt, desc_kmajor(a_addr + k * 32), bdesc, IDESC, 1u);
         }
       }
     }
@@ -99,5 +104,10 @@ int main() {
   run<64, false, 4>("SS N64 +wait/8");
   run<64, false, 7>("SS N64 +all/8");
   run<64, true, 7>("TS N64 +all/8");
+  run<128, false, 8>("SS N128 Bmn");
+  run<128, true, 8>("TS N128 Bmn");
+  run<128, true, 24>("TS N128 Bmn alt2");
+  run<64, false, 8>("SS N64 Bmn");
+  run<64, true, 8>("TS N64 Bmn");
   return 0;
 }
