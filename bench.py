@@ -242,21 +242,29 @@ def main():
     kern = {n: {"ms_avg": a[0] / a[1], "launches": a[1]} for n, a in agg.items()}
     peak_tf, peak_bw, peak_kind = peaks()
     fl_rank = workloads.flops(D, nnz_rank, A_head * B * H)
-    # algorithmic flops per launch of each tensor-core kernel (SURVEY 8(d) per-unit counts)
-    per_launch = {"tc_fwd": fl_rank["f_fwd"], "tc_delta": 4.0 * D * 4096 * nnz_rank,
-                  "tc_dq": 6.0 * D * 4096 * nnz_rank, "tc_dkdv": 8.0 * D * 4096 * nnz_rank}
+    # per launch of each tensor-core kernel: (a) the tcgen05 MMA flops it executes
+    # (roofline numerator, workloads.executed_flops) and (b) the algorithmic count of
+    # SURVEY 8(d) (reference algorithm: 2+R dense passes, no hi/lo halves)
+    exe = workloads.executed_flops(res.mask.words, N, D, causal)
+    per_alg = {"tc_fwd": fl_rank["f_fwd"], "tc_delta": 4.0 * D * 4096 * nnz_rank,
+               "tc_dq": 6.0 * D * 4096 * nnz_rank, "tc_dkdv": 8.0 * D * 4096 * nnz_rank}
     dom = max(kern, key=lambda n: kern[n]["ms_avg"] * kern[n]["launches"]) if kern else None
     roofline = None
-    if dom in per_launch:
-        ach = per_launch[dom] / (kern[dom]["ms_avg"] * 1e-3) / 1e12
+    for n in kern:
+        if n in exe:
+            kern[n]["tflops_executed"] = exe[n] / (kern[n]["ms_avg"] * 1e-3) / 1e12
+            kern[n]["frac_executed"] = kern[n]["tflops_executed"] / peak_tf
+            kern[n]["tflops_alg"] = per_alg[n] / (kern[n]["ms_avg"] * 1e-3) / 1e12
+    if dom in exe:
+        ach = kern[dom]["tflops_executed"]
         roofline = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak_tf,
                     "unit": "TFLOP/s", "frac": ach / peak_tf, "traffic": None,
+                    "basis": "executed tcgen05 MMA flops per launch (incl. hi/lo halves), "
+                             "workloads.executed_flops; tflops_alg = SURVEY 8(d) count",
+                    "achieved_alg": kern[dom]["tflops_alg"],
                     "peak_kind": f"{peak_kind} bf16 burst",
                     "share_of_step": kern[dom]["ms_avg"] * kern[dom]["launches"] /
                     (ms * args.steps)}
-        for n in kern:
-            if n in per_launch:
-                kern[n]["tflops"] = per_launch[n] / (kern[n]["ms_avg"] * 1e-3) / 1e12
     prof_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if roofline and os.path.exists(prof_file):
         try:

@@ -62,3 +62,42 @@ def flops(D: int, nnz: int, addressable: int, ref_passes: int = 3) -> dict:
     f_alg = f_eff + 2.0 * D * 4096 * (2 + ref_passes) * addressable
     f_fwd = 4.0 * D * 4096 * nnz + 2.0 * D * 4096 * (2 + ref_passes) * addressable
     return dict(f_eff=f_eff, f_alg=f_alg, f_fwd=f_fwd)
+
+
+def executed_flops(mask_words, n: int, d: int, causal: bool) -> dict:
+    """Tensor-core flops each kernel actually issues for one problem (all heads),
+    from the 64x64 block mask ([B][H][t_r][wpr] u32) -- the numerator of the
+    per-kernel roofline.  Counts every tcgen05 MMA the
+    kernels issue, including the hi/lo split halves; the forward's threshold
+    sweeps are counted without tile skipping (exact for inputs where no tile
+    is skippable, an upper bound otherwise).
+
+    tc_fwd   3 sweeps (MAX, HIST, CAND) of S over the causal 128x128 tiles of
+             each 128-row group + OUT (S and P V) over active tiles
+    tc_delta S, dP over active (128 rows x 128 keys) tiles
+    tc_dq    S, dP, dQ hi, dQ lo over active (128 x 128) tiles
+    tc_dkdv  S^T, dP^T, dV hi/lo, dK hi/lo over active (128 keys x 64 queries) units
+    """
+    import torch
+    w = mask_words.view(torch.int32)
+    Bh = w.shape[0] * w.shape[1]
+    t_r = w.shape[2]
+    t_c = n // 64
+    bits = ((w.reshape(Bh, t_r, -1, 1) >> torch.arange(32, device=w.device)) & 1).reshape(Bh, t_r, -1)
+    bits = bits[:, :, :t_c].bool()
+    g = bits.reshape(Bh, t_r // 2, 2, t_c // 2, 2).any(dim=4).any(dim=2)  # 128 x 128 tiles
+    u = bits.reshape(Bh, t_r, t_c // 2, 2).any(dim=3)                    # 64 q x 128 keys
+    tile = 2.0 * 128 * 128 * d
+    nr = t_r // 2
+    if causal:
+        J = torch.arange(t_c // 2)
+        rg = torch.arange(nr)
+        sweep_tiles = int(((J[None, :] <= rg[:, None]).sum())) * Bh
+    else:
+        sweep_tiles = nr * (t_c // 2) * Bh
+    act = int(g.sum())
+    units = int(u.sum())
+    return {"tc_fwd": (3 * sweep_tiles + 2 * act) * tile,
+            "tc_delta": 2 * act * tile,
+            "tc_dq": 4 * act * tile,
+            "tc_dkdv": 6 * units * (2.0 * 128 * 64 * d)}
