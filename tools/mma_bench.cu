@@ -11,15 +11,20 @@ using namespace adattn_b200::tc;
 
 // MODE bit0: commit to a side barrier every 8 MMAs; bit1: tcgen05 fence::after
 // every 8; bit2: mbarrier try_wait on an already-complete barrier every 8;
+// bit5: the bit2 wait uses mbarrier.test_wait (non-blocking spin) instead of try_wait;
+// bit6: warps 2-3 stream st.shared.v4 writes into a separate 32 KB region while
+// the MMAs run (the TMA tile arrivals' share of shared-memory bandwidth);
+// bit7 (with bit6): the side warps stream tcgen05.ld of 32 columns instead of smem writes
 // bit3: B operand MN-major (SW128, 64-element MN chunks 16 KB apart); bit4:
 // alternate two accumulators every 2 MMAs (hi/lo pairs into dV then dK)
 template <int N, bool TS, int NMMA, int MODE = 0>
-__global__ void __launch_bounds__(128, 1) bench(unsigned long long* out) {
+__global__ void __launch_bounds__(256, 1) bench(unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar, side, done;
   __shared__ uint32_t tbase;
+  __shared__ volatile uint32_t stop;
   const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += 256) reinterpret_cast<uint32_t*>(smem)[i] = 0;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_init(&side, 1);
@@ -28,6 +33,7 @@ __global__ void __launch_bounds__(128, 1) bench(unsigned long long* out) {
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(&tbase, 512);
+  if (threadIdx.x == 0) stop = 0;
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -44,7 +50,20 @@ __global__ void __launch_bounds__(128, 1) bench(unsigned long long* out) {
       if ((i & 7) == 0 && i) {
         if (MODE & 1)
           if (leader) umma_commit(&side);
-        if (MODE & 4) mbar_wait(&done, 0);
+        if (MODE & 4) {
+          if (MODE & 32) {
+            uint32_t ok = 0;
+            while (!ok)
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                  "selp.u32 %0, 1, 0, p;\n\t}"
+                  : "=r"(ok)
+                  : "r"(smem_u32(&done)), "r"(0u)
+                  : "memory");
+          } else {
+            mbar_wait(&done, 0);
+          }
+        }
         if (MODE & 2) tc_fence_after();
       }
       const uint64_t bdesc = BMN ? desc_mnmajor(b_addr + k * 2048, 16384)
@@ -65,6 +84,31 @@ __global__ void __launch_bounds__(128, 1) bench(unsigned long long* out) {
     mbar_wait(&bar, 0);
     const long long t1 = clock64();
     if (leader) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+    stop = 1;
+  } else if ((MODE & 64) && warp >= 2 && (warp < 4 || (MODE & 512))) {
+    unsigned long long nbytes = 0;
+    if (MODE & 128) {  // warps 2,3 read TMEM lanes 64-127, columns 0..127 (not the accumulator)
+      float acc = 0.f;
+      while (!stop) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + ((MODE & 256) ? 256 + r * 32 : r * 32), v);
+          tmem_wait_ld();
+          acc += v[0] + v[31];
+        }
+        nbytes += 4 * 32 * 32 * 4 * ((MODE & 512) ? 6 : 2);  // side warps
+      }
+      if (acc == 12345.f) out[0] = 0;
+    } else {
+      const uint32_t base = smem_u32(smem + 65536) + (threadIdx.x - 64) * 16;
+      while (!stop) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) st_shared_v4(base + r * 1024 % 32768, r, r, r, r);
+        nbytes += 8 * 16 * 64;
+      }
+    }
+    if (threadIdx.x == 64) out[148 + blockIdx.x] = nbytes;
   }
   tc_fence_before();
   __syncthreads();
@@ -75,20 +119,22 @@ template <int N, bool TS, int MODE = 0>
 void run(const char* name) {
   constexpr int NMMA = 4096;
   unsigned long long* d;
-  cudaMalloc(&d, 148 * 8);
+  cudaMalloc(&d, 2 * 148 * 8);
+  cudaMemset(d, 0, 2 * 148 * 8);
   auto k = bench<N, TS, NMMA, MODE>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  k<<<148, 128, 100 * 1024>>>(d);
-  k<<<148, 128, 100 * 1024>>>(d);
+  k<<<148, 256, 100 * 1024>>>(d);
+  k<<<148, 256, 100 * 1024>>>(d);
   cudaError_t e = cudaDeviceSynchronize();
-  unsigned long long h[148];
+  unsigned long long h[2 * 148];
   cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int i = 0; i < 148; ++i) avg += (double)h[i] / 148.0;
   const double cyc = avg / NMMA;
   const double macs = 128.0 * N * 16;
-  printf("%-18s %s  cycles/MMA %7.1f  MAC/cycle/SM %7.0f  (%.0f%% of 4096)\n", name,
-         e ? cudaGetErrorString(e) : "ok", cyc, macs / cyc, 100.0 * macs / cyc / 4096.0);
+  printf("%-18s %s  cycles/MMA %7.1f  MAC/cycle/SM %7.0f  (%.0f%% of 4096)  side-writes %.1f B/cycle\n", name,
+         e ? cudaGetErrorString(e) : "ok", cyc, macs / cyc, 100.0 * macs / cyc / 4096.0,
+         (double)h[148] / avg);
   cudaFree(d);
 }
 
@@ -108,6 +154,17 @@ int main() {
   run<128, true, 8>("TS N128 Bmn");
   run<128, true, 24>("TS N128 Bmn alt2");
   run<64, false, 8>("SS N64 Bmn");
+  run<128, false, 64>("SS N128 +smemwr");
+  run<128, false, 192>("SS N128 +tmemld");
+  run<128, true, 192>("TS N128 +tmemld");
+  run<128, false, 192 + 512>("SS N128 +tmemld6w");
+  run<128, false, 192 + 512 + 256>("SS N128 +tmemld6w-acc");
+  run<128, true, 64>("TS N128 +smemwr");
+  run<64, true, 64>("TS N64 +smemwr");
+  run<128, false, 4>("SS N128 +wait/8");
+  run<128, false, 36>("SS N128 +testwait/8");
+  run<128, true, 4>("TS N128 +wait/8");
+  run<128, true, 36>("TS N128 +testwait/8");
   run<64, true, 8>("TS N64 Bmn");
   return 0;
 }

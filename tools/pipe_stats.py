@@ -18,7 +18,7 @@ q, k, v, do = (workloads.gaussian(B, H, N, 128, 1.0, seed=1) if beta is None
                else workloads.anchored(B, H, N, 128, beta, True, seed=1))
 p = pa.AttentionProblem(q, k, v, alpha=alpha, causal=True)
 r = pa.forward(p); torch.cuda.synchronize()
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 48)()
 fn(buf, 1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); r = pa.forward(p); e1.record(); e1.synchronize()
@@ -33,3 +33,12 @@ ph = ["MAX", "HIST", "CAND sweep", "list REF+mask", "REF sweeps", "OUT (S+PV)", 
 tot = sum(st[8:15]) or 1
 for i, n in enumerate(ph):
     print(f"phase {n:16s} {100.0 * st[8 + i] / tot:5.1f}%")
+for s, n in enumerate(["MAX", "HIST", "CAND", "REF/decision", "OUT (S+PV)"]):
+    cyc, tiles = st[16 + 2 * s], st[17 + 2 * s]
+    ideal = 1024 if s == 4 else 512
+    if tiles:
+        print(f"MMA sweep {n:13s} cycles/rg-tile {cyc / tiles:8.1f}  (ideal {ideal}) tiles {tiles}"
+              f"  ring-wait/tile {st[32 + 2 * s] / tiles:7.1f}  S-buffer-wait/tile {st[33 + 2 * s] / tiles:7.1f}")
+    else:
+        print(f"MMA sweep {n:13s} cycles {cyc}")
+print("MMA issue+commit cycles per rg-tile: MAX", st[40] / max(st[17], 1), "HIST+CAND", st[41] / max(st[19] + st[21], 1))
