@@ -43,7 +43,7 @@ namespace {
 constexpr int BM = 256;  // query rows per CTA (delta, dQ)
 constexpr int BN = 64;   // keys per tile
 constexpr int NST = 4;
-constexpr int kThreads = 384;
+constexpr int kThreads = 320;  // 8 epilogue warps, producer, MMA issuer
 constexpr int kEpi = 256;
 
 struct BwdArgs {
@@ -210,7 +210,7 @@ struct DeltaSmem {
   static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
 };
 
-constexpr int kDeltaThreads = 128 + 512;
+constexpr int kDeltaThreads = 512 + 64;  // 16 epilogue warps, producer, MMA issuer
 
 template <int D, int AK>
 __global__ void __launch_bounds__(kDeltaThreads, 1)
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
     mbar_init(q_full, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
+  if (warp == 16) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
     return -1;
   };
 
-  if (warp == 0) {
+  if (warp == 16) {  // TMA producer
     const bool leader = elect_one_sync();
     const int qrow = bh * g.n + row0;
     if (leader) mbar_expect_tx(q_full, 2 * L::QB);
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
       load(&tm_k, krow0 + J * DBN);
       load(&tm_v, krow0 + J * DBN);
     }
-  } else if (warp == 1) {
+  } else if (warp == 17) {  // MMA issuer (highest warp id: scheduler priority)
     const bool leader = elect_one_sync();
     constexpr uint32_t IDESC_S = idesc_bf16_f32(128, DBN, false, false);
     const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ring_addr = smem_u32(sRing);
@@ -341,8 +341,8 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
       if (leader) umma_commit(&empty[vst]);
       r += 2;
     }
-  } else if (warp >= 4) {
-    const int ew = warp - 4;             // 0..15
+  } else if (warp < 16) {  // epilogue (warp % 4 = TMEM lane quarter)
+    const int ew = warp;             // 0..15
     const int rg = ew >> 3;              // row group
     const int half = (ew >> 2) & 1;      // keys 64*half .. +63 of each tile
     const int lq = warp & 3;             // TMEM lane quarter
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc(tmem, 512);
+  if (warp == 16) tmem_dealloc(tmem, 512);
 }
 
 // ===================================================================== dQ
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(q_full, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
+  if (warp == 8) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return -1;
   };
 
-  if (warp == 0) {
+  if (warp == 8) {  // TMA producer
     const bool leader = elect_one_sync();
     const int qrow = bh * g.n + row0;
     if (leader) mbar_expect_tx(q_full, 2 * L::QB);
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < NCH; ++c)
         if (leader) tma_load_2d(sV + vs * L::TILE + c * DBN * 128, &tm_v, &vfull[vs], c * 64, krow0 + J * DBN);
     }
-  } else if (warp == 1) {
+  } else if (warp == 9) {  // MMA issuer (highest warp id: scheduler priority)
     const bool leader = elect_one_sync();
     constexpr uint32_t IDESC_S = idesc_bf16_f32(128, DBN, false, false);
     constexpr uint32_t IDESC_DQ = idesc_bf16_f32(128, D, false, true);
@@ -583,8 +583,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (t > 0) dq_mma(t - 1);
     if (leader) umma_commit(acc_full);
-  } else if (warp >= 4) {
-    const int half = (warp - 4) >> 2;  // keys 64*half .. +63 of each tile
+  } else if (warp < 8) {  // epilogue (warp % 4 = TMEM lane quarter)
+    const int half = warp >> 2;  // keys 64*half .. +63 of each tile
     const int lq = warp & 3;
     const int e = lq * 32 + lane;      // local query row 0..127
     const int rb = e >> 6;
@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc(tmem, 512);
+  if (warp == 8) tmem_dealloc(tmem, 512);
 }
 
 // ================================================================= dK / dV
@@ -738,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(acc_full, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
+  if (warp == 8) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return -1;
   };
 
-  if (warp == 0) {
+  if (warp == 8) {  // TMA producer
     {
       const bool leader = elect_one_sync();
       const int krow = bh * g.m + key0;
@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++r;
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 9) {  // MMA issuer (highest warp id: scheduler priority)
     {
       const bool leader = elect_one_sync();
       constexpr uint32_t IDESC_S = idesc_bf16_f32(128, QT, false, false);
@@ -852,8 +852,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
 #endif
     }
-  } else if (warp >= 4) {
-    const int ew = warp - 4;
+  } else if (warp < 8) {  // epilogue (warp % 4 = TMEM lane quarter)
+    const int ew = warp;
     const int half = ew >> 2;          // query columns 32*half .. +31
     const int lq = warp & 3;
     const int key = lq * 32 + lane;    // 0..127 within the CTA
@@ -870,7 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       {
         BSTAT_T0();
         mbar_wait(&s_full[b], (u >> 1) & 1);
-        BSTAT_ADD(2, warp == 4 && lane == 0);
+        BSTAT_ADD(2, warp == 0 && lane == 0);
       }
       tc_fence_after();
       float s[32], dp[32];
@@ -931,7 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc(tmem, 512);
+  if (warp == 8) tmem_dealloc(tmem, 512);
 }
 
 template <typename K>
