@@ -863,6 +863,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       PASS_MARK(2);
       const bool ovf_any = bar_red_or(4, kEpi, ovf);
       if (!ovf_any) {
+        // The K ring is idle until the decision (producer and MMA warps wait on
+        // dec_bar): stage each thread's first `lcap` listed scores there
+        // ([i][thread] layout, conflict-free) so the refinement rounds read
+        // shared memory instead of waiting on L2 per entry.
+        float* sl = reinterpret_cast<float*>(sRing);
+        constexpr int lcap = NST * L::TILE / (kEpi * 4);
+        const int ns = cnt < lcap ? cnt : lcap;
+        for (int i0 = 0; i0 < ns; i0 += 8) {
+          uint32_t tmp[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) tmp[j] = i0 + j < ns ? lst[i0 + j].x : 0u;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (i0 + j < ns) sl[(i0 + j) * kEpi + tid] = __uint_as_float(tmp[j]);
+        }
         // refinement rounds on the lists (same RowSolve / row_step as the sweeps)
         for (;;) {
           bar_sync(bar_rg, 256);  // C / Chi published
@@ -870,7 +885,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float Chi = sRow[e * 4 + 3];
           double f = 0.0, f1 = 0.0, f2 = 0.0, fhi = 0.0;
           for (int i = 0; i < cnt; ++i) {
-            const float acc = __uint_as_float(lst[i].x);
+            const float acc = i < ns ? sl[i * kEpi + tid] : __uint_as_float(lst[i].x);
             const float t = fmaf(A1, acc, C);
             if (t > 0.f) {
               if constexpr (AK == AK15) {
@@ -923,12 +938,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         bar_sync(3, kEpi);
         {
           const float C = sRow[e * 4 + 2];
-          for (int i = 0; i < cnt; ++i) {
-            const uint2 en = lst[i];
-            if (fmaf(A1, __uint_as_float(en.x), C) > -1e-9f)
-              atomicOr(&smask[rb * wpr + (en.y >> 5)], 1u << (en.y & 31));
+          for (int i0 = 0; i0 < cnt; i0 += 8) {
+            uint2 en[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) en[j] = i0 + j < cnt ? lst[i0 + j] : make_uint2(0xFF800000u, 0u);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (fmaf(A1, __uint_as_float(en[j].x), C) > -1e-9f)
+                atomicOr(&smask[rb * wpr + (en[j].y >> 5)], 1u << (en[j].y & 31));
           }
         }
+        fence_proxy_async_smem();  // generic writes to the ring before its next TMA loads
         list_ok = true;
       }
       PASS_MARK(3);
