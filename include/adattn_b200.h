@@ -49,7 +49,8 @@ enum {
   ADATTN_ERR_INVALID = 1,
   ADATTN_ERR_UNSUPPORTED = 4,
   ADATTN_ERR_CUDA = 5,
-  ADATTN_ERR_WORKSPACE = 6
+  ADATTN_ERR_WORKSPACE = 6,
+  ADATTN_ERR_IO = 7
 };
 
 /* element types */
@@ -148,6 +149,30 @@ uint64_t adattn_b200_launch_count(void);
  * the number recorded and clears the log. */
 void adattn_b200_profile_enable(int on);
 int adattn_b200_profile_read(char* names, size_t names_len, double* ms, int max);
+
+/* ---- I/O around the hot path ----------------------------
+ * ATN1 tensor files, replacing adattn::save_tensor / load_tensor
+ * (tensor_io.hpp:28-29, tensor_io.cpp:39-112): dtype 0 = f32, 1 = f64,
+ * rank 1..3.  Errors: ADATTN_ERR_INVALID (bad arguments, the reference's
+ * std::invalid_argument) or ADATTN_ERR_IO (parse / file errors, the
+ * reference's std::runtime_error, message with the byte offset) and
+ * adattn_b200_io_last_error().  tensor_load with values == NULL only fills
+ * dtype, rank, dims and count. */
+int adattn_b200_tensor_save(const char* path, int dtype, int rank, const uint32_t* dims,
+                            const double* values);
+int adattn_b200_tensor_load(const char* path, int* dtype, int* rank, uint32_t* dims,
+                            double* values, size_t capacity, size_t* count);
+const char* adattn_b200_io_last_error(void);
+
+/* `atn attn`'s inputs (atn_main.cpp:227-232): Q = qscale N(0,1), then K, V and
+ * dO ~ N(0,1), [n][d] row-major, drawn in that order from Xoshiro256pp(seed)
+ * (rng.hpp:25-72; include/adattn_b200/rng.hpp). */
+void adattn_b200_attn_inputs(uint64_t seed, int32_t n, int32_t d, double qscale, double* q,
+                             double* k, double* v, double* dout);
+/* The generator's raw stream (pinning): n_next next() values and n_gauss
+ * gaussian() values, each from a fresh Xoshiro256pp(seed). */
+void adattn_b200_xoshiro(uint64_t seed, uint64_t* next_out, size_t n_next, double* gauss_out,
+                         size_t n_gauss);
 
 #ifdef __cplusplus
 }

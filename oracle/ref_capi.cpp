@@ -14,6 +14,7 @@
 #include "adattn/histogram.hpp"
 #include "adattn/hybrid.hpp"
 #include "adattn/rng.hpp"
+#include "adattn/tensor_io.hpp"
 #include "adattn_oracle.h"
 
 namespace {
@@ -223,6 +224,33 @@ int ref_hybrid_steps(const double* z, int n, double alpha, double init, double l
     if (final_tau) *final_tau = t.final_tau;
   });
   return steps;
+}
+
+// The reference's ATN1 tensor I/O (tensor_io.cpp:39-112), for byte-level
+// comparison with the product's csrc/io.cu.  Returns 0, or 1 with the
+// exception message in ref_last_error().
+int ref_save_tensor(const char* path, int dtype, int rank, const uint32_t* dims,
+                    const double* values) {
+  return guarded([&] {
+    adattn::Tensor t;
+    t.dtype = adattn::Dtype(dtype);
+    t.dims.assign(dims, dims + rank);
+    t.values.assign(values, values + t.count());
+    adattn::save_tensor(t, path);
+  });
+}
+
+int ref_load_tensor(const char* path, int* dtype, int* rank, uint32_t* dims, double* values,
+                    size_t capacity, size_t* count) {
+  return guarded([&] {
+    const adattn::Tensor t = adattn::load_tensor(path);
+    *dtype = int(t.dtype);
+    *rank = int(t.dims.size());
+    for (size_t i = 0; i < t.dims.size(); ++i) dims[i] = t.dims[i];
+    *count = t.values.size();
+    if (values && capacity >= t.values.size())
+      std::memcpy(values, t.values.data(), t.values.size() * sizeof(double));
+  });
 }
 
 }  // extern "C"

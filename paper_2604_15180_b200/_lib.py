@@ -18,6 +18,7 @@ ADATTN_ERR_INVALID = 1
 ADATTN_ERR_UNSUPPORTED = 4
 ADATTN_ERR_CUDA = 5
 ADATTN_ERR_WORKSPACE = 6
+ADATTN_ERR_IO = 7
 
 F32, BF16, F64 = 0, 1, 2
 PATH_AUTO, PATH_EXACT, PATH_TC = 0, 1, 2
@@ -30,6 +31,8 @@ EXPORTS = (
     "adattn_b200_backward", "adattn_b200_stats", "adattn_b200_mask_sparsity",
     "adattn_b200_run_host",
     "adattn_b200_launch_count", "adattn_b200_profile_enable", "adattn_b200_profile_read",
+    "adattn_b200_tensor_save", "adattn_b200_tensor_load", "adattn_b200_io_last_error",
+    "adattn_b200_attn_inputs", "adattn_b200_xoshiro",
 )
 
 
@@ -95,6 +98,17 @@ def load() -> C.CDLL:
         lib.adattn_b200_profile_enable.restype = None
         lib.adattn_b200_profile_read.argtypes = [C.c_char_p, C.c_size_t,
                                                  C.POINTER(C.c_double), C.c_int]
+        dp, u32p = C.POINTER(C.c_double), C.POINTER(C.c_uint32)
+        lib.adattn_b200_tensor_save.argtypes = [C.c_char_p, C.c_int, C.c_int, u32p, dp]
+        lib.adattn_b200_tensor_load.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                                u32p, dp, C.c_size_t, C.POINTER(C.c_size_t)]
+        lib.adattn_b200_io_last_error.restype = C.c_char_p
+        lib.adattn_b200_attn_inputs.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_double,
+                                                dp, dp, dp, dp]
+        lib.adattn_b200_attn_inputs.restype = None
+        lib.adattn_b200_xoshiro.argtypes = [C.c_uint64, C.POINTER(C.c_uint64), C.c_size_t, dp,
+                                            C.c_size_t]
+        lib.adattn_b200_xoshiro.restype = None
         if lib.adattn_b200_abi_version() != 1:
             raise RuntimeError("libadattn_b200.so ABI mismatch")
         _lib = lib
