@@ -150,6 +150,44 @@ uint64_t adattn_b200_launch_count(void);
 void adattn_b200_profile_enable(int on);
 int adattn_b200_profile_read(char* names, size_t names_len, double* ms, int max);
 
+/* ---- Row-wise thresholds on materialised scores ----
+ * The paper's inference variant and the reference's
+ * per-vector solver (atn solve / bench-solver): for each of `rows` score rows
+ * of length n (in_dtype F32 / BF16 / F64; mask[r*n+j] != 0 excludes an entry),
+ * center_scores (entmax.cpp:22-57) then
+ *   ADATTN_ROWS_HISTOGRAM_HYBRID: build_histogram + solve_histogram +
+ *     refine_bracket, hybrid_solve from tau_h (histogram.cpp, hybrid.cpp:35-106);
+ *   ADATTN_ROWS_HYBRID: hybrid_solve from the midpoint of [0, 1 - n^(1-alpha)];
+ *   ADATTN_ROWS_BISECTION: solve_bisection (entmax.cpp:128-164).
+ * Outputs (device pointers; all but tau nullable): tau on the centred scale
+ * (best iterate), residual f(tau), iterations (trace length - 1, or the
+ * bisection count), converged, probabilities [rows][n] fp32
+ * (entmax_apply), trace [rows][trace_len] of iterates (iteration 0 = start;
+ * the last iterate carried forward).  fp64 arithmetic; errors as the
+ * reference's exceptions (ADATTN_ERR_INVALID + message). */
+typedef enum {
+  ADATTN_ROWS_HISTOGRAM_HYBRID = 0,
+  ADATTN_ROWS_HYBRID = 1,
+  ADATTN_ROWS_BISECTION = 2
+} adattn_rows_method;
+
+typedef struct {
+  int64_t rows;
+  int32_t n;
+  int32_t in_dtype;
+  double alpha;
+  int32_t bins;      /* 2..32, histogram method */
+  int32_t max_iters;
+  double tol;
+  int32_t method;    /* adattn_rows_method */
+  int32_t trace_len; /* 0: no trace */
+} adattn_rows_problem;
+
+int adattn_b200_entmax_rows(const adattn_rows_problem* p, const void* scores,
+                            const uint8_t* mask, double* tau, double* residual,
+                            int32_t* iterations, int32_t* converged, float* probs,
+                            double* trace, void* stream);
+
 /* ---- I/O around the hot path ----------------------------
  * ATN1 tensor files, replacing adattn::save_tensor / load_tensor
  * (tensor_io.hpp:28-29, tensor_io.cpp:39-112): dtype 0 = f32, 1 = f64,

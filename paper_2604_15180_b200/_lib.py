@@ -32,7 +32,7 @@ EXPORTS = (
     "adattn_b200_run_host",
     "adattn_b200_launch_count", "adattn_b200_profile_enable", "adattn_b200_profile_read",
     "adattn_b200_tensor_save", "adattn_b200_tensor_load", "adattn_b200_io_last_error",
-    "adattn_b200_attn_inputs", "adattn_b200_xoshiro",
+    "adattn_b200_attn_inputs", "adattn_b200_xoshiro", "adattn_b200_entmax_rows",
 )
 
 
@@ -52,6 +52,15 @@ class Stats(C.Structure):
     _fields_ = [("block_sparsity", C.c_double), ("blocks_visited_fwd", C.c_uint64),
                 ("blocks_visited_bwd", C.c_uint64), ("flushes", C.c_uint64),
                 ("addressable_blocks", C.c_uint64), ("active_blocks", C.c_uint64)]
+
+
+class RowsProblem(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("n", C.c_int32), ("in_dtype", C.c_int32),
+                ("alpha", C.c_double), ("bins", C.c_int32), ("max_iters", C.c_int32),
+                ("tol", C.c_double), ("method", C.c_int32), ("trace_len", C.c_int32)]
+
+
+ROWS_HISTOGRAM_HYBRID, ROWS_HYBRID, ROWS_BISECTION = 0, 1, 2
 
 
 class AdattnError(RuntimeError):
@@ -109,6 +118,8 @@ def load() -> C.CDLL:
         lib.adattn_b200_xoshiro.argtypes = [C.c_uint64, C.POINTER(C.c_uint64), C.c_size_t, dp,
                                             C.c_size_t]
         lib.adattn_b200_xoshiro.restype = None
+        lib.adattn_b200_entmax_rows.argtypes = [C.POINTER(RowsProblem), vp, vp, vp, vp, vp, vp,
+                                                vp, vp, vp]
         if lib.adattn_b200_abi_version() != 1:
             raise RuntimeError("libadattn_b200.so ABI mismatch")
         _lib = lib

@@ -129,6 +129,51 @@ def cmd_attn(a):
     return 0
 
 
+def cmd_solve(a):
+    """cmd_solve (atn_main.cpp:139-200) on the GPU row solver (one row)."""
+    import torch
+
+    from . import rows, tensor_io
+    vals, _ = tensor_io.load_tensor(a.input)
+    if vals.ndim != 1:
+        raise ValueError("solve: input must be a rank-1 tensor")
+    if a.method == "exact":
+        if a.alpha not in (1.5, 2.0):
+            raise ValueError("solve: --method exact needs alpha 1.5 or 2.0")
+        from . import dense
+        s = torch.from_numpy(vals).cuda().unsqueeze(0)
+        mx = s.amax(dim=1, keepdim=True)
+        z = torch.where(s == mx, torch.ones_like(s), (a.alpha - 1.0) * (s - mx) + 1.0)
+        tau = float(dense._tau_exact(z, a.alpha)[0])
+        t = z[0] - tau
+        p = torch.where(t > 0, t.clamp(min=0) ** (1.0 / (a.alpha - 1.0)), torch.zeros_like(t))
+        out = {"alpha": a.alpha, "converged": True, "iterations": 0, "method": a.method,
+               "probabilities": p.cpu().tolist(), "residual": float(p.sum()) - 1.0, "tau": tau}
+    else:
+        s = torch.from_numpy(vals).cuda().unsqueeze(0)
+        r = rows.entmax_rows(s, a.alpha, a.method, a.bins, a.max_iters, a.tol, probs=True,
+                             trace_len=a.max_iters + 1 if a.method != "bisection" else 0)
+        out = {"alpha": a.alpha, "converged": bool(r.converged[0]), "method": a.method,
+               "iterations": int(r.iterations[0]), "probabilities": r.probs[0].double().cpu().tolist(),
+               "residual": float(r.residual[0]), "tau": float(r.tau[0])}
+        if r.trace is not None:
+            out["trace"] = [float(x) for x in r.trace[0][: int(r.iterations[0]) + 1].cpu()]
+    print(json.dumps(out, indent=2, sort_keys=True))
+    return 0
+
+
+def cmd_bench_solver(a):
+    """cmd_bench_solver (atn_main.cpp:204-220): one record per (method, iteration)."""
+    from . import rows
+    bins = [int(x) for x in a.bins_list.split(",") if x]
+    recs = [{"experiment": "bench-solver", "seed": a.seed,
+             "params": {"n": a.n, "alpha": a.alpha, "runs": a.runs, "method": m, "iteration": k},
+             "metrics": {"mae": mae}}
+            for m, k, mae in rows.solver_bench(a.n, a.alpha, bins, a.runs, a.seed, a.iters)]
+    emit_records(recs, a.out, ["n", "alpha", "runs", "method", "iteration"], ["mae"])
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="atn", description="AdaSplash-2 entmax attention tools (B200)")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -141,6 +186,22 @@ def main(argv=None) -> int:
     g.add_argument("--out", required=True)
     d = sub.add_parser("dump", help="print tensor header and summary stats")
     d.add_argument("file")
+    s = sub.add_parser("solve", help="threshold solve on one score vector")
+    s.add_argument("--alpha", type=float, required=True)
+    s.add_argument("--input", required=True)
+    s.add_argument("--method", default="histogram+hybrid",
+                   choices=["exact", "bisection", "hybrid", "histogram+hybrid"])
+    s.add_argument("--bins", type=int, default=8)
+    s.add_argument("--tol", type=float, default=1e-6)
+    s.add_argument("--max-iters", type=int, default=50)
+    b = sub.add_parser("bench-solver", help="solver convergence benchmark")
+    b.add_argument("--n", type=int, default=4096)
+    b.add_argument("--alpha", type=float, default=1.5)
+    b.add_argument("--bins-list", default="4,8,16")
+    b.add_argument("--runs", type=int, default=10)
+    b.add_argument("--seed", type=int, default=1)
+    b.add_argument("--iters", type=int, default=10)
+    b.add_argument("--out", default="json", choices=["json", "csv"])
     t = sub.add_parser("attn", help="tiled attention round trip")
     t.add_argument("--n", type=int, default=256)
     t.add_argument("--d", type=int, default=64)
@@ -158,7 +219,8 @@ def main(argv=None) -> int:
     t.add_argument("--dtype", default="f32", choices=["f32", "f64", "bf16"])
     a = ap.parse_args(argv)
     try:
-        return {"gen": cmd_gen, "dump": cmd_dump, "attn": cmd_attn}[a.cmd](a)
+        return {"gen": cmd_gen, "dump": cmd_dump, "attn": cmd_attn, "solve": cmd_solve,
+                "bench-solver": cmd_bench_solver}[a.cmd](a)
     except Exception as e:  # noqa: BLE001 -- the reference's catch-all (atn_main.cpp:416-419)
         sys.stderr.write(json.dumps({"error": str(e)}) + "\n")
         return 1

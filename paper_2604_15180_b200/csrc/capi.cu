@@ -16,6 +16,13 @@
 #include "tc.cuh"
 
 namespace adattn_b200 {
+cudaError_t entmax_rows(const adattn_rows_problem& p, const void* scores, const uint8_t* mask,
+                        double* tau, double* residual, int32_t* iterations, int32_t* converged,
+                        float* probs, double* trace, cudaStream_t st, int* row_err);
+const char* rows_error_message(int code);
+}  // namespace adattn_b200
+
+namespace adattn_b200 {
 
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -395,6 +402,36 @@ int adattn_b200_stats(const adattn_problem* p, const uint32_t* mask, adattn_stat
   int rc = check(p, &g);
   if (rc) return rc;
   return stats_impl(g, mask, out, (cudaStream_t)stream);
+}
+
+int adattn_b200_entmax_rows(const adattn_rows_problem* p, const void* scores,
+                            const uint8_t* mask, double* tau, double* residual,
+                            int32_t* iterations, int32_t* converged, float* probs,
+                            double* trace, void* stream) {
+  if (!p || !scores || !tau) return fail(ADATTN_ERR_INVALID, "entmax_rows: null argument");
+  if (!(p->alpha > 1.0)) return fail(ADATTN_ERR_INVALID, "center_scores: alpha must exceed 1");
+  if (p->n < 1) return fail(ADATTN_ERR_INVALID, "center_scores: empty score vector");
+  if (p->rows < 1 || p->rows > 0x7fffffffLL)
+    return fail(ADATTN_ERR_INVALID, "entmax_rows: rows must be in [1, 2^31)");
+  if (p->in_dtype != ADATTN_F32 && p->in_dtype != ADATTN_BF16 && p->in_dtype != ADATTN_F64)
+    return fail(ADATTN_ERR_INVALID, "entmax_rows: unknown input dtype");
+  if (p->trace_len < 0) return fail(ADATTN_ERR_INVALID, "entmax_rows: negative trace_len");
+  if (p->method == ADATTN_ROWS_HISTOGRAM_HYBRID) {
+    if (p->bins < 2) return fail(ADATTN_ERR_INVALID, "build_histogram: bins must be >= 2");
+    if (p->bins > 32)
+      return fail(ADATTN_ERR_UNSUPPORTED, "entmax_rows: bins > 32 is outside the GPU envelope");
+  } else if (p->method == ADATTN_ROWS_BISECTION) {
+    if (p->max_iters < 1)
+      return fail(ADATTN_ERR_INVALID, "solve_bisection: max_iters must be positive");
+  } else if (p->method != ADATTN_ROWS_HYBRID) {
+    return fail(ADATTN_ERR_INVALID, "entmax_rows: unknown method");
+  }
+  int row_err = 0;
+  const cudaError_t e = entmax_rows(*p, scores, mask, tau, residual, iterations, converged, probs,
+                                    trace, (cudaStream_t)stream, &row_err);
+  if (e) return fail(ADATTN_ERR_CUDA, std::string("entmax_rows: ") + cudaGetErrorString(e));
+  if (row_err) return fail(ADATTN_ERR_INVALID, rows_error_message(row_err));
+  return ADATTN_OK;
 }
 
 int adattn_b200_mask_sparsity(const uint32_t* mask, int32_t heads, int32_t t_r, int32_t t_c,
