@@ -222,8 +222,9 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
   constexpr int NCH = D / 64;
   const Geom& g = a.g;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-aligned base that stays in the shared address space (LDS/STS, not
+  // generic LD/ST, for every access through it)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem + L::OFF_Q;
   uint8_t* sDO = smem + L::OFF_DO;
   uint8_t* sRing = smem + L::OFF_RING;
@@ -445,8 +446,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int NCH = D / 64;
   const Geom& g = a.g;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-aligned base that stays in the shared address space (LDS/STS, not
+  // generic LD/ST, for every access through it)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem + L::OFF_Q;
   uint8_t* sDO = smem + L::OFF_DO;
   uint8_t* sK = smem + L::OFF_KR;
@@ -693,8 +695,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int NCH = D / 64;
   const Geom& g = a.g;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-aligned base that stays in the shared address space (LDS/STS, not
+  // generic LD/ST, for every access through it)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sK = smem + L::OFF_K;
   uint8_t* sV = smem + L::OFF_V;
   uint8_t* sSt = smem + L::OFF_ST;
@@ -802,6 +805,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           BSTAT_ADD(1, leader);
         }
         tc_fence_after();
+        BSTAT_T0();
         const uint32_t qb = st_addr + st * L::STAGE;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -818,6 +822,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         init = true;
         if (leader) umma_commit(&empty[st]);
+        BSTAT_ADD(6, leader);
       };
       for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1)) {
         const uint32_t st = u % KST;
@@ -829,6 +834,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t b = u & 1;
         const uint32_t qb = st_addr + st * L::STAGE;
+        BSTAT_T0();
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -838,6 +844,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       desc_kmajor(qb + L::QTB + c * QT * 128 + k * 32), IDESC_S, (c | k) != 0);
           }
         if (leader) umma_commit(&s_full[b]);
+        BSTAT_ADD(5, leader);
         if (prev >= 0) grad_mma(u - 1, prev_st);
         prev = i;
         prev_st = st;

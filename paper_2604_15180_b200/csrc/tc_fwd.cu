@@ -312,8 +312,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int NCH = D / 64;  // 128-byte chunks along d
   const Geom& g = a.g;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-aligned base that stays in the shared address space (LDS/STS, not
+  // generic LD/ST, for every access through it)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem + L::OFF_Q;
   uint8_t* sRing = smem + L::OFF_RING;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);

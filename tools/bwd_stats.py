@@ -22,3 +22,5 @@ mma = max(st[3], 1)
 print("units", st[4], "MMA cycles/unit", mma / max(st[4], 1))
 for i, n in enumerate(["mma_wait_stage(TMA)", "mma_wait_p_full(epi)", "epi_w4_wait_s_full"]):
     print(f"{n:24s} {st[i] / mma:6.3f} of MMA-warp cycles")
+print("issue-blocked per unit: S/dP", st[5] / max(st[4], 1), "grads", st[6] / max(st[4], 1),
+      "(pure MMA time 768 / 1024)")

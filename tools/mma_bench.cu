@@ -65,6 +65,11 @@ __global__ void __launch_bounds__(256, 1) bench(unsigned long long* out) {
           }
         }
         if (MODE & 2) tc_fence_after();
+        if (MODE & 1024) {  // issuing warp stalls ~256 cycles every 8 MMAs
+          const long long w0 = clock64();
+          while (clock64() - w0 < 256) {
+          }
+        }
       }
       const uint64_t bdesc = BMN ? desc_mnmajor(b_addr + k * 2048, 16384)
                                  : desc_kmajor(b_addr + k * 32);
@@ -138,6 +143,131 @@ void run(const char* name) {
   cudaFree(d);
 }
 
+
+// The dK/dV kernel's per-unit MMA sequence, no epilogue or TMA: per unit 8 x
+// (SS M128 N64 S^T, SS M128 N64 dP^T) interleaved, then 16 TS M128 N128
+// (dV hi/lo, dK hi/lo).  MODE bit0: commit after the S/dP block and after the
+// grads (the kernel's commits).
+template <int MODE>
+__global__ void __launch_bounds__(384, 1) bench_kv(unsigned long long* out, int units) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, side, side2;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5;
+  __shared__ volatile uint32_t stop;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += 384) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&side, 1);
+    mbar_init(&side2, 1);
+    mbar_arrive(&side2);
+    fence_barrier_init();
+    stop = 0;
+  }
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (warp == 1) {
+    const bool leader = elect_one_sync();
+    const uint32_t k_addr = smem_u32(smem), v_addr = smem_u32(smem + 32768),
+                   q_addr = smem_u32(smem + 65536), do_addr = smem_u32(smem + 65536 + 16384);
+    constexpr uint32_t IS = idesc_bf16_f32(128, 64, false, false);
+    constexpr uint32_t IG = idesc_bf16_f32(128, 128, false, true);
+    const long long t0 = clock64();
+    for (int u = 0; u < units; ++u) {
+      const uint32_t b = u & 1;
+      for (int c = 0; c < 2; ++c)
+        for (int k = 0; k < 4; ++k) {
+          if (leader) umma_bf16(tmem + b * 128, desc_kmajor(k_addr + c * 16384 + k * 32),
+                                desc_kmajor(q_addr + c * 8192 + k * 32), IS, (c | k) != 0);
+          if (leader) umma_bf16(tmem + b * 128 + 64, desc_kmajor(v_addr + c * 16384 + k * 32),
+                                desc_kmajor(do_addr + c * 8192 + k * 32), IS, (c | k) != 0);
+        }
+      if (MODE & 1) if (leader) umma_commit(&side);
+      if (MODE & 32) {  // a satisfied mbarrier wait + tcgen05 fence between the groups
+        mbar_wait(&side2, 0);
+        tc_fence_after();
+      }
+      if (MODE & 8) {  // the issuing warp stalls ~200 cycles between the groups
+        const long long w0 = clock64();
+        while (clock64() - w0 < 200) {
+        }
+      }
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t acol = 32 * (k >> 1) + 8 * (k & 1);
+        const uint64_t bdo = desc_mnmajor(do_addr + k * 2048, 8192);
+        const uint64_t bq = desc_mnmajor(q_addr + k * 2048, 8192);
+        if (leader) umma_bf16_ts(tmem + 256, tmem + (b ^ 1) * 128 + acol, bdo, IG, 1u);
+        if (leader) umma_bf16_ts(tmem + 256, tmem + (b ^ 1) * 128 + acol + 16, bdo, IG, 1u);
+        if (leader) umma_bf16_ts(tmem + 384, tmem + (b ^ 1) * 128 + 64 + acol, bq, IG, 1u);
+        if (leader) umma_bf16_ts(tmem + 384, tmem + (b ^ 1) * 128 + 64 + acol + 16, bq, IG, 1u);
+      }
+      if (MODE & 1) if (leader) umma_commit(&side);
+      if (MODE & 32) {
+        mbar_wait(&side2, 0);
+        tc_fence_after();
+      }
+      if (MODE & 16) {  // and ~400 cycles after the grads
+        const long long w0 = clock64();
+        while (clock64() - w0 < 400) {
+        }
+      }
+    }
+    if (leader) umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (leader) out[blockIdx.x] = (unsigned long long)(t1 - t0);
+    stop = 1;
+  } else if (warp >= 4 && (MODE & 2)) {
+    // epilogue-like TMEM traffic: 8 warps, per round ld 2 x 32 cols, st 4 x 16 cols
+    const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16) + ((warp >> 2) & 1) * 32;
+    uint32_t r[16];
+    float v[32];
+    float acc = 0.f;
+    while (!stop) {
+      tmem_ld32(tl, v);
+      tmem_ld32(tl + 64, v);
+      tmem_wait_ld();
+      for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(v[i] + v[i + 16]);
+      acc += v[3];
+      tmem_st16(tl, r);
+      tmem_st16(tl + 16, r);
+      tmem_st16(tl + 64, r);
+      tmem_st16(tl + 80, r);
+      tmem_wait_st();
+      if (MODE & 4)
+        for (int i = 0; i < 8; ++i)
+          st_shared_v4(smem_u32(smem) + 98304 + ((threadIdx.x * 16 + i * 4096) & 4095), i, i, i, i);
+    }
+    if (acc == 1234.f) out[0] = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int MODE>
+void run_kv(const char* name) {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  auto k = bench_kv<MODE>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const int units = 512;
+  k<<<148, 384, 100 * 1024>>>(d, units);
+  k<<<148, 384, 100 * 1024>>>(d, units);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += (double)h[i] / 148.0;
+  printf("%-22s %s  cycles/unit %7.1f  (ideal 1792 at 67%% SS N64 + 100%% TS)\n", name,
+         e ? cudaGetErrorString(e) : "ok", avg / units);
+  cudaFree(d);
+}
+
 int main() {
   run<64, false>("SS M128 N64");
   run<128, false>("SS M128 N128");
@@ -162,9 +292,19 @@ int main() {
   run<128, true, 64>("TS N128 +smemwr");
   run<64, true, 64>("TS N64 +smemwr");
   run<128, false, 4>("SS N128 +wait/8");
+  run<128, false, 1024>("SS N128 +256cyc gap/8");
+  run<128, true, 1024>("TS N128 +256cyc gap/8");
+  run<256, false, 1024>("SS N256 +256cyc gap/8");
   run<128, false, 36>("SS N128 +testwait/8");
   run<128, true, 4>("TS N128 +wait/8");
   run<128, true, 36>("TS N128 +testwait/8");
+  run_kv<0>("dkdv MMA sequence");
+  run_kv<1>("dkdv MMA seq +commits");
+  run_kv<2>("dkdv MMA seq +tmem ld/st");
+  run_kv<6>("dkdv MMA +tmem +smemwr");
+  run_kv<8>("dkdv MMA +200cyc gap");
+  run_kv<24>("dkdv MMA +200+400 gaps");
+  run_kv<33>("dkdv MMA +wait+fence x2");
   run<64, true, 8>("TS N64 Bmn");
   return 0;
 }
