@@ -790,6 +790,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), st_addr = smem_u32(sSt);
       mbar_wait(kv_full, 0);
       tc_fence_after();
+      // loop-invariant operand descriptors (stage 0; other stages add STAGE >> 4)
+      uint64_t dK[NCH], dV[NCH], dQk[NCH], dDOk[NCH];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        dK[c] = desc_kmajor(k_addr + c * KB * 128);
+        dV[c] = desc_kmajor(v_addr + c * KB * 128);
+        dQk[c] = desc_kmajor(st_addr + c * QT * 128);
+        dDOk[c] = desc_kmajor(st_addr + L::QTB + c * QT * 128);
+      }
+      const uint64_t dQmn = desc_mnmajor(st_addr, QT * 128);
+      const uint64_t dDOmn = desc_mnmajor(st_addr + L::QTB, QT * 128);
 #ifdef ADATTN_PIPE_STATS
       const long long t_m0 = clock64();
 #endif
@@ -806,14 +817,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_after();
         BSTAT_T0();
-        const uint32_t qb = st_addr + st * L::STAGE;
+        // stage st's Q / dO descriptors: the base descriptors + the stage offset
+        const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           // queries 16k..16k+15: packed pairs of half k>>1 at cols 32*(k>>1) + 8*(k&1)
-          // (hi) and +16 (lo)
+          // (hi) and +16 (lo); K step of 16 rows = 2048 B = +128 in the address field
           const uint32_t acol = 32 * (k >> 1) + 8 * (k & 1);
-          const uint64_t bdo = desc_mnmajor(qb + L::QTB + k * 16 * 128, QT * 128);
-          const uint64_t bq = desc_mnmajor(qb + k * 16 * 128, QT * 128);
+          const uint64_t bdo = dDOmn + so + (uint64_t)(128 * k);
+          const uint64_t bq = dQmn + so + (uint64_t)(128 * k);
           const uint32_t acc = (init || k > 0) ? 1u : 0u;
           if (leader) umma_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G, acc);
           if (leader) umma_bf16_ts(tmem + 256, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
@@ -833,15 +845,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_after();
         const uint32_t b = u & 1;
-        const uint32_t qb = st_addr + st * L::STAGE;
+        const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
         BSTAT_T0();
+#pragma unroll
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            if (leader) umma_bf16(tmem + b * 128, desc_kmajor(k_addr + c * KB * 128 + k * 32),
-                      desc_kmajor(qb + c * QT * 128 + k * 32), IDESC_S, (c | k) != 0);
-            if (leader) umma_bf16(tmem + b * 128 + 64, desc_kmajor(v_addr + c * KB * 128 + k * 32),
-                      desc_kmajor(qb + L::QTB + c * QT * 128 + k * 32), IDESC_S, (c | k) != 0);
+            if (leader) umma_bf16(tmem + b * 128, dK[c] + (uint64_t)(2 * k),
+                      dQk[c] + so + (uint64_t)(2 * k), IDESC_S, (c | k) != 0);
+            if (leader) umma_bf16(tmem + b * 128 + 64, dV[c] + (uint64_t)(2 * k),
+                      dDOk[c] + so + (uint64_t)(2 * k), IDESC_S, (c | k) != 0);
           }
         if (leader) umma_commit(&s_full[b]);
         BSTAT_ADD(5, leader);
