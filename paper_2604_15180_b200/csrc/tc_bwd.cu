@@ -308,34 +308,46 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
     mbar_wait(q_full, 0);
     tc_fence_after();
     uint32_t r = 0, uses[2] = {0, 0};
+    // loop-invariant descriptors (row group rg at +128 rows = 16 KB = +1024 in the field)
+    uint64_t dQd[NCH], dDOd[NCH], dR[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      dQd[c] = desc_kmajor(q_addr + c * BM * 128);
+      dDOd[c] = desc_kmajor(do_addr + c * BM * 128);
+      dR[c] = desc_kmajor(ring_addr + c * DBN * 128);
+    }
+    constexpr uint32_t kTileF = (uint32_t)L::TILE >> 4;
     for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
       const uint32_t kst = r % NST, vst = (r + 1) % NST;
       mbar_wait(&full[kst], (r / NST) & 1);
       mbar_wait(&full[vst], ((r + 1) / NST) & 1);
       tc_fence_after();
       const bool act1 = rg_active(1, J);
+      const uint64_t ko = (uint64_t)(kst * kTileF), vo = (uint64_t)(vst * kTileF);
+#pragma unroll
       for (int rg = 0; rg < 2; ++rg) {
         if (!rg_active(rg, J)) continue;
         mbar_wait(&s_free[rg], (uses[rg] & 1) ^ 1);
         tc_fence_after();
         const uint32_t sc = tmem + rg * 256;
+        const uint64_t ro = (uint64_t)(rg * 1024);
+#pragma unroll
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if (leader)
-              umma_bf16(sc, desc_kmajor(q_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
-                        desc_kmajor(ring_addr + kst * L::TILE + c * DBN * 128 + k * 32), IDESC_S,
-                        (c | k) != 0);
+              umma_bf16(sc, dQd[c] + ro + (uint64_t)(2 * k), dR[c] + ko + (uint64_t)(2 * k),
+                        IDESC_S, (c | k) != 0);
         // K_J's last reader issued: free its slot early (the next item, V_{J+1}, refills it)
         if (rg == 1 || !act1)
           if (leader) umma_commit(&empty[kst]);
+#pragma unroll
         for (int c = 0; c < NCH; ++c)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if (leader)
-              umma_bf16(sc + 128, desc_kmajor(do_addr + c * BM * 128 + rg * 128 * 128 + k * 32),
-                        desc_kmajor(ring_addr + vst * L::TILE + c * DBN * 128 + k * 32), IDESC_S,
-                        (c | k) != 0);
+              umma_bf16(sc + 128, dDOd[c] + ro + (uint64_t)(2 * k), dR[c] + vo + (uint64_t)(2 * k),
+                        IDESC_S, (c | k) != 0);
         if (leader) umma_commit(&s_full[rg]);
         ++uses[rg];
       }
@@ -542,15 +554,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     uint32_t t = 0;
     bool acc_init = false;
+    // loop-invariant descriptors; ring slot s adds s * (TILE >> 4) to the address field
+    uint64_t dQd[NCH], dDOd[NCH], dKs[NCH], dVs[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      dQd[c] = desc_kmajor(q_addr + c * QB_DQ * 128);
+      dDOd[c] = desc_kmajor(do_addr + c * QB_DQ * 128);
+      dKs[c] = desc_kmajor(k_addr + c * DBN * 128);
+      dVs[c] = desc_kmajor(v_addr + c * DBN * 128);
+    }
+    const uint64_t dKmn = desc_mnmajor(k_addr, DBN * 128);
+    constexpr uint32_t kTileF = (uint32_t)L::TILE >> 4;
     auto dq_mma = [&](uint32_t tt) {  // dQ += dS_tt K_tt (dS in S[tt&1], K in slot tt % NSK)
       const uint32_t b = tt & 1, ks = tt % NSK;
       mbar_wait(&ds_full[b], (tt >> 1) & 1);
       tc_fence_after();
+      const uint64_t bk = dKmn + (uint64_t)(ks * kTileF);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        // keys 16k..16k+15: chunk k>>1 (32 keys) at cols 32(k>>1): hi +8(k&1), lo +16+8(k&1)
+        // keys 16k..16k+15: chunk k>>1 (32 keys) at cols 32(k>>1): hi +8(k&1), lo +16+8(k&1);
+        // a 16-key K step of the MN-major operand is 2048 B = +128
         const uint32_t acol = b * 128 + 32 * (k >> 1) + 8 * (k & 1);
-        const uint64_t bd = desc_mnmajor(k_addr + ks * L::TILE + k * 16 * 128, DBN * 128);
+        const uint64_t bd = bk + (uint64_t)(128 * k);
         if (leader) umma_bf16_ts(tmem + 384, tmem + acol, bd, IDESC_DQ, (acc_init || k > 0) ? 1u : 0u);
         if (leader) umma_bf16_ts(tmem + 384, tmem + acol + 16, bd, IDESC_DQ, 1u);
       }
@@ -562,23 +587,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&kfull[ks], (t / NSK) & 1);
       tc_fence_after();
       // S[b] was last read by dQ_{t-2}, issued earlier (in-order tensor pipe)
+      const uint64_t ko = (uint64_t)(ks * kTileF), vo = (uint64_t)(vs * kTileF);
+#pragma unroll
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (leader)
-            umma_bf16(tmem + b * 128, desc_kmajor(q_addr + c * QB_DQ * 128 + k * 32),
-                      desc_kmajor(k_addr + ks * L::TILE + c * DBN * 128 + k * 32), IDESC_S,
-                      (c | k) != 0);
+            umma_bf16(tmem + b * 128, dQd[c] + (uint64_t)(2 * k), dKs[c] + ko + (uint64_t)(2 * k),
+                      IDESC_S, (c | k) != 0);
       mbar_wait(&vfull[vs], (t / NSV) & 1);
       if (t > 0) mbar_wait(dp_free, (t - 1) & 1);
       tc_fence_after();
+#pragma unroll
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (leader)
-            umma_bf16(tmem + 256, desc_kmajor(do_addr + c * QB_DQ * 128 + k * 32),
-                      desc_kmajor(v_addr + vs * L::TILE + c * DBN * 128 + k * 32), IDESC_S,
-                      (c | k) != 0);
+            umma_bf16(tmem + 256, dDOd[c] + (uint64_t)(2 * k), dVs[c] + vo + (uint64_t)(2 * k),
+                      IDESC_S, (c | k) != 0);
       if (leader) umma_commit(&s_full[b]);
       if (leader) umma_commit(&vempty[vs]);
       if (t > 0) dq_mma(t - 1);
