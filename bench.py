@@ -149,6 +149,8 @@ def main():
     ap.add_argument("--sweep", default="0.6,0.7,0.8,1.0",
                     help="anchored-generator betas ('' to skip)")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--alphas", default="1.25,2.0",
+                    help="extra alphas timed on the headline shape (comma list, '' = none)")
     ap.add_argument("--ref-n", type=int, default=4096)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -326,6 +328,19 @@ def main():
                       "tau_iters_avg": sres.row_steps.float().mean().item()})
         del qa, ka, va, da, pa_, sres
 
+    # ---- alpha sweep of BASELINE config 3 (same shape, N(0,1) inputs): alpha = 1.25 runs
+    # the refinement sweeps (candidate lists would overflow), alpha = 2 the lists
+    alpha_sweep = []
+    for a_s in [x for x in args.alphas.split(",") if x.strip()]:
+        pa_ = pa.AttentionProblem(q, k, v, alpha=float(a_s), causal=causal)
+        sms, sres, _, _ = timed(pa_, do, 1, 2)
+        sst = sres.stats
+        sfl = workloads.flops(D, sst.blocks_visited_fwd * world, A_head * B * H * world)
+        alpha_sweep.append({"alpha": float(a_s), "block_sparsity": sst.block_sparsity, "ms": sms,
+                            "tflops_eff": sfl["f_eff"] / (sms * 1e-3) / 1e12,
+                            "tau_iters_avg": sres.row_steps.float().mean().item()})
+        del pa_, sres
+
     # ---- CPU baseline (rank 0 at N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -353,6 +368,7 @@ def main():
             "tau_iters_avg": tau_iters, "tflops_alg": tflops_alg,
             "gpu_launches": int(launches), "kernels": kern, "roofline": roofline,
             "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu, "sweep": sweep,
+            "alpha_sweep": alpha_sweep,
             "validation_gather": validation,
         }
         print(json.dumps(line), flush=True)

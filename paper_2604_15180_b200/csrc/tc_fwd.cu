@@ -567,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // and one group's P computation overlaps the other group's MMAs.
     bool o_init[2] = {false, false};
     uint32_t pcnt[2] = {0, 0};
+    const uint64_t dVmn = desc_mnmajor(ring_addr, BN * 128);
     auto pv = [&](int rg, uint32_t vst) {
       {
         PSTAT_T0();
@@ -575,13 +576,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ++pcnt[rg];
       tc_fence_after();
+      const uint64_t bv = dVmn + (uint64_t)((vst * (uint32_t)L::TILE) >> 4);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        // keys 16k..16k+15: packed P pairs at TMEM cols rg*128 + 64*(k>>2) + 8*(k&3)
+        // keys 16k..16k+15: packed P pairs at TMEM cols rg*128 + 64*(k>>2) + 8*(k&3);
+        // a 16-key step of the MN-major V operand is 2048 B = +128
         const uint32_t acol = rg * 128 + 64 * (k >> 2) + 8 * (k & 3);
         if (leader)
-          umma_bf16_ts(tmem + 256 + rg * D, tmem + acol,
-                       desc_mnmajor(ring_addr + vst * L::TILE + k * 16 * 128, BN * 128), IDESC_PV,
+          umma_bf16_ts(tmem + 256 + rg * D, tmem + acol, bv + (uint64_t)(128 * k), IDESC_PV,
                        (o_init[rg] || k > 0) ? 1u : 0u);
       }
       o_init[rg] = true;
