@@ -495,19 +495,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                       (c | k) != 0);
     };
     // threshold passes: S double buffered per row group
+    // Both row groups' S buffers are claimed before either group's MMAs are
+    // issued, so the 16 MMAs of a tile go out back to back (the tensor pipe
+    // queues only about one MMA ahead: any gap in the issue stream idles it).
     auto s_tile = [&](int J, int set) {  // set < 0: every tile (MAX)
       const uint32_t st = wait_ring();
+      bool doit[2];
 #pragma unroll
       for (int rg = 0; rg < 2; ++rg) {
-        if (J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J))) continue;
+        doit[rg] = !(J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J)));
+        if (!doit[rg]) continue;
+        PSTAT_T0();
+        mbar_wait(&s_empty[(it[rg] & 1) * 2 + rg], ((it[rg] >> 1) & 1) ^ 1);
+        PSTAT_ADD(1);
+        PSTAT_ADD(33 + 2 * cur_sweep);
+      }
+      tc_fence_after();
+#pragma unroll
+      for (int rg = 0; rg < 2; ++rg) {
+        if (!doit[rg]) continue;
         const uint32_t b = it[rg] & 1;
-        {
-          PSTAT_T0();
-          mbar_wait(&s_empty[b * 2 + rg], ((it[rg] >> 1) & 1) ^ 1);
-          PSTAT_ADD(1);
-          PSTAT_ADD(33 + 2 * cur_sweep);
-        }
-        tc_fence_after();
         {
           PSTAT_T0();
           issue_s(tmem + b * 256 + rg * 128, rg, st);
