@@ -181,3 +181,37 @@ def test_tc_bins(bins):
     assert tau_err <= 1e-3 and out_err <= 2e-2
     with pytest.raises(Exception):
         run(q, k, v, None, "tc", alpha=1.5, causal=True, bins=32)
+
+
+@pytest.mark.parametrize("N,D,causal,beta", [(131072, 128, True, 1.0), (131072, 128, True, 0.6),
+                                             (65536, 64, False, None)])
+def test_tc_long_context_rows_vs_dense(N, D, causal, beta):
+    """BASELINE configs 4/5 shapes (one head): sampled rows of the TC forward against the
+    dense fp64 GPU reference over all N keys (dense.py); the masks' support covers every
+    key the dense reference activates; the backward runs and stays finite."""
+    from paper_2604_15180_b200 import dense, workloads
+    if beta is None:
+        q, k, v, do = inputs(31, 1, 1, N, D, 1.0)
+    else:
+        q, k, v, do = workloads.anchored(1, 1, N, D, beta, causal, seed=3, device=DEV)
+    _, rt, gt = run(q, k, v, do, "tc", alpha=1.5, causal=causal)
+    for name in ("dq", "dk", "dv"):
+        assert torch.isfinite(getattr(gt, name)).all()
+    rows = torch.tensor([0, 1, 63, 64, 1000, N // 2, N - 65, N - 1], device=DEV)
+    qs, ks, vs = q[0, 0], k[0, 0], v[0, 0]
+    s = (qs[rows].double() @ ks.double().t()) / D ** 0.5
+    if causal:
+        s = s.masked_fill(torch.arange(N, device=DEV)[None, :] > rows[:, None], float("-inf"))
+    mx = s.amax(dim=1, keepdim=True)
+    z = torch.where(s == mx, torch.ones_like(s), 0.5 * (s - mx) + 1.0)
+    tau = dense._tau_exact(z, 1.5)
+    p = torch.clamp(z - tau[:, None], min=0.0) ** 2
+    out = p @ vs.double()
+    err_o = (rt.out[0, 0][rows].double() - out).abs().max().item()
+    err_t = (rt.tau[0, 0][rows].double() - tau).abs().max().item()
+    print(N, D, causal, beta, "sparsity", rt.stats.block_sparsity, "out", err_o, "tau", err_t)
+    assert err_o < 2e-2 and err_t < 1e-3
+    bits = mask_bits(rt.mask.words, rt.mask.t_c)[0, 0]
+    act = (p > 0).reshape(len(rows), -1, 64).any(dim=2).cpu().numpy()
+    rb = (rows // 64).cpu().numpy()
+    assert np.all(bits[rb][act]), "a block the dense reference activates is missing from the mask"
