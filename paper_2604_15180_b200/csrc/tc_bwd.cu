@@ -14,6 +14,8 @@
 //                    used as the TMEM A operand of dV += P^T dO_i and
 //                    dK += dS^T Q_i (attention.cpp:464-506)
 #include <cuda.h>
+
+#include <cstdlib>
 #include <math_constants.h>
 
 #include "common.cuh"
@@ -693,6 +695,285 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8) tmem_dealloc(tmem, 512);
 }
 
+// ============================================================== dQ (pairs)
+// CTA-pair variant of the dQ kernel (cta_group::2, cluster of 2, D = 128): the
+// pair covers 256 query rows (rank r: rows +128r) and the leader issues every
+// MMA for both SMs with M = 256, so each SM feeds only half of every B operand
+// from its shared memory and the per-SM MMA issue count halves:
+//   S  = Q K_J^T : B half = keys 64r..64r+63 of K_J (all d)          (KS slot)
+//   dP = dO V_J^T: B half = keys 64r..64r+63 of V_J                   (VS slot)
+//   dQ += dS K_J : A = dS in each SM's TMEM, B half = d cols 64r..+63 (KD slot, MN-major)
+// Tiles are the union of both CTAs' active tiles; a CTA writes dS = 0 where its
+// own blocks are clear.  Barriers: full / q_full / ds_full / dp_free live in the
+// leader (TMA of both CTAs completes there; the peer's epilogue arrives
+// remotely); empty / s_full / acc_full in each CTA, armed by multicast commits.
+template <int D>
+struct Dq2Smem {
+  static_assert(D == 128, "pair dQ kernel: d = 128");
+  static constexpr int QB = QB_DQ * D * 2;     // own 128 rows of Q (and of dO)
+  static constexpr int HB = 64 * D * 2;        // 64 keys x d   (KS, VS slots)
+  static constexpr int KDB = DBN * 64 * 2;     // 128 keys x 64 d (KD slot)
+  static constexpr int NSK = 3, NSV = 3;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_DO = OFF_Q + QB;
+  static constexpr int OFF_KS = OFF_DO + QB;
+  static constexpr int OFF_KD = OFF_KS + NSK * HB;
+  static constexpr int OFF_VS = OFF_KD + NSK * KDB;
+  static constexpr int OFF_BAR = OFF_VS + NSV * HB;
+  static constexpr int OFF_MISC = OFF_BAR + 40 * 8;
+  static constexpr int OFF_MASK = OFF_MISC + 64;
+  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
+};
+
+template <int D, int AK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_dq2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kh,
+                  const __grid_constant__ CUtensorMap tm_kd, const __grid_constant__ CUtensorMap tm_vh,
+                  const __grid_constant__ CUtensorMap tm_do, const BwdArgs a) {
+  using L = Dq2Smem<D>;
+  constexpr int NSK = L::NSK, NSV = L::NSV;
+  constexpr int NCH = D / 64;
+  const Geom& g = a.g;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sQ = smem + L::OFF_Q;
+  uint8_t* sDO = smem + L::OFF_DO;
+  uint8_t* sKS = smem + L::OFF_KS;
+  uint8_t* sKD = smem + L::OFF_KD;
+  uint8_t* sVS = smem + L::OFF_VS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* kfull = bars;              // [NSK] leader: K_S + K_D of both CTAs
+  uint64_t* kempty = kfull + NSK;      // [NSK] each CTA
+  uint64_t* vfull = kempty + NSK;      // [NSV] leader
+  uint64_t* vempty = vfull + NSV;      // [NSV] each CTA
+  uint64_t* s_full = vempty + NSV;     // [2] each CTA
+  uint64_t* ds_full = s_full + 2;      // [2] leader, 16 warps
+  uint64_t* dp_free = ds_full + 2;     // leader, 16 warps
+  uint64_t* acc_full = dp_free + 1;    // each CTA
+  uint64_t* q_full = acc_full + 1;     // leader
+  volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
+  uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [4][wpr] (the pair's row blocks)
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool lead_cta = rank == 0;
+  const int npair = g.n / (2 * QB_DQ);
+  const int pair = (int)(blockIdx.x >> 1);
+  const int bh = pair / npair;  // head-major, heaviest pairs first
+  const int prow0 = (npair - 1 - pair % npair) * 2 * QB_DQ;
+  const int row0 = prow0 + (int)rank * QB_DQ;
+  const int nkt = g.m / DBN;
+  const int jmax = g.causal ? (prow0 + 2 * QB_DQ - 1) / DBN : nkt - 1;
+  const int wpr = g.wpr;
+
+  for (int i = tid; i < 4 * wpr; i += kThreads) {
+    const int rbi = i / wpr, w = i - rbi * wpr;
+    smask[i] = a.mask[((size_t)bh * g.t_r + (prow0 / 64 + rbi)) * wpr + w];
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NSK; ++i) {
+      mbar_init(&kfull[i], 1);
+      mbar_init(&kempty[i], 1);
+    }
+    for (int i = 0; i < NSV; ++i) {
+      mbar_init(&vfull[i], 1);
+      mbar_init(&vempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&ds_full[i], 16);
+    }
+    mbar_init(dp_free, 16);
+    mbar_init(acc_full, 1);
+    mbar_init(q_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 8) tmem_alloc_2sm(const_cast<uint32_t*>(s_tmem), 512);
+  tc_fence_before();
+  cluster_sync();  // barrier inits of both CTAs visible before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  auto bits2 = [&](int rb, int J) -> uint32_t {  // rb: 0..3 over the pair's 256 rows
+    return (smask[rb * wpr + ((2 * J) >> 5)] >> ((2 * J) & 31)) & 3u;
+  };
+  auto next_active = [&](int J) -> int {  // union over both CTAs' rows
+    for (; J <= jmax; ++J)
+      if (bits2(0, J) | bits2(1, J) | bits2(2, J) | bits2(3, J)) return J;
+    return -1;
+  };
+
+  if (warp == 8) {  // TMA producer (both CTAs load their own halves)
+    const bool leader = elect_one_sync();
+    const int qrow = bh * g.n + row0;
+    if (lead_cta && leader) mbar_expect_tx(q_full, 2 * 2 * L::QB);
+    for (int c = 0; c < NCH; ++c) {
+      if (leader) tma_load_2d_2sm(sQ + c * QB_DQ * 128, &tm_q, q_full, c * 64, qrow);
+      if (leader) tma_load_2d_2sm(sDO + c * QB_DQ * 128, &tm_do, q_full, c * 64, qrow);
+    }
+    uint32_t t = 0;
+    const int krow0 = bh * g.m;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1), ++t) {
+      const uint32_t ks = t % NSK, vs = t % NSV;
+      mbar_wait(&kempty[ks], ((t / NSK) & 1) ^ 1);
+      if (lead_cta && leader) mbar_expect_tx(&kfull[ks], 2 * (L::HB + L::KDB));
+      for (int c = 0; c < NCH; ++c)
+        if (leader)
+          tma_load_2d_2sm(sKS + ks * L::HB + c * 64 * 128, &tm_kh, &kfull[ks], c * 64,
+                          krow0 + J * DBN + 64 * (int)rank);
+      if (leader) tma_load_2d_2sm(sKD + ks * L::KDB, &tm_kd, &kfull[ks], 64 * (int)rank, krow0 + J * DBN);
+      mbar_wait(&vempty[vs], ((t / NSV) & 1) ^ 1);
+      if (lead_cta && leader) mbar_expect_tx(&vfull[vs], 2 * L::HB);
+      for (int c = 0; c < NCH; ++c)
+        if (leader)
+          tma_load_2d_2sm(sVS + vs * L::HB + c * 64 * 128, &tm_vh, &vfull[vs], c * 64,
+                          krow0 + J * DBN + 64 * (int)rank);
+    }
+  } else if (warp == 9) {  // MMA issuer: the pair leader only
+    if (lead_cta) {
+      const bool leader = elect_one_sync();
+      constexpr uint32_t IDESC_S = idesc_bf16_f32(256, DBN, false, false);
+      constexpr uint32_t IDESC_DQ = idesc_bf16_f32(256, D, false, true);
+      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO);
+      uint64_t dQd[NCH], dDOd[NCH], dKS[NCH], dVS[NCH];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        dQd[c] = desc_kmajor(q_addr + c * QB_DQ * 128);
+        dDOd[c] = desc_kmajor(do_addr + c * QB_DQ * 128);
+        dKS[c] = desc_kmajor(smem_u32(sKS) + c * 64 * 128);
+        dVS[c] = desc_kmajor(smem_u32(sVS) + c * 64 * 128);
+      }
+      const uint64_t dKD = desc_mnmajor(smem_u32(sKD), DBN * 128);
+      constexpr uint32_t kHF = (uint32_t)L::HB >> 4, kKDF = (uint32_t)L::KDB >> 4;
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      uint32_t t = 0;
+      bool acc_init = false;
+      auto dq_mma = [&](uint32_t tt) {
+        const uint32_t b = tt & 1, ks = tt % NSK;
+        mbar_wait(&ds_full[b], (tt >> 1) & 1);
+        tc_fence_after();
+        const uint64_t bk = dKD + (uint64_t)(ks * kKDF);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t acol = b * 128 + 32 * (k >> 1) + 8 * (k & 1);
+          const uint64_t bd = bk + (uint64_t)(128 * k);
+          if (leader) umma2_bf16_ts(tmem + 384, tmem + acol, bd, IDESC_DQ, (acc_init || k > 0) ? 1u : 0u);
+          if (leader) umma2_bf16_ts(tmem + 384, tmem + acol + 16, bd, IDESC_DQ, 1u);
+        }
+        acc_init = true;
+        if (leader) umma2_commit_mc(&kempty[ks]);
+      };
+      for (int J = next_active(0); J >= 0; J = next_active(J + 1), ++t) {
+        const uint32_t ks = t % NSK, vs = t % NSV, b = t & 1;
+        mbar_wait(&kfull[ks], (t / NSK) & 1);
+        tc_fence_after();
+        const uint64_t ko = (uint64_t)(ks * kHF), vo = (uint64_t)(vs * kHF);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (leader)
+              umma2_bf16(tmem + b * 128, dQd[c] + (uint64_t)(2 * k), dKS[c] + ko + (uint64_t)(2 * k),
+                         IDESC_S, (c | k) != 0);
+        mbar_wait(&vfull[vs], (t / NSV) & 1);
+        if (t > 0) mbar_wait(dp_free, (t - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (leader)
+              umma2_bf16(tmem + 256, dDOd[c] + (uint64_t)(2 * k), dVS[c] + vo + (uint64_t)(2 * k),
+                         IDESC_S, (c | k) != 0);
+        if (leader) umma2_commit_mc(&s_full[b]);
+        if (leader) umma2_commit_mc(&vempty[vs]);
+        if (t > 0) dq_mma(t - 1);
+      }
+      if (t > 0) dq_mma(t - 1);
+      if (leader) umma2_commit_mc(acc_full);
+    }
+  } else if (warp < 8) {  // epilogue (warp % 4 = TMEM lane quarter)
+    const int half = warp >> 2;
+    const int lq = warp & 3;
+    const int e = lq * 32 + lane;
+    const int rb = e >> 6;                // own row block 0/1
+    const int prb = (int)rank * 2 + rb;   // row block within the pair
+    const int grow = row0 + e;
+    const size_t orow = (size_t)bh * g.n + grow;
+    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16);
+    const float A1 = a.A1;
+    const float2 rc = a.rowc[orow];
+    // leader-CTA barriers as cluster addresses (local for the leader)
+    const uint32_t ds_full_c0 = mapa_shared(smem_u32(&ds_full[0]), 0);
+    const uint32_t ds_full_c1 = mapa_shared(smem_u32(&ds_full[1]), 0);
+    const uint32_t dp_free_c = mapa_shared(smem_u32(dp_free), 0);
+    uint32_t t = 0;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1), ++t) {
+      const uint32_t b = t & 1;
+      const bool mine = (bits2(prb, J) >> half) & 1u;
+      mbar_wait(&s_full[b], (t >> 1) & 1);
+      tc_fence_after();
+      const int k0 = J * DBN + half * 64;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float s[32], dp[32];
+        const uint32_t scol = tl + b * 128 + half * 64 + c * 32;
+        tmem_ld32(tl + 256 + half * 64 + c * 32, dp);
+        tmem_ld32(scol, s);
+        tmem_wait_ld();
+        if (c == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(dp_free_c);
+        }
+        const int c0 = k0 + 32 * c;
+        uint32_t hi[16], lo[16];
+        if (!mine) {
+#pragma unroll
+          for (int x = 0; x < 16; ++x) hi[x] = lo[x] = 0u;
+        } else if (g.causal && c0 + 31 > grow) {
+          ds_chunk<AK, true>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, grow - c0, hi, lo);
+        } else {
+          ds_chunk<AK, false>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, 0, hi, lo);
+        }
+        tmem_st16(scol, hi);
+        tmem_st16(scol + 16, lo);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(b ? ds_full_c1 : ds_full_c0);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    bool rany = false;
+    for (int w = 0; w < wpr; ++w) rany |= smask[prb * wpr + w] != 0u;
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      float o[32];
+      tmem_ld32(tl + 384 + half * (D / 2) + c * 32, o);
+      tmem_wait_ld();
+      const int x0 = half * (D / 2) + c * 32;
+      if (g.out_dtype == ADATTN_F64) {
+        double* dst = reinterpret_cast<double*>(a.dq) + orow * D + x0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) dst[i] = rany ? (double)(a.scale_f * o[i]) : 0.0;
+      } else {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.dq) + orow * D + x0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = rany ? make_float4(a.scale_f * o[4 * i], a.scale_f * o[4 * i + 1],
+                                      a.scale_f * o[4 * i + 2], a.scale_f * o[4 * i + 3])
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // the pair's MMAs and remote arrives are done before TMEM is freed
+  if (warp == 8) tmem_dealloc_2sm(tmem, 512);
+}
+
 // ================================================================= dK / dV
 constexpr int KB = 128;      // keys per CTA
 constexpr int QT = 64;       // query rows per unit (one reference tile)
@@ -980,6 +1261,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8) tmem_dealloc(tmem, 512);
 }
 
+// CTA-pair dQ kernel (d = 128), opt-in with ADATTN_DQ_PAIRS=1: correct, but measured
+// slower than the single-CTA kernel at C3 (28.6 vs 24.6 ms), see DESIGN.md 6.
+bool use_dq_pairs(const Geom& g) {
+  const char* s = std::getenv("ADATTN_DQ_PAIRS");
+  const int env = s ? std::atoi(s) : 0;
+  return env != 0 && g.d == 128 && g.dv == 128 && g.n % (2 * QB_DQ) == 0;
+}
+
 template <typename K>
 cudaError_t set_smem(K kern, size_t bytes) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -1010,7 +1299,16 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     note_launch();
     if ((e = cudaGetLastError())) return e;
   }
-  {
+  if (use_dq_pairs(g)) {
+    auto k1 = tc_dq2_kernel<128, AK>;
+    const size_t sm = Dq2Smem<128>::bytes(g.wpr);
+    if ((e = set_smem(k1, sm))) return e;
+    prof_begin("tc_dq", st);
+    k1<<<dim3((unsigned)((g.n / QB_DQ) * g.bh)), kThreads, sm, st>>>(m[8], m[10], m[1], m[11], m[9], a);
+    prof_end(st);
+    note_launch();
+    if ((e = cudaGetLastError())) return e;
+  } else {
     auto k1 = tc_dq_kernel<D, AK>;
     const size_t sm = DqSmem<D>::bytes(g.wpr);
     if ((e = set_smem(k1, sm))) return e;
@@ -1042,7 +1340,7 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
                      const double* row_max, const uint32_t* mask, const void* dout, void* dq,
                      void* dk, void* dv, double* delta, void* workspace, bool delta_only,
                      cudaStream_t st) {
-  CUtensorMap m[10];
+  CUtensorMap m[12];
   cudaError_t e;
   const uint64_t nq = (uint64_t)g.bh * g.n, nk = (uint64_t)g.bh * g.m;
   if ((e = make_tmap_2d(&m[0], q, nq, g.d, BM))) return e;
@@ -1055,6 +1353,8 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   if ((e = make_tmap_2d(&m[7], dout, nq, g.dv, QT))) return e;
   if ((e = make_tmap_2d(&m[8], q, nq, g.d, QB_DQ))) return e;
   if ((e = make_tmap_2d(&m[9], dout, nq, g.dv, QB_DQ))) return e;
+  if ((e = make_tmap_2d(&m[10], k, nk, g.d, 64))) return e;   // 64-key halves (pair dQ)
+  if ((e = make_tmap_2d(&m[11], v, nk, g.dv, 64))) return e;
   BwdArgs a;
   a.g = g;
   a.ncta_rows = g.n / BM;

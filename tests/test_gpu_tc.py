@@ -215,3 +215,20 @@ def test_tc_long_context_rows_vs_dense(N, D, causal, beta):
     act = (p > 0).reshape(len(rows), -1, 64).any(dim=2).cpu().numpy()
     rb = (rows // 64).cpu().numpy()
     assert np.all(bits[rb][act]), "a block the dense reference activates is missing from the mask"
+
+
+def test_tc_dq_cta_pairs_match_single(monkeypatch):
+    """The opt-in CTA-pair dQ kernel (cta_group::2, M = 256 across two SMs) gives the
+    single-CTA kernel's dQ (same per-tile arithmetic and K order)."""
+    q, k, v, do = inputs(77, 1, 2, 1024, 128, 1.0)
+    prob = pa.AttentionProblem(q, k, v, path="tc", alpha=1.5, causal=True)
+    res = pa.forward(prob)
+    monkeypatch.setenv("ADATTN_DQ_PAIRS", "0")
+    g1 = pa.backward(prob, res, do)
+    monkeypatch.setenv("ADATTN_DQ_PAIRS", "1")
+    g2 = pa.backward(prob, res, do)
+    torch.cuda.synchronize()
+    err = (g1.dq - g2.dq).abs().max().item()
+    print("pair vs single dq", err, g1.dq.abs().max().item())
+    assert err <= 1e-5 * max(1.0, g1.dq.abs().max().item())
+    assert torch.equal(g1.dk, g2.dk) and torch.equal(g1.dv, g2.dv)
