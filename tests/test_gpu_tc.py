@@ -218,7 +218,7 @@ def test_tc_long_context_rows_vs_dense(N, D, causal, beta):
 
 
 def test_tc_dq_cta_pairs_match_single(monkeypatch):
-    """The opt-in CTA-pair dQ kernel (cta_group::2, M = 256 across two SMs) gives the
+    """The CTA-pair dQ kernel (cta_group::2, M = 256 across two SMs) gives the
     single-CTA kernel's dQ (same per-tile arithmetic and K order)."""
     q, k, v, do = inputs(77, 1, 2, 1024, 128, 1.0)
     prob = pa.AttentionProblem(q, k, v, path="tc", alpha=1.5, causal=True)
