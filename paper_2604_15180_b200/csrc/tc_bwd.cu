@@ -1262,12 +1262,276 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8) tmem_dealloc(tmem, 512);
 }
 
+// ============================================================ dK / dV (pairs)
+// CTA-pair variant (cta_group::2, d = 128): the pair covers 256 keys (rank r:
+// keys +128r); the leader issues every MMA with M = 256.  Per 64-query unit i:
+//   S^T  = K Q_i^T  : B half = queries 32r..32r+31 of Q_i (all d)     (QS)
+//   dP^T = V dO_i^T : B half = queries 32r.. of dO_i                   (DS)
+//   dV += P^T dO_i  : A = P^T (own TMEM), B half = d cols 64r.. of dO_i (DD, MN-major)
+//   dK += dS^T Q_i  : A = dS^T, B half = d cols 64r.. of Q_i           (QD, MN-major)
+// Units are the union of both CTAs' active units; rowc (C, delta) of the unit
+// comes with a local bulk copy on a per-stage local barrier.
+template <int D>
+struct Kv2Smem {
+  static_assert(D == 128, "pair dK/dV kernel: d = 128");
+  static constexpr int KVB = KB * D * 2;
+  static constexpr int HB = 32 * D * 2;       // 32 queries x d (QS, DS)
+  static constexpr int DB = QT * 64 * 2;      // 64 queries x 64 d (QD, DD)
+  static constexpr int STAGE = 2 * HB + 2 * DB + 1024;  // + rowc[64]
+  static constexpr int KST2 = 4;
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + KVB;
+  static constexpr int OFF_ST = OFF_V + KVB;
+  static constexpr int OFF_BAR = OFF_ST + KST2 * STAGE;
+  static constexpr int OFF_MISC = OFF_BAR + 40 * 8;
+  static constexpr int OFF_UB = OFF_MISC + 64;
+  static size_t bytes(int t_r) { return 1024 + OFF_UB + t_r + 64; }
+};
+
+template <int D, int AK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_dkdv2_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_qd,
+                    const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_vb,
+                    const __grid_constant__ CUtensorMap tm_doh, const __grid_constant__ CUtensorMap tm_dod,
+                    const BwdArgs a) {
+  using L = Kv2Smem<D>;
+  constexpr int KS = L::KST2;
+  constexpr int NCH = D / 64;
+  const Geom& g = a.g;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sK = smem + L::OFF_K;
+  uint8_t* sV = smem + L::OFF_V;
+  uint8_t* sSt = smem + L::OFF_ST;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* full = bars;             // [KS] leader: QS, DS, QD, DD of both CTAs
+  uint64_t* empty = full + KS;       // [KS] each CTA (multicast commit)
+  uint64_t* rfull = empty + KS;      // [KS] each CTA: its rowc copy
+  uint64_t* s_full = rfull + KS;     // [2] each CTA
+  uint64_t* p_full = s_full + 2;     // [2] leader, 16 warps
+  uint64_t* kv_full = p_full + 2;    // leader
+  uint64_t* acc_full = kv_full + 1;  // each CTA
+  volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
+  uint8_t* ubits = smem + L::OFF_UB;  // [t_r]: bit 2r+kh = block (i, key tile kh of CTA r)
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool lead_cta = rank == 0;
+  const int npair = g.m / (2 * KB);
+  const int pair = (int)(blockIdx.x >> 1);
+  const int bh = pair / npair;          // head-major
+  const int kp = pair % npair;          // low key pairs (most query units) first
+  const int pkey0 = kp * 2 * KB;
+  const int key0 = pkey0 + (int)rank * KB;
+  const int pj0 = pkey0 / 64;           // first of the pair's four reference key tiles
+  const int i_first = g.causal ? pkey0 / QT : 0;
+
+  for (int i = threadIdx.x; i < g.t_r; i += kThreads) {
+    const uint32_t w = a.mask[((size_t)bh * g.t_r + i) * g.wpr + (pj0 >> 5)];
+    ubits[i] = (uint8_t)((w >> (pj0 & 31)) & 15u);
+  }
+  if (tid == 0) {
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&rfull[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 16);
+    }
+    mbar_init(kv_full, 1);
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 8) tmem_alloc_2sm(const_cast<uint32_t*>(s_tmem), 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  auto next_unit = [&](int i) -> int {
+    for (; i < g.t_r; ++i)
+      if (ubits[i]) return i;
+    return -1;
+  };
+
+  if (warp == 8) {  // TMA producer (both CTAs)
+    const bool leader = elect_one_sync();
+    const int krow = bh * g.m + key0;
+    if (lead_cta && leader) mbar_expect_tx(kv_full, 2 * 2 * L::KVB);
+    for (int c = 0; c < NCH; ++c) {
+      if (leader) tma_load_2d_2sm(sK + c * KB * 128, &tm_kb, kv_full, c * 64, krow);
+      if (leader) tma_load_2d_2sm(sV + c * KB * 128, &tm_vb, kv_full, c * 64, krow);
+    }
+    uint32_t u = 0;
+    for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
+      const uint32_t st = u % KS;
+      mbar_wait(&empty[st], ((u / KS) & 1) ^ 1);
+      uint8_t* base = sSt + st * L::STAGE;
+      const int qrow = bh * g.n + i * QT;
+      if (lead_cta && leader) mbar_expect_tx(&full[st], 2 * (2 * L::HB + 2 * L::DB));
+      for (int c = 0; c < NCH; ++c) {
+        if (leader) tma_load_2d_2sm(base + c * 32 * 128, &tm_qh, &full[st], c * 64, qrow + 32 * (int)rank);
+        if (leader) tma_load_2d_2sm(base + L::HB + c * 32 * 128, &tm_doh, &full[st], c * 64, qrow + 32 * (int)rank);
+      }
+      if (leader) tma_load_2d_2sm(base + 2 * L::HB, &tm_qd, &full[st], 64 * (int)rank, qrow);
+      if (leader) tma_load_2d_2sm(base + 2 * L::HB + L::DB, &tm_dod, &full[st], 64 * (int)rank, qrow);
+      if (leader) mbar_expect_tx(&rfull[st], QT * 8);
+      if (leader) bulk_load(base + 2 * L::HB + 2 * L::DB, a.rowc + qrow, QT * 8, &rfull[st]);
+    }
+  } else if (warp == 9) {  // MMA issuer: pair leader only
+    if (lead_cta) {
+      const bool leader = elect_one_sync();
+      constexpr uint32_t IDESC_S = idesc_bf16_f32(256, QT, false, false);
+      constexpr uint32_t IDESC_G = idesc_bf16_f32(256, D, false, true);
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), st_addr = smem_u32(sSt);
+      uint64_t dK[NCH], dV[NCH], dQS[NCH], dDS[NCH];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        dK[c] = desc_kmajor(k_addr + c * KB * 128);
+        dV[c] = desc_kmajor(v_addr + c * KB * 128);
+        dQS[c] = desc_kmajor(st_addr + c * 32 * 128);
+        dDS[c] = desc_kmajor(st_addr + L::HB + c * 32 * 128);
+      }
+      const uint64_t dQD = desc_mnmajor(st_addr + 2 * L::HB, QT * 128);
+      const uint64_t dDD = desc_mnmajor(st_addr + 2 * L::HB + L::DB, QT * 128);
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      uint32_t u = 0, prev_st = 0;
+      bool init = false;
+      int prev = -1;
+      auto grad_mma = [&](uint32_t uu, uint32_t st) {
+        const uint32_t b = uu & 1;
+        mbar_wait(&p_full[b], (uu >> 1) & 1);
+        tc_fence_after();
+        const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t acol = 32 * (k >> 1) + 8 * (k & 1);
+          const uint64_t bdo = dDD + so + (uint64_t)(128 * k);
+          const uint64_t bq = dQD + so + (uint64_t)(128 * k);
+          const uint32_t acc = (init || k > 0) ? 1u : 0u;
+          if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G, acc);
+          if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
+          if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol, bq, IDESC_G, acc);
+          if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol + 16, bq, IDESC_G, 1u);
+        }
+        init = true;
+        if (leader) umma2_commit_mc(&empty[st]);
+      };
+      for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
+        const uint32_t st = u % KS, b = u & 1;
+        mbar_wait(&full[st], (u / KS) & 1);
+        tc_fence_after();
+        const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (leader) umma2_bf16(tmem + b * 128, dK[c] + (uint64_t)(2 * k),
+                                   dQS[c] + so + (uint64_t)(2 * k), IDESC_S, (c | k) != 0);
+            if (leader) umma2_bf16(tmem + b * 128 + 64, dV[c] + (uint64_t)(2 * k),
+                                   dDS[c] + so + (uint64_t)(2 * k), IDESC_S, (c | k) != 0);
+          }
+        if (leader) umma2_commit_mc(&s_full[b]);
+        if (prev >= 0) grad_mma(u - 1, prev_st);
+        prev = i;
+        prev_st = st;
+      }
+      if (prev >= 0) grad_mma(u - 1, prev_st);
+      if (leader) umma2_commit_mc(acc_full);
+    }
+  } else if (warp < 8) {  // epilogue (warp % 4 = TMEM lane quarter)
+    const int half = warp >> 2;        // query columns 32*half .. +31
+    const int lq = warp & 3;
+    const int key = lq * 32 + lane;    // 0..127 within this CTA
+    const int gkey = key0 + key;
+    const int kbit = 2 * (int)rank + (key >> 6);
+    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16);
+    const float A1 = a.A1;
+    const uint32_t p_full_c0 = mapa_shared(smem_u32(&p_full[0]), 0);
+    const uint32_t p_full_c1 = mapa_shared(smem_u32(&p_full[1]), 0);
+    uint32_t u = 0;
+    bool any = false;
+    for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
+      const uint32_t st = u % KS, b = u & 1;
+      const bool mine = (ubits[i] >> kbit) & 1u;
+      any |= mine;
+      mbar_wait(&s_full[b], (u >> 1) & 1);
+      mbar_wait(&rfull[st], (u / KS) & 1);
+      tc_fence_after();
+      float s[32], dp[32];
+      tmem_ld32(tl + b * 128 + half * 32, s);
+      tmem_ld32(tl + b * 128 + 64 + half * 32, dp);
+      tmem_wait_ld();
+      const float2* rc = reinterpret_cast<const float2*>(sSt + st * L::STAGE + 2 * L::HB + 2 * L::DB);
+      uint32_t ph[16], pl[16], dh[16], dl[16];
+      const int q0 = i * QT + half * 32;
+      if (!mine) {
+#pragma unroll
+        for (int x = 0; x < 16; ++x) ph[x] = pl[x] = dh[x] = dl[x] = 0u;
+      } else if (g.causal && q0 < key0 + lq * 32 + 31) {
+        pds_chunk<AK, true>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, gkey - q0, ph, pl, dh, dl);
+      } else {
+        pds_chunk<AK, false>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, 0, ph, pl, dh, dl);
+      }
+      tmem_st16(tl + b * 128 + half * 32, ph);
+      tmem_st16(tl + b * 128 + half * 32 + 16, pl);
+      tmem_st16(tl + b * 128 + 64 + half * 32, dh);
+      tmem_st16(tl + b * 128 + 64 + half * 32 + 16, dl);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(b ? p_full_c1 : p_full_c0);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    any = __any_sync(0xffffffffu, any);
+    const size_t krow = (size_t)bh * g.m + gkey;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {  // 0: dV, 1: dK
+      void* base = which == 0 ? a.dv : a.dk;
+      const float mul = which == 0 ? 1.f : a.scale_f;
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        float o[32];
+        tmem_ld32(tl + 256 + which * D + half * (D / 2) + c * 32, o);
+        tmem_wait_ld();
+        const int x0 = half * (D / 2) + c * 32;
+        if (g.out_dtype == ADATTN_F64) {
+          double* dst = reinterpret_cast<double*>(base) + krow * D + x0;
+#pragma unroll
+          for (int x = 0; x < 32; ++x) dst[x] = any ? (double)(mul * o[x]) : 0.0;
+        } else {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + krow * D + x0);
+#pragma unroll
+          for (int x = 0; x < 8; ++x)
+            dst[x] = any ? make_float4(mul * o[4 * x], mul * o[4 * x + 1], mul * o[4 * x + 2],
+                                       mul * o[4 * x + 3])
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 8) tmem_dealloc_2sm(tmem, 512);
+}
+
 // CTA-pair dQ kernel for d = 128 (ADATTN_DQ_PAIRS=0 selects the single-CTA kernel):
 // 20.0 vs 24.6 ms at C3.
 bool use_dq_pairs(const Geom& g) {
   const char* s = std::getenv("ADATTN_DQ_PAIRS");
   const int env = s ? std::atoi(s) : 1;
   return env != 0 && g.d == 128 && g.dv == 128 && g.n % (2 * QB_DQ) == 0;
+}
+
+// CTA-pair dK/dV kernel for d = 128 (ADATTN_KV_PAIRS=0 selects the single-CTA kernel)
+bool use_kv_pairs(const Geom& g) {
+  const char* s = std::getenv("ADATTN_KV_PAIRS");
+  const int env = s ? std::atoi(s) : 1;
+  return env != 0 && g.d == 128 && g.dv == 128 && g.m % (2 * KB) == 0;
 }
 
 template <typename K>
@@ -1290,7 +1554,17 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     if ((e = cudaGetLastError())) return e;
   }
   if (delta_only) return cudaSuccess;
-  {
+  if (use_kv_pairs(g)) {
+    auto k2 = tc_dkdv2_kernel<128, AK>;
+    const size_t sm = Kv2Smem<128>::bytes(g.t_r);
+    if ((e = set_smem(k2, sm))) return e;
+    prof_begin("tc_dkdv", st);
+    k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
+                                                                   m[7], a);
+    prof_end(st);
+    note_launch();
+    if ((e = cudaGetLastError())) return e;
+  } else {
     auto k2 = tc_dkdv_kernel<D, AK>;
     const size_t sm = KvSmem<D>::bytes(g.t_r);
     if ((e = set_smem(k2, sm))) return e;
@@ -1341,7 +1615,7 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
                      const double* row_max, const uint32_t* mask, const void* dout, void* dq,
                      void* dk, void* dv, double* delta, void* workspace, bool delta_only,
                      cudaStream_t st) {
-  CUtensorMap m[12];
+  CUtensorMap m[14];
   cudaError_t e;
   const uint64_t nq = (uint64_t)g.bh * g.n, nk = (uint64_t)g.bh * g.m;
   if ((e = make_tmap_2d(&m[0], q, nq, g.d, BM))) return e;
@@ -1356,6 +1630,8 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   if ((e = make_tmap_2d(&m[9], dout, nq, g.dv, QB_DQ))) return e;
   if ((e = make_tmap_2d(&m[10], k, nk, g.d, 64))) return e;   // 64-key halves (pair dQ)
   if ((e = make_tmap_2d(&m[11], v, nk, g.dv, 64))) return e;
+  if ((e = make_tmap_2d(&m[12], q, nq, g.d, 32))) return e;     // 32-query halves (pair dK/dV)
+  if ((e = make_tmap_2d(&m[13], dout, nq, g.dv, 32))) return e;
   BwdArgs a;
   a.g = g;
   a.ncta_rows = g.n / BM;

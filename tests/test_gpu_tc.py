@@ -232,3 +232,22 @@ def test_tc_dq_cta_pairs_match_single(monkeypatch):
     print("pair vs single dq", err, g1.dq.abs().max().item())
     assert err <= 1e-5 * max(1.0, g1.dq.abs().max().item())
     assert torch.equal(g1.dk, g2.dk) and torch.equal(g1.dv, g2.dv)
+
+
+def test_tc_dkdv_cta_pairs_match_single(monkeypatch):
+    """The CTA-pair dK/dV kernel (cta_group::2, 256 keys per pair) gives the single-CTA
+    kernel's dK and dV (same per-unit arithmetic and query order)."""
+    for causal in (True, False):
+        q, k, v, do = inputs(78, 1, 2, 1024, 128, 1.0)
+        prob = pa.AttentionProblem(q, k, v, path="tc", alpha=1.5, causal=causal)
+        res = pa.forward(prob)
+        monkeypatch.setenv("ADATTN_KV_PAIRS", "0")
+        g1 = pa.backward(prob, res, do)
+        monkeypatch.setenv("ADATTN_KV_PAIRS", "1")
+        g2 = pa.backward(prob, res, do)
+        torch.cuda.synchronize()
+        for n in ("dk", "dv"):
+            a, b = getattr(g1, n), getattr(g2, n)
+            err = (a - b).abs().max().item()
+            print("pair vs single", causal, n, err)
+            assert err <= 1e-5 * max(1.0, a.abs().max().item())
