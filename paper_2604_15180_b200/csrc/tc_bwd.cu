@@ -422,6 +422,238 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
   if (warp == 16) tmem_dealloc(tmem, 512);
 }
 
+// ============================================================ delta (pairs)
+// CTA-pair variant (cta_group::2, d = 128): each CTA keeps its 256 rows (two
+// row groups); the leader's M = 256 MMAs cover row group g of both CTAs, with
+// each SM supplying half of the K_J / V_J tile (keys 64r..64r+63).
+template <int D>
+struct Delta2Smem {
+  static_assert(D == 128, "pair delta kernel: d = 128");
+  static constexpr int QB = BM * D * 2;
+  static constexpr int HB = 64 * D * 2;  // 64 keys x d
+  static constexpr int NST = 5;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_DO = OFF_Q + QB;
+  static constexpr int OFF_RING = OFF_DO + QB;
+  static constexpr int OFF_BAR = OFF_RING + NST * HB;
+  static constexpr int OFF_MISC = OFF_BAR + 32 * 8;
+  static constexpr int OFF_RED = OFF_RING;  // [256] x 2 f64 half-1 partials (ring drained)
+  static constexpr int OFF_MASK = OFF_MISC + 64;
+  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 8 * wpr * 4 + 64; }
+};
+
+template <int D, int AK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
+    tc_delta2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kh,
+                     const __grid_constant__ CUtensorMap tm_vh, const __grid_constant__ CUtensorMap tm_do,
+                     const BwdArgs a) {
+  using L = Delta2Smem<D>;
+  constexpr int NST = L::NST;
+  constexpr int NCH = D / 64;
+  const Geom& g = a.g;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sQ = smem + L::OFF_Q;
+  uint8_t* sDO = smem + L::OFF_DO;
+  uint8_t* sRing = smem + L::OFF_RING;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* full = bars;              // [NST] leader
+  uint64_t* empty = bars + NST;       // [NST] each CTA
+  uint64_t* s_full = bars + 2 * NST;  // [2 rg] each CTA
+  uint64_t* s_free = s_full + 2;      // [2 rg] leader, 16 warps
+  uint64_t* q_full = s_free + 2;      // leader
+  volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
+  double* sRed = reinterpret_cast<double*>(smem + L::OFF_RED);
+  uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [8][wpr]: the pair's row blocks
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool lead_cta = rank == 0;
+  const int wpr = g.wpr;
+  const int npair = a.ncta_rows / 2;
+  const int pair = (int)(blockIdx.x >> 1);
+  const int bh = pair / npair;
+  const int prow0 = (npair - 1 - pair % npair) * 2 * BM;  // heaviest pairs first
+  const int row0 = prow0 + (int)rank * BM;
+  const int nkt = g.m / DBN;
+  const int jmax = g.causal ? (prow0 + 2 * BM - 1) / DBN : nkt - 1;
+
+  for (int i = tid; i < 8 * wpr; i += kDeltaThreads) {
+    const int rbi = i / wpr, w = i - rbi * wpr;
+    smask[i] = a.mask[((size_t)bh * g.t_r + (prow0 / 64 + rbi)) * wpr + w];
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 16);
+    }
+    mbar_init(q_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 16) tmem_alloc_2sm(const_cast<uint32_t*>(s_tmem), 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  // pair row block pb (0..7: CTA pb/4, row group (pb/2)&1), key blocks 2J, 2J+1
+  auto bits2 = [&](int pb, int J) -> uint32_t {
+    return (smask[pb * wpr + ((2 * J) >> 5)] >> ((2 * J) & 31)) & 3u;
+  };
+  auto rg_active = [&](int rg, int J) -> bool {  // row group rg of either CTA
+    return (bits2(2 * rg, J) | bits2(2 * rg + 1, J) | bits2(4 + 2 * rg, J) | bits2(5 + 2 * rg, J)) != 0;
+  };
+  auto next_active = [&](int J) -> int {
+    for (; J <= jmax; ++J)
+      if (rg_active(0, J) || rg_active(1, J)) return J;
+    return -1;
+  };
+
+  if (warp == 16) {  // TMA producer (both CTAs)
+    const bool leader = elect_one_sync();
+    const int qrow = bh * g.n + row0;
+    if (lead_cta && leader) mbar_expect_tx(q_full, 2 * 2 * L::QB);
+    for (int c = 0; c < NCH; ++c) {
+      if (leader) tma_load_2d_2sm(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
+      if (leader) tma_load_2d_2sm(sDO + c * BM * 128, &tm_do, q_full, c * 64, qrow);
+    }
+    uint32_t r = 0;
+    auto load = [&](const CUtensorMap* tm, int row) {
+      const uint32_t st = r % NST, ph = (r / NST) & 1;
+      mbar_wait(&empty[st], ph ^ 1);
+      if (lead_cta && leader) mbar_expect_tx(&full[st], 2 * L::HB);
+      for (int c = 0; c < NCH; ++c)
+        if (leader) tma_load_2d_2sm(sRing + st * L::HB + c * 64 * 128, tm, &full[st], c * 64, row);
+      ++r;
+    };
+    const int krow0 = bh * g.m + 64 * (int)rank;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      load(&tm_kh, krow0 + J * DBN);
+      load(&tm_vh, krow0 + J * DBN);
+    }
+  } else if (warp == 17) {  // MMA issuer: pair leader only
+    if (lead_cta) {
+      const bool leader = elect_one_sync();
+      constexpr uint32_t IDESC_S = idesc_bf16_f32(256, DBN, false, false);
+      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ring_addr = smem_u32(sRing);
+      uint64_t dQd[NCH], dDOd[NCH], dR[NCH];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        dQd[c] = desc_kmajor(q_addr + c * BM * 128);
+        dDOd[c] = desc_kmajor(do_addr + c * BM * 128);
+        dR[c] = desc_kmajor(ring_addr + c * 64 * 128);
+      }
+      constexpr uint32_t kHF = (uint32_t)L::HB >> 4;
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      uint32_t r = 0, uses[2] = {0, 0};
+      for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+        const uint32_t kst = r % NST, vst = (r + 1) % NST;
+        mbar_wait(&full[kst], (r / NST) & 1);
+        mbar_wait(&full[vst], ((r + 1) / NST) & 1);
+        tc_fence_after();
+        const bool act1 = rg_active(1, J);
+        const uint64_t ko = (uint64_t)(kst * kHF), vo = (uint64_t)(vst * kHF);
+#pragma unroll
+        for (int rg = 0; rg < 2; ++rg) {
+          if (!rg_active(rg, J)) continue;
+          mbar_wait(&s_free[rg], (uses[rg] & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t sc = tmem + rg * 256;
+          const uint64_t ro = (uint64_t)(rg * 1024);  // +128 rows (16 KB) in the address field
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (leader)
+                umma2_bf16(sc, dQd[c] + ro + (uint64_t)(2 * k), dR[c] + ko + (uint64_t)(2 * k),
+                           IDESC_S, (c | k) != 0);
+          if (rg == 1 || !act1)
+            if (leader) umma2_commit_mc(&empty[kst]);
+#pragma unroll
+          for (int c = 0; c < NCH; ++c)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (leader)
+                umma2_bf16(sc + 128, dDOd[c] + ro + (uint64_t)(2 * k), dR[c] + vo + (uint64_t)(2 * k),
+                           IDESC_S, (c | k) != 0);
+          if (leader) umma2_commit_mc(&s_full[rg]);
+          ++uses[rg];
+        }
+        if (leader) umma2_commit_mc(&empty[vst]);
+        r += 2;
+      }
+    }
+  } else if (warp < 16) {  // epilogue
+    const int ew = warp;
+    const int rg = ew >> 3;
+    const int half = (ew >> 2) & 1;
+    const int lq = warp & 3;
+    const int e = rg * 128 + lq * 32 + lane;
+    const int rb = e >> 6;                 // own row block 0..3
+    const int pb = 4 * (int)rank + rb;     // pair row block 0..7
+    const int grow = row0 + e;
+    const size_t orow = (size_t)bh * g.n + grow;
+    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + rg * 256 + half * 64;
+    const float A1 = a.A1;
+    const double B = 1.0 - (g.alpha - 1.0) * a.row_max[orow];
+    const float C = (float)(B - a.tau[orow]);
+    const uint32_t s_free_c = mapa_shared(smem_u32(&s_free[rg]), 0);
+    double num = 0.0, den = 0.0;
+    uint32_t uses = 0;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      if (!rg_active(rg, J)) continue;
+      mbar_wait(&s_full[rg], uses & 1);
+      ++uses;
+      tc_fence_after();
+      const bool mine = (bits2(pb, J) >> half) & 1u;
+      const int k0 = J * DBN + half * 64;
+      float s[32], dp[32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tmem_ld32(tl + c * 32, s);
+        tmem_ld32(tl + 128 + c * 32, dp);
+        tmem_wait_ld();
+        if (c == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(s_free_c);
+        }
+        if (mine) {
+          const int c0 = k0 + 32 * c;
+          float n32, d32;
+          if (g.causal && c0 + 31 > grow)
+            delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, grow - c0, n32, d32);
+          else
+            delta_chunk<AK, false>(s, dp, A1, C, a.e0f, a.e1f, 0, n32, d32);
+          num += (double)n32;
+          den += (double)d32;
+        }
+      }
+    }
+    bar_sync(1, 512);
+    if (half == 1) {
+      sRed[2 * e] = num;
+      sRed[2 * e + 1] = den;
+    }
+    bar_sync(1, 512);
+    if (half == 0) {
+      num += sRed[2 * e];
+      den += sRed[2 * e + 1];
+      const double dlt = den > 0.0 ? num / den : 0.0;
+      a.delta[orow] = dlt;
+      a.rowc[orow] = make_float2(C, (float)dlt);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 16) tmem_dealloc_2sm(tmem, 512);
+}
+
 // ===================================================================== dQ
 // Query-major dQ kernel: 128 rows per CTA, 128-key tiles.  Per tile J:
 //   S_J = Q K_J^T (SS, N=128) into S[J&1], dP_J = dO V_J^T into dP,
@@ -1527,6 +1759,15 @@ bool use_dq_pairs(const Geom& g) {
   return env != 0 && g.d == 128 && g.dv == 128 && g.n % (2 * QB_DQ) == 0;
 }
 
+// CTA-pair delta kernel for d = 128, opt-in (ADATTN_DELTA_PAIRS=1): bit-identical but
+// not faster than the single-CTA kernel at C3 (16.8 vs 15.9 ms; the per-group S/dP
+// buffers are released only when both CTAs' epilogues have read them).
+bool use_delta_pairs(const Geom& g, int ncta_rows) {
+  const char* s = std::getenv("ADATTN_DELTA_PAIRS");
+  const int env = s ? std::atoi(s) : 0;
+  return env != 0 && g.d == 128 && g.dv == 128 && ncta_rows % 2 == 0;
+}
+
 // CTA-pair dK/dV kernel for d = 128 (ADATTN_KV_PAIRS=0 selects the single-CTA kernel)
 bool use_kv_pairs(const Geom& g) {
   const char* s = std::getenv("ADATTN_KV_PAIRS");
@@ -1543,7 +1784,16 @@ template <int D, int AK>
 cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool delta_only,
                     cudaStream_t st) {
   cudaError_t e;
-  {
+  if (use_delta_pairs(g, a.ncta_rows)) {
+    auto k0 = tc_delta2_kernel<128, AK>;
+    const size_t sm = Delta2Smem<128>::bytes(g.wpr);
+    if ((e = set_smem(k0, sm))) return e;
+    prof_begin("tc_delta", st);
+    k0<<<dim3((unsigned)(a.ncta_rows * g.bh)), kDeltaThreads, sm, st>>>(m[0], m[10], m[11], m[3], a);
+    prof_end(st);
+    note_launch();
+    if ((e = cudaGetLastError())) return e;
+  } else {
     auto k0 = tc_delta_kernel<D, AK>;
     const size_t sm = DeltaSmem<D>::bytes(g.wpr);
     if ((e = set_smem(k0, sm))) return e;

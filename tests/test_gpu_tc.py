@@ -251,3 +251,20 @@ def test_tc_dkdv_cta_pairs_match_single(monkeypatch):
             err = (a - b).abs().max().item()
             print("pair vs single", causal, n, err)
             assert err <= 1e-5 * max(1.0, a.abs().max().item())
+
+
+def test_tc_delta_cta_pairs_match_single(monkeypatch):
+    """The CTA-pair delta kernel gives the single-CTA kernel's delta."""
+    for causal in (True, False):
+        q, k, v, do = inputs(79, 1, 2, 1024, 128, 1.0)
+        prob = pa.AttentionProblem(q, k, v, path="tc", alpha=1.5, causal=causal)
+        res = pa.forward(prob)
+        monkeypatch.setenv("ADATTN_DELTA_PAIRS", "0")
+        g1 = pa.backward(prob, res, do)
+        monkeypatch.setenv("ADATTN_DELTA_PAIRS", "1")
+        g2 = pa.backward(prob, res, do)
+        torch.cuda.synchronize()
+        err = (g1.delta - g2.delta).abs().max().item()
+        print("pair vs single delta", causal, err)
+        assert err <= 1e-9 * max(1.0, g1.delta.abs().max().item())
+        assert torch.equal(g1.dq, g2.dq)
