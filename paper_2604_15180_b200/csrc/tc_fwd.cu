@@ -42,6 +42,12 @@ namespace adattn_b200 {
 namespace tc {
 namespace {
 
+#ifdef ADATTN_FWD_SLEEP
+#define MBAR_WAIT mbar_wait_sleep
+#else
+#define MBAR_WAIT mbar_wait
+#endif
+
 constexpr int BM = 256;        // query rows per CTA
 constexpr int BN = 128;        // keys per S tile (two 64-key reference tiles)
 constexpr int NST = 4;         // ring stages
@@ -117,7 +123,7 @@ struct FwdSmem {
   static constexpr int OFF_CNT = OFF_RING + NST * TILE;   // [256][16] u32 (HIST combine)
   static constexpr int OFF_PART = OFF_CNT;                // [256][4] f64 (REF combine, reuses)
   static constexpr int OFF_BAR = OFF_CNT + BM * 16 * 4;
-  static constexpr int NBAR = 2 * NST + 18;
+  static constexpr int NBAR = 4 * NST + 20;  // pair ring: 2*NST items of TILE/2
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
   static constexpr int OFF_ROW = OFF_MISC + 64;  // [256][4] f32 per-row scratch
   static constexpr int OFF_MASK = OFF_ROW + BM * 4 * 4;
@@ -126,9 +132,11 @@ struct FwdSmem {
   __host__ __device__ static int off_tmax(int wpr) { return OFF_MASK + 4 * wpr * 4; }
   __host__ __device__ static int off_thr(int wpr, int nkt) { return off_tmax(wpr) + 2 * nkt * 4; }
   __host__ __device__ static int off_act(int wpr, int nkt) { return off_thr(wpr, nkt) + 16; }
-  static size_t bytes(int wpr, int nkt) {
-    return 1024 + off_act(wpr, nkt) + 4 * ((nkt + 31) / 32) * 4 + 64;
-  }
+  // CTA pairs: union activity sets [2][2][aw], union mask [4][wpr], exchange flags [2]
+  __host__ __device__ static int off_actu(int wpr, int nkt) { return off_act(wpr, nkt) + 4 * ((nkt + 31) / 32) * 4; }
+  __host__ __device__ static int off_pm(int wpr, int nkt) { return off_actu(wpr, nkt) + 4 * ((nkt + 31) / 32) * 4; }
+  __host__ __device__ static int off_xf(int wpr, int nkt) { return off_pm(wpr, nkt) + 4 * wpr * 4; }
+  static size_t bytes(int wpr, int nkt) { return 1024 + off_xf(wpr, nkt) + 16 + 64; }
 };
 
 // Order-preserving float <-> u32 (atomicMax / atomicMin on floats in smem).
@@ -231,13 +239,17 @@ __device__ __forceinline__ uint32_t shl_clamp(uint32_t a, uint32_t s) {
 
 // HIST binning of a 32-element slice, nibble-packed.  w = nb c (z + 1) with
 // c = 1 - 2^-20 maps bin k of z (k/nb <= z < (k+1)/nb) to floor(w) = nb + k and
-// z < 0 below nb; fadd.rd(w, 2^23) puts floor(w) in the mantissa, so
-// sh = 4 (bits - (2^23 + nb)) is 4k for counted bins and a huge (clamped)
-// shift for z < 0: one FFMA2 + FADD2 + IMAD + SHF + IADD per element.
+// z < 0 below nb; F = fadd.rd(w, 2^23) = 2^23 + floor(w) exactly, and
+// G = F 2^-147 - (2^23 + nb) 2^-147 = 4k 2^-149 exactly: a denormal whose bit
+// pattern IS the nibble shift 4k (z < 0: negative, sign bit set -> a clamped
+// shift, counted nowhere).  Per element pair: FFMA2 + FADD2.RD + FFMA2 on the
+// FMA pipe and 2 SHF + 1 IADD3 on the ALU pipe (the integer shift-amount
+// arithmetic of a bit-pattern approach would load the ALU pipe, which bounds
+// this sweep).  Needs denormals preserved (no -ftz).
 // Three nibble accumulators (<= 11 elements each) fold into the 8-bit
 // even/odd-bin fields hE (bins 0,2,4,6) / hO (1,3,5,7).
 template <int NW>  // nibble words: bins <= 8 (1) or <= 16 (2)
-__device__ __forceinline__ void hist_nib(const float* v, float2 Aw, float2 Bw, uint32_t K,
+__device__ __forceinline__ void hist_nib(const float* v, float2 Aw, float2 Bw, float2 Kf,
                                          uint32_t* hE, uint32_t* hO) {
   uint32_t n[3][NW];
 #pragma unroll
@@ -245,12 +257,14 @@ __device__ __forceinline__ void hist_nib(const float* v, float2 Aw, float2 Bw, u
 #pragma unroll
     for (int w = 0; w < NW; ++w) n[a][w] = 0;
   const float2 M = make_float2(8388608.f, 8388608.f);
+  const float2 S = make_float2(0x1p-147f, 0x1p-147f);
 #pragma unroll
   for (int x = 0; x < 16; ++x) {
     const float2 wv = __ffma2_rn(Aw, make_float2(v[2 * x], v[2 * x + 1]), Bw);
     const float2 F = __fadd2_rd(wv, M);
-    const uint32_t s0 = __float_as_uint(F.x) * 4u + K;
-    const uint32_t s1 = __float_as_uint(F.y) * 4u + K;
+    const float2 G = __ffma2_rn(F, S, Kf);
+    const uint32_t s0 = __float_as_uint(G.x);
+    const uint32_t s1 = __float_as_uint(G.y);
     const int a0 = (2 * x) < 11 ? 0 : ((2 * x) < 22 ? 1 : 2);
     const int a1 = (2 * x + 1) < 11 ? 0 : ((2 * x + 1) < 22 ? 1 : 2);
 #pragma unroll
@@ -271,7 +285,7 @@ __device__ __forceinline__ void hist_nib(const float* v, float2 Aw, float2 Bw, u
 // bins 0..8NW-1 into cnt[].  Per tile the 8-bit fields (<= 64) fold into
 // 16-bit fields, drained to cnt every 512 tiles.
 template <int NW, typename ActFn, typename TileFn>
-__device__ __forceinline__ void hist_sweep(int jl, float2 Aw, float2 Bw, uint32_t K, uint32_t* cnt,
+__device__ __forceinline__ void hist_sweep(int jl, float2 Aw, float2 Bw, float2 Kf, uint32_t* cnt,
                                            ActFn&& active, TileFn&& tile) {
   uint32_t W[NW][4];
 #pragma unroll
@@ -304,11 +318,16 @@ __device__ __forceinline__ void hist_sweep(int jl, float2 Aw, float2 Bw, uint32_
   drain();
 }
 
-template <int D, int AK>
+template <int D, int AK, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                  const __grid_constant__ CUtensorMap tm_v, const FwdArgs a) {
+                  const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_v,
+                  const FwdArgs a) {
   using L = FwdSmem<D>;
+  static_assert(!PAIR || D == 128, "CTA pairs split K and V tiles in 64-row / 64-column halves");
+  // ring: NST tiles, or (pairs) 2*NST items of half a tile (this CTA's half of K or V)
+  constexpr int NSTR = PAIR ? 2 * NST : NST;
+  constexpr uint32_t ITEM = PAIR ? L::TILE / 2 : L::TILE;
   constexpr int NCH = D / 64;  // 128-byte chunks along d
   const Geom& g = a.g;
   extern __shared__ uint8_t smem_raw[];
@@ -318,15 +337,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sQ = smem + L::OFF_Q;
   uint8_t* sRing = smem + L::OFF_RING;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
-  uint64_t* full = bars;               // [NST]
-  uint64_t* empty = bars + NST;        // [NST]
-  uint64_t* s_full = bars + 2 * NST;   // [2 buffers][2 row groups]
+  uint64_t* full = bars;               // [NSTR]
+  uint64_t* empty = bars + NSTR;       // [NSTR]
+  uint64_t* s_full = bars + 2 * NSTR;  // [2 buffers][2 row groups]
   uint64_t* s_empty = s_full + 4;      // [2][2]
   uint64_t* p_full = s_empty + 4;      // [2 row groups]
   uint64_t* o_full = p_full + 2;
   uint64_t* q_full = o_full + 1;
   uint64_t* dec_bar = q_full + 1;
   uint64_t* plan_bar = dec_bar + 1;  // activity set published (phase 0: HIST, 1: CAND)
+  uint64_t* xbar = plan_bar + 1;     // [2] pair exchanges (the peer arrives)
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
   volatile uint32_t* s_tmem = misc;  // TMEM base
   volatile uint32_t* s_decision = misc + 1;
@@ -338,63 +358,93 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* sTmax = reinterpret_cast<uint32_t*>(smem + L::off_tmax(g.wpr));   // [2][nkt]
   uint32_t* sThr = reinterpret_cast<uint32_t*>(smem + L::off_thr(g.wpr, nkt_));  // [2 sets][2 rg]
   uint32_t* sAct = reinterpret_cast<uint32_t*>(smem + L::off_act(g.wpr, nkt_));  // [2][2][aw]
+  // pairs: the MMAs are joint, so sweeps and the output pass run over the union
+  // of both CTAs' activity sets / masks (extra tiles only add exact zeros)
+  uint32_t* sActU = PAIR ? reinterpret_cast<uint32_t*>(smem + L::off_actu(g.wpr, nkt_)) : sAct;
+  uint32_t* sPm = PAIR ? reinterpret_cast<uint32_t*>(smem + L::off_pm(g.wpr, nkt_)) : smask;
+  volatile uint32_t* xflag = reinterpret_cast<volatile uint32_t*>(smem + L::off_xf(g.wpr, nkt_));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // head-major (the head's K/V stay L2-resident across its CTAs' sweeps),
   // heaviest causal row blocks first within a head
-  const int bh = blockIdx.x / a.ncta_rows;
-  const int crow = a.ncta_rows - 1 - (int)(blockIdx.x % a.ncta_rows);
-  const int row0 = crow * BM;
+  uint32_t rank = 0;
+  if constexpr (PAIR) rank = cluster_ctarank();
+  const bool lead_cta = rank == 0;
+  int bh, row0, lim0;  // lim0: first row of the rows whose causal limits the MMAs follow
+  if constexpr (PAIR) {  // a pair = 512 rows: CTA r owns rows prow0 + 256 r ..
+    const int npair = a.ncta_rows >> 1, pair = (int)(blockIdx.x >> 1);
+    bh = pair / npair;
+    const int prow0 = (npair - 1 - pair % npair) * 2 * BM;
+    row0 = prow0 + (int)rank * BM;
+    lim0 = prow0 + BM;
+  } else {
+    bh = blockIdx.x / a.ncta_rows;
+    row0 = (a.ncta_rows - 1 - (int)(blockIdx.x % a.ncta_rows)) * BM;
+    lim0 = row0;
+  }
   const int nkt = g.m / BN;                              // 128-key tiles
-  const int Jmax = g.causal ? (row0 + BM - 1) / BN : nkt - 1;
+  const int Jmax = g.causal ? (lim0 + BM - 1) / BN : nkt - 1;
   const int wpr = g.wpr;
-  int rg_jlim[2];
-  rg_jlim[0] = g.causal ? (row0 + 127) / BN : nkt - 1;
+  int rg_jlim[2], own_jlim[2];  // tiles issued per row group (pair: CTA 1's rows) / own rows'
+  rg_jlim[0] = g.causal ? (lim0 + 127) / BN : nkt - 1;
   rg_jlim[1] = Jmax;
+  own_jlim[0] = g.causal ? (row0 + 127) / BN : nkt - 1;
+  own_jlim[1] = g.causal ? (row0 + BM - 1) / BN : nkt - 1;
 
   if (tid == 0) {
-    for (int i = 0; i < NST; ++i) {
+    for (int i = 0; i < NSTR; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
+    constexpr uint32_t kArr = PAIR ? 16 : 8;  // epilogue warps of a row group (both CTAs)
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);
+      mbar_init(&s_empty[i], kArr);
     }
-    mbar_init(&p_full[0], 8);
-    mbar_init(&p_full[1], 8);
+    mbar_init(&p_full[0], kArr);
+    mbar_init(&p_full[1], kArr);
     mbar_init(o_full, 1);
     mbar_init(q_full, 1);
     mbar_init(dec_bar, 1);
     mbar_init(plan_bar, 1);
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
     fence_barrier_init();
   }
   for (int i = tid; i < 2 * nkt_; i += kThreads) sTmax[i] = 0u;  // < every encoded float
   if (tid < 4) sThr[tid] = 0xFFFFFFFFu;
-  if (warp == kWarpProd) tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
+  if (warp == kWarpProd) {
+    if constexpr (PAIR) tmem_alloc_2sm(const_cast<uint32_t*>(s_tmem), 512);
+    else tmem_alloc(const_cast<uint32_t*>(s_tmem), 512);
+  }
   if (warp == kWarpProd && lane == 0) {
     prefetch_tmap(&tm_q);
-    prefetch_tmap(&tm_k);
+    prefetch_tmap(PAIR ? &tm_kh : &tm_k);
     prefetch_tmap(&tm_v);
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // both CTAs' barriers initialised before remote arrives / TMA
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
   // threshold-sweep activity: set s (0: HIST, 1: CAND / REF), row group rg, tile J
-  auto act = [&](int s, int rg, int J) -> bool {
-    return (sAct[(s * 2 + rg) * aw + (J >> 5)] >> (J & 31)) & 1u;
+  auto act = [&](int s, int rg, int J) -> bool {  // union (pairs) -- the tiles issued
+    return (sActU[(s * 2 + rg) * aw + (J >> 5)] >> (J & 31)) & 1u;
+  };
+  auto act_own = [&](int s, int rg, int J) -> bool {
+    return !PAIR || ((sAct[(s * 2 + rg) * aw + (J >> 5)] >> (J & 31)) & 1u);
   };
   auto act_any = [&](int s, int J) -> bool { return act(s, 0, J) || act(s, 1, J); };
 
   // output-pass activity of row group rg for 128-key tile J (reference blocks
   // (2rg, 2J), (2rg, 2J+1), (2rg+1, 2J), (2rg+1, 2J+1))
-  auto out_active = [&](int rg, int J) -> bool {
+  auto out_active_m = [&](const uint32_t* m, int rg, int J) -> bool {
     const uint32_t bits = 3u << ((2 * J) & 31);
     const int w = (2 * J) >> 5;
-    return ((smask[(2 * rg) * wpr + w] | smask[(2 * rg + 1) * wpr + w]) & bits) != 0;
+    return ((m[(2 * rg) * wpr + w] | m[(2 * rg + 1) * wpr + w]) & bits) != 0;
   };
+  auto out_active = [&](int rg, int J) -> bool { return out_active_m(sPm, rg, J); };
   auto next_active = [&](int J) -> int {  // first active key tile >= J, or -1
     for (; J <= Jmax; ++J)
       if (out_active(0, J) || out_active(1, J)) return J;
@@ -405,58 +455,87 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ producer
     const bool leader = elect_one_sync();
     const int qrow = bh * g.n + row0;
-    if (leader) mbar_expect_tx(q_full, L::QBYTES);
-    for (int c = 0; c < NCH; ++c)
-      if (leader) tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
+    if (leader && lead_cta) mbar_expect_tx(q_full, (PAIR ? 2 : 1) * L::QBYTES);
+    for (int c = 0; c < NCH; ++c) {
+      if constexpr (PAIR) {
+        if (leader) tma_load_2d_2sm(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
+      } else {
+        if (leader) tma_load_2d(sQ + c * BM * 128, &tm_q, q_full, c * 64, qrow);
+      }
+    }
     uint32_t r = 0;
-    auto load = [&](const CUtensorMap* tm, int row) {
-      const uint32_t st = r % NST, ph = (r / NST) & 1;
+    const int krow0 = bh * g.m;
+    // one ring item: K or V of 128-key tile J (pairs: this CTA's half -- keys
+    // 64 rank .. +63 of K, columns 64 rank .. +63 of V -- completing on the
+    // leader's barrier)
+    auto load = [&](bool is_v, int J) {
+      const uint32_t st = r % NSTR, ph = (r / NSTR) & 1;
       {
         PSTAT_T0();
-        mbar_wait(&empty[st], ph ^ 1);
+        MBAR_WAIT(&empty[st], ph ^ 1);
         PSTAT_ADD(3);
       }
-      if (leader) mbar_expect_tx(&full[st], L::TILE);
-      for (int c = 0; c < NCH; ++c)
-        if (leader) tma_load_2d(sRing + st * L::TILE + c * BN * 128, tm, &full[st], c * 64, row);
+      uint8_t* dst = sRing + st * ITEM;
+      const int row = krow0 + J * BN;
+      if constexpr (PAIR) {
+        if (leader && lead_cta) mbar_expect_tx(&full[st], 2 * ITEM);
+        if (is_v) {
+          if (leader) tma_load_2d_2sm(dst, &tm_v, &full[st], 64 * (int)rank, row);
+        } else {
+          for (int c = 0; c < NCH; ++c)
+            if (leader)
+              tma_load_2d_2sm(dst + c * 64 * 128, &tm_kh, &full[st], c * 64, row + 64 * (int)rank);
+        }
+      } else {
+        if (leader) mbar_expect_tx(&full[st], L::TILE);
+        for (int c = 0; c < NCH; ++c)
+          if (leader) tma_load_2d(dst + c * BN * 128, is_v ? &tm_v : &tm_k, &full[st], c * 64, row);
+      }
       ++r;
     };
-    const int krow0 = bh * g.m;
-    for (int J = 0; J <= Jmax; ++J) load(&tm_k, krow0 + J * BN);  // MAX
-    mbar_wait(plan_bar, 0);
+    for (int J = 0; J <= Jmax; ++J) load(false, J);  // MAX
+    MBAR_WAIT(plan_bar, 0);
     for (int J = 0; J <= Jmax; ++J)  // HIST: tiles that can hold z >= 0
-      if (act_any(0, J)) load(&tm_k, krow0 + J * BN);
-    mbar_wait(plan_bar, 1);
+      if (act_any(0, J)) load(false, J);
+    MBAR_WAIT(plan_bar, 1);
     uint32_t dround = 0;
     bool out_now = false;
     if (a.cand) {  // CAND sweep: tiles that can hold z > lo - eps
       for (int J = 0; J <= Jmax; ++J)
-        if (act_any(1, J)) load(&tm_k, krow0 + J * BN);
-      mbar_wait(dec_bar, 0);
+        if (act_any(1, J)) load(false, J);
+      MBAR_WAIT(dec_bar, 0);
       dround = 1;
       out_now = *s_decision == DEC_OUT;
     }
     if (!out_now)
       for (uint32_t ref = 0;; ++ref) {
         for (int J = 0; J <= Jmax; ++J)
-          if (act_any(1, J)) load(&tm_k, krow0 + J * BN);
-        mbar_wait(dec_bar, (dround + ref) & 1);
+          if (act_any(1, J)) load(false, J);
+        MBAR_WAIT(dec_bar, (dround + ref) & 1);
         if (*s_decision == DEC_OUT) break;
       }
     int prev = -1;
     for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
-      load(&tm_k, krow0 + J * BN);
-      if (prev >= 0) load(&tm_v, krow0 + prev * BN);
+      load(false, J);
+      if (prev >= 0) load(true, prev);
       prev = J;
     }
-    if (prev >= 0) load(&tm_v, krow0 + prev * BN);
-  } else if (warp == kWarpMma) {
+    if (prev >= 0) load(true, prev);
+  } else if (warp == kWarpMma && (!PAIR || lead_cta)) {
     // ------------------------------------------------------------ MMA issuer
+    // (pairs: the leader issues M=256 MMAs over both CTAs' rows)
     const bool leader = elect_one_sync();
-    constexpr uint32_t IDESC_S = idesc_bf16_f32(128, BN, false, false);
-    constexpr uint32_t IDESC_PV = idesc_bf16_f32(128, D, false, true);
+    constexpr uint32_t IDESC_S = idesc_bf16_f32(PAIR ? 256 : 128, BN, false, false);
+    constexpr uint32_t IDESC_PV = idesc_bf16_f32(PAIR ? 256 : 128, D, false, true);
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (PAIR) {
+        if (leader) umma2_commit_mc(bar);
+      } else {
+        if (leader) umma_commit(bar);
+      }
+    };
     const uint32_t q_addr = smem_u32(sQ), ring_addr = smem_u32(sRing);
-    mbar_wait(q_full, 0);
+    MBAR_WAIT(q_full, 0);
     tc_fence_after();
 #ifdef ADATTN_PIPE_STATS
     const long long t_mma0 = clock64();
@@ -475,24 +554,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     int cur_sweep = 0;  // stats: [32+2s] ring waits, [33+2s] S-buffer waits of sweep s
     (void)cur_sweep;
     auto wait_ring = [&]() -> uint32_t {
-      const uint32_t st = r % NST;
+      const uint32_t st = r % NSTR;
       PSTAT_T0();
-      mbar_wait(&full[st], (r / NST) & 1);
+      MBAR_WAIT(&full[st], (r / NSTR) & 1);
       PSTAT_ADD(0);
       PSTAT_ADD(32 + 2 * cur_sweep);
       tc_fence_after();
       return st;
     };
     auto issue_s = [&](uint32_t d_t, int rg, uint32_t st) {
-      const uint64_t dk = dK0 + (uint64_t)((st * (uint32_t)L::TILE) >> 4);
+      const uint64_t dk = dK0 + (uint64_t)((st * ITEM) >> 4);
+      constexpr uint32_t CH = (PAIR ? 64 : BN) * 128;  // bytes per 64-column chunk of d
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (leader)
-            umma_bf16(d_t, dQ[rg][c] + (uint64_t)(2 * k),
-                      dk + (uint64_t)(((uint32_t)(c * BN * 128) >> 4) + 2 * k), IDESC_S,
-                      (c | k) != 0);
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t bk = dk + (uint64_t)(((uint32_t)(c * CH) >> 4) + 2 * k);
+          if constexpr (PAIR) {
+            if (leader) umma2_bf16(d_t, dQ[rg][c] + (uint64_t)(2 * k), bk, IDESC_S, (c | k) != 0);
+          } else {
+            if (leader) umma_bf16(d_t, dQ[rg][c] + (uint64_t)(2 * k), bk, IDESC_S, (c | k) != 0);
+          }
+        }
     };
     // threshold passes: S double buffered per row group
     // Both row groups' S buffers are claimed before either group's MMAs are
@@ -506,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         doit[rg] = !(J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J)));
         if (!doit[rg]) continue;
         PSTAT_T0();
-        mbar_wait(&s_empty[(it[rg] & 1) * 2 + rg], ((it[rg] >> 1) & 1) ^ 1);
+        MBAR_WAIT(&s_empty[(it[rg] & 1) * 2 + rg], ((it[rg] >> 1) & 1) ^ 1);
         PSTAT_ADD(1);
         PSTAT_ADD(33 + 2 * cur_sweep);
       }
@@ -518,13 +601,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         {
           PSTAT_T0();
           issue_s(tmem + b * 256 + rg * 128, rg, st);
-          if (leader) umma_commit(&s_full[b * 2 + rg]);
-          PSTAT_ADD(40 + (cur_sweep == 0 ? 0 : 1));  // [40] MAX, [41] other sweeps: issue cycles
+          commit(&s_full[b * 2 + rg]);
+          PSTAT_ADD(44 + (cur_sweep == 0 ? 0 : 1));  // [44] MAX, [45] other sweeps: issue cycles
         }
         ++it[rg];
         ++nt;
       }
-      if (leader) umma_commit(&empty[st]);
+      commit(&empty[st]);
       ++r;
     };
 #ifdef ADATTN_PIPE_STATS
@@ -545,18 +628,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     for (int J = 0; J <= Jmax; ++J) s_tile(J, -1);  // MAX
     sweep_mark(0);
-    mbar_wait(plan_bar, 0);
+    MBAR_WAIT(plan_bar, 0);
     for (int J = 0; J <= Jmax; ++J)
       if (act_any(0, J)) s_tile(J, 0);  // HIST
     sweep_mark(1);
-    mbar_wait(plan_bar, 1);
+    MBAR_WAIT(plan_bar, 1);
     uint32_t dround = 0;
     bool out_now = false;
     if (a.cand) {  // CAND sweep
       for (int J = 0; J <= Jmax; ++J)
         if (act_any(1, J)) s_tile(J, 1);
       sweep_mark(2);
-      mbar_wait(dec_bar, 0);
+      MBAR_WAIT(dec_bar, 0);
       dround = 1;
       out_now = *s_decision == DEC_OUT;
     }
@@ -564,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t ref = 0;; ++ref) {
         for (int J = 0; J <= Jmax; ++J)
           if (act_any(1, J)) s_tile(J, 1);
-        mbar_wait(dec_bar, (dround + ref) & 1);
+        MBAR_WAIT(dec_bar, (dround + ref) & 1);
         if (*s_decision == DEC_OUT) break;
       }
     sweep_mark(3);  // REF sweeps (fallback) + waiting for the decision
@@ -574,24 +657,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     // and one group's P computation overlaps the other group's MMAs.
     bool o_init[2] = {false, false};
     uint32_t pcnt[2] = {0, 0};
-    const uint64_t dVmn = desc_mnmajor(ring_addr, BN * 128);
+    const uint64_t dVmn = desc_mnmajor(ring_addr, BN * 128);  // (pairs: one 64-column chunk)
     auto pv = [&](int rg, uint32_t vst) {
       {
         PSTAT_T0();
-        mbar_wait(&p_full[rg], pcnt[rg] & 1);
+        MBAR_WAIT(&p_full[rg], pcnt[rg] & 1);
         PSTAT_ADD(2);
       }
       ++pcnt[rg];
       tc_fence_after();
-      const uint64_t bv = dVmn + (uint64_t)((vst * (uint32_t)L::TILE) >> 4);
+      const uint64_t bv = dVmn + (uint64_t)((vst * ITEM) >> 4);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         // keys 16k..16k+15: packed P pairs at TMEM cols rg*128 + 64*(k>>2) + 8*(k&3);
         // a 16-key step of the MN-major V operand is 2048 B = +128
         const uint32_t acol = rg * 128 + 64 * (k >> 2) + 8 * (k & 3);
-        if (leader)
-          umma_bf16_ts(tmem + 256 + rg * D, tmem + acol, bv + (uint64_t)(128 * k), IDESC_PV,
-                       (o_init[rg] || k > 0) ? 1u : 0u);
+        const uint32_t acc = (o_init[rg] || k > 0) ? 1u : 0u;
+        if constexpr (PAIR) {
+          if (leader) umma2_bf16_ts(tmem + 256 + rg * D, tmem + acol, bv + (uint64_t)(128 * k), IDESC_PV, acc);
+        } else {
+          if (leader) umma_bf16_ts(tmem + 256 + rg * D, tmem + acol, bv + (uint64_t)(128 * k), IDESC_PV, acc);
+        }
       }
       o_init[rg] = true;
     };
@@ -601,9 +687,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t kst = wait_ring();  // K(J) is ring item r
       uint32_t vst = 0;
       if (prev >= 0) {
-        vst = (r + 1) % NST;  // V(prev) follows K(J) in the producer's order
+        vst = (r + 1) % NSTR;  // V(prev) follows K(J) in the producer's order
         PSTAT_T0();
-        mbar_wait(&full[vst], ((r + 1) / NST) & 1);
+        MBAR_WAIT(&full[vst], ((r + 1) / NSTR) & 1);
         PSTAT_ADD(0);
         tc_fence_after();
       }
@@ -615,13 +701,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (act[rg]) {
           ++nt;
           issue_s(tmem + rg * 128, rg, kst);
-          if (leader) umma_commit(&s_full[rg]);
+          commit(&s_full[rg]);
         }
       }
-      if (leader) umma_commit(&empty[kst]);
+      commit(&empty[kst]);
       ++r;
       if (prev >= 0) {
-        if (leader) umma_commit(&empty[vst]);
+        commit(&empty[vst]);
         ++r;
       }
       prev = J;
@@ -633,10 +719,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int rg = 0; rg < 2; ++rg)
         if (prev_act[rg]) pv(rg, vst);
-      if (leader) umma_commit(&empty[vst]);
+      commit(&empty[vst]);
       ++r;
     }
-    if (leader) umma_commit(o_full);
+    commit(o_full);
     sweep_mark(4);
 #ifdef ADATTN_PIPE_STATS
     if (leader) {
@@ -654,8 +740,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grow = row0 + e;        // query row within the head
     const int rb = e >> 6;            // 64-row reference tile within the CTA
     const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + rg * 128 + half * 64;
-    const int jl = rg_jlim[rg];
+    const int jl = rg_jlim[rg];       // tiles the MMA warp issues to this row group
+    const int own_jl = own_jlim[rg];  // ... of which this CTA's rows can see (causal)
     const int bar_rg = 1 + rg;        // named barrier of this row group (256 threads)
+    // S-buffer / P handshakes go to the pair leader's barriers (its MMA warp waits on them)
+    auto arrive_mma = [&](uint64_t* bar) {
+      if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+      else mbar_arrive(bar);
+    };
+    // pair exchanges (all epilogue threads): afterwards the peer's shared-memory
+    // state written before its matching exchange is visible through DSMEM
+    uint32_t xk = 0;
+    auto pair_xchg = [&]() {
+      bar_sync(3, kEpi);
+      if (tid == 0) {
+        uint64_t* xb = &xbar[xk & 1];
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        mbar_arrive_cluster_release(mapa_shared(smem_u32(xb), rank ^ 1u));
+        mbar_wait_cluster(xb, (xk >> 1) & 1);
+      }
+      ++xk;
+      bar_sync(3, kEpi);
+    };
+    auto peer_ld = [&](const volatile uint32_t* p) -> uint32_t {
+      return ld_shared_cluster(mapa_shared(smem_u32(const_cast<const uint32_t*>(p)), rank ^ 1u));
+    };
+    auto pair_or = [&](bool v) -> bool {  // v: CTA-uniform
+      if (tid == 0) xflag[xk & 1] = v ? 1u : 0u;
+      pair_xchg();
+      return v || peer_ld(&xflag[(xk - 1) & 1]) != 0u;
+    };
+    auto pair_or_words = [&](uint32_t* dst, const uint32_t* src, int n) {  // dst = src | peer src
+      pair_xchg();
+      for (int i = tid; i < n; i += kEpi) dst[i] = src[i] | peer_ld(&src[i]);
+      bar_sync(3, kEpi);
+    };
+    (void)pair_or;
+    (void)pair_or_words;
     const float A1 = a.A1;
     uint32_t it = 0;                  // threshold tiles consumed (S buffer it & 1, its use it >> 1)
 
@@ -670,18 +791,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     auto load_chunk = [&](uint32_t col, int J, int c) {
+#ifdef ADATTN_PIPE_STATS
+      const long long _tl = clock64();
+#endif
       tmem_ld32(tl + col + c * 32, v);
       tmem_wait_ld();
+#ifdef ADATTN_PIPE_STATS
+      if (tid == 0) {  // [46] TMEM load + wait cycles of thread 0, [47] loads
+        atomicAdd(&g_pipe_stats[46], (unsigned long long)(clock64() - _tl));
+        atomicAdd(&g_pipe_stats[47], 1ull);
+      }
+#endif
       mask_chunk(v, J, c);
     };
     // threshold-pass tile: wait, run body on chunks 0 and 1, release the buffer
-    auto tau_tile = [&](int J, auto&& body) {
+    // (own == false: a tile issued for the peer CTA's rows only -- release it unread)
+    auto tau_tile = [&](int J, bool own, auto&& body) {
       const uint32_t b = it & 1;
+      if (PAIR && !own) {
+        MBAR_WAIT(&s_full[b * 2 + rg], (it >> 1) & 1);
+        ++it;
+        __syncwarp();
+        if (lane == 0) arrive_mma(&s_empty[b * 2 + rg]);
+        return;
+      }
       {
 #ifdef ADATTN_PIPE_STATS
         const long long _tw = clock64();
 #endif
-        mbar_wait(&s_full[b * 2 + rg], (it >> 1) & 1);
+        MBAR_WAIT(&s_full[b * 2 + rg], (it >> 1) & 1);
 #ifdef ADATTN_PIPE_STATS
         if (warp == 0 && lane == 0) atomicAdd(&g_pipe_stats[4], (unsigned long long)(clock64() - _tw));
 #endif
@@ -693,7 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       load_chunk(b * 256, J, 1);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[b * 2 + rg]);
+      if (lane == 0) arrive_mma(&s_empty[b * 2 + rg]);
       body(static_cast<const float*>(v));
     };
 
@@ -707,10 +845,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     float mraw = -CUDART_INF_F;
     for (int J = 0; J <= jl; ++J) {
       float tmx = -CUDART_INF_F;
-      tau_tile(J, [&](const float* v) {
+      const bool own = J <= own_jl;
+      tau_tile(J, own, [&](const float* v) {
 #pragma unroll
         for (int i = 0; i < 32; i += 2) tmx = fmaxf(tmx, fmaxf(v[i], v[i + 1]));
       });
+      if (!own) continue;
       mraw = fmaxf(mraw, tmx);
       tmx = warp_max(tmx);
       if (lane == 0) atomicMax(&sTmax[rg * nkt_ + J], f2ord(tmx));
@@ -736,11 +876,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t bits = 0;
         for (int b = 0; b < 32; ++b) {
           const int J = 32 * w + b;
-          if (J <= rg_jlim[r] && sTmax[r * nkt_ + J] >= th) bits |= 1u << b;
+          if (J <= own_jlim[r] && sTmax[r * nkt_ + J] >= th) bits |= 1u << b;
         }
         sAct[(s * 2 + r) * aw + w] = bits;
       }
       bar_sync(3, kEpi);
+      if constexpr (PAIR) pair_or_words(sActU + s * 2 * aw, sAct + s * 2 * aw, 2 * aw);
       if (tid == 0) mbar_arrive(plan_bar);
     };
     {
@@ -760,16 +901,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 Aw = make_float2(A1 * (float)nb * cw, A1 * (float)nb * cw);
       const float bw = (float)((B + 1.0) * (double)nb * (double)cw);
       const float2 Bw = make_float2(bw, bw);
-      const uint32_t K = 0u - 4u * (0x4B000000u + (uint32_t)nb);
+      const float kf = -(0x1p-124f + (float)nb * 0x1p-147f);  // -(2^23 + nb) 2^-147, exact
+      const float2 K = make_float2(kf, kf);
       if (nb <= 8)
         hist_sweep<1>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
                       [&](int J, uint32_t* hE, uint32_t* hO) {
-          tau_tile(J, [&](const float* v) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
+          tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
         });
       else
         hist_sweep<2>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
                       [&](int J, uint32_t* hE, uint32_t* hO) {
-          tau_tile(J, [&](const float* v) { hist_nib<2>(v, Aw, Bw, K, hE, hO); });
+          tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<2>(v, Aw, Bw, K, hE, hO); });
         });
     }
     PASS_MARK(1);
@@ -836,42 +978,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool ovf = (int)smid >= a.cand_slots;  // (uniform: one CTA per SM)
       int cnt = 0;
       {
-        uint32_t ucnt = 0;
+        uint2* wp = lst;  // next free entry
         for (int J = 0; J <= jl; ++J) {
           if (!act(1, rg, J)) continue;
           const uint32_t blk = (uint32_t)(2 * J + half);
           // a tile appends <= 64 entries; warp-uniform (the append votes are warp-collective)
-          ovf = __any_sync(0xffffffffu, ovf || (int)ucnt > cap - 64);
-          tau_tile(J, [&](const float* v) {
+          ovf = __any_sync(0xffffffffu, ovf || (int)(wp - lst) > cap - 64);
+          tau_tile(J, act_own(1, rg, J), [&](const float* v) {
             if (ovf) return;
             // candidates are rare (~0.3% of scores): a warp vote per column
             // keeps the common path at compare + vote + branch
 #pragma unroll
             for (int i = 0; i < 32; i += 2)
               asm volatile(
-                  "{\n\t.reg .pred p0, p1, pa, q;\n\t.reg .u64 ad;\n\t"
+                  "{\n\t.reg .pred p0, p1, pa, q;\n\t"
                   "setp.gt.f32 p0, %1, %3;\n\t"
                   "setp.gt.f32 p1, %2, %3;\n\t"
                   "or.pred pa, p0, p1;\n\t"
                   "vote.sync.any.pred q, pa, 0xffffffff;\n\t"
                   "@!q bra.uni CAND_SKIP_%=;\n\t"
-                  "mad.wide.u32 ad, %0, 8, %4;\n\t"
-                  "@p0 st.global.v2.b32 [ad], {%5, %7};\n\t"
-                  "@p0 add.u32 %0, %0, 1;\n\t"
-                  "mad.wide.u32 ad, %0, 8, %4;\n\t"
-                  "@p1 st.global.v2.b32 [ad], {%6, %7};\n\t"
-                  "@p1 add.u32 %0, %0, 1;\n\t"
+                  "@p0 st.global.v2.b32 [%0], {%4, %6};\n\t"
+                  "@p0 add.u64 %0, %0, 8;\n\t"
+                  "@p1 st.global.v2.b32 [%0], {%5, %6};\n\t"
+                  "@p1 add.u64 %0, %0, 8;\n\t"
                   "CAND_SKIP_%=:\n\t}"
-                  : "+r"(ucnt)
-                  : "f"(v[i]), "f"(v[i + 1]), "f"(theta), "l"(lst), "r"(__float_as_uint(v[i])),
+                  : "+l"(wp)
+                  : "f"(v[i]), "f"(v[i + 1]), "f"(theta), "r"(__float_as_uint(v[i])),
                     "r"(__float_as_uint(v[i + 1])), "r"(blk)
                   : "memory");
           });
         }
-        cnt = (int)ucnt;
+        cnt = (int)(wp - lst);
       }
       PASS_MARK(2);
-      const bool ovf_any = bar_red_or(4, kEpi, ovf);
+      bool ovf_any = bar_red_or(4, kEpi, ovf);
+      if constexpr (PAIR) ovf_any = pair_or(ovf_any);  // both CTAs take the same path
       if (!ovf_any) {
         // The K ring is idle until the decision (producer and MMA warps wait on
         // dec_bar): stage each thread's first `lcap` listed scores there
@@ -963,6 +1104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       PASS_MARK(3);
       bar_sync(3, kEpi);
+      if (PAIR && list_ok) pair_or_words(sPm, smask, 4 * wpr);
       if (tid == 0) {
         *s_decision = list_ok ? DEC_OUT : DEC_REF;
         mbar_arrive(dec_bar);
@@ -980,7 +1122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int J = 0; J <= jl; ++J) {
         if (!act(1, rg, J)) continue;
         float mx_t = -CUDART_INF_F;
-        tau_tile(J, [&](const float* v) {
+        tau_tile(J, act_own(1, rg, J), [&](const float* v) {
           float s0, s1, s2, mx;
           ref_slice<AK>(v, A1, C, a.e0f, a.e1f, a.e2f, s0, s1, s2, mx);
           if (first_pass && need_sec) {
@@ -1018,7 +1160,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         sRow[e * 4 + 2] = (float)(B - rs.tau);
       }
       first_pass = false;
-      const bool any = bar_red_or(4, kEpi, stepped);
+      bool any = bar_red_or(4, kEpi, stepped);
+      if constexpr (PAIR) {
+        any = pair_or(any);
+        if (!any) pair_or_words(sPm, smask, 4 * wpr);
+      }
       if (tid == 0) {
         *s_decision = any ? DEC_REF : DEC_OUT;
         mbar_arrive(dec_bar);
@@ -1036,17 +1182,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
         if (!out_active(rg, J)) continue;
         any_out = true;
-        mbar_wait(&s_full[rg], ob & 1);  // output-pass S lives in buffer 0
+        // pairs: a tile active for the peer's rows only gets P = 0 without reading S
+        const bool own = !PAIR || out_active_m(smask, rg, J);
+        MBAR_WAIT(&s_full[rg], ob & 1);  // output-pass S lives in buffer 0
         ++ob;
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          load_chunk(0, J, c);
           uint32_t pk[16];
+          if (own) {
+            load_chunk(0, J, c);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 t = __ffma2_rn(A2, make_float2(v[2 * i], v[2 * i + 1]), C2);
-            pk[i] = pack_bf16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f));
+            for (int i = 0; i < 16; ++i) {
+              const float2 t = __ffma2_rn(A2, make_float2(v[2 * i], v[2 * i + 1]), C2);
+              pk[i] = pack_bf16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f));
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
           }
           // packed P of keys 64*half + 32c .. +31 -> TMEM cols 64*half + 16c .. +15
           tmem_st16(tl + c * 16, pk);
@@ -1054,11 +1207,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[rg]);
+        if (lane == 0) arrive_mma(&p_full[rg]);
       }
       // write O (fp32 or fp64): this thread's half of the row's dv columns
       const size_t orow = (size_t)bh * g.n + grow;
-      mbar_wait(o_full, 0);
+      MBAR_WAIT(o_full, 0);
       PASS_MARK(5);
       tc_fence_after();
       const bool written = __any_sync(0xffffffffu, any_out);
@@ -1097,34 +1250,65 @@ __global__ void __launch_bounds__(kThreads, 1)
     PASS_MARK(6);
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == kWarpProd) tmem_dealloc(tmem, 512);
+  if constexpr (PAIR) {
+    cluster_sync();  // the pair's MMAs, remote arrives and DSMEM reads are done
+    if (warp == kWarpProd) tmem_dealloc_2sm(tmem, 512);
+  } else {
+    __syncthreads();
+    if (warp == kWarpProd) tmem_dealloc(tmem, 512);
+  }
 }
 
-template <int D, int AK>
+template <int D, int AK, bool PAIR>
 cudaError_t launch_fwd(const Geom& g, const CUtensorMap& tq, const CUtensorMap& tk,
-                       const CUtensorMap& tv, const FwdArgs& a, cudaStream_t st) {
+                       const CUtensorMap& tkh, const CUtensorMap& tv, const FwdArgs& a,
+                       cudaStream_t st) {
   const size_t smem = FwdSmem<D>::bytes(g.wpr, g.m / BN);
-  auto kern = tc_fwd_kernel<D, AK>;
+  auto kern = tc_fwd_kernel<D, AK, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
   const dim3 grid((unsigned)(a.ncta_rows * g.bh));
   prof_begin("tc_fwd", st);
-  kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, a);
+  if constexpr (PAIR) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tkh, tv, a);
+  } else {
+    kern<<<grid, kThreads, smem, st>>>(tq, tk, tkh, tv, a);
+  }
   prof_end(st);
   note_launch();
-  return cudaGetLastError();
+  return e ? e : cudaGetLastError();
 }
 
-template <int D>
+template <int D, bool PAIR>
 cudaError_t launch_fwd_d(const Geom& g, int ak, const CUtensorMap& tq, const CUtensorMap& tk,
-                         const CUtensorMap& tv, const FwdArgs& a, cudaStream_t st) {
+                         const CUtensorMap& tkh, const CUtensorMap& tv, const FwdArgs& a,
+                         cudaStream_t st) {
   switch (ak) {
-    case AK15: return launch_fwd<D, AK15>(g, tq, tk, tv, a, st);
-    case AK2: return launch_fwd<D, AK2>(g, tq, tk, tv, a, st);
-    case AK125: return launch_fwd<D, AK125>(g, tq, tk, tv, a, st);
-    default: return launch_fwd<D, AKGEN>(g, tq, tk, tv, a, st);
+    case AK15: return launch_fwd<D, AK15, PAIR>(g, tq, tk, tkh, tv, a, st);
+    case AK2: return launch_fwd<D, AK2, PAIR>(g, tq, tk, tkh, tv, a, st);
+    case AK125: return launch_fwd<D, AK125, PAIR>(g, tq, tk, tkh, tv, a, st);
+    default: return launch_fwd<D, AKGEN, PAIR>(g, tq, tk, tkh, tv, a, st);
   }
+}
+
+// CTA pairs for the forward (ADATTN_FWD_PAIRS=0/1 overrides the default)
+bool use_fwd_pairs(const Geom& g) {
+  if (g.d != 128 || g.dv != 128 || (g.n / BM) % 2 != 0) return false;
+  const char* s = std::getenv("ADATTN_FWD_PAIRS");
+  if (s && *s) return s[0] != '0';
+  return true;  // C3: forward 41.1 -> 37.0 ms (tools/ab.py, interleaved medians)
 }
 
 }  // namespace
@@ -1139,10 +1323,11 @@ int alpha_kind(double alpha) {
 cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                     double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,
                     cudaStream_t st) {
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tkh, tv;
   cudaError_t e;
   if ((e = make_tmap_2d(&tq, q, (uint64_t)g.bh * g.n, g.d, BM))) return e;
   if ((e = make_tmap_2d(&tk, k, (uint64_t)g.bh * g.m, g.d, BN))) return e;
+  if ((e = make_tmap_2d(&tkh, k, (uint64_t)g.bh * g.m, g.d, 64))) return e;
   if ((e = make_tmap_2d(&tv, v, (uint64_t)g.bh * g.m, g.dv, BN))) return e;
   FwdArgs a;
   a.g = g;
@@ -1162,8 +1347,9 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.cand_cap = cp.cap;
   a.cand_slots = cp.slots;
   const int ak = alpha_kind(g.alpha);
-  if (g.d == 64) return launch_fwd_d<64>(g, ak, tq, tk, tv, a, st);
-  return launch_fwd_d<128>(g, ak, tq, tk, tv, a, st);
+  if (g.d == 64) return launch_fwd_d<64, false>(g, ak, tq, tk, tkh, tv, a, st);
+  if (use_fwd_pairs(g)) return launch_fwd_d<128, true>(g, ak, tq, tk, tkh, tv, a, st);
+  return launch_fwd_d<128, false>(g, ak, tq, tk, tkh, tv, a, st);
 }
 
 }  // namespace tc

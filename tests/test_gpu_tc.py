@@ -268,3 +268,49 @@ def test_tc_delta_cta_pairs_match_single(monkeypatch):
         print("pair vs single delta", causal, err)
         assert err <= 1e-9 * max(1.0, g1.delta.abs().max().item())
         assert torch.equal(g1.dq, g2.dq)
+
+
+FWD_PAIR_CASES = [
+    # (B, H, N, alpha, causal, qscale, cand_cap)
+    (1, 2, 2048, 1.5, True, 1.0, None),
+    (1, 2, 2048, 1.5, False, 1.0, None),
+    (1, 1, 1024, 2.0, True, 1.0, None),
+    (1, 1, 1024, 1.25, True, 1.0, None),
+    (1, 1, 1024, 1.75, False, 4.0, None),
+    (1, 1, 2048, 1.5, True, 1.0, "0"),    # REF sweeps only
+    (1, 2, 2048, 1.5, True, 1.0, "64"),   # some CTAs overflow: the pair falls back together
+    (1, 1, 8192, 1.5, True, 0.6, None),
+]
+
+
+@pytest.mark.parametrize("case", FWD_PAIR_CASES, ids=[str(c) for c in FWD_PAIR_CASES])
+def test_tc_fwd_cta_pairs_match_single(case, monkeypatch):
+    """The CTA-pair forward (cta_group::2: M=256 MMAs over two CTAs' rows, each
+    SM holding half of every K / V tile) gives the single-CTA forward's
+    thresholds, masks and outputs.  Sweeps and the output pass run over the
+    union of the two CTAs' activity sets, which only adds exact zeros; when one
+    CTA of a pair overflows its candidate list both take the sweep refinement,
+    which agrees with the list refinement to fp32 summation order."""
+    B, H, N, alpha, causal, qs, cap = case
+    q, k, v, _ = inputs(hash(case) % 977 + 3, B, H, N, 128, qs)
+    if cap is None:
+        monkeypatch.delenv("ADATTN_CAND_CAP", raising=False)
+    else:
+        monkeypatch.setenv("ADATTN_CAND_CAP", cap)
+    monkeypatch.setenv("ADATTN_FWD_PAIRS", "0")
+    _, r1, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_FWD_PAIRS", "1")
+    _, r2, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
+    tau_err = (r1.tau - r2.tau).abs().max().item()
+    out_err = (r1.out - r2.out).abs().max().item()
+    print(case, f"pair vs single: tau {tau_err:.2e} out {out_err:.2e}")
+    assert torch.equal(r1.row_max, r2.row_max)
+    if cap == "64":
+        assert tau_err <= 1e-6 and out_err <= 1e-5
+        nd = (r1.mask.words != r2.mask.words).sum().item()
+        assert nd <= max(1, r1.mask.words.numel() // 1000)
+    else:
+        assert torch.equal(r1.tau, r2.tau)
+        assert torch.equal(r1.row_steps, r2.row_steps)
+        assert torch.equal(r1.mask.words, r2.mask.words)
+        assert torch.equal(r1.out, r2.out)

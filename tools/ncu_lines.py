@@ -36,3 +36,6 @@ print(f"samples {TS:.0f} warp-instr {TI:.3e}")
 print("by instructions executed:")
 for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
     print(f"  {100*v[1]/TI:5.1f}%I {100*v[0]/TS:5.1f}%S {k[0]}:{k[1]} {k[2]}")
+print("by stall samples:")
+for k, v in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
+    print(f"  {100*v[1]/TI:5.1f}%I {100*v[0]/TS:5.1f}%S {k[0]}:{k[1]} {k[2]}")

@@ -41,4 +41,5 @@ for s, n in enumerate(["MAX", "HIST", "CAND", "REF/decision", "OUT (S+PV)"]):
               f"  ring-wait/tile {st[32 + 2 * s] / tiles:7.1f}  S-buffer-wait/tile {st[33 + 2 * s] / tiles:7.1f}")
     else:
         print(f"MMA sweep {n:13s} cycles {cyc}")
-print("MMA issue+commit cycles per rg-tile: MAX", st[40] / max(st[17], 1), "HIST+CAND", st[41] / max(st[19] + st[21], 1))
+print("MMA issue+commit cycles per rg-tile: MAX", st[44] / max(st[17], 1), "HIST+CAND", st[45] / max(st[19] + st[21], 1))
+print("epilogue thread 0: TMEM ld32+wait cycles per load", st[46] / max(st[47], 1), "loads", st[47])
