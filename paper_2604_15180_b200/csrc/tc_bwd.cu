@@ -66,6 +66,21 @@ struct BwdArgs {
 
 enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 
+// Compensated (Kahan) fp32 running sum: the per-row delta sums see one add per
+// 32-key chunk, and an FP64 add per chunk stalled the delta epilogue on the
+// FP64 pipe (ncu: DADD held ~30% of the warp-stall samples).  The compensated
+// fp32 sum keeps the error at the level of the fp32 chunk partials themselves.
+struct KahanF {
+  float s = 0.f, c = 0.f;
+  __device__ __forceinline__ void add(float x) {
+    const float y = x - c;
+    const float t = s + y;
+    c = (t - s) - y;
+    s = t;
+  }
+  __device__ __forceinline__ double get() const { return (double)s - (double)c; }
+};
+
 // u = p^(2-alpha) = t^(e0-1) for t > 0, else 0; p = t^e0
 template <int AK>
 __device__ __forceinline__ void pu_of(float t, float e0f, float e1f, float& p, float& u) {
@@ -369,7 +384,7 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
     const float A1 = a.A1;
     const double B = 1.0 - (g.alpha - 1.0) * a.row_max[orow];
     const float C = (float)(B - a.tau[orow]);
-    double num = 0.0, den = 0.0;
+    KahanF num, den;  // fp32 compensated sums of the fp32 chunk partials (no FP64 pipe)
     uint32_t uses = 0;
     for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
       if (!rg_active(rg, J)) continue;
@@ -396,8 +411,8 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
             delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, grow - c0, n32, d32);
           else
             delta_chunk<AK, false>(s, dp, A1, C, a.e0f, a.e1f, 0, n32, d32);
-          num += (double)n32;
-          den += (double)d32;
+          num.add(n32);
+          den.add(d32);
         }
       }
     }
@@ -405,14 +420,14 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
     // reads) are complete, so the ring can hold the half-1 partials
     bar_sync(1, 512);
     if (half == 1) {
-      sRed[2 * e] = num;
-      sRed[2 * e + 1] = den;
+      sRed[2 * e] = num.get();
+      sRed[2 * e + 1] = den.get();
     }
     bar_sync(1, 512);
     if (half == 0) {
-      num += sRed[2 * e];
-      den += sRed[2 * e + 1];
-      const double dlt = den > 0.0 ? num / den : 0.0;
+      const double nm = num.get() + sRed[2 * e];
+      const double dn = den.get() + sRed[2 * e + 1];
+      const double dlt = dn > 0.0 ? nm / dn : 0.0;
       a.delta[orow] = dlt;
       a.rowc[orow] = make_float2(C, (float)dlt);
     }
@@ -603,7 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
     const double B = 1.0 - (g.alpha - 1.0) * a.row_max[orow];
     const float C = (float)(B - a.tau[orow]);
     const uint32_t s_free_c = mapa_shared(smem_u32(&s_free[rg]), 0);
-    double num = 0.0, den = 0.0;
+    KahanF num, den;  // fp32 compensated sums of the fp32 chunk partials (no FP64 pipe)
     uint32_t uses = 0;
     for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
       if (!rg_active(rg, J)) continue;
@@ -630,21 +645,240 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
             delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, grow - c0, n32, d32);
           else
             delta_chunk<AK, false>(s, dp, A1, C, a.e0f, a.e1f, 0, n32, d32);
-          num += (double)n32;
-          den += (double)d32;
+          num.add(n32);
+          den.add(d32);
         }
       }
     }
     bar_sync(1, 512);
     if (half == 1) {
-      sRed[2 * e] = num;
-      sRed[2 * e + 1] = den;
+      sRed[2 * e] = num.get();
+      sRed[2 * e + 1] = den.get();
     }
     bar_sync(1, 512);
     if (half == 0) {
-      num += sRed[2 * e];
-      den += sRed[2 * e + 1];
-      const double dlt = den > 0.0 ? num / den : 0.0;
+      const double nm = num.get() + sRed[2 * e];
+      const double dn = den.get() + sRed[2 * e + 1];
+      const double dlt = dn > 0.0 ? nm / dn : 0.0;
+      a.delta[orow] = dlt;
+      a.rowc[orow] = make_float2(C, (float)dlt);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 16) tmem_dealloc_2sm(tmem, 512);
+}
+
+// ============================================================ delta (pairs, 128 rows)
+// CTA-pair variant with 128 query rows per CTA (256 per pair): the leader's
+// M = 256 MMAs cover both CTAs' rows, each SM holds half of every K_J / V_J
+// tile, and with one row group per CTA the TMEM holds TWO S/dP buffers, so the
+// MMAs of tile J+1 never wait for the epilogue of tile J (the 256-row kernels
+// single-buffer S/dP per row group).  16 epilogue warps: TMEM lane quarter x
+// 32-key column quarter of the 128-key tile.
+template <int D>
+struct Delta3Smem {
+  static_assert(D == 128, "pair delta kernel: d = 128");
+  static constexpr int QB = 128 * D * 2;
+  static constexpr int HB = 64 * D * 2;  // 64 keys x d
+  static constexpr int NST = 8;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_DO = OFF_Q + QB;
+  static constexpr int OFF_RING = OFF_DO + QB;
+  static constexpr int OFF_BAR = OFF_RING + NST * HB;
+  static constexpr int OFF_MISC = OFF_BAR + 32 * 8;
+  static constexpr int OFF_RED = OFF_RING;  // [4][128] x 2 f64 partials (ring drained)
+  static constexpr int OFF_MASK = OFF_MISC + 64;
+  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
+};
+
+template <int D, int AK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
+    tc_delta3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kh,
+                     const __grid_constant__ CUtensorMap tm_vh, const __grid_constant__ CUtensorMap tm_do,
+                     const BwdArgs a) {
+  using L = Delta3Smem<D>;
+  constexpr int NST = L::NST;
+  constexpr int NCH = D / 64;
+  constexpr int QR = 128;  // query rows per CTA
+  const Geom& g = a.g;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sQ = smem + L::OFF_Q;
+  uint8_t* sDO = smem + L::OFF_DO;
+  uint8_t* sRing = smem + L::OFF_RING;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* full = bars;              // [NST] leader
+  uint64_t* empty = bars + NST;       // [NST] each CTA
+  uint64_t* s_full = bars + 2 * NST;  // [2 buffers] each CTA
+  uint64_t* s_free = s_full + 2;      // [2 buffers] leader, 32 warps
+  uint64_t* q_full = s_free + 2;      // leader
+  volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
+  double* sRed = reinterpret_cast<double*>(smem + L::OFF_RED);
+  uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [4][wpr]: the pair's row blocks
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool lead_cta = rank == 0;
+  const int wpr = g.wpr;
+  const int npair = g.n / (2 * QR);
+  const int pair = (int)(blockIdx.x >> 1);
+  const int bh = pair / npair;
+  const int prow0 = (npair - 1 - pair % npair) * 2 * QR;  // heaviest pairs first
+  const int row0 = prow0 + (int)rank * QR;
+  const int nkt = g.m / DBN;
+  const int jmax = g.causal ? (prow0 + 2 * QR - 1) / DBN : nkt - 1;
+
+  for (int i = tid; i < 4 * wpr; i += kDeltaThreads) {
+    const int rbi = i / wpr, w = i - rbi * wpr;
+    smask[i] = a.mask[((size_t)bh * g.t_r + (prow0 / 64 + rbi)) * wpr + w];
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 32);
+    }
+    mbar_init(q_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 16) tmem_alloc_2sm(const_cast<uint32_t*>(s_tmem), 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  // pair row block pb (0..3: CTA pb/2), key blocks 2J, 2J+1
+  auto bits2 = [&](int pb, int J) -> uint32_t {
+    return (smask[pb * wpr + ((2 * J) >> 5)] >> ((2 * J) & 31)) & 3u;
+  };
+  auto next_active = [&](int J) -> int {
+    for (; J <= jmax; ++J)
+      if (bits2(0, J) | bits2(1, J) | bits2(2, J) | bits2(3, J)) return J;
+    return -1;
+  };
+
+  if (warp == 16) {  // TMA producer (both CTAs)
+    const bool leader = elect_one_sync();
+    const int qrow = bh * g.n + row0;
+    if (lead_cta && leader) mbar_expect_tx(q_full, 2 * 2 * L::QB);
+    for (int c = 0; c < NCH; ++c) {
+      if (leader) tma_load_2d_2sm(sQ + c * QR * 128, &tm_q, q_full, c * 64, qrow);
+      if (leader) tma_load_2d_2sm(sDO + c * QR * 128, &tm_do, q_full, c * 64, qrow);
+    }
+    uint32_t r = 0;
+    auto load = [&](const CUtensorMap* tm, int row) {
+      const uint32_t st = r % NST, ph = (r / NST) & 1;
+      mbar_wait(&empty[st], ph ^ 1);
+      if (lead_cta && leader) mbar_expect_tx(&full[st], 2 * L::HB);
+      for (int c = 0; c < NCH; ++c)
+        if (leader) tma_load_2d_2sm(sRing + st * L::HB + c * 64 * 128, tm, &full[st], c * 64, row);
+      ++r;
+    };
+    const int krow0 = bh * g.m + 64 * (int)rank;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      load(&tm_kh, krow0 + J * DBN);
+      load(&tm_vh, krow0 + J * DBN);
+    }
+  } else if (warp == 17) {  // MMA issuer: pair leader only
+    if (lead_cta) {
+      const bool leader = elect_one_sync();
+      constexpr uint32_t IDESC_S = idesc_bf16_f32(256, DBN, false, false);
+      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ring_addr = smem_u32(sRing);
+      uint64_t dQd[NCH], dDOd[NCH], dR[NCH];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        dQd[c] = desc_kmajor(q_addr + c * QR * 128);
+        dDOd[c] = desc_kmajor(do_addr + c * QR * 128);
+        dR[c] = desc_kmajor(ring_addr + c * 64 * 128);
+      }
+      constexpr uint32_t kHF = (uint32_t)L::HB >> 4;
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      uint32_t r = 0, t = 0;
+      for (int J = next_active(0); J >= 0; J = next_active(J + 1), ++t) {
+        const uint32_t kst = r % NST, vst = (r + 1) % NST, b = t & 1;
+        mbar_wait(&full[kst], (r / NST) & 1);
+        mbar_wait(&s_free[b], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint64_t ko = (uint64_t)(kst * kHF), vo = (uint64_t)(vst * kHF);
+        const uint32_t sc = tmem + b * 256;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (leader)
+              umma2_bf16(sc, dQd[c] + (uint64_t)(2 * k), dR[c] + ko + (uint64_t)(2 * k), IDESC_S,
+                         (c | k) != 0);
+        if (leader) umma2_commit_mc(&empty[kst]);
+        mbar_wait(&full[vst], ((r + 1) / NST) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (leader)
+              umma2_bf16(sc + 128, dDOd[c] + (uint64_t)(2 * k), dR[c] + vo + (uint64_t)(2 * k),
+                         IDESC_S, (c | k) != 0);
+        if (leader) umma2_commit_mc(&s_full[b]);
+        if (leader) umma2_commit_mc(&empty[vst]);
+        r += 2;
+      }
+    }
+  } else if (warp < 16) {  // epilogue
+    const int lq = warp & 3;              // TMEM lane quarter
+    const int cq = warp >> 2;             // keys 32 cq .. +31 of each 128-key tile
+    const int e = lq * 32 + lane;         // local row 0..127
+    const int pb = 2 * (int)rank + (e >> 6);  // pair row block 0..3
+    const int grow = row0 + e;
+    const size_t orow = (size_t)bh * g.n + grow;
+    const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + cq * 32;
+    const float A1 = a.A1;
+    const double B = 1.0 - (g.alpha - 1.0) * a.row_max[orow];
+    const float C = (float)(B - a.tau[orow]);
+    const uint32_t s_free_c0 = mapa_shared(smem_u32(&s_free[0]), 0);
+    const uint32_t s_free_c1 = mapa_shared(smem_u32(&s_free[1]), 0);
+    KahanF num, den;  // fp32 compensated sums of the fp32 chunk partials (no FP64 pipe)
+    uint32_t t = 0;
+    for (int J = next_active(0); J >= 0; J = next_active(J + 1), ++t) {
+      const uint32_t b = t & 1;
+      mbar_wait(&s_full[b], (t >> 1) & 1);
+      tc_fence_after();
+      float s[32], dp[32];
+      tmem_ld32(tl + b * 256, s);
+      tmem_ld32(tl + b * 256 + 128, dp);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(b ? s_free_c1 : s_free_c0);
+      if ((bits2(pb, J) >> (cq >> 1)) & 1u) {  // the reference visits set blocks only
+        const int c0 = J * DBN + 32 * cq;
+        float n32, d32;
+        if (g.causal && c0 + 31 > grow)
+          delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, grow - c0, n32, d32);
+        else
+          delta_chunk<AK, false>(s, dp, A1, C, a.e0f, a.e1f, 0, n32, d32);
+        num.add(n32);
+        den.add(d32);
+      }
+    }
+    // every epilogue thread has passed its last s_full wait: the pair's MMAs
+    // reading this CTA's ring are complete, so the ring can hold the partials
+    bar_sync(1, 512);
+    sRed[(cq * 128 + e) * 2] = num.get();
+    sRed[(cq * 128 + e) * 2 + 1] = den.get();
+    bar_sync(1, 512);
+    if (cq == 0) {
+      double nm = 0.0, dn = 0.0;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        nm += sRed[(q4 * 128 + e) * 2];
+        dn += sRed[(q4 * 128 + e) * 2 + 1];
+      }
+      const double dlt = dn > 0.0 ? nm / dn : 0.0;
       a.delta[orow] = dlt;
       a.rowc[orow] = make_float2(C, (float)dlt);
     }
@@ -1762,10 +1996,12 @@ bool use_dq_pairs(const Geom& g) {
 // CTA-pair delta kernel for d = 128, opt-in (ADATTN_DELTA_PAIRS=1): bit-identical but
 // not faster than the single-CTA kernel at C3 (16.8 vs 15.9 ms; the per-group S/dP
 // buffers are released only when both CTAs' epilogues have read them).
-bool use_delta_pairs(const Geom& g, int ncta_rows) {
+// delta kernel: 0 single-CTA (256 rows), 1 pair (256 rows per CTA), 2 pair with
+// 128 rows per CTA and double-buffered S/dP (ADATTN_DELTA_PAIRS overrides)
+int delta_mode(const Geom& g, int ncta_rows) {
+  if (g.d != 128 || g.dv != 128 || ncta_rows % 2 != 0) return 0;
   const char* s = std::getenv("ADATTN_DELTA_PAIRS");
-  const int env = s ? std::atoi(s) : 0;
-  return env != 0 && g.d == 128 && g.dv == 128 && ncta_rows % 2 == 0;
+  return s && *s ? std::atoi(s) : 1;  // C3: 15.1 (single) / 11.4 (1) / 12.6 (2) ms
 }
 
 // CTA-pair dK/dV kernel for d = 128 (ADATTN_KV_PAIRS=0 selects the single-CTA kernel)
@@ -1784,7 +2020,17 @@ template <int D, int AK>
 cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool delta_only,
                     cudaStream_t st) {
   cudaError_t e;
-  if (use_delta_pairs(g, a.ncta_rows)) {
+  const int dmode = delta_mode(g, a.ncta_rows);
+  if (dmode == 2) {
+    auto k0 = tc_delta3_kernel<128, AK>;
+    const size_t sm = Delta3Smem<128>::bytes(g.wpr);
+    if ((e = set_smem(k0, sm))) return e;
+    prof_begin("tc_delta", st);
+    k0<<<dim3((unsigned)((g.n / 128) * g.bh)), kDeltaThreads, sm, st>>>(m[8], m[10], m[11], m[9], a);
+    prof_end(st);
+    note_launch();
+    if ((e = cudaGetLastError())) return e;
+  } else if (dmode == 1) {
     auto k0 = tc_delta2_kernel<128, AK>;
     const size_t sm = Delta2Smem<128>::bytes(g.wpr);
     if ((e = set_smem(k0, sm))) return e;

@@ -112,6 +112,7 @@ struct FwdArgs {
   uint2* cand;
   int cand_cap;
   int cand_slots;
+  int sep_issue;
 };
 
 template <int D>
@@ -584,6 +585,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto s_tile = [&](int J, int set) {  // set < 0: every tile (MAX)
       const uint32_t st = wait_ring();
       bool doit[2];
+      if (a.sep_issue) {  // experiment: each row group waits for its own buffer only
+#pragma unroll
+        for (int rg = 0; rg < 2; ++rg) {
+          if (J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J))) continue;
+          const uint32_t b = it[rg] & 1;
+          MBAR_WAIT(&s_empty[b * 2 + rg], ((it[rg] >> 1) & 1) ^ 1);
+          tc_fence_after();
+          issue_s(tmem + b * 256 + rg * 128, rg, st);
+          commit(&s_full[b * 2 + rg]);
+          ++it[rg];
+          ++nt;
+        }
+        commit(&empty[st]);
+        ++r;
+        return;
+      }
 #pragma unroll
       for (int rg = 0; rg < 2; ++rg) {
         doit[rg] = !(J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J)));
@@ -906,7 +923,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (nb <= 8)
         hist_sweep<1>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
                       [&](int J, uint32_t* hE, uint32_t* hO) {
+#ifdef ADATTN_EXP_HIST_EMPTY
+          tau_tile(J, act_own(0, rg, J), [&](const float* v) { hE[0] += __float_as_uint(v[0]) & 1u; });
+#else
           tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
+#endif
         });
       else
         hist_sweep<2>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
@@ -1346,6 +1367,10 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.cand = (cp.cap > 0 && ws) ? reinterpret_cast<uint2*>(ws) : nullptr;
   a.cand_cap = cp.cap;
   a.cand_slots = cp.slots;
+  {
+    const char* e = std::getenv("ADATTN_FWD_SEP");
+    a.sep_issue = (e && *e == '1') ? 1 : 0;
+  }
   const int ak = alpha_kind(g.alpha);
   if (g.d == 64) return launch_fwd_d<64, false>(g, ak, tq, tk, tkh, tv, a, st);
   if (use_fwd_pairs(g)) return launch_fwd_d<128, true>(g, ak, tq, tk, tkh, tv, a, st);

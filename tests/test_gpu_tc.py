@@ -253,21 +253,31 @@ def test_tc_dkdv_cta_pairs_match_single(monkeypatch):
             assert err <= 1e-5 * max(1.0, a.abs().max().item())
 
 
-def test_tc_delta_cta_pairs_match_single(monkeypatch):
-    """The CTA-pair delta kernel gives the single-CTA kernel's delta."""
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_tc_delta_cta_pairs_match_single(monkeypatch, mode):
+    """The CTA-pair delta kernels (mode 1: 256 rows per CTA; mode 2: 128 rows
+    per CTA, double-buffered S/dP) give the single-CTA kernel's delta: the same
+    fp32 32-key partial sums, combined in a different order in mode 2."""
     for causal in (True, False):
-        q, k, v, do = inputs(79, 1, 2, 1024, 128, 1.0)
-        prob = pa.AttentionProblem(q, k, v, path="tc", alpha=1.5, causal=causal)
-        res = pa.forward(prob)
-        monkeypatch.setenv("ADATTN_DELTA_PAIRS", "0")
-        g1 = pa.backward(prob, res, do)
-        monkeypatch.setenv("ADATTN_DELTA_PAIRS", "1")
-        g2 = pa.backward(prob, res, do)
-        torch.cuda.synchronize()
-        err = (g1.delta - g2.delta).abs().max().item()
-        print("pair vs single delta", causal, err)
-        assert err <= 1e-9 * max(1.0, g1.delta.abs().max().item())
-        assert torch.equal(g1.dq, g2.dq)
+        for alpha in (1.5, 2.0, 1.25):
+            q, k, v, do = inputs(79, 1, 2, 1024, 128, 1.0)
+            prob = pa.AttentionProblem(q, k, v, path="tc", alpha=alpha, causal=causal)
+            res = pa.forward(prob)
+            monkeypatch.setenv("ADATTN_DELTA_PAIRS", "0")
+            g1 = pa.backward(prob, res, do)
+            monkeypatch.setenv("ADATTN_DELTA_PAIRS", mode)
+            g2 = pa.backward(prob, res, do)
+            torch.cuda.synchronize()
+            err = (g1.delta - g2.delta).abs().max().item()
+            print("pair vs single delta", mode, causal, alpha, err)
+            # mode 2 combines four compensated fp32 column-quarter sums instead of two
+            tol = 1e-12 if mode == "1" else 1e-6
+            assert err <= tol * max(1.0, g1.delta.abs().max().item())
+            if mode == "1":
+                assert torch.equal(g1.dq, g2.dq)
+            for n in ("dq", "dk", "dv"):
+                a, b = getattr(g1, n), getattr(g2, n)
+                assert (a - b).abs().max().item() <= 1e-5 * max(1.0, a.abs().max().item())
 
 
 FWD_PAIR_CASES = [

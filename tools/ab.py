@@ -25,11 +25,14 @@ q, k, v, do = (workloads.gaussian(B, H, N, 128, 1.0, seed=1) if beta is None
                else workloads.anchored(B, H, N, 128, float(beta), True, seed=1))
 p = pa.AttentionProblem(q, k, v, alpha=alpha, causal=True)
 ts = {a: [] for a, _, _ in vars_}
+kts = {a: {} for a, _, _ in vars_}
 for rep in range(reps + 1):
     for a, lib, env in vars_:
         L._lib = lib
         old = {kk: os.environ.get(kk) for kk in env}
         os.environ.update(env)
+        L.profile_read()
+        L.profile_enable(True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         r = pa.forward(p)
@@ -37,6 +40,11 @@ for rep in range(reps + 1):
             pa.backward(p, r, do)
         e1.record()
         e1.synchronize()
+        L.profile_enable(False)
+        kt = L.profile_read()
+        if rep:
+            for name, ms in kt:
+                kts[a].setdefault(name, []).append(ms)
         for kk, vv in old.items():
             if vv is None:
                 os.environ.pop(kk, None)
@@ -49,3 +57,4 @@ for a, _, _ in vars_:
     m = statistics.median(ts[a])
     base = base or m
     print(f"{a:60s} median {m:8.2f} ms  ({m / base:.3f})  min {min(ts[a]):.2f} max {max(ts[a]):.2f}")
+    print("    " + "  ".join(f"{k} {statistics.median(v):.2f}" for k, v in kts[a].items()))
