@@ -38,6 +38,24 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// [rows x cols] bf16 row-major viewed as (64 cols, rows, cols/64 chunks): one
+// box of `box_rows` rows carries every 64-column chunk, landing in shared memory
+// chunk-major ([chunk][row][64 cols], SWIZZLE_128B) -- the layout of
+// cols/64 separate 2-D boxes, in one TMA instruction.
+cudaError_t make_tmap_3d_chunks(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                                uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[3] = {64, rows, cols / 64};
+  cuuint64_t strides[2] = {cols * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, (cuuint32_t)(cols / 64)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 namespace {
 __global__ void nsmid_probe(int* out) {
   uint32_t v;

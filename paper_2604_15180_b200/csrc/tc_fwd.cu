@@ -72,6 +72,37 @@ enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 __device__ unsigned long long g_pipe_stats[48];
 __device__ int g_cur_sweep_dummy;
 #endif
+#ifdef ADATTN_PIPE_TRACE
+// event trace of CTA 0 (dev tool): per tracing thread a private 16K-entry
+// region (role), fire-and-forget stores of type << 56 | tile << 40 | clock64
+__device__ unsigned long long g_trace[64 << 12];
+__device__ unsigned int g_trace_n;
+inline void* g_trace_ptr() {
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_trace);
+  return p;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// role: 0 producer, 1 MMA, 2 + warp (epilogue warps); +32 for CTA 1 of the pair
+#define TRACE(role, type, J)                                                                \
+  if (blockIdx.x < 2 && _tn < (1u << 12)) {                                                 \
+    g_trace[(((role) + 32 * blockIdx.x) << 12) + _tn++] =                                   \
+        ((unsigned long long)(type) << 56) | ((unsigned long long)((J) & 0xFFFF) << 40) |   \
+        ((unsigned long long)clock64() & 0xFFFFFFFFFFull);                                  \
+  }
+#define TRACE_DECL unsigned _tn = 0
+#else
+#define TRACE(role, type, J) \
+  do {                       \
+  } while (0)
+#define TRACE_DECL \
+  do {             \
+  } while (0)
+#endif
 namespace {
 #ifdef ADATTN_PIPE_STATS
 #define PSTAT_T0() const long long _t0 = clock64()
@@ -465,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     uint32_t r = 0;
+    TRACE_DECL;
     const int krow0 = bh * g.m;
     // one ring item: K or V of 128-key tile J (pairs: this CTA's half -- keys
     // 64 rank .. +63 of K, columns 64 rank .. +63 of V -- completing on the
@@ -475,6 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         PSTAT_T0();
         MBAR_WAIT(&empty[st], ph ^ 1);
         PSTAT_ADD(3);
+        if (leader) TRACE(0, 1, J);
       }
       uint8_t* dst = sRing + st * ITEM;
       const int row = krow0 + J * BN;
@@ -483,9 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (is_v) {
           if (leader) tma_load_2d_2sm(dst, &tm_v, &full[st], 64 * (int)rank, row);
         } else {
-          for (int c = 0; c < NCH; ++c)
-            if (leader)
-              tma_load_2d_2sm(dst + c * 64 * 128, &tm_kh, &full[st], c * 64, row + 64 * (int)rank);
+          if (leader) tma_load_3d_2sm(dst, &tm_kh, &full[st], row + 64 * (int)rank);
         }
       } else {
         if (leader) mbar_expect_tx(&full[st], L::TILE);
@@ -544,6 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // it[rg]: threshold tiles issued to row group rg (S buffer b = it & 1, that
     // buffer's previous uses = it >> 1); indices stay compile-time (no local memory)
     uint32_t it[2] = {0, 0}, r = 0, nt = 0;  // nt: row-group tiles issued (stats)
+    TRACE_DECL;
     // operand descriptors, precomputed: the start-address field advances 2 (32 B)
     // per 16-element K step
     uint64_t dQ[2][NCH];
@@ -566,17 +598,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_s = [&](uint32_t d_t, int rg, uint32_t st) {
       const uint64_t dk = dK0 + (uint64_t)((st * ITEM) >> 4);
       constexpr uint32_t CH = (PAIR ? 64 : BN) * 128;  // bytes per 64-column chunk of d
+      if constexpr (D == 128) {
+        if (leader)
+          umma_ss_d128<(PAIR ? 2 : 1), ((BM * 128) >> 4), ((int)(CH >> 4))>(d_t, dQ[rg][0], dk, IDESC_S, 0u);
+      } else {
 #pragma unroll
-      for (int c = 0; c < NCH; ++c)
+        for (int c = 0; c < NCH; ++c)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint64_t bk = dk + (uint64_t)(((uint32_t)(c * CH) >> 4) + 2 * k);
-          if constexpr (PAIR) {
-            if (leader) umma2_bf16(d_t, dQ[rg][c] + (uint64_t)(2 * k), bk, IDESC_S, (c | k) != 0);
-          } else {
-            if (leader) umma_bf16(d_t, dQ[rg][c] + (uint64_t)(2 * k), bk, IDESC_S, (c | k) != 0);
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t bk = dk + (uint64_t)(((uint32_t)(c * CH) >> 4) + 2 * k);
+            if constexpr (PAIR) {
+              if (leader) umma2_bf16(d_t, dQ[rg][c] + (uint64_t)(2 * k), bk, IDESC_S, (c | k) != 0);
+            } else {
+              if (leader) umma_bf16(d_t, dQ[rg][c] + (uint64_t)(2 * k), bk, IDESC_S, (c | k) != 0);
+            }
           }
-        }
+      }
     };
     // threshold passes: S double buffered per row group
     // Both row groups' S buffers are claimed before either group's MMAs are
@@ -584,6 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // queues only about one MMA ahead: any gap in the issue stream idles it).
     auto s_tile = [&](int J, int set) {  // set < 0: every tile (MAX)
       const uint32_t st = wait_ring();
+      if (leader) TRACE(1, 2, J);
       bool doit[2];
       if (a.sep_issue) {  // experiment: each row group waits for its own buffer only
 #pragma unroll
@@ -606,10 +644,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         doit[rg] = !(J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J)));
         if (!doit[rg]) continue;
         PSTAT_T0();
+        if (leader) TRACE(1, 12 + rg, J);
         MBAR_WAIT(&s_empty[(it[rg] & 1) * 2 + rg], ((it[rg] >> 1) & 1) ^ 1);
+        if (leader) TRACE(1, 14 + rg, J);
         PSTAT_ADD(1);
         PSTAT_ADD(33 + 2 * cur_sweep);
       }
+      if (leader) TRACE(1, 3, J);
       tc_fence_after();
 #pragma unroll
       for (int rg = 0; rg < 2; ++rg) {
@@ -620,6 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           issue_s(tmem + b * 256 + rg * 128, rg, st);
           commit(&s_full[b * 2 + rg]);
           PSTAT_ADD(44 + (cur_sweep == 0 ? 0 : 1));  // [44] MAX, [45] other sweeps: issue cycles
+          if (leader) TRACE(1, 4 + rg, J);
         }
         ++it[rg];
         ++nt;
@@ -762,7 +804,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int bar_rg = 1 + rg;        // named barrier of this row group (256 threads)
     // S-buffer / P handshakes go to the pair leader's barriers (its MMA warp waits on them)
     auto arrive_mma = [&](uint64_t* bar) {
-      if constexpr (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
+      if (PAIR && !lead_cta) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
       else mbar_arrive(bar);
     };
     // pair exchanges (all epilogue threads): afterwards the peer's shared-memory
@@ -796,6 +838,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     (void)pair_or_words;
     const float A1 = a.A1;
     uint32_t it = 0;                  // threshold tiles consumed (S buffer it & 1, its use it >> 1)
+    TRACE_DECL;
 
     float v[32];
     // 32-key chunk c (0/1) of this thread's 64 keys of tile J, from buffer column base
@@ -840,6 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef ADATTN_PIPE_STATS
         if (warp == 0 && lane == 0) atomicAdd(&g_pipe_stats[4], (unsigned long long)(clock64() - _tw));
 #endif
+        if (lane == 0) TRACE(2 + warp, 6 + rg, J);
       }
       ++it;
       tc_fence_after();
@@ -849,7 +893,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) arrive_mma(&s_empty[b * 2 + rg]);
+      if (lane == 0) TRACE(2 + warp, 8 + rg, J);
       body(static_cast<const float*>(v));
+      if (lane == 0) TRACE(2 + warp, 10 + rg, J);
     };
 
 #ifdef ADATTN_PIPE_STATS
@@ -1348,7 +1394,7 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   cudaError_t e;
   if ((e = make_tmap_2d(&tq, q, (uint64_t)g.bh * g.n, g.d, BM))) return e;
   if ((e = make_tmap_2d(&tk, k, (uint64_t)g.bh * g.m, g.d, BN))) return e;
-  if ((e = make_tmap_2d(&tkh, k, (uint64_t)g.bh * g.m, g.d, 64))) return e;
+  if ((e = make_tmap_3d_chunks(&tkh, k, (uint64_t)g.bh * g.m, g.d, 64))) return e;
   if ((e = make_tmap_2d(&tv, v, (uint64_t)g.bh * g.m, g.dv, BN))) return e;
   FwdArgs a;
   a.g = g;
@@ -1380,6 +1426,14 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
 }  // namespace tc
 }  // namespace adattn_b200
 
+#ifdef ADATTN_PIPE_TRACE
+extern "C" unsigned adattn_b200_trace_read(unsigned long long* out, int reset) {
+  const unsigned n = 64u << 12;
+  if (out) cudaMemcpyFromSymbol(out, adattn_b200::tc::g_trace, sizeof(unsigned long long) * n);
+  if (reset) cudaMemset(adattn_b200::tc::g_trace_ptr(), 0, sizeof(unsigned long long) * n);
+  return n;
+}
+#endif
 #ifdef ADATTN_PIPE_STATS
 extern "C" void adattn_b200_pipe_stats(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, adattn_b200::tc::g_pipe_stats, sizeof(unsigned long long) * 48);

@@ -13,6 +13,8 @@ namespace tc {
 // (128 B, SWIZZLE_128B) x box_rows rows.
 cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
                          uint32_t box_rows);
+cudaError_t make_tmap_3d_chunks(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                                uint32_t box_rows);
 
 int alpha_kind(double alpha);
 
