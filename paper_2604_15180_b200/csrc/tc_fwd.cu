@@ -57,8 +57,15 @@ constexpr int kEpi = kEpiWarps * 32;
 // (also TMEM alloc), 17 MMA issuer.  The MMA warp has the highest id: the
 // scheduler's arbitration favours high warp ids, so MMA issue is not starved
 // by the ALU-heavy epilogue warps sharing its SM sub-partition.
+// Two MMA-issuing warps (17: row group 0, 18: row group 1), on different SM
+// sub-partitions: the tensor pipe queues only about one MMA ahead, so every
+// cycle an issuing warp spends outside tcgen05.mma (barrier waits, commits,
+// bookkeeping -- and the issue slots it loses to the ALU-heavy epilogue warps
+// of its sub-partition) idles the pipe; two independent issuers fill each
+// other's gaps.
+constexpr bool kDualMma = true;
 constexpr int kWarpProd = kEpiWarps, kWarpMma = kEpiWarps + 1;
-constexpr int kThreads = (kEpiWarps + 2) * 32;
+constexpr int kThreads = (kEpiWarps + (kDualMma ? 3 : 2)) * 32;
 constexpr int DEC_REF = 0, DEC_OUT = 1;
 
 enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
@@ -143,7 +150,6 @@ struct FwdArgs {
   uint2* cand;
   int cand_cap;
   int cand_slots;
-  int sep_issue;
 };
 
 template <int D>
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     for (int i = 0; i < NSTR; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], kDualMma ? 2 : 1);  // a commit from each MMA warp
     }
     constexpr uint32_t kArr = PAIR ? 16 : 8;  // epilogue warps of a row group (both CTAs)
     for (int i = 0; i < 4; ++i) {
@@ -435,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&p_full[0], kArr);
     mbar_init(&p_full[1], kArr);
-    mbar_init(o_full, 1);
+    mbar_init(o_full, kDualMma ? 2 : 1);
     mbar_init(q_full, 1);
     mbar_init(dec_bar, 1);
     mbar_init(plan_bar, 1);
@@ -553,9 +559,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       prev = J;
     }
     if (prev >= 0) load(true, prev);
-  } else if (warp == kWarpMma && (!PAIR || lead_cta)) {
-    // ------------------------------------------------------------ MMA issuer
-    // (pairs: the leader issues M=256 MMAs over both CTAs' rows)
+  } else if ((warp == kWarpMma || (kDualMma && warp == kWarpMma + 1)) && (!PAIR || lead_cta)) {
+    // ------------------------------------------------------------ MMA issuers
+    // (pairs: the leader issues M=256 MMAs over both CTAs' rows).  rgm: the row
+    // groups this warp issues for; both warps walk every ring item.
+    const uint32_t rgm = kDualMma ? (1u << (warp - kWarpMma)) : 3u;
     const bool leader = elect_one_sync();
     constexpr uint32_t IDESC_S = idesc_bf16_f32(PAIR ? 256 : 128, BN, false, false);
     constexpr uint32_t IDESC_PV = idesc_bf16_f32(PAIR ? 256 : 128, D, false, true);
@@ -623,25 +631,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t st = wait_ring();
       if (leader) TRACE(1, 2, J);
       bool doit[2];
-      if (a.sep_issue) {  // experiment: each row group waits for its own buffer only
-#pragma unroll
-        for (int rg = 0; rg < 2; ++rg) {
-          if (J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J))) continue;
-          const uint32_t b = it[rg] & 1;
-          MBAR_WAIT(&s_empty[b * 2 + rg], ((it[rg] >> 1) & 1) ^ 1);
-          tc_fence_after();
-          issue_s(tmem + b * 256 + rg * 128, rg, st);
-          commit(&s_full[b * 2 + rg]);
-          ++it[rg];
-          ++nt;
-        }
-        commit(&empty[st]);
-        ++r;
-        return;
-      }
 #pragma unroll
       for (int rg = 0; rg < 2; ++rg) {
-        doit[rg] = !(J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J)));
+        doit[rg] = ((rgm >> rg) & 1u) && !(J > rg_jlim[rg] || (set >= 0 && !act(set, rg, J)));
         if (!doit[rg]) continue;
         PSTAT_T0();
         if (leader) TRACE(1, 12 + rg, J);
@@ -755,6 +747,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool act[2];
 #pragma unroll
       for (int rg = 0; rg < 2; ++rg) {
+        if (!((rgm >> rg) & 1u)) {
+          act[rg] = false;
+          continue;
+        }
         if (prev >= 0 && prev_act[rg]) pv(rg, vst);
         act[rg] = out_active(rg, J);
         if (act[rg]) {
@@ -1375,7 +1371,9 @@ bool use_fwd_pairs(const Geom& g) {
   if (g.d != 128 || g.dv != 128 || (g.n / BM) % 2 != 0) return false;
   const char* s = std::getenv("ADATTN_FWD_PAIRS");
   if (s && *s) return s[0] != '0';
-  return true;  // C3: forward 41.1 -> 37.0 ms (tools/ab.py, interleaved medians)
+  // With two MMA-issuing warps the single-CTA forward is the faster one at C3
+  // (35.4 vs 37.9 ms, tools/ab.py); before, pairs won (37.0 vs 41.1 ms).
+  return false;
 }
 
 }  // namespace
@@ -1413,10 +1411,7 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.cand = (cp.cap > 0 && ws) ? reinterpret_cast<uint2*>(ws) : nullptr;
   a.cand_cap = cp.cap;
   a.cand_slots = cp.slots;
-  {
-    const char* e = std::getenv("ADATTN_FWD_SEP");
-    a.sep_issue = (e && *e == '1') ? 1 : 0;
-  }
+
   const int ak = alpha_kind(g.alpha);
   if (g.d == 64) return launch_fwd_d<64, false>(g, ak, tq, tk, tkh, tv, a, st);
   if (use_fwd_pairs(g)) return launch_fwd_d<128, true>(g, ak, tq, tk, tkh, tv, a, st);
