@@ -168,6 +168,9 @@ struct HostCtx {
   void* buf[16] = {};
   size_t cap[16] = {};
   cudaStream_t stream = nullptr;
+  static constexpr int kMaxChunks = 8;
+  cudaStream_t streams[3] = {};  // host->device, kernels, device->host
+  cudaEvent_t in_ready[kMaxChunks] = {}, done[kMaxChunks] = {};
   void* get(int slot, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (cap[slot] < bytes) {
@@ -462,8 +465,16 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
   if (path < 0) return -path;
   HostCtx& c = host_ctx();
   std::lock_guard<std::mutex> lock(c.mu);
-  if (!c.stream && cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking) != cudaSuccess)
-    return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: stream create failed");
+  if (!c.stream) {
+    for (int i = 0; i < 3; ++i)
+      if (cudaStreamCreateWithFlags(&c.streams[i], cudaStreamNonBlocking) != cudaSuccess)
+        return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: stream create failed");
+    c.stream = c.streams[1];
+    for (int i = 0; i < HostCtx::kMaxChunks; ++i)
+      if (cudaEventCreateWithFlags(&c.in_ready[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c.done[i], cudaEventDisableTiming) != cudaSuccess)
+        return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: event create failed");
+  }
   const size_t ei = elem_size(p->in_dtype), eo = elem_size(p->out_dtype);
   const size_t BH = (size_t)g.bh;
   const size_t nq = BH * g.n * g.d, nk = BH * g.m * g.d, nv = BH * g.m * g.dv;
@@ -476,44 +487,81 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
   double* dTau = (double*)c.get(4, nrow * 8);
   double* dRm = (double*)c.get(5, nrow * 8);
   uint32_t* dMask = (uint32_t*)c.get(6, mwords * 4);
-  const size_t wsf = adattn_b200_forward_workspace(p);
-  const size_t wsb = adattn_b200_backward_workspace(p);
+  void *dDO = nullptr, *dDQ = nullptr, *dDK = nullptr, *dDV = nullptr;
+  double* dDl = nullptr;
+  if (dout) {
+    dDO = c.get(8, no * ei);
+    dDQ = c.get(9, nq * eo);
+    dDK = c.get(10, nk * eo);
+    dDV = c.get(11, nv * eo);
+    dDl = (double*)c.get(12, nrow * 8);
+    if (!dDO || !dDQ || !dDK || !dDV || !dDl)
+      return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: device allocation failed");
+  }
+  // Heads are independent: the call runs as a pipeline over chunks of heads on
+  // three streams -- host->device copies of chunk i+1 and device->host copies
+  // of chunk i-1 overlap the kernels of chunk i.  Each chunk is a sub-problem
+  // (batch 1, `hc` heads) over the same buffers at the chunk's offset.
+  int nch = (int)std::min<size_t>((size_t)HostCtx::kMaxChunks, BH);
+  while (nch > 1 && (BH % (size_t)nch != 0 || BH / (size_t)nch < 4)) --nch;
+  const size_t hc = BH / (size_t)nch;
+  adattn_problem sp = *p;
+  sp.batch = 1;
+  sp.heads = (int32_t)hc;
+  const size_t wsf = adattn_b200_forward_workspace(&sp);
+  const size_t wsb = adattn_b200_backward_workspace(&sp);
   void* ws = c.get(7, std::max(wsf, wsb));
   if (!dQ || !dK || !dV || !dO || !dTau || !dRm || !dMask || !ws)
     return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: device allocation failed");
-  cudaStream_t st = c.stream;
-  cudaMemcpyAsync(dQ, q, nq * ei, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(dK, k, nk * ei, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(dV, v, nv * ei, cudaMemcpyHostToDevice, st);
-  rc = adattn_b200_forward(p, dQ, dK, dV, dO, dTau, dRm, dMask, nullptr, ws, std::max(wsf, wsb),
-                           st);
-  if (rc) return rc;
-  if (dout) {
-    void* dDO = c.get(8, no * ei);
-    void* dDQ = c.get(9, nq * eo);
-    void* dDK = c.get(10, nk * eo);
-    void* dDV = c.get(11, nv * eo);
-    double* dDl = (double*)c.get(12, nrow * 8);
-    if (!dDO || !dDQ || !dDK || !dDV || !dDl)
-      return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: device allocation failed");
-    cudaMemcpyAsync(dDO, dout, no * ei, cudaMemcpyHostToDevice, st);
-    rc = adattn_b200_backward(p, dQ, dK, dV, dTau, dRm, dMask, dDO, dDQ, dDK, dDV, dDl, ws,
-                              std::max(wsf, wsb), st);
+  cudaStream_t sin = c.streams[0], sc = c.streams[1], sout = c.streams[2];
+  auto cb = [](const void* base, size_t off) { return (const char*)base + off; };
+  auto mb = [](void* base, size_t off) { return (char*)base + off; };
+  const size_t cq = hc * g.n * g.d * ei, ck = hc * g.m * g.d * ei, cv = hc * g.m * g.dv * ei;
+  const size_t cdo = hc * g.n * g.dv * ei, co = hc * g.n * g.dv * eo;
+  const size_t cgq = hc * g.n * g.d * eo, cgk = hc * g.m * g.d * eo, cgv = hc * g.m * g.dv * eo;
+  const size_t crow = hc * g.n, cmw = hc * g.t_r * g.wpr;
+  for (int i = 0; i < nch; ++i) {
+    const size_t h = (size_t)i;
+    cudaMemcpyAsync(mb(dQ, h * cq), cb(q, h * cq), cq, cudaMemcpyHostToDevice, sin);
+    cudaMemcpyAsync(mb(dK, h * ck), cb(k, h * ck), ck, cudaMemcpyHostToDevice, sin);
+    cudaMemcpyAsync(mb(dV, h * cv), cb(v, h * cv), cv, cudaMemcpyHostToDevice, sin);
+    if (dout) cudaMemcpyAsync(mb(dDO, h * cdo), cb(dout, h * cdo), cdo, cudaMemcpyHostToDevice, sin);
+    cudaEventRecord(c.in_ready[i], sin);
+    cudaStreamWaitEvent(sc, c.in_ready[i], 0);
+    rc = adattn_b200_forward(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv), mb(dO, h * co),
+                             dTau + h * crow, dRm + h * crow, dMask + h * cmw, nullptr, ws,
+                             std::max(wsf, wsb), sc);
     if (rc) return rc;
-    if (dq) cudaMemcpyAsync(dq, dDQ, nq * eo, cudaMemcpyDeviceToHost, st);
-    if (dk) cudaMemcpyAsync(dk, dDK, nk * eo, cudaMemcpyDeviceToHost, st);
-    if (dv) cudaMemcpyAsync(dv, dDV, nv * eo, cudaMemcpyDeviceToHost, st);
-    if (delta) cudaMemcpyAsync(delta, dDl, nrow * 8, cudaMemcpyDeviceToHost, st);
+    if (dout) {
+      rc = adattn_b200_backward(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv),
+                                dTau + h * crow, dRm + h * crow, dMask + h * cmw,
+                                mb(dDO, h * cdo), mb(dDQ, h * cgq), mb(dDK, h * cgk),
+                                mb(dDV, h * cgv), dDl + h * crow, ws, std::max(wsf, wsb), sc);
+      if (rc) return rc;
+    }
+    cudaEventRecord(c.done[i], sc);
+    cudaStreamWaitEvent(sout, c.done[i], 0);
+    if (dout) {
+      if (dq) cudaMemcpyAsync(mb(dq, h * cgq), mb(dDQ, h * cgq), cgq, cudaMemcpyDeviceToHost, sout);
+      if (dk) cudaMemcpyAsync(mb(dk, h * cgk), mb(dDK, h * cgk), cgk, cudaMemcpyDeviceToHost, sout);
+      if (dv) cudaMemcpyAsync(mb(dv, h * cgv), mb(dDV, h * cgv), cgv, cudaMemcpyDeviceToHost, sout);
+      if (delta)
+        cudaMemcpyAsync(delta + h * crow, dDl + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
+    }
+    if (out) cudaMemcpyAsync(mb(out, h * co), mb(dO, h * co), co, cudaMemcpyDeviceToHost, sout);
+    if (tau) cudaMemcpyAsync(tau + h * crow, dTau + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
+    if (row_max)
+      cudaMemcpyAsync(row_max + h * crow, dRm + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
+    if (mask)
+      cudaMemcpyAsync(mask + h * cmw, dMask + h * cmw, cmw * 4, cudaMemcpyDeviceToHost, sout);
   }
-  if (out) cudaMemcpyAsync(out, dO, no * eo, cudaMemcpyDeviceToHost, st);
-  if (tau) cudaMemcpyAsync(tau, dTau, nrow * 8, cudaMemcpyDeviceToHost, st);
-  if (row_max) cudaMemcpyAsync(row_max, dRm, nrow * 8, cudaMemcpyDeviceToHost, st);
-  if (mask) cudaMemcpyAsync(mask, dMask, mwords * 4, cudaMemcpyDeviceToHost, st);
   if (stats) {
-    rc = adattn_b200_stats(p, dMask, stats, st);
+    rc = adattn_b200_stats(p, dMask, stats, sc);  // whole problem (synchronises sc)
     if (rc) return rc;
   }
-  cudaError_t e = cudaStreamSynchronize(st);
+  cudaError_t e = cudaStreamSynchronize(sout);
+  if (!e) e = cudaStreamSynchronize(sc);
+  if (!e) e = cudaStreamSynchronize(sin);
   if (e) return cuda_fail(e, "adattn_b200_run_host");
   return ADATTN_OK;
 }
