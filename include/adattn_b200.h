@@ -135,7 +135,7 @@ int adattn_b200_mask_sparsity(const uint32_t* mask, int32_t heads, int32_t t_r, 
 /* End-to-end call on HOST buffers (the reference's value-semantics calling
  * convention): uploads inputs, runs forward (+ backward when dout != NULL),
  * downloads results.  Device buffers are cached between calls.  Heads are
- * independent, so the call runs as a pipeline over chunks of heads (up to 8,
+ * independent, so the call runs as a pipeline over chunks of heads (up to 16,
  * >= 4 heads each) on three streams: uploads of chunk i+1 and downloads of
  * chunk i-1 overlap the kernels of chunk i (pinned host buffers overlap fully).
  * Results are identical to the device entry points. */

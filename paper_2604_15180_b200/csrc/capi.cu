@@ -168,7 +168,7 @@ struct HostCtx {
   void* buf[16] = {};
   size_t cap[16] = {};
   cudaStream_t stream = nullptr;
-  static constexpr int kMaxChunks = 8;
+  static constexpr int kMaxChunks = 16;
   cudaStream_t streams[3] = {};  // host->device, kernels, device->host
   cudaEvent_t in_ready[kMaxChunks] = {}, done[kMaxChunks] = {};
   void* get(int slot, size_t bytes) {
@@ -502,8 +502,10 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
   // three streams -- host->device copies of chunk i+1 and device->host copies
   // of chunk i-1 overlap the kernels of chunk i.  Each chunk is a sub-problem
   // (batch 1, `hc` heads) over the same buffers at the chunk's offset.
-  int nch = (int)std::min<size_t>((size_t)HostCtx::kMaxChunks, BH);
-  while (nch > 1 && (BH % (size_t)nch != 0 || BH / (size_t)nch < 4)) --nch;
+  int maxch = HostCtx::kMaxChunks;
+  if (const char* e = std::getenv("ADATTN_HOST_CHUNKS")) maxch = std::max(1, std::min(maxch, std::atoi(e)));
+  int nch = (int)std::min<size_t>((size_t)maxch, BH);
+  while (nch > 1 && (BH % (size_t)nch != 0 || BH / (size_t)nch < 4)) --nch;  // >= 4 heads per chunk
   const size_t hc = BH / (size_t)nch;
   adattn_problem sp = *p;
   sp.batch = 1;
