@@ -127,6 +127,20 @@ int adattn_b200_backward(const adattn_problem* p, const void* q, const void* k,
 int adattn_b200_stats(const adattn_problem* p, const uint32_t* mask, adattn_stats* out,
                       void* stream);
 
+/* Nonzero-block lists of a forward's device mask (all B*H heads, head-major):
+ *   rowptr[bh*t_r + 1], cols[nnz]: per row block, its active key blocks in the
+ *     order PackedBlockMask::for_each_set visits them (ascending j;
+ *     bitpack.hpp:85-92) -- the lists the output pass walks (attention.cpp:334-352);
+ *   colptr[bh*t_c + 1], rows[nnz]: per key block, its active query blocks in
+ *     ascending i (PackedBlockMask::transposed, bitpack.cpp:138-143) -- the
+ *     key-major backward sweep (attention.cpp:464-506).
+ * Pointer arrays are exclusive prefix sums (entry [count] = nnz, i.e.
+ * adattn_stats.active_blocks); block indices are local to the head.  Any output
+ * may be NULL (rowptr is required for cols, colptr for rows).  Enqueued on
+ * `stream`; device pointers. */
+int adattn_b200_block_lists(const adattn_problem* p, const uint32_t* mask, int64_t* rowptr,
+                            int32_t* cols, int64_t* colptr, int32_t* rows, void* stream);
+
 /* block_sparsity (attention.cpp:541-551) of a device mask of `heads` x t_r x
  * ceil(t_c/32) words, aggregated over heads; synchronises `stream`. */
 int adattn_b200_mask_sparsity(const uint32_t* mask, int32_t heads, int32_t t_r, int32_t t_c,

@@ -6,10 +6,11 @@ kernels behind a C-ABI (include/adattn_b200.h, libadattn_b200.so), with a
 Python mirror of the reference interface in :mod:`.attention`.
 """
 from .attention import (AttentionGradients, AttentionProblem, AttentionResult, AttentionStats,
-                        PackedBlockMask, PhaseTimings, backward, block_sparsity, compute_delta,
-                        forward)
+                        BlockLists, PackedBlockMask, PhaseTimings, backward, block_lists,
+                        block_sparsity, compute_delta, forward)
 
 __all__ = [
     "AttentionProblem", "AttentionResult", "AttentionGradients", "AttentionStats",
     "PackedBlockMask", "PhaseTimings", "forward", "compute_delta", "backward", "block_sparsity",
+    "BlockLists", "block_lists",
 ]

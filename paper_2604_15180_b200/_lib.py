@@ -33,6 +33,7 @@ EXPORTS = (
     "adattn_b200_launch_count", "adattn_b200_profile_enable", "adattn_b200_profile_read",
     "adattn_b200_tensor_save", "adattn_b200_tensor_load", "adattn_b200_io_last_error",
     "adattn_b200_attn_inputs", "adattn_b200_xoshiro", "adattn_b200_entmax_rows",
+    "adattn_b200_block_lists",
 )
 
 
@@ -101,6 +102,7 @@ def load() -> C.CDLL:
         lib.adattn_b200_stats.argtypes = [P, vp, S, vp]
         lib.adattn_b200_mask_sparsity.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                                   S, vp]
+        lib.adattn_b200_block_lists.argtypes = [P, vp, vp, vp, vp, vp, vp]
         lib.adattn_b200_run_host.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, S]
         lib.adattn_b200_launch_count.restype = C.c_uint64
         lib.adattn_b200_profile_enable.argtypes = [C.c_int]

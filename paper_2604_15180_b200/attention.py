@@ -325,3 +325,36 @@ def block_sparsity(mask: PackedBlockMask, causal: bool) -> float:
     _lib.check(lib.adattn_b200_mask_sparsity(_ptr(words), words.shape[0], mask.t_r, mask.t_c,
                                              int(bool(causal)), C.byref(st), _stream()))
     return float(st.block_sparsity)
+
+
+@dataclass
+class BlockLists:
+    """Nonzero-block lists of a forward's mask (all heads, head-major), on the device.
+
+    ``rowptr[h*t_r + i] .. rowptr[h*t_r + i + 1]`` indexes ``cols``: the active key
+    blocks of row block i of head h, in PackedBlockMask::for_each_set order
+    (bitpack.hpp:85-92); ``colptr`` / ``rows`` are the transposed lists (active
+    query blocks of each key block, ascending; PackedBlockMask::transposed,
+    bitpack.cpp:138-143).  Block indices are local to the head."""
+    rowptr: torch.Tensor
+    cols: torch.Tensor
+    colptr: torch.Tensor
+    rows: torch.Tensor
+
+
+def block_lists(p: AttentionProblem, res: AttentionResult) -> BlockLists:
+    """Per-row-block lists of the active key blocks (and their transpose) that
+    the output pass and the key-major backward sweep visit (csrc/lists.cu)."""
+    pb = p.c_problem()
+    lib = _lib.load()
+    words = res.mask.words.contiguous()
+    dev = words.device
+    bh = pb.batch * pb.heads
+    nnz = int(res.stats.blocks_visited_fwd)  # = popcount of the mask
+    rowptr = torch.empty(bh * res.mask.t_r + 1, dtype=torch.int64, device=dev)
+    colptr = torch.empty(bh * res.mask.t_c + 1, dtype=torch.int64, device=dev)
+    cols = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    rows = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    _lib.check(lib.adattn_b200_block_lists(C.byref(pb), _ptr(words), _ptr(rowptr), _ptr(cols),
+                                           _ptr(colptr), _ptr(rows), _stream()))
+    return BlockLists(rowptr, cols[:nnz], colptr, rows[:nnz])

@@ -437,6 +437,19 @@ int adattn_b200_entmax_rows(const adattn_rows_problem* p, const void* scores,
   return ADATTN_OK;
 }
 
+int adattn_b200_block_lists(const adattn_problem* p, const uint32_t* mask, int64_t* rowptr,
+                            int32_t* cols, int64_t* colptr, int32_t* rows, void* stream) {
+  Geom g;
+  int rc = check(p, &g);
+  if (rc) return rc;
+  if (!mask) return fail(ADATTN_ERR_INVALID, "block_lists: null mask");
+  if ((cols && !rowptr) || (rows && !colptr))
+    return fail(ADATTN_ERR_INVALID, "block_lists: list without its pointer array");
+  cudaError_t e = block_lists(g, mask, rowptr, cols, colptr, rows, (cudaStream_t)stream);
+  if (e) return cuda_fail(e, "adattn_b200_block_lists");
+  return ADATTN_OK;
+}
+
 int adattn_b200_mask_sparsity(const uint32_t* mask, int32_t heads, int32_t t_r, int32_t t_c,
                               int32_t causal, adattn_stats* out, void* stream) {
   if (heads < 1 || t_r < 1 || t_c < 1)

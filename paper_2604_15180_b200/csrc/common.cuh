@@ -193,6 +193,10 @@ __device__ __forceinline__ bool row_step(RowSolve& rs, double alpha, double refi
 // Launch accounting (exported through adattn_b200_launch_count).
 void note_launch();
 
+// Per-row-block active key-block lists and their transpose (csrc/lists.cu).
+cudaError_t block_lists(const Geom& g, const uint32_t* mask, int64_t* rowptr, int32_t* cols,
+                        int64_t* colptr, int32_t* rows, cudaStream_t st);
+
 // Optional per-kernel event timing (adattn_b200_profile_enable).
 void prof_begin(const char* name, cudaStream_t st);
 void prof_end(cudaStream_t st);
