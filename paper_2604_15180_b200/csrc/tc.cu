@@ -91,7 +91,8 @@ CandPlan cand_plan(const Geom& g) {
   CandPlan p{0, 0};
   int cap = 256;
   if (const char* s = std::getenv("ADATTN_CAND_CAP")) cap = std::atoi(s);
-  if (cap < 64 || g.alpha < 1.4) return p;
+  const char* force = std::getenv("ADATTN_CAND_FORCE");  // experiment: lists for any alpha
+  if (cap < 64 || (g.alpha < 1.4 && !(force && *force == '1'))) return p;
   cap = (cap + 63) / 64 * 64;
   p.slots = nsmid_slots();
   if (p.slots <= 0) return p;
