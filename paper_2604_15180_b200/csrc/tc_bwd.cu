@@ -58,6 +58,10 @@ struct BwdArgs {
   const uint32_t* mask;
   double* delta;
   float2* rowc;  // [bh*n] {C, delta}
+  // fp16 dO copy for dV = P^T dO with P in fp16 (pair dK/dV kernel); f16_bad != 0
+  // when some |dO| does not fit fp16 (the kernel then keeps the bf16 hi/lo path)
+  const uint32_t* f16_bad;
+  int dv_f16;
   void* dq;
   void* dk;
   void* dv;
@@ -174,7 +178,7 @@ __device__ __forceinline__ void delta_chunk(const float* s, const float* dp, flo
 // dS^T = u (dp - delta_q), both split into bf16 hi + lo pairs.  rc[q] =
 // (C_q, delta_q) from shared memory.  MASKED: queries q < lim (above the causal
 // diagonal for this key) are outside the support.
-template <int AK, bool MASKED>
+template <int AK, bool MASKED, bool F16P = false>
 __device__ __forceinline__ void pds_chunk(const float* s, const float* dp, const float2* rc,
                                           float A1, float e0f, float e1f, int lim, uint32_t* ph,
                                           uint32_t* pl, uint32_t* dh, uint32_t* dl) {
@@ -197,7 +201,11 @@ __device__ __forceinline__ void pds_chunk(const float* s, const float* dp, const
     }
     const float2 d = __fadd2_rn(make_float2(dp[2 * x], dp[2 * x + 1]), make_float2(-c.y, -c.w));
     const float2 ds = __fmul2_rn(u, d);
-    split_bf16x2(p.x, p.y, ph[x], pl[x]);
+    if constexpr (F16P) {
+      ph[x] = pack_f16x2(p.x, p.y);  // p in [0, 1]: fp16 keeps 11 bits (bf16 hi + lo: ~16)
+    } else {
+      split_bf16x2(p.x, p.y, ph[x], pl[x]);
+    }
     split_bf16x2(ds.x, ds.y, dh[x], dl[x]);
   }
 }
@@ -1737,6 +1745,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   dK += dS^T Q_i  : A = dS^T, B half = d cols 64r.. of Q_i           (QD, MN-major)
 // Units are the union of both CTAs' active units; rowc (C, delta) of the unit
 // comes with a local bulk copy on a per-stage local barrier.
+// dO (bf16) -> fp16 for the fp16 dV product; flags any value fp16 cannot hold
+// (|x| > 65504 or non-finite), in which case the dK/dV kernel keeps bf16 hi/lo.
+__global__ void do_to_f16(const __nv_bfloat162* __restrict__ src, __half2* __restrict__ dst,
+                          size_t n2, uint32_t* bad) {
+  bool b = false;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float2 f = __bfloat1622float2(src[i]);
+    b |= !(fabsf(f.x) <= 65504.f) || !(fabsf(f.y) <= 65504.f);
+    dst[i] = __floats2half2_rn(f.x, f.y);
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
 template <int D>
 struct Kv2Smem {
   static_assert(D == 128, "pair dK/dV kernel: d = 128");
@@ -1759,8 +1781,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_dkdv2_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_qd,
                     const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_vb,
                     const __grid_constant__ CUtensorMap tm_doh, const __grid_constant__ CUtensorMap tm_dod,
-                    const BwdArgs a) {
+                    const __grid_constant__ CUtensorMap tm_dod16, const BwdArgs a) {
   using L = Kv2Smem<D>;
+  // dV = P^T dO in fp16 (P exact range [0, 1]; dO copied to fp16) -- one MMA per
+  // K step instead of the bf16 hi + lo pair -- unless some |dO| exceeds fp16
+  const bool f16 = a.dv_f16 && *a.f16_bad == 0u;
   constexpr int KS = L::KST2;
   constexpr int NCH = D / 64;
   const Geom& g = a.g;
@@ -1842,7 +1867,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (leader) tma_load_2d_2sm(base + L::HB + c * 32 * 128, &tm_doh, &full[st], c * 64, qrow + 32 * (int)rank);
       }
       if (leader) tma_load_2d_2sm(base + 2 * L::HB, &tm_qd, &full[st], 64 * (int)rank, qrow);
-      if (leader) tma_load_2d_2sm(base + 2 * L::HB + L::DB, &tm_dod, &full[st], 64 * (int)rank, qrow);
+      if (leader)
+        tma_load_2d_2sm(base + 2 * L::HB + L::DB, f16 ? &tm_dod16 : &tm_dod, &full[st], 64 * (int)rank, qrow);
       if (leader) mbar_expect_tx(&rfull[st], QT * 8);
       if (leader) bulk_load(base + 2 * L::HB + 2 * L::DB, a.rowc + qrow, QT * 8, &rfull[st]);
     }
@@ -1851,6 +1877,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool leader = elect_one_sync();
       constexpr uint32_t IDESC_S = idesc_bf16_f32(256, QT, false, false);
       constexpr uint32_t IDESC_G = idesc_bf16_f32(256, D, false, true);
+      constexpr uint32_t IDESC_G16 = idesc_f16_f32(256, D, false, true);
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), st_addr = smem_u32(sSt);
       uint64_t dK[NCH], dV[NCH], dQS[NCH], dDS[NCH];
 #pragma unroll
@@ -1878,8 +1905,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint64_t bdo = dDD + so + (uint64_t)(128 * k);
           const uint64_t bq = dQD + so + (uint64_t)(128 * k);
           const uint32_t acc = (init || k > 0) ? 1u : 0u;
-          if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G, acc);
-          if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
+          if (f16) {
+            if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G16, acc);
+          } else {
+            if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G, acc);
+            if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
+          }
           if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol, bq, IDESC_G, acc);
           if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol + 16, bq, IDESC_G, 1u);
         }
@@ -1938,12 +1969,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int x = 0; x < 16; ++x) ph[x] = pl[x] = dh[x] = dl[x] = 0u;
       } else if (g.causal && q0 < key0 + lq * 32 + 31) {
-        pds_chunk<AK, true>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, gkey - q0, ph, pl, dh, dl);
+        if (f16) pds_chunk<AK, true, true>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, gkey - q0, ph, pl, dh, dl);
+        else pds_chunk<AK, true>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, gkey - q0, ph, pl, dh, dl);
       } else {
-        pds_chunk<AK, false>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, 0, ph, pl, dh, dl);
+        if (f16) pds_chunk<AK, false, true>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, 0, ph, pl, dh, dl);
+        else pds_chunk<AK, false>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, 0, ph, pl, dh, dl);
       }
       tmem_st16(tl + b * 128 + half * 32, ph);
-      tmem_st16(tl + b * 128 + half * 32 + 16, pl);
+      if (!f16) tmem_st16(tl + b * 128 + half * 32 + 16, pl);
       tmem_st16(tl + b * 128 + 64 + half * 32, dh);
       tmem_st16(tl + b * 128 + 64 + half * 32 + 16, dl);
       tmem_wait_st();
@@ -2004,6 +2037,12 @@ int delta_mode(const Geom& g, int ncta_rows) {
   return s && *s ? std::atoi(s) : 1;  // C3: 15.1 (single) / 11.4 (1) / 12.6 (2) ms
 }
 
+// dV = P^T dO with fp16 operands in the pair dK/dV kernel (ADATTN_DV_F16=0: bf16 hi + lo)
+bool dv_f16_enabled() {
+  const char* s = std::getenv("ADATTN_DV_F16");
+  return !(s && *s == '0');
+}
+
 // CTA-pair dK/dV kernel for d = 128 (ADATTN_KV_PAIRS=0 selects the single-CTA kernel)
 bool use_kv_pairs(const Geom& g) {
   const char* s = std::getenv("ADATTN_KV_PAIRS");
@@ -2056,7 +2095,7 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     if ((e = set_smem(k2, sm))) return e;
     prof_begin("tc_dkdv", st);
     k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
-                                                                   m[7], a);
+                                                                   m[7], m[14], a);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
@@ -2105,13 +2144,16 @@ cudaError_t run_bwd_d(const Geom& g, int ak, const CUtensorMap* m, const BwdArgs
 
 }  // namespace
 
-size_t backward_workspace(const Geom& g) { return (size_t)g.bh * g.n * sizeof(float2) + 256; }
+// rowc [bh*n] float2, then (fp16 dV product) an fp16 copy of dO and its range flag
+static size_t ws_rowc(const Geom& g) { return ((size_t)g.bh * g.n * sizeof(float2) + 255) / 256 * 256; }
+static size_t ws_do16(const Geom& g) { return (size_t)g.bh * g.n * g.dv * 2; }
+size_t backward_workspace(const Geom& g) { return ws_rowc(g) + ws_do16(g) + 256; }
 
 cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v, const double* tau,
                      const double* row_max, const uint32_t* mask, const void* dout, void* dq,
                      void* dk, void* dv, double* delta, void* workspace, bool delta_only,
                      cudaStream_t st) {
-  CUtensorMap m[14];
+  CUtensorMap m[15];
   cudaError_t e;
   const uint64_t nq = (uint64_t)g.bh * g.n, nk = (uint64_t)g.bh * g.m;
   if ((e = make_tmap_2d(&m[0], q, nq, g.d, BM))) return e;
@@ -2139,6 +2181,22 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   a.mask = mask;
   a.delta = delta;
   a.rowc = reinterpret_cast<float2*>(workspace);
+  a.dv_f16 = 0;
+  a.f16_bad = nullptr;
+  m[14] = m[7];
+  if (!delta_only && use_kv_pairs(g) && dv_f16_enabled()) {
+    uint8_t* w8 = reinterpret_cast<uint8_t*>(workspace);
+    __half2* do16 = reinterpret_cast<__half2*>(w8 + ws_rowc(g));
+    uint32_t* bad = reinterpret_cast<uint32_t*>(w8 + ws_rowc(g) + ws_do16(g));
+    if ((e = cudaMemsetAsync(bad, 0, 4, st))) return e;
+    const size_t n2 = (size_t)g.bh * g.n * g.dv / 2;
+    do_to_f16<<<4 * 148, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat162*>(dout), do16, n2, bad);
+    note_launch();
+    if ((e = cudaGetLastError())) return e;
+    if ((e = make_tmap_2d(&m[14], do16, nq, g.dv, QT))) return e;
+    a.dv_f16 = 1;
+    a.f16_bad = bad;
+  }
   a.dq = dq;
   a.dk = dk;
   a.dv = dv;

@@ -230,6 +230,11 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool a_mn, b
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
          ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// Both operands fp16.
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 // A operand fp16 (probabilities / score gradients), B operand bf16 (inputs).
 __host__ __device__ constexpr uint32_t idesc_f16a_bf16b_f32(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4) | (0u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |

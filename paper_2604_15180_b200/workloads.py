@@ -64,7 +64,7 @@ def flops(D: int, nnz: int, addressable: int, ref_passes: int = 3) -> dict:
     return dict(f_eff=f_eff, f_alg=f_alg, f_fwd=f_fwd)
 
 
-def executed_flops(mask_words, n: int, d: int, causal: bool) -> dict:
+def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None) -> dict:
     """Tensor-core flops each kernel actually issues for one problem (all heads),
     from the 64x64 block mask ([B][H][t_r][wpr] u32) -- the numerator of the
     per-kernel roofline.  Counts every tcgen05 MMA the
@@ -76,7 +76,9 @@ def executed_flops(mask_words, n: int, d: int, causal: bool) -> dict:
              each 128-row group + OUT (S and P V) over active tiles
     tc_delta S, dP over active (128 rows x 128 keys) tiles
     tc_dq    S, dP, dQ hi, dQ lo over active (128 x 128) tiles
-    tc_dkdv  S^T, dP^T, dV hi/lo, dK hi/lo over active (128 keys x 64 queries) units
+    tc_dkdv  S^T, dP^T, dV (fp16 P and dO: one product; bf16 hi/lo with
+             ADATTN_DV_F16=0 or for d != 128), dK hi/lo over active
+             (128 keys x 64 queries) units
     """
     import torch
     w = mask_words.view(torch.int32)
@@ -97,7 +99,11 @@ def executed_flops(mask_words, n: int, d: int, causal: bool) -> dict:
         sweep_tiles = nr * (t_c // 2) * Bh
     act = int(g.sum())
     units = int(u.sum())
+    if dv_f16 is None:  # the library's default (csrc/tc_bwd.cu dv_f16_enabled, pair kernel)
+        import os
+        dv_f16 = (d == 128 and os.environ.get("ADATTN_DV_F16", "1") != "0"
+                  and os.environ.get("ADATTN_KV_PAIRS", "1") != "0")
     return {"tc_fwd": (3 * sweep_tiles + 2 * act) * tile,
             "tc_delta": 2 * act * tile,
             "tc_dq": 4 * act * tile,
-            "tc_dkdv": 6 * units * (2.0 * 128 * 64 * d)}
+            "tc_dkdv": (5 if dv_f16 else 6) * units * (2.0 * 128 * 64 * d)}

@@ -236,7 +236,9 @@ def test_tc_dq_cta_pairs_match_single(monkeypatch):
 
 def test_tc_dkdv_cta_pairs_match_single(monkeypatch):
     """The CTA-pair dK/dV kernel (cta_group::2, 256 keys per pair) gives the single-CTA
-    kernel's dK and dV (same per-unit arithmetic and query order)."""
+    kernel's dK and dV (same per-unit arithmetic and query order; bf16 hi/lo dV here --
+    the fp16 dV product is checked in test_tc_dv_f16_matches_hilo)."""
+    monkeypatch.setenv("ADATTN_DV_F16", "0")
     for causal in (True, False):
         q, k, v, do = inputs(78, 1, 2, 1024, 128, 1.0)
         prob = pa.AttentionProblem(q, k, v, path="tc", alpha=1.5, causal=causal)
@@ -324,3 +326,42 @@ def test_tc_fwd_cta_pairs_match_single(case, monkeypatch):
         assert torch.equal(r1.row_steps, r2.row_steps)
         assert torch.equal(r1.mask.words, r2.mask.words)
         assert torch.equal(r1.out, r2.out)
+
+
+@pytest.mark.parametrize("alpha", [1.5, 2.0, 1.25])
+def test_tc_dv_f16_matches_hilo(monkeypatch, alpha):
+    """dV = P^T dO with fp16 operands (P in [0, 1], dO copied to fp16: one MMA per
+    K step) against the bf16 hi + lo pair: within 2^-9 of max|dV| (the fp16
+    rounding of P), dK and dQ untouched; and against the exact path within the
+    bf16 gradient bar (2e-2)."""
+    q, k, v, do = inputs(81, 1, 2, 4096, 128, 1.0)
+    prob = pa.AttentionProblem(q, k, v, path="tc", alpha=alpha, causal=True)
+    res = pa.forward(prob)
+    monkeypatch.setenv("ADATTN_DV_F16", "0")
+    g0 = pa.backward(prob, res, do)
+    monkeypatch.setenv("ADATTN_DV_F16", "1")
+    g1 = pa.backward(prob, res, do)
+    torch.cuda.synchronize()
+    scale = g0.dv.abs().max().item()
+    err = (g1.dv - g0.dv).abs().max().item()
+    print("fp16 dV vs hi/lo", alpha, err, scale)
+    assert err <= 2.0 ** -9 * max(1.0, scale)
+    assert torch.equal(g0.dk, g1.dk) and torch.equal(g0.dq, g1.dq)
+    _, rx, gx = run(q, k, v, do, "exact", alpha=alpha, causal=True)
+    assert (g1.dv.double() - gx.dv).abs().max().item() <= 2e-2
+
+
+def test_tc_dv_f16_out_of_range_falls_back(monkeypatch):
+    """A dO entry fp16 cannot hold (|x| > 65504) sets the device flag and the dK/dV
+    kernel keeps the bf16 hi/lo product: identical to ADATTN_DV_F16=0."""
+    q, k, v, do = inputs(82, 1, 2, 1024, 128, 1.0)
+    do = do.clone()
+    do[0, 1, 5, 7] = 1.0e6
+    prob = pa.AttentionProblem(q, k, v, path="tc", alpha=1.5, causal=True)
+    res = pa.forward(prob)
+    monkeypatch.setenv("ADATTN_DV_F16", "0")
+    g0 = pa.backward(prob, res, do)
+    monkeypatch.setenv("ADATTN_DV_F16", "1")
+    g1 = pa.backward(prob, res, do)
+    torch.cuda.synchronize()
+    assert torch.equal(g0.dv, g1.dv) and torch.equal(g0.dk, g1.dk)
