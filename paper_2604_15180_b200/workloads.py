@@ -75,7 +75,8 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None) -> dic
     tc_fwd   3 sweeps (MAX, HIST, CAND) of S over the causal 128x128 tiles of
              each 128-row group + OUT (S and P V) over active tiles
     tc_delta S, dP over active (128 rows x 128 keys) tiles
-    tc_dq    S, dP, dQ hi, dQ lo over active (128 x 128) tiles
+    tc_dq    S, dP, dQ (fp16 sigma dS and K: one product; bf16 hi/lo otherwise)
+             over active (128 x 128) tiles
     tc_dkdv  S^T, dP^T, dV (fp16 P and dO: one product; bf16 hi/lo with
              ADATTN_DV_F16=0 or for d != 128), dK hi/lo over active
              (128 keys x 64 queries) units
@@ -99,11 +100,15 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None) -> dic
         sweep_tiles = nr * (t_c // 2) * Bh
     act = int(g.sum())
     units = int(u.sum())
+    import os
     if dv_f16 is None:  # the library's default (csrc/tc_bwd.cu dv_f16_enabled, pair kernel)
-        import os
         dv_f16 = (d == 128 and os.environ.get("ADATTN_DV_F16", "1") != "0"
                   and os.environ.get("ADATTN_KV_PAIRS", "1") != "0")
+    ds_f16 = d == 128 and os.environ.get("ADATTN_DS_F16", "0") == "1"  # opt-in (alpha <= 2, data in range)
+    kv_pairs = os.environ.get("ADATTN_KV_PAIRS", "1") != "0"
+    dq_pairs = os.environ.get("ADATTN_DQ_PAIRS", "1") != "0"
     return {"tc_fwd": (3 * sweep_tiles + 2 * act) * tile,
             "tc_delta": 2 * act * tile,
-            "tc_dq": 4 * act * tile,
-            "tc_dkdv": (5 if dv_f16 else 6) * units * (2.0 * 128 * 64 * d)}
+            "tc_dq": (3 if ds_f16 and dq_pairs else 4) * act * tile,
+            "tc_dkdv": (4 + (0 if dv_f16 else 1) + (0 if ds_f16 and kv_pairs else 1))
+            * units * (2.0 * 128 * 64 * d)}

@@ -365,3 +365,39 @@ def test_tc_dv_f16_out_of_range_falls_back(monkeypatch):
     g1 = pa.backward(prob, res, do)
     torch.cuda.synchronize()
     assert torch.equal(g0.dv, g1.dv) and torch.equal(g0.dk, g1.dk)
+
+
+@pytest.mark.parametrize("alpha", [1.5, 2.0])
+def test_tc_ds_f16_opt_in(monkeypatch, alpha):
+    """Opt-in fp16 dS products (ADATTN_DS_F16=1: dQ = (sigma dS) K, dK = (sigma dS)^T Q
+    with a power-of-two sigma from the |dS| bound, fp16 Q/K copies): within 2^-8 of
+    max|grad| of the bf16 hi/lo products and within the 2e-2 bar of the exact path;
+    alpha > 2 (u = p^(2-alpha) unbounded) keeps hi/lo."""
+    q, k, v, do = inputs(83, 1, 2, 4096, 128, 1.0)
+    prob = pa.AttentionProblem(q, k, v, path="tc", alpha=alpha, causal=True)
+    res = pa.forward(prob)
+    monkeypatch.setenv("ADATTN_DS_F16", "0")
+    g0 = pa.backward(prob, res, do)
+    monkeypatch.setenv("ADATTN_DS_F16", "1")
+    g1 = pa.backward(prob, res, do)
+    torch.cuda.synchronize()
+    _, rx, gx = run(q, k, v, do, "exact", alpha=alpha, causal=True)
+    for n in ("dq", "dk"):
+        a, b = getattr(g0, n), getattr(g1, n)
+        err = (a - b).abs().max().item()
+        print("fp16 dS vs hi/lo", alpha, n, err, a.abs().max().item())
+        assert err <= 2.0 ** -8 * max(1.0, a.abs().max().item())
+        assert (b.double() - getattr(gx, n)).abs().max().item() <= 2e-2
+    assert torch.equal(g0.dv, g1.dv)
+
+
+def test_tc_ds_f16_alpha_above_two_keeps_hilo(monkeypatch):
+    q, k, v, do = inputs(84, 1, 1, 1024, 128, 1.0)
+    prob = pa.AttentionProblem(q, k, v, path="tc", alpha=2.5, causal=True)
+    res = pa.forward(prob)
+    monkeypatch.setenv("ADATTN_DS_F16", "0")
+    g0 = pa.backward(prob, res, do)
+    monkeypatch.setenv("ADATTN_DS_F16", "1")
+    g1 = pa.backward(prob, res, do)
+    torch.cuda.synchronize()
+    assert torch.equal(g0.dq, g1.dq) and torch.equal(g0.dk, g1.dk)
