@@ -2286,8 +2286,8 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
       note_launch();
     };
     cvt(dout, want_dv ? do16 : nullptr, (size_t)g.bh * g.n * g.dv, &plan->max_do);
-    cvt(v, nullptr, (size_t)g.bh * g.m * g.dv, &plan->max_v);
     if (want_ds) {
+      cvt(v, nullptr, (size_t)g.bh * g.m * g.dv, &plan->max_v);
       cvt(q, q16, (size_t)g.bh * g.n * g.d, &plan->max_q);
       cvt(k, k16, (size_t)g.bh * g.m * g.d, &plan->max_k);
     }

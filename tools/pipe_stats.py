@@ -4,7 +4,7 @@ prints per-role wait fractions and per-phase cycle shares of the forward.
 import ctypes as C, os, sys
 sys.path.insert(0, ".")
 import paper_2604_15180_b200._lib as L
-L.LIB_PATH = os.path.abspath("paper_2604_15180_b200/libadattn_b200_stats.so")
+L.LIB_PATH = os.path.abspath(os.environ.get("LIB", "paper_2604_15180_b200/libadattn_b200_stats.so"))
 import torch
 import paper_2604_15180_b200 as pa
 from paper_2604_15180_b200 import workloads
