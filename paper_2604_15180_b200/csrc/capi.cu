@@ -170,7 +170,7 @@ struct HostCtx {
   cudaStream_t stream = nullptr;
   static constexpr int kMaxChunks = 16;
   cudaStream_t streams[3] = {};  // host->device, kernels, device->host
-  cudaEvent_t in_ready[kMaxChunks] = {}, done[kMaxChunks] = {};
+  cudaEvent_t in_ready[kMaxChunks] = {}, done[kMaxChunks] = {}, fwd_done[kMaxChunks] = {};
   void* get(int slot, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (cap[slot] < bytes) {
@@ -485,7 +485,8 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
     c.stream = c.streams[1];
     for (int i = 0; i < HostCtx::kMaxChunks; ++i)
       if (cudaEventCreateWithFlags(&c.in_ready[i], cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&c.done[i], cudaEventDisableTiming) != cudaSuccess)
+          cudaEventCreateWithFlags(&c.done[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c.fwd_done[i], cudaEventDisableTiming) != cudaSuccess)
         return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: event create failed");
   }
   const size_t ei = elem_size(p->in_dtype), eo = elem_size(p->out_dtype);
@@ -547,6 +548,15 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
                              dTau + h * crow, dRm + h * crow, dMask + h * cmw, nullptr, ws,
                              std::max(wsf, wsb), sc);
     if (rc) return rc;
+    // the forward's outputs go back while the chunk's backward runs
+    cudaEventRecord(c.fwd_done[i], sc);
+    cudaStreamWaitEvent(sout, c.fwd_done[i], 0);
+    if (out) cudaMemcpyAsync(mb(out, h * co), mb(dO, h * co), co, cudaMemcpyDeviceToHost, sout);
+    if (tau) cudaMemcpyAsync(tau + h * crow, dTau + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
+    if (row_max)
+      cudaMemcpyAsync(row_max + h * crow, dRm + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
+    if (mask)
+      cudaMemcpyAsync(mask + h * cmw, dMask + h * cmw, cmw * 4, cudaMemcpyDeviceToHost, sout);
     if (dout) {
       rc = adattn_b200_backward(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv),
                                 dTau + h * crow, dRm + h * crow, dMask + h * cmw,
@@ -563,12 +573,6 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
       if (delta)
         cudaMemcpyAsync(delta + h * crow, dDl + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
     }
-    if (out) cudaMemcpyAsync(mb(out, h * co), mb(dO, h * co), co, cudaMemcpyDeviceToHost, sout);
-    if (tau) cudaMemcpyAsync(tau + h * crow, dTau + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
-    if (row_max)
-      cudaMemcpyAsync(row_max + h * crow, dRm + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
-    if (mask)
-      cudaMemcpyAsync(mask + h * cmw, dMask + h * cmw, cmw * 4, cudaMemcpyDeviceToHost, sout);
   }
   if (stats) {
     rc = adattn_b200_stats(p, dMask, stats, sc);  // whole problem (synchronises sc)
