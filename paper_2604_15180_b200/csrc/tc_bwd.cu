@@ -1922,10 +1922,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint8_t* base = sSt + st * L::STAGE;
       const int qrow = bh * g.n + i * QT;
       if (lead_cta && leader) mbar_expect_tx(&full[st], 2 * (2 * L::HB + 2 * L::DB));
-      for (int c = 0; c < NCH; ++c) {
-        if (leader) tma_load_2d_2sm(base + c * 32 * 128, &tm_qh, &full[st], c * 64, qrow + 32 * (int)rank);
-        if (leader) tma_load_2d_2sm(base + L::HB + c * 32 * 128, &tm_doh, &full[st], c * 64, qrow + 32 * (int)rank);
-      }
+      // one 3-D box per 32-query half carries both d chunks (TMA costs ~240 cycles per
+      // box below 16 KB: 7 boxes per unit outran the unit's MMAs, 5 do not)
+      if (leader) tma_load_3d_2sm(base, &tm_qh, &full[st], qrow + 32 * (int)rank);
+      if (leader) tma_load_3d_2sm(base + L::HB, &tm_doh, &full[st], qrow + 32 * (int)rank);
       if (leader) tma_load_2d_2sm(base + 2 * L::HB, f16s ? &tm_qd16 : &tm_qd, &full[st], 64 * (int)rank, qrow);
       if (leader)
         tma_load_2d_2sm(base + 2 * L::HB + L::DB, f16 ? &tm_dod16 : &tm_dod, &full[st], 64 * (int)rank, qrow);
@@ -2250,8 +2250,9 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   if ((e = make_tmap_2d(&m[9], dout, nq, g.dv, QB_DQ))) return e;
   if ((e = make_tmap_2d(&m[10], k, nk, g.d, 64))) return e;   // 64-key halves (pair dQ)
   if ((e = make_tmap_2d(&m[11], v, nk, g.dv, 64))) return e;
-  if ((e = make_tmap_2d(&m[12], q, nq, g.d, 32))) return e;     // 32-query halves (pair dK/dV)
-  if ((e = make_tmap_2d(&m[13], dout, nq, g.dv, 32))) return e;
+  // 32-query halves (pair dK/dV), both d chunks per box
+  if ((e = make_tmap_3d_chunks(&m[12], q, nq, g.d, 32))) return e;
+  if ((e = make_tmap_3d_chunks(&m[13], dout, nq, g.dv, 32))) return e;
   BwdArgs a;
   a.g = g;
   a.ncta_rows = g.n / BM;
