@@ -2227,8 +2227,14 @@ static size_t ws_rowc(const Geom& g) { return ((size_t)g.bh * g.n * sizeof(float
 static size_t ws_h(const Geom& g, int cols, int rows) {
   return ((size_t)g.bh * rows * cols * 2 + 255) / 256 * 256;
 }
+// only what the enabled fp16 products need (ADATTN_DV_F16 / ADATTN_DS_F16 are read
+// here and again at launch: change them between the query and the call and the
+// C-ABI's workspace check fails loudly)
 size_t backward_workspace(const Geom& g) {
-  return ws_rowc(g) + ws_h(g, g.dv, g.n) + ws_h(g, g.d, g.n) + ws_h(g, g.d, g.m) + 256;
+  const bool pairs = g.d == 128 && g.dv == 128;
+  const bool dvh = pairs && dv_f16_enabled(), dsh = pairs && ds_f16_enabled();
+  return ws_rowc(g) + (dvh || dsh ? ws_h(g, g.dv, g.n) : 0) +
+         (dsh ? ws_h(g, g.d, g.n) + ws_h(g, g.d, g.m) : 0) + 256;
 }
 
 cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v, const double* tau,
@@ -2276,10 +2282,14 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
     size_t off = ws_rowc(g);
     __half2* do16 = reinterpret_cast<__half2*>(w8 + off);
     off += ws_h(g, g.dv, g.n);
-    __half2* q16 = reinterpret_cast<__half2*>(w8 + off);
-    off += ws_h(g, g.d, g.n);
-    __half2* k16 = reinterpret_cast<__half2*>(w8 + off);
-    off += ws_h(g, g.d, g.m);
+    __half2* q16 = nullptr;
+    __half2* k16 = nullptr;
+    if (want_ds) {
+      q16 = reinterpret_cast<__half2*>(w8 + off);
+      off += ws_h(g, g.d, g.n);
+      k16 = reinterpret_cast<__half2*>(w8 + off);
+      off += ws_h(g, g.d, g.m);
+    }
     F16Plan* plan = reinterpret_cast<F16Plan*>(w8 + off);
     if ((e = cudaMemsetAsync(plan, 0, sizeof(F16Plan), st))) return e;
     auto cvt = [&](const void* src, __half2* dst, size_t elems, uint32_t* mx) {
@@ -2296,8 +2306,10 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
     note_launch();
     if ((e = cudaGetLastError())) return e;
     if ((e = make_tmap_2d(&m[14], do16, nq, g.dv, QT))) return e;
-    if ((e = make_tmap_2d(&m[15], k16, nk, g.d, DBN))) return e;
-    if ((e = make_tmap_2d(&m[16], q16, nq, g.d, QT))) return e;
+    if (want_ds) {
+      if ((e = make_tmap_2d(&m[15], k16, nk, g.d, DBN))) return e;
+      if ((e = make_tmap_2d(&m[16], q16, nq, g.d, QT))) return e;
+    }
     a.f16 = plan;
   }
   a.dq = dq;
