@@ -1844,7 +1844,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // fp16 gradient products (F16Plan): dV = P^T dO (P in [0, 1]) and dK = (sigma dS)^T Q,
   // one MMA per K step each instead of the bf16 hi + lo pairs
   const bool f16 = a.f16 && a.f16->dv_ok;
-  const bool f16s = a.f16 && a.f16->ds_ok;
+  const bool f16s = f16 && a.f16->ds_ok;  // (fp16 dS only together with fp16 P: 3 epilogue variants)
   const float sig = f16s ? a.f16->sigma : 1.f;
   constexpr int KS = L::KST2;
   constexpr int NCH = D / 64;
@@ -2037,9 +2037,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int lim = msk ? gkey - q0 : 0;
         const float2* r2 = rc + half * 32;
 #define PDS(M, FP, FS) pds_chunk<AK, M, FP, FS>(s, dp, r2, A1, a.e0f, a.e1f, lim, ph, pl, dh, dl, sig)
-        if (f16 && f16s) { if (msk) PDS(true, true, true); else PDS(false, true, true); }
+        if (f16s) { if (msk) PDS(true, true, true); else PDS(false, true, true); }
         else if (f16) { if (msk) PDS(true, true, false); else PDS(false, true, false); }
-        else if (f16s) { if (msk) PDS(true, false, true); else PDS(false, false, true); }
         else { if (msk) PDS(true, false, false); else PDS(false, false, false); }
 #undef PDS
       }
