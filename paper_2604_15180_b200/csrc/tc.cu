@@ -100,9 +100,20 @@ CandPlan cand_plan(const Geom& g) {
   return p;
 }
 
-size_t forward_workspace(const Geom& g) {
+// O = P V with fp16 P (in [0, 1]) and an fp16 copy of V (ADATTN_PV_F16=0: bf16 P)
+bool pv_f16_enabled() {
+  const char* s = std::getenv("ADATTN_PV_F16");
+  return !(s && *s == '0');
+}
+
+// candidate lists, then (fp16 P V) the fp16 copy of V and its range maximum
+size_t forward_cand_bytes(const Geom& g) {
   const CandPlan p = cand_plan(g);
-  return p.cap > 0 ? (size_t)p.slots * 512 * (size_t)p.cap * 8 : 0;
+  return p.cap > 0 ? ((size_t)p.slots * 512 * (size_t)p.cap * 8 + 255) / 256 * 256 : 0;
+}
+size_t forward_workspace(const Geom& g) {
+  return forward_cand_bytes(g) +
+         (pv_f16_enabled() ? ((size_t)g.bh * g.m * g.dv * 2 + 255) / 256 * 256 + 256 : 0);
 }
 
 }  // namespace tc

@@ -150,7 +150,24 @@ struct FwdArgs {
   uint2* cand;
   int cand_cap;
   int cand_slots;
+  // fp16 P V: max |V| (float bits) of the fp16 V copy; nullptr -> bf16 P
+  const uint32_t* v16_max;
 };
+
+// V (bf16) -> fp16 and max |V| (NaN orders above +inf: fails the range test)
+__global__ void v_to_f16_max(const __nv_bfloat162* __restrict__ src, __half2* __restrict__ dst,
+                             size_t n2, uint32_t* maxbits) {
+  uint32_t m = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float2 f = __bfloat1622float2(src[i]);
+    m = max(m, max(__float_as_uint(fabsf(f.x)), __float_as_uint(fabsf(f.y))));
+    dst[i] = __floats2half2_rn(f.x, f.y);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, m);
+}
 
 template <int D>
 struct FwdSmem {
@@ -360,7 +377,9 @@ template <int D, int AK, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_v,
-                  const FwdArgs a) {
+                  const __grid_constant__ CUtensorMap tm_v16, const FwdArgs a) {
+  // O = P V in fp16 (P in [0, 1], V copied to fp16) unless some |V| exceeds fp16
+  const bool pvf16 = a.v16_max != nullptr && __uint_as_float(*a.v16_max) <= 65504.f;
   using L = FwdSmem<D>;
   static_assert(!PAIR || D == 128, "CTA pairs split K and V tiles in 64-row / 64-column halves");
   // ring: NST tiles, or (pairs) 2*NST items of half a tile (this CTA's half of K or V)
@@ -520,14 +539,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (PAIR) {
         if (leader && lead_cta) mbar_expect_tx(&full[st], 2 * ITEM);
         if (is_v) {
-          if (leader) tma_load_2d_2sm(dst, &tm_v, &full[st], 64 * (int)rank, row);
+          if (leader) tma_load_2d_2sm(dst, pvf16 ? &tm_v16 : &tm_v, &full[st], 64 * (int)rank, row);
         } else {
           if (leader) tma_load_3d_2sm(dst, &tm_kh, &full[st], row + 64 * (int)rank);
         }
       } else {
         if (leader) mbar_expect_tx(&full[st], L::TILE);
         for (int c = 0; c < NCH; ++c)
-          if (leader) tma_load_2d(dst + c * BN * 128, is_v ? &tm_v : &tm_k, &full[st], c * 64, row);
+          if (leader)
+            tma_load_2d(dst + c * BN * 128, is_v ? (pvf16 ? &tm_v16 : &tm_v) : &tm_k, &full[st], c * 64, row);
       }
       ++r;
     };
@@ -566,7 +586,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t rgm = kDualMma ? (1u << (warp - kWarpMma)) : 3u;
     const bool leader = elect_one_sync();
     constexpr uint32_t IDESC_S = idesc_bf16_f32(PAIR ? 256 : 128, BN, false, false);
-    constexpr uint32_t IDESC_PV = idesc_bf16_f32(PAIR ? 256 : 128, D, false, true);
+    constexpr uint32_t IDESC_PV_BF = idesc_bf16_f32(PAIR ? 256 : 128, D, false, true);
+    constexpr uint32_t IDESC_PV16 = idesc_f16_f32(PAIR ? 256 : 128, D, false, true);
+    const uint32_t IDESC_PV = pvf16 ? IDESC_PV16 : IDESC_PV_BF;
     auto commit = [&](uint64_t* bar) {
       if constexpr (PAIR) {
         if (leader) umma2_commit_mc(bar);
@@ -1258,7 +1280,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float2 t = __ffma2_rn(A2, make_float2(v[2 * i], v[2 * i + 1]), C2);
-              pk[i] = pack_bf16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f));
+              pk[i] = pvf16 ? pack_f16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f))
+                            : pack_bf16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f));
             }
           } else {
 #pragma unroll
@@ -1324,8 +1347,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int D, int AK, bool PAIR>
 cudaError_t launch_fwd(const Geom& g, const CUtensorMap& tq, const CUtensorMap& tk,
-                       const CUtensorMap& tkh, const CUtensorMap& tv, const FwdArgs& a,
-                       cudaStream_t st) {
+                       const CUtensorMap& tkh, const CUtensorMap& tv, const CUtensorMap& tv16,
+                       const FwdArgs& a, cudaStream_t st) {
   const size_t smem = FwdSmem<D>::bytes(g.wpr, g.m / BN);
   auto kern = tc_fwd_kernel<D, AK, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1345,9 +1368,9 @@ cudaError_t launch_fwd(const Geom& g, const CUtensorMap& tq, const CUtensorMap& 
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tkh, tv, a);
+    e = cudaLaunchKernelEx(&cfg, kern, tq, tk, tkh, tv, tv16, a);
   } else {
-    kern<<<grid, kThreads, smem, st>>>(tq, tk, tkh, tv, a);
+    kern<<<grid, kThreads, smem, st>>>(tq, tk, tkh, tv, tv16, a);
   }
   prof_end(st);
   note_launch();
@@ -1356,13 +1379,13 @@ cudaError_t launch_fwd(const Geom& g, const CUtensorMap& tq, const CUtensorMap& 
 
 template <int D, bool PAIR>
 cudaError_t launch_fwd_d(const Geom& g, int ak, const CUtensorMap& tq, const CUtensorMap& tk,
-                         const CUtensorMap& tkh, const CUtensorMap& tv, const FwdArgs& a,
-                         cudaStream_t st) {
+                         const CUtensorMap& tkh, const CUtensorMap& tv, const CUtensorMap& tv16,
+                         const FwdArgs& a, cudaStream_t st) {
   switch (ak) {
-    case AK15: return launch_fwd<D, AK15, PAIR>(g, tq, tk, tkh, tv, a, st);
-    case AK2: return launch_fwd<D, AK2, PAIR>(g, tq, tk, tkh, tv, a, st);
-    case AK125: return launch_fwd<D, AK125, PAIR>(g, tq, tk, tkh, tv, a, st);
-    default: return launch_fwd<D, AKGEN, PAIR>(g, tq, tk, tkh, tv, a, st);
+    case AK15: return launch_fwd<D, AK15, PAIR>(g, tq, tk, tkh, tv, tv16, a, st);
+    case AK2: return launch_fwd<D, AK2, PAIR>(g, tq, tk, tkh, tv, tv16, a, st);
+    case AK125: return launch_fwd<D, AK125, PAIR>(g, tq, tk, tkh, tv, tv16, a, st);
+    default: return launch_fwd<D, AKGEN, PAIR>(g, tq, tk, tkh, tv, tv16, a, st);
   }
 }
 
@@ -1388,7 +1411,7 @@ int alpha_kind(double alpha) {
 cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                     double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,
                     cudaStream_t st) {
-  CUtensorMap tq, tk, tkh, tv;
+  CUtensorMap tq, tk, tkh, tv, tv16;
   cudaError_t e;
   if ((e = make_tmap_2d(&tq, q, (uint64_t)g.bh * g.n, g.d, BM))) return e;
   if ((e = make_tmap_2d(&tk, k, (uint64_t)g.bh * g.m, g.d, BN))) return e;
@@ -1411,11 +1434,25 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.cand = (cp.cap > 0 && ws) ? reinterpret_cast<uint2*>(ws) : nullptr;
   a.cand_cap = cp.cap;
   a.cand_slots = cp.slots;
+  a.v16_max = nullptr;
+  tv16 = tv;
+  if (pv_f16_enabled() && ws) {
+    uint8_t* w8 = reinterpret_cast<uint8_t*>(ws) + forward_cand_bytes(g);
+    __half2* v16 = reinterpret_cast<__half2*>(w8);
+    uint32_t* vmax = reinterpret_cast<uint32_t*>(w8 + ((size_t)g.bh * g.m * g.dv * 2 + 255) / 256 * 256);
+    if ((e = cudaMemsetAsync(vmax, 0, 4, st))) return e;
+    v_to_f16_max<<<4 * 148, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat162*>(v), v16,
+                                          (size_t)g.bh * g.m * g.dv / 2, vmax);
+    note_launch();
+    if ((e = cudaGetLastError())) return e;
+    if ((e = make_tmap_2d(&tv16, v16, (uint64_t)g.bh * g.m, g.dv, BN))) return e;
+    a.v16_max = vmax;
+  }
 
   const int ak = alpha_kind(g.alpha);
-  if (g.d == 64) return launch_fwd_d<64, false>(g, ak, tq, tk, tkh, tv, a, st);
-  if (use_fwd_pairs(g)) return launch_fwd_d<128, true>(g, ak, tq, tk, tkh, tv, a, st);
-  return launch_fwd_d<128, false>(g, ak, tq, tk, tkh, tv, a, st);
+  if (g.d == 64) return launch_fwd_d<64, false>(g, ak, tq, tk, tkh, tv, tv16, a, st);
+  if (use_fwd_pairs(g)) return launch_fwd_d<128, true>(g, ak, tq, tk, tkh, tv, tv16, a, st);
+  return launch_fwd_d<128, false>(g, ak, tq, tk, tkh, tv, tv16, a, st);
 }
 
 }  // namespace tc

@@ -25,6 +25,8 @@ struct CandPlan {
 };
 CandPlan cand_plan(const Geom& g);
 size_t forward_workspace(const Geom& g);
+size_t forward_cand_bytes(const Geom& g);
+bool pv_f16_enabled();
 
 cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                     double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,

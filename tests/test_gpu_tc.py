@@ -401,3 +401,55 @@ def test_tc_ds_f16_alpha_above_two_keeps_hilo(monkeypatch):
     g1 = pa.backward(prob, res, do)
     torch.cuda.synchronize()
     assert torch.equal(g0.dq, g1.dq) and torch.equal(g0.dk, g1.dk)
+
+
+@pytest.mark.parametrize("N,D,causal,alpha", [(8192, 128, True, 1.5), (16384, 64, False, 1.5),
+                                               (8192, 128, True, 2.0)])
+def test_tc_config_sizes_vs_exact(N, D, causal, alpha):
+    """BASELINE config shapes per head (C2: N=8192 d=128 causal; C4: N=16384 d=64
+    non-causal), default path with every production switch, against the EXACT path
+    (pinned to the compiled reference in test_gpu_exact.py): tau, out and the
+    gradients within the bf16 bars, masks identical up to the slack rule."""
+    q, k, v, do = inputs(N + D + int(alpha * 10), 1, 1, N, D, 1.0)
+    _, rx, gx = run(q, k, v, do, "exact", alpha=alpha, causal=causal)
+    _, rt, gt = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    tau_err = (rt.tau - rx.tau).abs().max().item()
+    out_err = (rt.out - rx.out).abs().max().item()
+    errs = {n: (getattr(gt, n) - getattr(gx, n)).abs().max().item() for n in ("dq", "dk", "dv")}
+    bx, bt = mask_bits(rx.mask.words, rx.mask.t_c), mask_bits(rt.mask.words, rt.mask.t_c)
+    diff = bx != bt
+    print(N, D, causal, alpha, f"tau {tau_err:.2e} out {out_err:.2e}", errs, "mask diffs", int(diff.sum()))
+    assert tau_err <= 1e-3 and out_err <= 2e-2
+    for n in errs:
+        assert errs[n] <= 2e-2, (n, errs[n])
+    if diff.any():
+        margin = block_margin(q, k, rx, alpha, causal).cpu().numpy()
+        assert np.all(np.abs(margin[diff] + 1e-9) <= 1e-5), margin[diff]
+
+
+def test_tc_pv_f16_vs_bf16(monkeypatch):
+    """O = P V with fp16 P (default; V copied to fp16) is closer to the exact path than
+    bf16 P (ADATTN_PV_F16=0), and both stay within the 2e-2 bar; tau and masks are
+    untouched (the output pass only)."""
+    q, k, v, _ = inputs(85, 1, 2, 4096, 128, 1.0)
+    _, rx, _ = run(q, k, v, None, "exact", alpha=1.5, causal=True)
+    monkeypatch.setenv("ADATTN_PV_F16", "0")
+    _, rb, _ = run(q, k, v, None, "tc", alpha=1.5, causal=True)
+    monkeypatch.setenv("ADATTN_PV_F16", "1")
+    _, rf, _ = run(q, k, v, None, "tc", alpha=1.5, causal=True)
+    eb = (rb.out - rx.out).abs().max().item()
+    ef = (rf.out - rx.out).abs().max().item()
+    print("out err bf16 P", eb, "fp16 P", ef)
+    assert ef <= 2e-2 and eb <= 2e-2 and ef < eb
+    assert torch.equal(rb.tau, rf.tau) and torch.equal(rb.mask.words, rf.mask.words)
+
+
+def test_tc_pv_f16_out_of_range_keeps_bf16(monkeypatch):
+    q, k, v, _ = inputs(86, 1, 1, 1024, 128, 1.0)
+    v = v.clone()
+    v[0, 0, 3, 9] = 1.0e6
+    monkeypatch.setenv("ADATTN_PV_F16", "0")
+    _, rb, _ = run(q, k, v, None, "tc", alpha=1.5, causal=True)
+    monkeypatch.setenv("ADATTN_PV_F16", "1")
+    _, rf, _ = run(q, k, v, None, "tc", alpha=1.5, causal=True)
+    assert torch.equal(rb.out, rf.out)
