@@ -1224,15 +1224,16 @@ struct Dq2Smem {
   static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
 };
 
-template <int D, int AK>
+template <int D, int AK, bool DSF16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_dq2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kh,
                   const __grid_constant__ CUtensorMap tm_kd, const __grid_constant__ CUtensorMap tm_vh,
                   const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_kd16,
                   const BwdArgs a) {
   using L = Dq2Smem<D>;
-  // dQ = (sigma dS) K in fp16 (F16Plan): one MMA per K step instead of hi + lo
-  const bool f16s = a.f16 && a.f16->ds_ok;
+  // dQ = (sigma dS) K in fp16 (F16Plan): one MMA per K step instead of hi + lo.
+  // DSF16 = false (the default) compiles the fp16 branches out of the issue loop.
+  const bool f16s = DSF16 && a.f16 && a.f16->ds_ok;
   const float sig = f16s ? a.f16->sigma : 1.f;
   constexpr int NSK = L::NSK, NSV = L::NSV;
   constexpr int NCH = D / 64;
@@ -1833,7 +1834,7 @@ struct Kv2Smem {
   static size_t bytes(int t_r) { return 1024 + OFF_UB + t_r + 64; }
 };
 
-template <int D, int AK>
+template <int D, int AK, bool DSF16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_dkdv2_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_qd,
                     const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_vb,
@@ -1844,7 +1845,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // fp16 gradient products (F16Plan): dV = P^T dO (P in [0, 1]) and dK = (sigma dS)^T Q,
   // one MMA per K step each instead of the bf16 hi + lo pairs
   const bool f16 = a.f16 && a.f16->dv_ok;
-  const bool f16s = f16 && a.f16->ds_ok;  // (fp16 dS only together with fp16 P: 3 epilogue variants)
+  const bool f16s = DSF16 && f16 && a.f16->ds_ok;  // (fp16 dS only with fp16 P: 3 epilogue variants)
   const float sig = f16s ? a.f16->sigma : 1.f;
   constexpr int KS = L::KST2;
   constexpr int NCH = D / 64;
@@ -2166,7 +2167,7 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
   }
   if (delta_only) return cudaSuccess;
   if (use_kv_pairs(g)) {
-    auto k2 = tc_dkdv2_kernel<128, AK>;
+    auto k2 = ds_f16_enabled() ? tc_dkdv2_kernel<128, AK, true> : tc_dkdv2_kernel<128, AK, false>;
     const size_t sm = Kv2Smem<128>::bytes(g.t_r);
     if ((e = set_smem(k2, sm))) return e;
     prof_begin("tc_dkdv", st);
@@ -2186,7 +2187,7 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     if ((e = cudaGetLastError())) return e;
   }
   if (use_dq_pairs(g)) {
-    auto k1 = tc_dq2_kernel<128, AK>;
+    auto k1 = ds_f16_enabled() ? tc_dq2_kernel<128, AK, true> : tc_dq2_kernel<128, AK, false>;
     const size_t sm = Dq2Smem<128>::bytes(g.wpr);
     if ((e = set_smem(k1, sm))) return e;
     prof_begin("tc_dq", st);
