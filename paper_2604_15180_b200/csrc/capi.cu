@@ -168,7 +168,7 @@ struct HostCtx {
   void* buf[16] = {};
   size_t cap[16] = {};
   cudaStream_t stream = nullptr;
-  static constexpr int kMaxChunks = 16;
+  static constexpr int kMaxChunks = 64;
   cudaStream_t streams[3] = {};  // host->device, kernels, device->host
   cudaEvent_t in_ready[kMaxChunks] = {}, done[kMaxChunks] = {}, fwd_done[kMaxChunks] = {};
   void* get(int slot, size_t bytes) {
@@ -516,14 +516,26 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
   // three streams -- host->device copies of chunk i+1 and device->host copies
   // of chunk i-1 overlap the kernels of chunk i.  Each chunk is a sub-problem
   // (batch 1, `hc` heads) over the same buffers at the chunk's offset.
-  int maxch = HostCtx::kMaxChunks;
-  if (const char* e = std::getenv("ADATTN_HOST_CHUNKS")) maxch = std::max(1, std::min(maxch, std::atoi(e)));
-  int nch = (int)std::min<size_t>((size_t)maxch, BH);
-  while (nch > 1 && (BH % (size_t)nch != 0 || BH / (size_t)nch < 4)) --nch;  // >= 4 heads per chunk
-  const size_t hc = BH / (size_t)nch;
+  // Chunk schedule: equal chunks of >= 4 heads, at most 16 (measured at C3: 16 chunks
+  // e2e 117.6 ms vs 8: 122.5; a 2 / 15 x 4 / 2 taper: 127.8 -- the last big chunk's
+  // downloads outlast the short final chunk); ADATTN_HOST_CHUNKS=n forces n chunks.
+  std::vector<std::pair<size_t, size_t>> chunks;  // (first head, heads)
+  {
+    int nch = 16, minh = 4;
+    const char* env = std::getenv("ADATTN_HOST_CHUNKS");
+    if (env && *env) {
+      nch = std::max(1, std::min(HostCtx::kMaxChunks, std::atoi(env)));
+      minh = 1;
+    }
+    nch = (int)std::min<size_t>((size_t)nch, BH);
+    while (nch > 1 && (BH % (size_t)nch != 0 || BH / (size_t)nch < (size_t)minh)) --nch;
+    for (int i = 0; i < nch; ++i) chunks.push_back({i * (BH / nch), BH / nch});
+  }
+  size_t hmax = 0;
+  for (auto& ch : chunks) hmax = std::max(hmax, ch.second);
   adattn_problem sp = *p;
   sp.batch = 1;
-  sp.heads = (int32_t)hc;
+  sp.heads = (int32_t)hmax;
   const size_t wsf = adattn_b200_forward_workspace(&sp);
   const size_t wsb = adattn_b200_backward_workspace(&sp);
   void* ws = c.get(7, std::max(wsf, wsb));
@@ -532,16 +544,19 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
   cudaStream_t sin = c.streams[0], sc = c.streams[1], sout = c.streams[2];
   auto cb = [](const void* base, size_t off) { return (const char*)base + off; };
   auto mb = [](void* base, size_t off) { return (char*)base + off; };
-  const size_t cq = hc * g.n * g.d * ei, ck = hc * g.m * g.d * ei, cv = hc * g.m * g.dv * ei;
-  const size_t cdo = hc * g.n * g.dv * ei, co = hc * g.n * g.dv * eo;
-  const size_t cgq = hc * g.n * g.d * eo, cgk = hc * g.m * g.d * eo, cgv = hc * g.m * g.dv * eo;
-  const size_t crow = hc * g.n, cmw = hc * g.t_r * g.wpr;
-  for (int i = 0; i < nch; ++i) {
-    const size_t h = (size_t)i;
-    cudaMemcpyAsync(mb(dQ, h * cq), cb(q, h * cq), cq, cudaMemcpyHostToDevice, sin);
-    cudaMemcpyAsync(mb(dK, h * ck), cb(k, h * ck), ck, cudaMemcpyHostToDevice, sin);
-    cudaMemcpyAsync(mb(dV, h * cv), cb(v, h * cv), cv, cudaMemcpyHostToDevice, sin);
-    if (dout) cudaMemcpyAsync(mb(dDO, h * cdo), cb(dout, h * cdo), cdo, cudaMemcpyHostToDevice, sin);
+  // per-head sizes
+  const size_t cq = (size_t)g.n * g.d * ei, ck = (size_t)g.m * g.d * ei, cv = (size_t)g.m * g.dv * ei;
+  const size_t cdo = (size_t)g.n * g.dv * ei, co = (size_t)g.n * g.dv * eo;
+  const size_t cgq = (size_t)g.n * g.d * eo, cgk = (size_t)g.m * g.d * eo, cgv = (size_t)g.m * g.dv * eo;
+  const size_t crow = g.n, cmw = (size_t)g.t_r * g.wpr;
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    const size_t h = chunks[i].first, hn = chunks[i].second;
+    sp.heads = (int32_t)hn;
+    cudaMemcpyAsync(mb(dQ, h * cq), cb(q, h * cq), hn * cq, cudaMemcpyHostToDevice, sin);
+    cudaMemcpyAsync(mb(dK, h * ck), cb(k, h * ck), hn * ck, cudaMemcpyHostToDevice, sin);
+    cudaMemcpyAsync(mb(dV, h * cv), cb(v, h * cv), hn * cv, cudaMemcpyHostToDevice, sin);
+    if (dout)
+      cudaMemcpyAsync(mb(dDO, h * cdo), cb(dout, h * cdo), hn * cdo, cudaMemcpyHostToDevice, sin);
     cudaEventRecord(c.in_ready[i], sin);
     cudaStreamWaitEvent(sc, c.in_ready[i], 0);
     rc = adattn_b200_forward(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv), mb(dO, h * co),
@@ -551,12 +566,13 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
     // the forward's outputs go back while the chunk's backward runs
     cudaEventRecord(c.fwd_done[i], sc);
     cudaStreamWaitEvent(sout, c.fwd_done[i], 0);
-    if (out) cudaMemcpyAsync(mb(out, h * co), mb(dO, h * co), co, cudaMemcpyDeviceToHost, sout);
-    if (tau) cudaMemcpyAsync(tau + h * crow, dTau + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
+    if (out) cudaMemcpyAsync(mb(out, h * co), mb(dO, h * co), hn * co, cudaMemcpyDeviceToHost, sout);
+    if (tau)
+      cudaMemcpyAsync(tau + h * crow, dTau + h * crow, hn * crow * 8, cudaMemcpyDeviceToHost, sout);
     if (row_max)
-      cudaMemcpyAsync(row_max + h * crow, dRm + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
+      cudaMemcpyAsync(row_max + h * crow, dRm + h * crow, hn * crow * 8, cudaMemcpyDeviceToHost, sout);
     if (mask)
-      cudaMemcpyAsync(mask + h * cmw, dMask + h * cmw, cmw * 4, cudaMemcpyDeviceToHost, sout);
+      cudaMemcpyAsync(mask + h * cmw, dMask + h * cmw, hn * cmw * 4, cudaMemcpyDeviceToHost, sout);
     if (dout) {
       rc = adattn_b200_backward(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv),
                                 dTau + h * crow, dRm + h * crow, dMask + h * cmw,
@@ -567,11 +583,11 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
     cudaEventRecord(c.done[i], sc);
     cudaStreamWaitEvent(sout, c.done[i], 0);
     if (dout) {
-      if (dq) cudaMemcpyAsync(mb(dq, h * cgq), mb(dDQ, h * cgq), cgq, cudaMemcpyDeviceToHost, sout);
-      if (dk) cudaMemcpyAsync(mb(dk, h * cgk), mb(dDK, h * cgk), cgk, cudaMemcpyDeviceToHost, sout);
-      if (dv) cudaMemcpyAsync(mb(dv, h * cgv), mb(dDV, h * cgv), cgv, cudaMemcpyDeviceToHost, sout);
+      if (dq) cudaMemcpyAsync(mb(dq, h * cgq), mb(dDQ, h * cgq), hn * cgq, cudaMemcpyDeviceToHost, sout);
+      if (dk) cudaMemcpyAsync(mb(dk, h * cgk), mb(dDK, h * cgk), hn * cgk, cudaMemcpyDeviceToHost, sout);
+      if (dv) cudaMemcpyAsync(mb(dv, h * cgv), mb(dDV, h * cgv), hn * cgv, cudaMemcpyDeviceToHost, sout);
       if (delta)
-        cudaMemcpyAsync(delta + h * crow, dDl + h * crow, crow * 8, cudaMemcpyDeviceToHost, sout);
+        cudaMemcpyAsync(delta + h * crow, dDl + h * crow, hn * crow * 8, cudaMemcpyDeviceToHost, sout);
     }
   }
   if (stats) {
