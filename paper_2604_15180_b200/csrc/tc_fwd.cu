@@ -1071,25 +1071,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           ovf = __any_sync(0xffffffffu, ovf || (int)(wp - lst) > cap - 64);
           tau_tile(J, act_own(1, rg, J), [&](const float* v) {
             if (ovf) return;
-            // candidates are rare (~0.3% of scores): a warp vote per column
-            // keeps the common path at compare + vote + branch
+            // candidates are rare (~0.3% of scores): one 3-input max + warp vote per
+            // 4 scores keeps the common path at 2 FMNMX + compare + vote + branch
 #pragma unroll
-            for (int i = 0; i < 32; i += 2)
+            for (int i = 0; i < 32; i += 4)
               asm volatile(
-                  "{\n\t.reg .pred p0, p1, pa, q;\n\t"
-                  "setp.gt.f32 p0, %1, %3;\n\t"
-                  "setp.gt.f32 p1, %2, %3;\n\t"
-                  "or.pred pa, p0, p1;\n\t"
+                  "{\n\t.reg .pred p0, p1, p2, p3, pa, q;\n\t.reg .f32 m;\n\t"
+                  "max.f32 m, %1, %2, %3;\n\t"
+                  "max.f32 m, m, %4;\n\t"
+                  "setp.gt.f32 pa, m, %5;\n\t"
                   "vote.sync.any.pred q, pa, 0xffffffff;\n\t"
                   "@!q bra.uni CAND_SKIP_%=;\n\t"
-                  "@p0 st.global.v2.b32 [%0], {%4, %6};\n\t"
+                  "setp.gt.f32 p0, %1, %5;\n\t"
+                  "setp.gt.f32 p1, %2, %5;\n\t"
+                  "setp.gt.f32 p2, %3, %5;\n\t"
+                  "setp.gt.f32 p3, %4, %5;\n\t"
+                  "@p0 st.global.v2.b32 [%0], {%6, %10};\n\t"
                   "@p0 add.u64 %0, %0, 8;\n\t"
-                  "@p1 st.global.v2.b32 [%0], {%5, %6};\n\t"
+                  "@p1 st.global.v2.b32 [%0], {%7, %10};\n\t"
                   "@p1 add.u64 %0, %0, 8;\n\t"
+                  "@p2 st.global.v2.b32 [%0], {%8, %10};\n\t"
+                  "@p2 add.u64 %0, %0, 8;\n\t"
+                  "@p3 st.global.v2.b32 [%0], {%9, %10};\n\t"
+                  "@p3 add.u64 %0, %0, 8;\n\t"
                   "CAND_SKIP_%=:\n\t}"
                   : "+l"(wp)
-                  : "f"(v[i]), "f"(v[i + 1]), "f"(theta), "r"(__float_as_uint(v[i])),
-                    "r"(__float_as_uint(v[i + 1])), "r"(blk)
+                  : "f"(v[i]), "f"(v[i + 1]), "f"(v[i + 2]), "f"(v[i + 3]), "f"(theta),
+                    "r"(__float_as_uint(v[i])), "r"(__float_as_uint(v[i + 1])),
+                    "r"(__float_as_uint(v[i + 2])), "r"(__float_as_uint(v[i + 3])), "r"(blk)
                   : "memory");
           });
         }
