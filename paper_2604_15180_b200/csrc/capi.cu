@@ -170,7 +170,8 @@ struct HostCtx {
   cudaStream_t stream = nullptr;
   static constexpr int kMaxChunks = 64;
   cudaStream_t streams[3] = {};  // host->device, kernels, device->host
-  cudaEvent_t in_ready[kMaxChunks] = {}, done[kMaxChunks] = {}, fwd_done[kMaxChunks] = {};
+  cudaEvent_t in_ready[kMaxChunks] = {}, done[kMaxChunks] = {}, fwd_done[kMaxChunks] = {},
+              do_ready[kMaxChunks] = {};
   void* get(int slot, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (cap[slot] < bytes) {
@@ -486,7 +487,8 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
     for (int i = 0; i < HostCtx::kMaxChunks; ++i)
       if (cudaEventCreateWithFlags(&c.in_ready[i], cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&c.done[i], cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&c.fwd_done[i], cudaEventDisableTiming) != cudaSuccess)
+          cudaEventCreateWithFlags(&c.fwd_done[i], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c.do_ready[i], cudaEventDisableTiming) != cudaSuccess)
         return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: event create failed");
   }
   const size_t ei = elem_size(p->in_dtype), eo = elem_size(p->out_dtype);
@@ -516,20 +518,35 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
   // three streams -- host->device copies of chunk i+1 and device->host copies
   // of chunk i-1 overlap the kernels of chunk i.  Each chunk is a sub-problem
   // (batch 1, `hc` heads) over the same buffers at the chunk's offset.
-  // Chunk schedule: equal chunks of >= 4 heads, at most 16 (measured at C3: 16 chunks
-  // e2e 117.6 ms vs 8: 122.5; a 2 / 15 x 4 / 2 taper: 127.8 -- the last big chunk's
-  // downloads outlast the short final chunk); ADATTN_HOST_CHUNKS=n forces n chunks.
+  // Chunk schedule: two 2-head chunks at each end (short pipeline fill: the first
+  // forward needs only its q, k, v; short drain: the last backward's gradients are the
+  // only transfer left) and ~16 equal chunks of >= 4 heads in between (few kernel
+  // tails).  A 2 / 15 x 4 / 2 taper measured slower (a big chunk's downloads outlast a
+  // short final chunk).  ADATTN_HOST_CHUNKS=n forces n equal chunks.
   std::vector<std::pair<size_t, size_t>> chunks;  // (first head, heads)
   {
-    int nch = 16, minh = 4;
     const char* env = std::getenv("ADATTN_HOST_CHUNKS");
     if (env && *env) {
-      nch = std::max(1, std::min(HostCtx::kMaxChunks, std::atoi(env)));
-      minh = 1;
+      int nch = std::max(1, std::min(HostCtx::kMaxChunks, std::atoi(env)));
+      nch = (int)std::min<size_t>((size_t)nch, BH);
+      while (nch > 1 && BH % (size_t)nch != 0) --nch;
+      for (int i = 0; i < nch; ++i) chunks.push_back({i * (BH / nch), BH / nch});
+    } else if (BH >= 24) {
+      const size_t mid = BH - 8;
+      const size_t nm = std::min<size_t>(16, mid / 4);
+      size_t h0 = 0;
+      for (int e = 0; e < 2; ++e, h0 += 2) chunks.push_back({h0, 2});
+      for (size_t i = 0; i < nm; ++i) {
+        const size_t n = mid / nm + (i < mid % nm ? 1 : 0);
+        chunks.push_back({h0, n});
+        h0 += n;
+      }
+      for (int e = 0; e < 2; ++e, h0 += 2) chunks.push_back({h0, 2});
+    } else {
+      int nch = (int)std::min<size_t>(16, BH);
+      while (nch > 1 && (BH % (size_t)nch != 0 || BH / (size_t)nch < 4)) --nch;
+      for (int i = 0; i < nch; ++i) chunks.push_back({i * (BH / nch), BH / nch});
     }
-    nch = (int)std::min<size_t>((size_t)nch, BH);
-    while (nch > 1 && (BH % (size_t)nch != 0 || BH / (size_t)nch < (size_t)minh)) --nch;
-    for (int i = 0; i < nch; ++i) chunks.push_back({i * (BH / nch), BH / nch});
   }
   size_t hmax = 0;
   for (auto& ch : chunks) hmax = std::max(hmax, ch.second);
@@ -555,9 +572,11 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
     cudaMemcpyAsync(mb(dQ, h * cq), cb(q, h * cq), hn * cq, cudaMemcpyHostToDevice, sin);
     cudaMemcpyAsync(mb(dK, h * ck), cb(k, h * ck), hn * ck, cudaMemcpyHostToDevice, sin);
     cudaMemcpyAsync(mb(dV, h * cv), cb(v, h * cv), hn * cv, cudaMemcpyHostToDevice, sin);
-    if (dout)
-      cudaMemcpyAsync(mb(dDO, h * cdo), cb(dout, h * cdo), hn * cdo, cudaMemcpyHostToDevice, sin);
     cudaEventRecord(c.in_ready[i], sin);
+    if (dout) {  // dO lands while the chunk's forward runs
+      cudaMemcpyAsync(mb(dDO, h * cdo), cb(dout, h * cdo), hn * cdo, cudaMemcpyHostToDevice, sin);
+      cudaEventRecord(c.do_ready[i], sin);
+    }
     cudaStreamWaitEvent(sc, c.in_ready[i], 0);
     rc = adattn_b200_forward(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv), mb(dO, h * co),
                              dTau + h * crow, dRm + h * crow, dMask + h * cmw, nullptr, ws,
@@ -574,6 +593,7 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
     if (mask)
       cudaMemcpyAsync(mask + h * cmw, dMask + h * cmw, hn * cmw * 4, cudaMemcpyDeviceToHost, sout);
     if (dout) {
+      cudaStreamWaitEvent(sc, c.do_ready[i], 0);
       rc = adattn_b200_backward(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv),
                                 dTau + h * crow, dRm + h * crow, dMask + h * cmw,
                                 mb(dDO, h * cdo), mb(dDQ, h * cgq), mb(dDK, h * cgk),
