@@ -149,10 +149,12 @@ int adattn_b200_mask_sparsity(const uint32_t* mask, int32_t heads, int32_t t_r, 
 /* End-to-end call on HOST buffers (the reference's value-semantics calling
  * convention): uploads inputs, runs forward (+ backward when dout != NULL),
  * downloads results.  Device buffers are cached between calls.  Heads are
- * independent, so the call runs as a pipeline over chunks of heads (up to 16,
- * >= 4 heads each) on three streams: uploads of chunk i+1 and downloads of
- * chunk i-1 overlap the kernels of chunk i (pinned host buffers overlap fully).
- * Results are identical to the device entry points. */
+ * independent, so the call runs as a pipeline over chunks of heads on three
+ * streams (uploads / kernels / downloads): 2-head chunks at both ends, ~16
+ * chunks of >= 4 heads in between; a chunk's forward starts once its q, k, v
+ * are resident and its forward outputs go back while its backward runs.
+ * ADATTN_HOST_CHUNKS=n forces n equal chunks.  Results are identical to the
+ * device entry points. */
 int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, const void* v,
                          const void* dout, void* out, double* tau, double* row_max,
                          uint32_t* mask, void* dq, void* dk, void* dv, double* delta,
