@@ -81,20 +81,7 @@ struct F16Plan {
   float sigma, inv_sigma;
 };
 
-// Compensated (Kahan) fp32 running sum: the per-row delta sums see one add per
-// 32-key chunk, and an FP64 add per chunk stalled the delta epilogue on the
-// FP64 pipe (ncu: DADD held ~30% of the warp-stall samples).  The compensated
-// fp32 sum keeps the error at the level of the fp32 chunk partials themselves.
-struct KahanF {
-  float s = 0.f, c = 0.f;
-  __device__ __forceinline__ void add(float x) {
-    const float y = x - c;
-    const float t = s + y;
-    c = (t - s) - y;
-    s = t;
-  }
-  __device__ __forceinline__ double get() const { return (double)s - (double)c; }
-};
+// KahanF: tc_common.cuh
 
 // u = p^(2-alpha) = t^(e0-1) for t > 0, else 0; p = t^e0
 template <int AK>

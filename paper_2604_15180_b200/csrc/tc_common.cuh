@@ -461,3 +461,23 @@ __device__ __forceinline__ uint32_t ld_shared_cluster(uint32_t cluster_addr) {
 }
 }  // namespace tc
 }  // namespace adattn_b200
+
+namespace adattn_b200 {
+namespace tc {
+// Compensated (Kahan) fp32 running sum: the per-row sums of the delta kernel and of the
+// forward's REF sweeps see one add per 32-key chunk, and an FP64 add per chunk
+// stalled those epilogues on the FP64 pipe (ncu: DADD held ~30% of the delta
+// kernel's warp-stall samples).  The compensated
+// fp32 sum keeps the error at the level of the fp32 chunk partials themselves.
+struct KahanF {
+  float s = 0.f, c = 0.f;
+  __device__ __forceinline__ void add(float x) {
+    const float y = x - c;
+    const float t = s + y;
+    c = (t - s) - y;
+    s = t;
+  }
+  __device__ __forceinline__ double get() const { return (double)s - (double)c; }
+};
+}  // namespace tc
+}  // namespace adattn_b200

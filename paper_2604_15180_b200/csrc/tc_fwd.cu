@@ -1212,7 +1212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       bar_sync(3, kEpi);  // C/Chi published, masks cleared, counts consumed
       const float C = sRow[e * 4 + 2];
       const float Chi = sRow[e * 4 + 3];
-      double f = 0.0, f1 = 0.0, f2 = 0.0, fhi = 0.0;
+      KahanF f, f1, f2, fhi;  // compensated fp32 over the fp32 slice sums
       for (int J = 0; J <= jl; ++J) {
         if (!act(1, rg, J)) continue;
         float mx_t = -CUDART_INF_F;
@@ -1226,11 +1226,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float th = fmaf(A1, v[i], Chi);
               if (th > 0.f) shi += exp2f(a.e0f * __log2f(th));
             }
-            fhi += (double)shi;
+            fhi.add(shi);
           }
-          f += (double)s0;
-          f1 += (double)s1;
-          f2 += (double)s2;
+          f.add(s0);
+          f1.add(s1);
+          f2.add(s2);
           mx_t = fmaxf(mx_t, mx);
         });
         const int jt = 2 * J + half;  // reference key tile of this thread's half
@@ -1238,18 +1238,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           atomicOr(&smask[rb * wpr + (jt >> 5)], 1u << (jt & 31));
       }
       if (half == 1) {
-        sPart[e * 4 + 0] = f;
-        sPart[e * 4 + 1] = f1;
-        sPart[e * 4 + 2] = f2;
-        sPart[e * 4 + 3] = fhi;
+        sPart[e * 4 + 0] = f.get();
+        sPart[e * 4 + 1] = f1.get();
+        sPart[e * 4 + 2] = f2.get();
+        sPart[e * 4 + 3] = fhi.get();
       }
       bar_sync(bar_rg, 256);
       bool stepped = false;
       if (half == 0 && !rs.done) {
-        rs.f = -1.0 + (f + sPart[e * 4 + 0]);
-        rs.f1 = -e0 * (f1 + sPart[e * 4 + 1]);
-        rs.f2 = e0 * (e0 - 1.0) * (f2 + sPart[e * 4 + 2]);
-        if (first_pass) rs.f_hi = -1.0 + (fhi + sPart[e * 4 + 3]);
+        rs.f = -1.0 + (f.get() + sPart[e * 4 + 0]);
+        rs.f1 = -e0 * (f1.get() + sPart[e * 4 + 1]);
+        rs.f2 = e0 * (e0 - 1.0) * (f2.get() + sPart[e * 4 + 2]);
+        if (first_pass) rs.f_hi = -1.0 + (fhi.get() + sPart[e * 4 + 3]);
         stepped = row_step(rs, g.alpha, g.refine_tol, g.refine_iters, need_sec);
         sRow[e * 4 + 2] = (float)(B - rs.tau);
       }
