@@ -1289,8 +1289,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float2 t = __ffma2_rn(A2, make_float2(v[2 * i], v[2 * i + 1]), C2);
-              pk[i] = pvf16 ? pack_f16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f))
-                            : pack_bf16x2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f));
+              float2 pp;
+              if constexpr (AK == AK15 || AK == AK125 || AK == AK2) {  // packed powers
+                const float2 tp = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
+                if constexpr (AK == AK2) {
+                  pp = tp;
+                } else {
+                  pp = __fmul2_rn(tp, tp);
+                  if constexpr (AK == AK125) pp = __fmul2_rn(pp, pp);
+                }
+              } else {
+                pp = make_float2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f));
+              }
+              pk[i] = pvf16 ? pack_f16x2(pp.x, pp.y) : pack_bf16x2(pp.x, pp.y);
             }
           } else {
 #pragma unroll
