@@ -1974,15 +1974,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         mbar_wait(&full[st], (u / KS) & 1);
         tc_fence_after();
         const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (leader) umma2_bf16(tmem + b * 128, dK[c] + (uint64_t)(2 * k),
-                                   dQS[c] + so + (uint64_t)(2 * k), IDESC_S, (c | k) != 0);
-            if (leader) umma2_bf16(tmem + b * 128 + 64, dV[c] + (uint64_t)(2 * k),
-                                   dDS[c] + so + (uint64_t)(2 * k), IDESC_S, (c | k) != 0);
-          }
+        // S^T and dP^T as two 8-MMA chains (descriptors stepped inside one asm block)
+        if (leader) {
+          umma_ss_d128<2, ((KB * 128) >> 4), ((32 * 128) >> 4)>(tmem + b * 128, dK[0], dQS[0] + so, IDESC_S, 0u);
+          umma_ss_d128<2, ((KB * 128) >> 4), ((32 * 128) >> 4)>(tmem + b * 128 + 64, dV[0], dDS[0] + so, IDESC_S, 0u);
+        }
         if (leader) umma2_commit_mc(&s_full[b]);
         if (prev >= 0) grad_mma(u - 1, prev_st);
         prev = i;
