@@ -1804,6 +1804,8 @@ __global__ void f16_plan_kernel(F16Plan* pl, float alpha, int d, int want_dv, in
   pl->inv_sigma = 1.f / sigma;
 }
 
+constexpr int kKvThreads = 352;  // pair dK/dV: 8 epilogue warps, producer, 2 MMA issuers
+
 template <int D>
 struct Kv2Smem {
   static_assert(D == 128, "pair dK/dV kernel: d = 128");
@@ -1822,7 +1824,7 @@ struct Kv2Smem {
 };
 
 template <int D, int AK, bool DSF16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
     tc_dkdv2_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_qd,
                     const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_vb,
                     const __grid_constant__ CUtensorMap tm_doh, const __grid_constant__ CUtensorMap tm_dod,
@@ -1850,6 +1852,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* p_full = s_full + 2;     // [2] leader, 16 warps
   uint64_t* kv_full = p_full + 2;    // leader
   uint64_t* acc_full = kv_full + 1;  // each CTA
+  uint64_t* grad_done = acc_full + 1;  // [2] leader: gradient MMAs of the unit in S buffer b done
   volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
   uint8_t* ubits = smem + L::OFF_UB;  // [t_r]: bit 2r+kh = block (i, key tile kh of CTA r)
 
@@ -1865,14 +1868,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int pj0 = pkey0 / 64;           // first of the pair's four reference key tiles
   const int i_first = g.causal ? pkey0 / QT : 0;
 
-  for (int i = threadIdx.x; i < g.t_r; i += kThreads) {
+  for (int i = threadIdx.x; i < g.t_r; i += kKvThreads) {
     const uint32_t w = a.mask[((size_t)bh * g.t_r + i) * g.wpr + (pj0 >> 5)];
     ubits[i] = (uint8_t)((w >> (pj0 & 31)) & 15u);
   }
   if (tid == 0) {
     for (int i = 0; i < KS; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], 2);  // S^T/dP^T reads (warp 9) and gradient reads (warp 10)
       mbar_init(&rfull[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -1881,6 +1884,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     mbar_init(kv_full, 1);
     mbar_init(acc_full, 1);
+    mbar_init(&grad_done[0], 1);
+    mbar_init(&grad_done[1], 1);
     fence_barrier_init();
   }
   if (warp == 8) tmem_alloc_2sm(const_cast<uint32_t*>(s_tmem), 512);
@@ -1920,72 +1925,93 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (leader) mbar_expect_tx(&rfull[st], QT * 8);
       if (leader) bulk_load(base + 2 * L::HB + 2 * L::DB, a.rowc + qrow, QT * 8, &rfull[st]);
     }
-  } else if (warp == 9) {  // MMA issuer: pair leader only
+  } else if (warp == 9 || warp == 10) {  // MMA issuers: pair leader only
+    // Two issuing warps on different SM sub-partitions: warp 9 issues S^T / dP^T of
+    // every unit, warp 10 the gradient products; the tensor pipe queues about one MMA
+    // ahead, so each warp's waits and bookkeeping are covered by the other's MMAs.
+    // S buffer b = u & 1: S^T/dP^T(u + 2) waits until the gradients of unit u (which
+    // read P/dS(u) from that buffer) are done (grad_done[b]).
     if (lead_cta) {
       const bool leader = elect_one_sync();
       constexpr uint32_t IDESC_S = idesc_bf16_f32(256, QT, false, false);
       constexpr uint32_t IDESC_G = idesc_bf16_f32(256, D, false, true);
       constexpr uint32_t IDESC_G16 = idesc_f16_f32(256, D, false, true);
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), st_addr = smem_u32(sSt);
-      uint64_t dK[NCH], dV[NCH], dQS[NCH], dDS[NCH];
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        dK[c] = desc_kmajor(k_addr + c * KB * 128);
-        dV[c] = desc_kmajor(v_addr + c * KB * 128);
-        dQS[c] = desc_kmajor(st_addr + c * 32 * 128);
-        dDS[c] = desc_kmajor(st_addr + L::HB + c * 32 * 128);
-      }
-      const uint64_t dQD = desc_mnmajor(st_addr + 2 * L::HB, QT * 128);
-      const uint64_t dDD = desc_mnmajor(st_addr + 2 * L::HB + L::DB, QT * 128);
       mbar_wait(kv_full, 0);
       tc_fence_after();
-      uint32_t u = 0, prev_st = 0;
-      bool init = false;
-      int prev = -1;
-      auto grad_mma = [&](uint32_t uu, uint32_t st) {
-        const uint32_t b = uu & 1;
-        mbar_wait(&p_full[b], (uu >> 1) & 1);
-        tc_fence_after();
-        const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
+#ifdef ADATTN_PIPE_STATS
+      const long long t_m0 = clock64();
+#endif
+      uint32_t u = 0;
+      if (warp == 9) {
+        const uint64_t dK0 = desc_kmajor(k_addr), dV0 = desc_kmajor(v_addr);
+        const uint64_t dQS0 = desc_kmajor(st_addr), dDS0 = desc_kmajor(st_addr + L::HB);
+        for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
+          const uint32_t st = u % KS, b = u & 1;
+          {
+            BSTAT_T0();
+            mbar_wait(&full[st], (u / KS) & 1);
+            BSTAT_ADD(0, leader);
+          }
+          mbar_wait(&grad_done[b], ((u >> 1) & 1) ^ 1);
+          tc_fence_after();
+          BSTAT_T0();
+          const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
+          // S^T and dP^T as two 8-MMA chains (descriptors stepped inside one asm block)
+          if (leader) {
+            umma_ss_d128<2, ((KB * 128) >> 4), ((32 * 128) >> 4)>(tmem + b * 128, dK0, dQS0 + so, IDESC_S, 0u);
+            umma_ss_d128<2, ((KB * 128) >> 4), ((32 * 128) >> 4)>(tmem + b * 128 + 64, dV0, dDS0 + so, IDESC_S, 0u);
+          }
+          if (leader) umma2_commit_mc(&s_full[b]);
+          if (leader) umma2_commit_mc(&empty[st]);
+          BSTAT_ADD(5, leader);
+        }
+      } else {
+        const uint64_t dQD = desc_mnmajor(st_addr + 2 * L::HB, QT * 128);
+        const uint64_t dDD = desc_mnmajor(st_addr + 2 * L::HB + L::DB, QT * 128);
+        bool init = false;
+        for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
+          const uint32_t st = u % KS, b = u & 1;
+          {
+            BSTAT_T0();
+            mbar_wait(&p_full[b], (u >> 1) & 1);
+            BSTAT_ADD(1, leader);
+          }
+          tc_fence_after();
+          BSTAT_T0();
+          const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t acol = 32 * (k >> 1) + 8 * (k & 1);
-          const uint64_t bdo = dDD + so + (uint64_t)(128 * k);
-          const uint64_t bq = dQD + so + (uint64_t)(128 * k);
-          const uint32_t acc = (init || k > 0) ? 1u : 0u;
-          if (f16) {
-            if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G16, acc);
-          } else {
-            if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G, acc);
-            if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t acol = 32 * (k >> 1) + 8 * (k & 1);
+            const uint64_t bdo = dDD + so + (uint64_t)(128 * k);
+            const uint64_t bq = dQD + so + (uint64_t)(128 * k);
+            const uint32_t acc = (init || k > 0) ? 1u : 0u;
+            if (f16) {
+              if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G16, acc);
+            } else {
+              if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G, acc);
+              if (leader) umma2_bf16_ts(tmem + 256, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
+            }
+            if (f16s) {
+              if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol, bq, IDESC_G16, acc);
+            } else {
+              if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol, bq, IDESC_G, acc);
+              if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol + 16, bq, IDESC_G, 1u);
+            }
           }
-          if (f16s) {
-            if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol, bq, IDESC_G16, acc);
-          } else {
-            if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol, bq, IDESC_G, acc);
-            if (leader) umma2_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol + 16, bq, IDESC_G, 1u);
-          }
+          init = true;
+          if (leader) umma2_commit_mc(&grad_done[b]);
+          if (leader) umma2_commit_mc(&empty[st]);
+          BSTAT_ADD(6, leader);
         }
-        init = true;
-        if (leader) umma2_commit_mc(&empty[st]);
-      };
-      for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
-        const uint32_t st = u % KS, b = u & 1;
-        mbar_wait(&full[st], (u / KS) & 1);
-        tc_fence_after();
-        const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
-        // S^T and dP^T as two 8-MMA chains (descriptors stepped inside one asm block)
-        if (leader) {
-          umma_ss_d128<2, ((KB * 128) >> 4), ((32 * 128) >> 4)>(tmem + b * 128, dK[0], dQS[0] + so, IDESC_S, 0u);
-          umma_ss_d128<2, ((KB * 128) >> 4), ((32 * 128) >> 4)>(tmem + b * 128 + 64, dV[0], dDS[0] + so, IDESC_S, 0u);
-        }
-        if (leader) umma2_commit_mc(&s_full[b]);
-        if (prev >= 0) grad_mma(u - 1, prev_st);
-        prev = i;
-        prev_st = st;
+        if (leader) umma2_commit_mc(acc_full);
       }
-      if (prev >= 0) grad_mma(u - 1, prev_st);
-      if (leader) umma2_commit_mc(acc_full);
+#ifdef ADATTN_PIPE_STATS
+      if (leader && warp == 10) {
+        atomicAdd(&g_bwd_stats[3], (unsigned long long)(clock64() - t_m0));
+        atomicAdd(&g_bwd_stats[4], (unsigned long long)u);
+      }
+#endif
     }
   } else if (warp < 8) {  // epilogue (warp % 4 = TMEM lane quarter)
     const int half = warp >> 2;        // query columns 32*half .. +31
@@ -2003,7 +2029,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t st = u % KS, b = u & 1;
       const bool mine = (ubits[i] >> kbit) & 1u;
       any |= mine;
-      mbar_wait(&s_full[b], (u >> 1) & 1);
+      {
+        BSTAT_T0();
+        mbar_wait(&s_full[b], (u >> 1) & 1);
+        BSTAT_ADD(2, warp == 0 && lane == 0);
+      }
       mbar_wait(&rfull[st], (u / KS) & 1);
       tc_fence_after();
       float s[32], dp[32];
@@ -2154,7 +2184,7 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     const size_t sm = Kv2Smem<128>::bytes(g.t_r);
     if ((e = set_smem(k2, sm))) return e;
     prof_begin("tc_dkdv", st);
-    k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
+    k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kKvThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
                                                                    m[7], m[14], m[16], a);
     prof_end(st);
     note_launch();
