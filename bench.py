@@ -192,8 +192,12 @@ def main():
         return r, g
 
     def timed(p, dout, warm, steps, profile=False):
+        # warm-up holds the previous step's results exactly like the timed loop, so the
+        # caching allocator owns both result sets before timing (a cudaMalloc of a few
+        # GB inside the first timed step stalled it by up to ~10 ms)
+        res = g = None
         for _ in range(warm):
-            step(p, dout)
+            res, g = step(p, dout)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
