@@ -987,11 +987,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (nb <= 8)
         hist_sweep<1>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
                       [&](int J, uint32_t* hE, uint32_t* hO) {
-#ifdef ADATTN_EXP_HIST_EMPTY
-          tau_tile(J, act_own(0, rg, J), [&](const float* v) { hE[0] += __float_as_uint(v[0]) & 1u; });
-#else
           tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
-#endif
         });
       else
         hist_sweep<2>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
