@@ -13,10 +13,12 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda"
 
 
-@pytest.mark.parametrize("bh,pinned", [((2, 8), True), ((1, 3), False), ((4, 16), True)])
-def test_run_host_matches_device_path(bh, pinned):
+@pytest.mark.parametrize("bh,pinned,N", [((2, 8), True, 1024), ((1, 3), False, 1024),
+                                         ((4, 16), True, 1024), ((2, 13), True, 512)])
+def test_run_host_matches_device_path(bh, pinned, N):
+    """(2, 13): 26 heads -> 2-head end chunks around unequal middle chunks (5, 5, 4, 4)."""
     B, H = bh
-    N, D = 1024, 128
+    D = 128
     g = torch.Generator(device="cpu").manual_seed(B * 100 + H)
     q, k, v, do = ((torch.randn(B, H, N, D, generator=g)).to(torch.bfloat16) for _ in range(4))
     prob = pa.AttentionProblem(q.to(DEV), k.to(DEV), v.to(DEV), path="tc", alpha=1.5, causal=True)
