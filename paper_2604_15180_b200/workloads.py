@@ -54,6 +54,32 @@ def anchored(B, H, N, D, beta, causal=True, seed=0, device="cuda", dtype=torch.b
     return q.to(dtype), k.to(dtype), v.to(dtype), do.to(dtype)
 
 
+def gaussian_heads(heads, N, D, qscale=1.0, seed=0, device="cuda", dtype=torch.bfloat16):
+    """``[1, len(heads), N, D]`` q, k, v, dO where head h is drawn from its own
+    generator (seed + h): a head's values do not depend on how the B x H heads are
+    sharded over ranks, so a sharded run is comparable head by head with a
+    single-GPU run of the same heads (bench.py validation)."""
+    heads = list(heads)
+    out = [torch.empty(1, len(heads), N, D, dtype=dtype, device=device) for _ in range(4)]
+    for i, h in enumerate(heads):
+        g = torch.Generator(device=device).manual_seed(seed + h)
+        for j, s in enumerate((qscale, 1.0, 1.0, 1.0)):
+            out[j][0, i] = (s * torch.randn(N, D, generator=g, device=device)).to(dtype)
+    return tuple(out)
+
+
+def anchored_heads(heads, N, D, beta, causal=True, seed=0, device="cuda",
+                   dtype=torch.bfloat16):
+    """Per-head-seeded ``anchored`` inputs, ``[1, len(heads), N, D]`` (see gaussian_heads)."""
+    heads = list(heads)
+    out = [torch.empty(1, len(heads), N, D, dtype=dtype, device=device) for _ in range(4)]
+    for i, h in enumerate(heads):
+        parts = anchored(1, 1, N, D, beta, causal, seed=seed + h, device=device, dtype=dtype)
+        for j in range(4):
+            out[j][0, i] = parts[j][0, 0]
+    return tuple(out)
+
+
 def flops(D: int, nnz: int, addressable: int, ref_passes: int = 3) -> dict:
     """F_eff = 14 d 4096 nnz (fwd QK^T+PV, bwd S, dP, dV, dK, dQ
     over active 64x64 blocks); F_alg = F_eff + 2 d 4096 (2 + R) A (max, histogram and

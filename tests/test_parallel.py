@@ -65,3 +65,61 @@ def test_gloo_world2_collectives():
     assert out[1][2] is None
     g = out[0][2]
     assert len(g) == 6 and g[0][0] == 0.0 and g[3][0] == 1.0
+
+
+def test_bench_self_launch_plumbing_gloo():
+    """`bench.py --gpus 2` outside torchrun re-executes itself under
+    torch.distributed.run with 2 ranks; --plumbing-check runs the multi-rank host
+    path (head sharding, per-head-seeded inputs, one digest gather, comparison
+    with a single-rank recomputation of all heads, max-over-ranks timing) under
+    gloo with an input digest in place of the GPU kernels."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--plumbing-check"], capture_output=True, text=True, timeout=300,
+                         env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = lines[0]
+    assert rec["n_ranks"] == 2 and rec["max_over_ranks"] == 2.0
+    assert rec["shards"] == [[0, 3], [3, 3]]
+    assert rec["validation"]["heads"] == 6
+    assert rec["validation"]["bitwise_equal_to_1gpu_run"] is True
+
+
+def test_digest_gather_uneven_shards_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_digest_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, g = q.get(timeout=120)
+        res[r] = g
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[1] is None
+    assert res[0] == [[float(h), 2.0 * h] for h in range(5)]
+
+
+def _digest_worker(rank, world, port, q):
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        start, count = parallel.shard_heads(5, world, rank)
+        dig = torch.tensor([[float(h), 2.0 * h] for h in range(start, start + count)],
+                           dtype=torch.float64)
+        g = bench.gather_digests(dig, 5, world, rank)
+        q.put((rank, None if g is None else g.tolist()))
+    finally:
+        dist.destroy_process_group()
