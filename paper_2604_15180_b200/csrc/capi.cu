@@ -121,14 +121,14 @@ int resolve(const adattn_problem* p, const Geom& g) {
   if (p->path == ADATTN_PATH_TC) {
     if (!tc_ok)
       return -fail(ADATTN_ERR_UNSUPPORTED,
-                   "adattn_b200: tensor-core path needs bf16 inputs, block 64x64, d=dv in "
-                   "{64,128}, bins<=32 (" + tc_envelope() + ")");
+                   "adattn_b200: tensor-core path needs " + tc_envelope());
     return ADATTN_PATH_TC;
   }
   if (p->path == ADATTN_PATH_AUTO && tc_ok) return ADATTN_PATH_TC;
   if (!exact_supported(g))
     return -fail(ADATTN_ERR_UNSUPPORTED,
-                 "adattn_b200: exact path supports block_r, block_c <= 64 and d, dv <= 128");
+                 "adattn_b200: exact path supports block_r, block_c <= 64, d, dv <= 128 and "
+                 "batch*heads <= 65535");
   return ADATTN_PATH_EXACT;
 }
 

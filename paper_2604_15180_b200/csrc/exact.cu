@@ -587,8 +587,10 @@ cudaError_t prep(K kernel, size_t smem) {
 
 }  // namespace
 
+// (grid.y carries the head index: at most 65535 heads per call)
 bool exact_supported(const Geom& g) {
-  return g.block_r <= kTile && g.block_c <= kTile && g.d <= 128 && g.dv <= 128;
+  return g.block_r <= kTile && g.block_c <= kTile && g.d <= 128 && g.dv <= 128 &&
+         g.bh <= 65535;
 }
 
 static size_t fwd_smem(const Geom& g) {

@@ -25,7 +25,6 @@ namespace {
 constexpr int kRowThreads = 256;
 enum RowErr { RE_NONE = 0, RE_MASKED = 1, RE_NONFINITE = 2, RE_STRADDLE = 3 };
 
-__device__ int g_rows_err;
 
 struct RowsArgs {
   adattn_rows_problem p;
@@ -37,6 +36,7 @@ struct RowsArgs {
   int32_t* converged;
   float* probs;
   double* trace;
+  int* err;  // per-call error word (RowsError)
 };
 
 __device__ __forceinline__ double load_s(const void* base, size_t i, int dt) {
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kRowThreads) entmax_rows_kernel(const RowsArgs
   block_sum<2>(cv, red);
   const int visible = (int)cv[0];
   if (cv[1] > 0.0 || visible == 0) {
-    if (threadIdx.x == 0) atomicMax(&g_rows_err, visible == 0 ? RE_MASKED : RE_NONFINITE);
+    if (threadIdx.x == 0) atomicMax(a.err, visible == 0 ? RE_MASKED : RE_NONFINITE);
     return;
   }
   auto zval = [&](int j) -> double {  // centred score; masked -> -inf
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kRowThreads) entmax_rows_kernel(const RowsArgs
     f_eval3(3, taus, d3);
     const double slack = 1e-9;  // kStraddleSlack
     if (d3[0].f < -slack || d3[1].f > slack) {
-      if (threadIdx.x == 0) atomicMax(&g_rows_err, RE_STRADDLE);
+      if (threadIdx.x == 0) atomicMax(a.err, RE_STRADDLE);
       return;
     }
     double tau = init;
@@ -266,17 +266,17 @@ const char* rows_error_message(int code) {
 cudaError_t entmax_rows(const adattn_rows_problem& p, const void* scores, const uint8_t* mask,
                         double* tau, double* residual, int32_t* iterations, int32_t* converged,
                         float* probs, double* trace, cudaStream_t st, int* row_err) {
-  const int zero = 0;
-  cudaError_t e = cudaMemcpyToSymbolAsync(g_rows_err, &zero, sizeof(int), 0,
-                                          cudaMemcpyHostToDevice, st);
+  // per-call error word (concurrent calls on different streams do not share it)
+  int* err = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&err), sizeof(int), st);
   if (e) return e;
-  RowsArgs a{p, scores, mask, tau, residual, iterations, converged, probs, trace};
+  if ((e = cudaMemsetAsync(err, 0, sizeof(int), st))) return e;
+  RowsArgs a{p, scores, mask, tau, residual, iterations, converged, probs, trace, err};
   entmax_rows_kernel<<<(unsigned)p.rows, kRowThreads, 0, st>>>(a);
   note_launch();
   if ((e = cudaGetLastError())) return e;
-  if ((e = cudaMemcpyFromSymbolAsync(row_err, g_rows_err, sizeof(int), 0, cudaMemcpyDeviceToHost,
-                                     st)))
-    return e;
+  if ((e = cudaMemcpyAsync(row_err, err, sizeof(int), cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaFreeAsync(err, st))) return e;
   return cudaStreamSynchronize(st);
 }
 

@@ -1,10 +1,12 @@
 // tc.cu -- dispatch for the bf16 tensor-core path and its TMA descriptor helper.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
 #include "tc.cuh"
+#include "tc_common.cuh"
 #include "tc_host.cuh"
 
 namespace adattn_b200 {
@@ -106,6 +108,56 @@ bool pv_f16_enabled() {
   return !(s && *s == '0');
 }
 
+// blocks [h * bpp, (h + 1) * bpp) cover head h's n2 bf16 pairs
+__global__ void absmax_bf16_kernel(const __nv_bfloat162* __restrict__ src, size_t n2, int bpp,
+                                   uint32_t* maxbits) {
+  const int h = blockIdx.x / bpp, b = blockIdx.x - h * bpp;
+  src += (size_t)h * n2;
+  uint32_t m = 0;
+  for (size_t i = b * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)bpp * blockDim.x) {
+    const float2 f = __bfloat1622float2(src[i]);
+    m = max(m, max(__float_as_uint(fabsf(f.x)), __float_as_uint(fabsf(f.y))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(maxbits + h, m);
+}
+
+__global__ void f16_scaled_kernel(const __nv_bfloat162* __restrict__ src, __half2* __restrict__ dst,
+                                  size_t n2, int bpp, const uint32_t* maxbits) {
+  const int h = blockIdx.x / bpp, b = blockIdx.x - h * bpp;
+  const uint32_t mb = maxbits[h];
+  if (!f16_copy_ok(mb)) return;  // the kernels keep the head's bf16 operand
+  const float s = f16_pow2_scale(mb);
+  src += (size_t)h * n2;
+  dst += (size_t)h * n2;
+  for (size_t i = b * (size_t)blockDim.x + threadIdx.x; i < n2; i += (size_t)bpp * blockDim.x) {
+    const float2 f = __bfloat1622float2(src[i]);
+    dst[i] = __floats2half2_rn(f.x * s, f.y * s);
+  }
+}
+
+static int blocks_per_head(int heads) { return std::max(1, std::min(64, 4 * 148 / heads)); }
+
+cudaError_t f16_absmax(const void* src, int heads, size_t elems, uint32_t* maxbits,
+                       cudaStream_t st) {
+  const int bpp = blocks_per_head(heads);
+  absmax_bf16_kernel<<<heads * bpp, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat162*>(src),
+                                                  elems / 2, bpp, maxbits);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t f16_convert_scaled(const void* src, void* dst, int heads, size_t elems,
+                               const uint32_t* maxbits, cudaStream_t st) {
+  const int bpp = blocks_per_head(heads);
+  f16_scaled_kernel<<<heads * bpp, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat162*>(src),
+                                                 reinterpret_cast<__half2*>(dst), elems / 2, bpp,
+                                                 maxbits);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // candidate lists, then (fp16 P V) the fp16 copy of V and its range maximum
 size_t forward_cand_bytes(const Geom& g) {
   const CandPlan p = cand_plan(g);
@@ -113,7 +165,8 @@ size_t forward_cand_bytes(const Geom& g) {
 }
 size_t forward_workspace(const Geom& g) {
   return forward_cand_bytes(g) +
-         (pv_f16_enabled() ? ((size_t)g.bh * g.m * g.dv * 2 + 255) / 256 * 256 + 256 : 0);
+         (pv_f16_enabled() ? ((size_t)g.bh * g.m * g.dv * 2 + 255) / 256 * 256 +
+                                 ((size_t)g.bh * 4 + 255) / 256 * 256 : 0);
 }
 
 }  // namespace tc

@@ -75,10 +75,14 @@ enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 //         |dS| <= 2 d max|dO| max|V| (|dp|, |delta| <= d max|dO| max|V|) so the
 //         power-of-two sigma puts every sigma dS within 2^15; results are
 //         scaled back by 1/sigma (exact).
+//  The fp16 copies of dO, Q and K are scaled by powers of two (f16_pow2_scale,
+//  tc_common.cuh) so small operands do not underflow; inv_* undo them.
+//  One plan per head (a head's results never depend on the other heads).
 struct F16Plan {
-  uint32_t max_do, max_v, max_q, max_k;  // |x| maxima as float bits
   int dv_ok, ds_ok;
   float sigma, inv_sigma;
+  float inv_do, inv_q, inv_k;
+  int pad;
 };
 
 // KahanF: tc_common.cuh
@@ -1220,8 +1224,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   using L = Dq2Smem<D>;
   // dQ = (sigma dS) K in fp16 (F16Plan): one MMA per K step instead of hi + lo.
   // DSF16 = false (the default) compiles the fp16 branches out of the issue loop.
-  const bool f16s = DSF16 && a.f16 && a.f16->ds_ok;
-  const float sig = f16s ? a.f16->sigma : 1.f;
   constexpr int NSK = L::NSK, NSV = L::NSV;
   constexpr int NCH = D / 64;
   const Geom& g = a.g;
@@ -1251,6 +1253,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int npair = g.n / (2 * QB_DQ);
   const int pair = (int)(blockIdx.x >> 1);
   const int bh = pair / npair;  // head-major, heaviest pairs first
+  const F16Plan* pl = a.f16 ? a.f16 + bh : nullptr;  // the head's fp16 plan
+  const bool f16s = DSF16 && pl && pl->ds_ok;
+  const float sig = f16s ? pl->sigma : 1.f;
   const int prow0 = (npair - 1 - pair % npair) * 2 * QB_DQ;
   const int row0 = prow0 + (int)rank * QB_DQ;
   const int nkt = g.m / DBN;
@@ -1446,7 +1451,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    const float oscale = a.scale_f * (f16s ? a.f16->inv_sigma : 1.f);
+    const float oscale = a.scale_f * (f16s ? pl->inv_sigma * pl->inv_k : 1.f);
     bool rany = false;
     for (int w = 0; w < wpr; ++w) rany |= smask[prb * wpr + w] != 0u;
 #pragma unroll
@@ -1770,28 +1775,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   dK += dS^T Q_i  : A = dS^T, B half = d cols 64r.. of Q_i           (QD, MN-major)
 // Units are the union of both CTAs' active units; rowc (C, delta) of the unit
 // comes with a local bulk copy on a per-stage local barrier.
-// bf16 -> fp16 copy (dst may be null: maximum only) and max |x| as float bits
-// (NaN orders above +inf, so a non-finite input fails every fp16 range test).
-__global__ void to_f16_max(const __nv_bfloat162* __restrict__ src, __half2* __restrict__ dst,
-                           size_t n2, uint32_t* maxbits) {
-  uint32_t m = 0;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const float2 f = __bfloat1622float2(src[i]);
-    m = max(m, max(__float_as_uint(fabsf(f.x)), __float_as_uint(fabsf(f.y))));
-    if (dst) dst[i] = __floats2half2_rn(f.x, f.y);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, m);
-}
-
-__global__ void f16_plan_kernel(F16Plan* pl, float alpha, int d, int want_dv, int want_ds) {
-  const float mdo = __uint_as_float(pl->max_do), mv = __uint_as_float(pl->max_v);
-  const float mq = __uint_as_float(pl->max_q), mk = __uint_as_float(pl->max_k);
-  pl->dv_ok = want_dv && mdo <= 65504.f;
+// mx: per-head |x| maxima (float bits) of dO, V, Q, K at mx[0..bh), mx[bh..2bh), ...
+__global__ void f16_plan_kernel(F16Plan* plans, const uint32_t* mx, int bh, float alpha, int d,
+                                int want_dv, int want_ds) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= bh) return;
+  F16Plan* pl = plans + h;
+  const uint32_t bdo = mx[h], bv = mx[bh + h], bq = mx[2 * bh + h], bk = mx[3 * bh + h];
+  const float mdo = __uint_as_float(bdo), mv = __uint_as_float(bv);
+  pl->dv_ok = want_dv && f16_copy_ok(bdo);
+  pl->inv_do = 1.f / f16_pow2_scale(bdo);
+  pl->inv_q = 1.f / f16_pow2_scale(bq);
+  pl->inv_k = 1.f / f16_pow2_scale(bk);
   const float bound = 2.f * (float)d * mdo * mv;  // >= max |dS| (alpha <= 2)
-  int ok = want_ds && alpha <= 2.f && mq <= 65504.f && mk <= 65504.f && bound < 3.0e38f;
+  int ok = want_ds && alpha <= 2.f && f16_copy_ok(bq) && f16_copy_ok(bk) && bound < 3.0e38f;
   float sigma = 1.f;
   if (ok && bound > 0.f) {
     int ex;
@@ -1833,9 +1830,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
   using L = Kv2Smem<D>;
   // fp16 gradient products (F16Plan): dV = P^T dO (P in [0, 1]) and dK = (sigma dS)^T Q,
   // one MMA per K step each instead of the bf16 hi + lo pairs
-  const bool f16 = a.f16 && a.f16->dv_ok;
-  const bool f16s = DSF16 && f16 && a.f16->ds_ok;  // (fp16 dS only with fp16 P: 3 epilogue variants)
-  const float sig = f16s ? a.f16->sigma : 1.f;
   constexpr int KS = L::KST2;
   constexpr int NCH = D / 64;
   const Geom& g = a.g;
@@ -1862,6 +1856,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
   const int npair = g.m / (2 * KB);
   const int pair = (int)(blockIdx.x >> 1);
   const int bh = pair / npair;          // head-major
+  const F16Plan* pl = a.f16 ? a.f16 + bh : nullptr;  // the head's fp16 plan
+  const bool f16 = pl && pl->dv_ok;
+  const bool f16s = DSF16 && f16 && pl->ds_ok;  // (fp16 dS only with fp16 P: 3 epilogue variants)
+  const float sig = f16s ? pl->sigma : 1.f;
   const int kp = pair % npair;          // low key pairs (most query units) first
   const int pkey0 = kp * 2 * KB;
   const int key0 = pkey0 + (int)rank * KB;
@@ -2072,7 +2070,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
 #pragma unroll
     for (int which = 0; which < 2; ++which) {  // 0: dV, 1: dK
       void* base = which == 0 ? a.dv : a.dk;
-      const float mul = which == 0 ? 1.f : a.scale_f * (f16s ? a.f16->inv_sigma : 1.f);
+      const float mul = which == 0 ? (f16 ? pl->inv_do : 1.f)
+                                   : a.scale_f * (f16s ? pl->inv_sigma * pl->inv_q : 1.f);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
         float o[32];
@@ -2240,6 +2239,10 @@ static size_t ws_rowc(const Geom& g) { return ((size_t)g.bh * g.n * sizeof(float
 static size_t ws_h(const Geom& g, int cols, int rows) {
   return ((size_t)g.bh * rows * cols * 2 + 255) / 256 * 256;
 }
+// per-head plans + 4 per-head maxima
+static size_t ws_plan(const Geom& g) {
+  return ((size_t)g.bh * (sizeof(F16Plan) + 16) + 255) / 256 * 256;
+}
 // only what the enabled fp16 products need (ADATTN_DV_F16 / ADATTN_DS_F16 are read
 // here and again at launch: change them between the query and the call and the
 // C-ABI's workspace check fails loudly)
@@ -2247,7 +2250,7 @@ size_t backward_workspace(const Geom& g) {
   const bool pairs = g.d == 128 && g.dv == 128;
   const bool dvh = pairs && dv_f16_enabled(), dsh = pairs && ds_f16_enabled();
   return ws_rowc(g) + (dvh || dsh ? ws_h(g, g.dv, g.n) : 0) +
-         (dsh ? ws_h(g, g.d, g.n) + ws_h(g, g.d, g.m) : 0) + 256;
+         (dsh ? ws_h(g, g.d, g.n) + ws_h(g, g.d, g.m) : 0) + ws_plan(g);
 }
 
 cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v, const double* tau,
@@ -2304,20 +2307,27 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
       off += ws_h(g, g.d, g.m);
     }
     F16Plan* plan = reinterpret_cast<F16Plan*>(w8 + off);
-    if ((e = cudaMemsetAsync(plan, 0, sizeof(F16Plan), st))) return e;
-    auto cvt = [&](const void* src, __half2* dst, size_t elems, uint32_t* mx) {
-      to_f16_max<<<4 * 148, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat162*>(src), dst, elems / 2, mx);
-      note_launch();
-    };
-    cvt(dout, want_dv ? do16 : nullptr, (size_t)g.bh * g.n * g.dv, &plan->max_do);
+    uint32_t* mx = reinterpret_cast<uint32_t*>(plan + g.bh);  // [4][bh]
+    const int H = g.bh;
+    if ((e = cudaMemsetAsync(mx, 0, 16 * (size_t)H, st))) return e;
+    // per head: dO [n][dv], V [m][dv], Q [n][d], K [m][d]
+    const size_t eo = (size_t)g.n * g.dv, ev = (size_t)g.m * g.dv;
+    const size_t eq = (size_t)g.n * g.d, ek = (size_t)g.m * g.d;
+    if ((e = f16_absmax(dout, H, eo, mx, st))) return e;
     if (want_ds) {
-      cvt(v, nullptr, (size_t)g.bh * g.m * g.dv, &plan->max_v);
-      cvt(q, q16, (size_t)g.bh * g.n * g.d, &plan->max_q);
-      cvt(k, k16, (size_t)g.bh * g.m * g.d, &plan->max_k);
+      if ((e = f16_absmax(v, H, ev, mx + H, st))) return e;
+      if ((e = f16_absmax(q, H, eq, mx + 2 * H, st))) return e;
+      if ((e = f16_absmax(k, H, ek, mx + 3 * H, st))) return e;
     }
-    f16_plan_kernel<<<1, 1, 0, st>>>(plan, (float)g.alpha, g.d, want_dv ? 1 : 0, want_ds ? 1 : 0);
+    f16_plan_kernel<<<(H + 127) / 128, 128, 0, st>>>(plan, mx, H, (float)g.alpha, g.d,
+                                                     want_dv ? 1 : 0, want_ds ? 1 : 0);
     note_launch();
     if ((e = cudaGetLastError())) return e;
+    if (want_dv && (e = f16_convert_scaled(dout, do16, H, eo, mx, st))) return e;
+    if (want_ds) {
+      if ((e = f16_convert_scaled(q, q16, H, eq, mx + 2 * H, st))) return e;
+      if ((e = f16_convert_scaled(k, k16, H, ek, mx + 3 * H, st))) return e;
+    }
     if ((e = make_tmap_2d(&m[14], do16, nq, g.dv, QT))) return e;
     if (want_ds) {
       if ((e = make_tmap_2d(&m[15], k16, nk, g.d, DBN))) return e;

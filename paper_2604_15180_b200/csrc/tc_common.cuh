@@ -289,6 +289,23 @@ __device__ __forceinline__ void bar_sync(int id, int nthreads) {
   asm volatile("barrier.cta.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// fp16 operand copies are scaled by a power of two s = 2^(15 - e), mx in
+// [2^(e-1), 2^e), so the largest |x| s lands in [2^14, 2^15): no overflow, and
+// values down to 2^-29 of the maximum stay normal fp16 (an unscaled copy
+// underflows below 6.1e-5 in absolute terms).  s is exact, so the kernels undo
+// it with one multiply by 1/s in their epilogue.  `maxbits` is max |x| as
+// float bits (NaN orders above +inf); a copy with a non-finite entry is not used.
+__host__ __device__ __forceinline__ bool f16_copy_ok(uint32_t maxbits) {
+  return maxbits <= 0x7F7FFFFFu;  // finite
+}
+__device__ __forceinline__ float f16_pow2_scale(uint32_t maxbits) {
+  const float mx = __uint_as_float(maxbits);
+  if (!(mx > 0.f) || !f16_copy_ok(maxbits)) return 1.f;
+  int ex;
+  frexpf(mx, &ex);
+  return ldexpf(1.f, max(-126, min(15 - ex, 126)));
+}
+
 }  // namespace tc
 }  // namespace adattn_b200
 

@@ -150,24 +150,9 @@ struct FwdArgs {
   uint2* cand;
   int cand_cap;
   int cand_slots;
-  // fp16 P V: max |V| (float bits) of the fp16 V copy; nullptr -> bf16 P
+  // fp16 P V: per head, max |V| (float bits) of the scaled fp16 V copy; nullptr -> bf16 P
   const uint32_t* v16_max;
 };
-
-// V (bf16) -> fp16 and max |V| (NaN orders above +inf: fails the range test)
-__global__ void v_to_f16_max(const __nv_bfloat162* __restrict__ src, __half2* __restrict__ dst,
-                             size_t n2, uint32_t* maxbits) {
-  uint32_t m = 0;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n2;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const float2 f = __bfloat1622float2(src[i]);
-    m = max(m, max(__float_as_uint(fabsf(f.x)), __float_as_uint(fabsf(f.y))));
-    dst[i] = __floats2half2_rn(f.x, f.y);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, m);
-}
 
 template <int D>
 struct FwdSmem {
@@ -378,8 +363,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_v,
                   const __grid_constant__ CUtensorMap tm_v16, const FwdArgs a) {
-  // O = P V in fp16 (P in [0, 1], V copied to fp16) unless some |V| exceeds fp16
-  const bool pvf16 = a.v16_max != nullptr && __uint_as_float(*a.v16_max) <= 65504.f;
   using L = FwdSmem<D>;
   static_assert(!PAIR || D == 128, "CTA pairs split K and V tiles in 64-row / 64-column halves");
   // ring: NST tiles, or (pairs) 2*NST items of half a tile (this CTA's half of K or V)
@@ -439,6 +422,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     row0 = (a.ncta_rows - 1 - (int)(blockIdx.x % a.ncta_rows)) * BM;
     lim0 = row0;
   }
+  // O = P V in fp16 (P in [0, 1], the head's V copied to fp16 scaled by a power of
+  // two s, undone on O) unless the head's V holds a non-finite value
+  const bool pvf16 = a.v16_max != nullptr && f16_copy_ok(a.v16_max[bh]);
+  const float oinv = pvf16 ? 1.f / f16_pow2_scale(a.v16_max[bh]) : 1.f;
   const int nkt = g.m / BN;                              // 128-key tiles
   const int Jmax = g.causal ? (lim0 + BM - 1) / BN : nkt - 1;
   const int wpr = g.wpr;
@@ -1323,10 +1310,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float o[32];
         tmem_ld32(to + c * 32, o);
         tmem_wait_ld();
-        if (!written) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = 0.f;
-        }
+        for (int i = 0; i < 32; ++i) o[i] = written ? o[i] * oinv : 0.f;
         const int x0 = half * (D / 2) + c * 32;
         if (g.out_dtype == ADATTN_F64) {
           double* dst = reinterpret_cast<double*>(a.out) + orow * D + x0;
@@ -1456,11 +1441,10 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
     uint8_t* w8 = reinterpret_cast<uint8_t*>(ws) + forward_cand_bytes(g);
     __half2* v16 = reinterpret_cast<__half2*>(w8);
     uint32_t* vmax = reinterpret_cast<uint32_t*>(w8 + ((size_t)g.bh * g.m * g.dv * 2 + 255) / 256 * 256);
-    if ((e = cudaMemsetAsync(vmax, 0, 4, st))) return e;
-    v_to_f16_max<<<4 * 148, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat162*>(v), v16,
-                                          (size_t)g.bh * g.m * g.dv / 2, vmax);
-    note_launch();
-    if ((e = cudaGetLastError())) return e;
+    const size_t ve = (size_t)g.m * g.dv;  // per head
+    if ((e = cudaMemsetAsync(vmax, 0, 4 * (size_t)g.bh, st))) return e;
+    if ((e = f16_absmax(v, g.bh, ve, vmax, st))) return e;
+    if ((e = f16_convert_scaled(v, v16, g.bh, ve, vmax, st))) return e;
     if ((e = make_tmap_2d(&tv16, v16, (uint64_t)g.bh * g.m, g.dv, BN))) return e;
     a.v16_max = vmax;
   }

@@ -28,6 +28,16 @@ size_t forward_workspace(const Geom& g);
 size_t forward_cand_bytes(const Geom& g);
 bool pv_f16_enabled();
 
+// Power-of-two-scaled fp16 copies of bf16 operands (tc_common.cuh f16_pow2_scale),
+// per head (`heads` consecutive blocks of `elems` values, elems even), so a head's
+// results never depend on the other heads of the call (chunked run_host, sharded
+// multi-GPU runs).  f16_absmax: atomicMax of max |x| (float bits) into
+// maxbits[h] (caller zeroes them); f16_convert_scaled: dst = fp16(src * s(maxbits[h])).
+cudaError_t f16_absmax(const void* src, int heads, size_t elems, uint32_t* maxbits,
+                       cudaStream_t st);
+cudaError_t f16_convert_scaled(const void* src, void* dst, int heads, size_t elems,
+                               const uint32_t* maxbits, cudaStream_t st);
+
 cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                     double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,
                     cudaStream_t st);
