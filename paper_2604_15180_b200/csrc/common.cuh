@@ -64,8 +64,10 @@ __device__ inline double f_h_eval_dev(const uint32_t* counts, int bins, double w
 
 // solve_histogram (reference histogram.cpp:73-161) + refine_bracket (163-165).
 // Writes tau_h and the refinement bracket [tau_h, tau_h + 1/B].
+// floor_out (optional): the bracket floor edge index (-1: no edge with f_h >= 0).
 __device__ inline void solve_histogram_dev(const uint32_t* counts, int bins, double alpha,
-                                           double& tau_h, double& lo_out, double& hi_out) {
+                                           double& tau_h, double& lo_out, double& hi_out,
+                                           int* floor_out = nullptr) {
   const int B = bins;
   const double w = 1.0 / bins;
   const double e0 = 1.0 / (alpha - 1.0);
@@ -89,6 +91,7 @@ __device__ inline void solve_histogram_dev(const uint32_t* counts, int bins, dou
     s1 += counts[k] * v;
     s2 += counts[k] * v * v;
   }
+  if (floor_out) *floor_out = floor_k;
   double th = 0.0;
   if (floor_k >= 0) {
     const double lo = floor_k * w;

@@ -91,7 +91,7 @@ static int nsmid_slots() {
 // ADATTN_CAND_CAP overrides the per-thread capacity (0 disables the lists).
 CandPlan cand_plan(const Geom& g) {
   CandPlan p{0, 0};
-  int cap = 256;
+  int cap = 512;
   if (const char* s = std::getenv("ADATTN_CAND_CAP")) cap = std::atoi(s);
   const char* force = std::getenv("ADATTN_CAND_FORCE");  // experiment: lists for any alpha
   if (cap < 64 || (g.alpha < 1.4 && !(force && *force == '1'))) return p;

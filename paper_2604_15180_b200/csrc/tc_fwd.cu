@@ -67,6 +67,7 @@ constexpr bool kDualMma = true;
 constexpr int kWarpProd = kEpiWarps, kWarpMma = kEpiWarps + 1;
 constexpr int kThreads = (kEpiWarps + (kDualMma ? 3 : 2)) * 32;
 constexpr int DEC_REF = 0, DEC_OUT = 1;
+constexpr int kTop = 8;  // list mode: largest per-tile maxima kept per thread in the MAX sweep
 
 enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 
@@ -540,17 +541,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     for (int J = 0; J <= Jmax; ++J) load(false, J);  // MAX
     MBAR_WAIT(plan_bar, 0);
-    for (int J = 0; J <= Jmax; ++J)  // HIST: tiles that can hold z >= 0
-      if (act_any(0, J)) load(false, J);
-    MBAR_WAIT(plan_bar, 1);
     uint32_t dround = 0;
     bool out_now = false;
-    if (a.cand) {  // CAND sweep: tiles that can hold z > lo - eps
+    auto hist_loads = [&]() {  // HIST: tiles that can hold z >= 0
+      for (int J = 0; J <= Jmax; ++J)
+        if (act_any(0, J)) load(false, J);
+    };
+    if (!a.cand) {
+      hist_loads();
+      MBAR_WAIT(plan_bar, 1);
+    } else {  // CAND sweep (list mode): tiles that can hold z > k_s / B - eps
       for (int J = 0; J <= Jmax; ++J)
         if (act_any(1, J)) load(false, J);
       MBAR_WAIT(dec_bar, 0);
       dround = 1;
       out_now = *s_decision == DEC_OUT;
+      if (!out_now) hist_loads();  // list overflow: HIST, then REF sweeps
     }
     if (!out_now)
       for (uint32_t ref = 0;; ++ref) {
@@ -689,19 +695,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int J = 0; J <= Jmax; ++J) s_tile(J, -1);  // MAX
     sweep_mark(0);
     MBAR_WAIT(plan_bar, 0);
-    for (int J = 0; J <= Jmax; ++J)
-      if (act_any(0, J)) s_tile(J, 0);  // HIST
-    sweep_mark(1);
-    MBAR_WAIT(plan_bar, 1);
     uint32_t dround = 0;
     bool out_now = false;
-    if (a.cand) {  // CAND sweep
+    auto hist_tiles = [&]() {
+      for (int J = 0; J <= Jmax; ++J)
+        if (act_any(0, J)) s_tile(J, 0);  // HIST
+      sweep_mark(1);
+    };
+    if (!a.cand) {
+      hist_tiles();
+      MBAR_WAIT(plan_bar, 1);
+    } else {  // CAND sweep (list mode)
       for (int J = 0; J <= Jmax; ++J)
         if (act_any(1, J)) s_tile(J, 1);
       sweep_mark(2);
       MBAR_WAIT(dec_bar, 0);
       dround = 1;
       out_now = *s_decision == DEC_OUT;
+      if (!out_now) hist_tiles();  // list overflow: HIST, then REF sweeps
     }
     if (!out_now)
       for (uint32_t ref = 0;; ++ref) {
@@ -910,6 +921,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Also the per-(row group, tile) maximum raw score, for the activity sets
     // of the later sweeps (tiles whose every score is below every row's
     // threshold are skipped there).
+    // List mode (candidate lists enabled): the thread also keeps the kTop largest
+    // of its per-tile maxima (distinct scores); their histogram bounds the
+    // bracket floor from below (f_h only grows with more entries), which sets
+    // the candidate threshold of the single CAND sweep that replaces the HIST
+    // sweep (see the CAND pass below).
+    const bool list_mode = a.cand != nullptr;
+    float top[kTop];
+#pragma unroll
+    for (int i = 0; i < kTop; ++i) top[i] = -CUDART_INF_F;
     float mraw = -CUDART_INF_F;
     for (int J = 0; J <= jl; ++J) {
       float tmx = -CUDART_INF_F;
@@ -919,6 +939,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 32; i += 2) tmx = fmaxf(tmx, fmaxf(v[i], v[i + 1]));
       });
       if (!own) continue;
+      if (list_mode) {  // sorted insert (descending) of the tile's max: 2 kTop - 1 FMNMX
+#pragma unroll
+        for (int t = kTop - 1; t > 0; --t) top[t] = fmaxf(top[t], fminf(top[t - 1], tmx));
+        top[0] = fmaxf(top[0], tmx);
+      }
       mraw = fmaxf(mraw, tmx);
       tmx = warp_max(tmx);
       if (lane == 0) atomicMax(&sTmax[rg * nkt_ + J], f2ord(tmx));
@@ -934,7 +959,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // activity set 0 (HIST): tile J of row group rg can hold a binned score
     // (z >= 0 <=> acc >= -B/A1) only if its max reaches the group's lowest
     // row threshold (lowered by a few ulps: a superset)
-    auto publish_set = [&](int s, float thr) {
+    auto publish_set = [&](int s, float thr, bool arrive) {
       thr = warp_min(thr);
       if (lane == 0) atomicMin(&sThr[s * 2 + rg], f2ord(thr));
       bar_sync(3, kEpi);
@@ -950,20 +975,57 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       bar_sync(3, kEpi);
       if constexpr (PAIR) pair_or_words(sActU + s * 2 * aw, sAct + s * 2 * aw, 2 * aw);
-      if (tid == 0) mbar_arrive(plan_bar);
+      if (arrive && tid == 0) mbar_arrive(plan_bar);
     };
+    // (list mode: one plan_bar arrival after both sets -- consecutive arrivals
+    // could run a waiter's parity two phases behind)
     {
       float th = (float)(-B / (double)A1);
       th -= 4e-7f * fabsf(th) + 1e-30f;
-      publish_set(0, th);
+      publish_set(0, th, !list_mode);
     }
 
-    // ---- pass HIST (attention.cpp:201-232): counts of min(floor(B z), B-1), z >= 0
+    // combine the two key halves' counts (bins < kmin dropped: incomplete in
+    // list mode) and solve; the half-0 thread owns the row's solver state
     const int nb = g.bins;  // 2..16 on this path (tc_supported)
+    uint32_t* row_cnt = sCnt + e * 16;
+    RowSolve rs;
+    rs.tau = 0.0;
+    rs.lo = rs.hi = 0.0;
+    rs.steps = 0;
+    rs.done = true;
+    auto solve_counts = [&](const uint32_t* cnt, int kmin) {
+      if (half == 1) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) row_cnt[k] = cnt[k];
+      }
+      bar_sync(bar_rg, 256);
+      if (half == 0) {
+        uint32_t c32[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          c32[k] = (k < nb && k >= kmin) ? cnt[k & 15] + row_cnt[k & 15] : 0u;
+        double th, lo, hi;
+        solve_histogram_dev(c32, nb, g.alpha, th, lo, hi);
+        rs.tau = th;
+        rs.lo = lo;
+        rs.hi = hi;
+        rs.f = rs.f1 = rs.f2 = rs.f_hi = 0.0;
+        rs.sec_tau = rs.sec_f = rs.best_tau = 0.0;
+        rs.best_af = CUDART_INF;
+        rs.steps = 0;
+        rs.sec_seeded = false;
+        rs.done = false;
+        sRow[e * 4 + 2] = (float)(B - rs.tau);
+        sRow[e * 4 + 3] = (float)(B - rs.hi);
+      }
+    };
+
+    // ---- pass HIST (attention.cpp:201-232): counts of min(floor(B z), B-1), z >= 0
+    auto hist_solve = [&]() {
     uint32_t cnt[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) cnt[k] = 0;
-    uint32_t* row_cnt = sCnt + e * 16;
     {
       const float cw = 1.0f - 0x1p-20f;  // keeps z = 1 (the row max) inside bin nb-1
       const float2 Aw = make_float2(A1 * (float)nb * cw, A1 * (float)nb * cw);
@@ -983,36 +1045,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         });
     }
     PASS_MARK(1);
-    // combine the two key halves; the half-0 thread owns the row's solver state
-    RowSolve rs;
-    rs.tau = 0.0;
-    rs.lo = rs.hi = 0.0;
-    rs.steps = 0;
-    rs.done = true;
-    if (half == 1) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) row_cnt[k] = cnt[k];
-    }
-    bar_sync(bar_rg, 256);
-    if (half == 0) {
-      uint32_t c32[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k)
-        c32[k] = k < nb ? cnt[k & 15] + row_cnt[k & 15] : 0u;
-      double th, lo, hi;
-      solve_histogram_dev(c32, nb, g.alpha, th, lo, hi);
-      rs.tau = th;
-      rs.lo = lo;
-      rs.hi = hi;
-      rs.f = rs.f1 = rs.f2 = rs.f_hi = 0.0;
-      rs.sec_tau = rs.sec_f = rs.best_tau = 0.0;
-      rs.best_af = CUDART_INF;
-      rs.steps = 0;
-      rs.sec_seeded = false;
-      rs.done = false;
-      sRow[e * 4 + 2] = (float)(B - rs.tau);
-      sRow[e * 4 + 3] = (float)(B - rs.hi);
-    }
+    solve_counts(cnt, 0);
+    };
 
     const bool need_sec = g.alpha > 2.0;
     const double e0 = g.e0;
@@ -1020,23 +1054,63 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t dround = 0;
     bool list_ok = false;
 
-    // ---- pass CAND: every score that can matter for tau in [lo, hi] or for
-    // the mask (z > lo - eps) is appended to a per-thread list as (raw score,
-    // 64-key block); the refinement (attention.cpp:234-332) then runs on the
-    // lists with no further sweeps.  Exact: f, f', f'' and the mask only see
-    // z > tau - 1e-9 >= lo - 1e-9, and each listed term is evaluated with the
-    // sweep's own formula t = A1*acc + (B - tau).  Overflow -> REF sweeps.
-    // activity set 1 (CAND / REF sweeps): scores below lo - eps contribute to
-    // neither f, f', f'' (tau >= lo) nor the mask (z > tau - 1e-9)
+    // ---- pass CAND: every score that can matter for the histogram solve, for
+    // tau in [lo, hi] or for the mask is appended to a per-thread list as (raw
+    // score, 64-key block); histogram, solve_histogram and the refinement
+    // (attention.cpp:201-332) then run on the lists with no further sweeps.
+    //
+    // List mode skips the HIST sweep.  The rows' kTop-per-thread largest scores
+    // form a subset histogram whose bracket floor k_s bounds the full
+    // histogram's floor k from below: f_h(e) = -1 + sum over bins above e of
+    // count * (edge - e)^e0 only grows when entries are added, so the largest
+    // edge with f_h >= 0 only moves up.  solve_histogram reads only the bins
+    // above its floor (histogram.cpp:104-159), so the bins >= k_s -- complete in
+    // a list of every score with z > k_s / B - eps -- give the exact tau_h, and
+    // tau >= tau_h >= k_s / B covers f, f', f'' and the mask (z > tau - 1e-9).
+    // Sweep mode (alpha < 1.4: lists too long) keeps HIST and the REF sweeps;
+    // a list overflow falls back to them too.
+    // Each listed term is evaluated with the sweeps' formula t = A1*acc + (B - tau).
+    int k_s = 0;  // (half 0, list mode) subset floor: bins >= k_s are complete
+    if (!list_mode) hist_solve();
+    if (list_mode) {
+      float* row_top = reinterpret_cast<float*>(row_cnt);
+      if (half == 1) {
+#pragma unroll
+        for (int i = 0; i < kTop; ++i) row_top[i] = top[i];
+      }
+      bar_sync(bar_rg, 256);
+      if (half == 0) {
+        uint32_t c32[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) c32[k] = 0u;
+        auto bin_in = [&](float acc) {
+          const float z = fmaf(A1, acc, Bf);
+          if (z >= 0.f) ++c32[min((int)((float)nb * z), nb - 1)];
+        };
+#pragma unroll
+        for (int i = 0; i < kTop; ++i) {
+          bin_in(top[i]);
+          bin_in(row_top[i]);
+        }
+        double th, lo, hi;
+        int fl;
+        solve_histogram_dev(c32, nb, g.alpha, th, lo, hi, &fl);
+        k_s = fl > 0 ? fl : 0;
+      }
+    }
+    // activity set 1 (CAND / REF sweeps): scores with z <= lo - eps (sweep mode:
+    // lo = tau_h; list mode: k_s / B <= tau_h) reach neither the solve, nor
+    // f, f', f'' (tau >= lo), nor the mask (z > tau - 1e-9)
     if (half == 0) {
       const float eps_t = 1e-6f * (2.f + fabsf(Bf));  // fp32 slack of z (|B| scale)
-      sRow[e * 4 + 0] = (float)(B - rs.lo) + eps_t;
+      const double lo_set = list_mode ? (double)k_s / nb : rs.lo;
+      sRow[e * 4 + 0] = (float)(B - lo_set) + eps_t;
     }
     bar_sync(bar_rg, 256);
     // z > lo - eps  <=>  acc > theta (A1 > 0), lowered by a few ulps (superset)
     float theta = -sRow[e * 4 + 0] / A1;
     theta -= 4e-7f * fabsf(theta) + 1e-30f;
-    publish_set(1, theta);
+    publish_set(1, theta, true);
 
     if (a.cand) {
       uint32_t smid;
@@ -1086,6 +1160,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           });
         }
         cnt = (int)(wp - lst);
+#ifdef ADATTN_PIPE_STATS
+        // [26] listed entries, [27] listing threads, [28] longest list, [29] overflowed threads
+        atomicAdd(&g_pipe_stats[26], (unsigned long long)cnt);
+        atomicAdd(&g_pipe_stats[27], 1ull);
+        atomicMax(&g_pipe_stats[28], (unsigned long long)cnt);
+        if (ovf) atomicAdd(&g_pipe_stats[29], 1ull);
+#endif
       }
       PASS_MARK(2);
       bool ovf_any = bar_red_or(4, kEpi, ovf);
@@ -1098,13 +1179,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* sl = reinterpret_cast<float*>(sRing);
         constexpr int lcap = NST * L::TILE / (kEpi * 4);
         const int ns = cnt < lcap ? cnt : lcap;
-        for (int i0 = 0; i0 < ns; i0 += 8) {
+        // the histogram of the listed scores (list mode), read in the same pass
+        uint32_t hc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) hc[k] = 0u;
+        for (int i0 = 0; i0 < cnt; i0 += 8) {
           uint32_t tmp[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) tmp[j] = i0 + j < ns ? lst[i0 + j].x : 0u;
+          for (int j = 0; j < 8; ++j) tmp[j] = i0 + j < cnt ? lst[i0 + j].x : 0xFF800000u;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < 8; ++j) {
             if (i0 + j < ns) sl[(i0 + j) * kEpi + tid] = __uint_as_float(tmp[j]);
+            const float z = fmaf(A1, __uint_as_float(tmp[j]), Bf);
+            if (z >= 0.f) {
+              const int k = min((int)((float)nb * z), nb - 1);
+#pragma unroll
+              for (int q = 0; q < 16; ++q) hc[q] += q == k ? 1u : 0u;
+            }
+          }
+        }
+        if (list_mode) {
+          solve_counts(hc, half == 0 ? k_s : 0);
+          // sPart (refinement partials) aliases the count rows of the OTHER row
+          // group (sCnt): both groups finish reading counts before any writes them
+          bar_sync(3, kEpi);
         }
         // refinement rounds on the lists (same RowSolve / row_step as the sweeps)
         for (;;) {
@@ -1112,8 +1210,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float C = sRow[e * 4 + 2];
           const float Chi = sRow[e * 4 + 3];
           double f = 0.0, f1 = 0.0, f2 = 0.0, fhi = 0.0;
-          for (int i = 0; i < cnt; ++i) {
-            const float acc = i < ns ? sl[i * kEpi + tid] : __uint_as_float(lst[i].x);
+          for (int i0 = 0; i0 < cnt; i0 += 8) {
+            // 8 loads in flight (entries past the staged ones come from L2)
+            float accs[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int i = i0 + j;
+              accs[j] = i < ns ? sl[i * kEpi + tid]
+                               : (i < cnt ? __uint_as_float(lst[i].x) : -CUDART_INF_F);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+            const float acc = accs[j];
             const float t = fmaf(A1, acc, C);
             if (t > 0.f) {
               if constexpr (AK == AK15) {
@@ -1140,6 +1248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (first_pass && need_sec) {
               const float th = fmaf(A1, acc, Chi);
               if (th > 0.f) fhi += (double)exp2f(a.e0f * __log2f(th));
+            }
             }
           }
           if (half == 1) {
@@ -1187,6 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(dec_bar);
       }
       dround = 1;
+      if (!list_ok) hist_solve();  // fallback: the exact histogram by the HIST sweep
     }
 
     // ---- passes REF (attention.cpp:234-332): sweeps (no lists, or a list overflowed)

@@ -43,3 +43,6 @@ for s, n in enumerate(["MAX", "HIST", "CAND", "REF/decision", "OUT (S+PV)"]):
         print(f"MMA sweep {n:13s} cycles {cyc}")
 print("MMA issue+commit cycles per rg-tile: MAX", st[44] / max(st[17], 1), "HIST+CAND", st[45] / max(st[19] + st[21], 1))
 print("epilogue thread 0: TMEM ld32+wait cycles per load", st[46] / max(st[47], 1), "loads", st[47])
+if st[27]:
+    print(f"candidate lists: mean {st[26] / st[27]:.1f} entries/thread, longest {st[28]}, "
+          f"overflowed threads {st[29]} of {st[27]}")
