@@ -8,6 +8,7 @@
  *
  *   adattn_b200_forward        <- adattn::forward        include/adattn/attention.hpp:72-76
  *                                                         (src/attention.cpp:157-361)
+ *   adattn_b200_forward_timed  <- adattn::forward with a PhaseTimings* (attention.hpp:62-76)
  *   adattn_b200_compute_delta  <- adattn::compute_delta  attention.hpp:82-85 (attention.cpp:411-446)
  *   adattn_b200_backward       <- adattn::backward       attention.hpp:87-92 (attention.cpp:448-539)
  *   adattn_b200_stats          <- AttentionStats fill + adattn::block_sparsity
@@ -109,6 +110,16 @@ int adattn_b200_forward(const adattn_problem* p, const void* q, const void* k, c
                         void* out, double* tau, double* row_max, uint32_t* mask,
                         int32_t* row_steps, void* workspace, size_t workspace_bytes,
                         void* stream);
+
+/* forward + PhaseTimings (attention.hpp:62-66; filled by the reference at
+ * attention.cpp:196-199, 229-232, 329-332, 352): phase_ms[0..3] = row max,
+ * histogram (+ tau_h), refinement (+ mask), output.  The forward's duration
+ * (CUDA events on `stream`) split by the share of CTA time each phase took
+ * (one %globaltimer-stamped thread per CTA).  Synchronises `stream`. */
+int adattn_b200_forward_timed(const adattn_problem* p, const void* q, const void* k,
+                              const void* v, void* out, double* tau, double* row_max,
+                              uint32_t* mask, int32_t* row_steps, void* workspace,
+                              size_t workspace_bytes, void* stream, double* phase_ms);
 
 int adattn_b200_compute_delta(const adattn_problem* p, const void* q, const void* k,
                               const void* v, const double* tau, const double* row_max,

@@ -33,7 +33,7 @@ EXPORTS = (
     "adattn_b200_launch_count", "adattn_b200_profile_enable", "adattn_b200_profile_read",
     "adattn_b200_tensor_save", "adattn_b200_tensor_load", "adattn_b200_io_last_error",
     "adattn_b200_attn_inputs", "adattn_b200_xoshiro", "adattn_b200_entmax_rows",
-    "adattn_b200_block_lists",
+    "adattn_b200_block_lists", "adattn_b200_forward_timed",
 )
 
 
@@ -95,6 +95,8 @@ def load() -> C.CDLL:
         lib.adattn_b200_backward_workspace.argtypes = [P]
         lib.adattn_b200_backward_workspace.restype = C.c_size_t
         lib.adattn_b200_forward.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+        lib.adattn_b200_forward_timed.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                                  C.c_size_t, vp, C.POINTER(C.c_double)]
         lib.adattn_b200_compute_delta.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                                   C.c_size_t, vp]
         lib.adattn_b200_backward.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,

@@ -210,9 +210,12 @@ class AttentionGradients:
 
 @dataclass
 class PhaseTimings:
-    """Mirror of PhaseTimings (attention.hpp:62-66).  The GPU forward runs all
-    four phases inside one kernel per query tile, so only ms[0] (the whole
-    forward, CUDA events) is filled."""
+    """Mirror of PhaseTimings (attention.hpp:62-66): ms[0..3] += row max,
+    histogram, refinement, output time of a forward (attention.cpp:196-199,
+    229-232, 329-332, 352), filled like the reference only when
+    ``threads <= 1``.  The GPU forward runs the four phases inside one kernel;
+    its CUDA-event duration is split by the share of CTA time each phase took
+    (adattn_b200_forward_timed)."""
     ms: list = field(default_factory=lambda: [0.0, 0.0, 0.0, 0.0])
 
 
@@ -236,9 +239,8 @@ _torch_out = {_lib.F32: torch.float32, _lib.F64: torch.float64}
 
 def forward(p: AttentionProblem, threads: int = 1,
             timings: Optional[PhaseTimings] = None) -> AttentionResult:
-    """Tiled alpha-entmax forward (attention.cpp:157-361).  ``threads`` is
-    accepted for signature parity and ignored (work goes to the current stream)."""
-    del threads
+    """Tiled alpha-entmax forward (attention.cpp:157-361).  ``threads`` only
+    gates ``timings`` as in the reference (work goes to the current stream)."""
     pb = p.c_problem()
     lib = _lib.load()
     _lib.check(lib.adattn_b200_validate(C.byref(pb)))
@@ -255,17 +257,15 @@ def forward(p: AttentionProblem, threads: int = 1,
     steps = torch.empty(lead + (n,), dtype=torch.int32, device=dev)
     ws_bytes = lib.adattn_b200_forward_workspace(C.byref(pb))
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
-    ev = None
-    if timings is not None:
-        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-        ev[0].record()
-    _lib.check(lib.adattn_b200_forward(C.byref(pb), _ptr(p.q), _ptr(p.k), _ptr(p.v), _ptr(out),
-                                       _ptr(tau), _ptr(row_max), _ptr(words), _ptr(steps),
-                                       _ptr(ws), ws_bytes, _stream()))
-    if ev is not None:
-        ev[1].record()
-        ev[1].synchronize()
-        timings.ms[0] += ev[0].elapsed_time(ev[1])
+    args = (C.byref(pb), _ptr(p.q), _ptr(p.k), _ptr(p.v), _ptr(out), _ptr(tau), _ptr(row_max),
+            _ptr(words), _ptr(steps), _ptr(ws), ws_bytes, _stream())
+    if timings is not None and threads <= 1:  # attention.cpp:170
+        ph = (C.c_double * 4)()
+        _lib.check(lib.adattn_b200_forward_timed(*args, ph))
+        for i in range(4):
+            timings.ms[i] += ph[i]
+    else:
+        _lib.check(lib.adattn_b200_forward(*args))
     return AttentionResult(out, tau, row_max, PackedBlockMask(words, t_r, t_c), steps, pb)
 
 

@@ -293,13 +293,17 @@ size_t adattn_b200_backward_workspace(const adattn_problem* p) {
   return resolve(p, g) == ADATTN_PATH_TC ? tc_backward_workspace(g) : 16;
 }
 
-int adattn_b200_forward(const adattn_problem* p, const void* q, const void* k, const void* v,
-                        void* out, double* tau, double* row_max, uint32_t* mask,
-                        int32_t* row_steps, void* workspace, size_t workspace_bytes,
-                        void* stream) {
+}  // extern "C"
+
+namespace {
+int forward_impl(const adattn_problem* p, const void* q, const void* k, const void* v,
+                 void* out, double* tau, double* row_max, uint32_t* mask, int32_t* row_steps,
+                 void* workspace, size_t workspace_bytes, void* stream,
+                 unsigned long long* phase_ns) {
   Geom g;
   int rc = check(p, &g);
   if (rc) return rc;
+  g.phase_ns = phase_ns;
   const int path = resolve(p, g);
   if (path < 0) return -path;
   if (!q || !k || !v || !out || !tau || !row_max || !mask)
@@ -314,6 +318,50 @@ int adattn_b200_forward(const adattn_problem* p, const void* q, const void* k, c
     e = exact_forward(g, q, k, v, out, tau, row_max, mask, row_steps, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "adattn_b200_forward");
+  return ADATTN_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int adattn_b200_forward(const adattn_problem* p, const void* q, const void* k, const void* v,
+                        void* out, double* tau, double* row_max, uint32_t* mask,
+                        int32_t* row_steps, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  return forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace, workspace_bytes,
+                      stream, nullptr);
+}
+
+int adattn_b200_forward_timed(const adattn_problem* p, const void* q, const void* k,
+                              const void* v, void* out, double* tau, double* row_max,
+                              uint32_t* mask, int32_t* row_steps, void* workspace,
+                              size_t workspace_bytes, void* stream, double* phase_ms) {
+  if (!phase_ms) return fail(ADATTN_ERR_INVALID, "adattn_b200_forward_timed: null phase_ms");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* acc = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&acc), 4 * sizeof(unsigned long long), st);
+  if (!e) e = cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), st);
+  if (!e) e = cudaEventCreate(&e0);
+  if (!e) e = cudaEventCreate(&e1);
+  if (!e) e = cudaEventRecord(e0, st);
+  if (e) return cuda_fail(e, "adattn_b200_forward_timed");
+  int rc = forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
+                        workspace_bytes, stream, acc);
+  unsigned long long ns[4] = {0, 0, 0, 0};
+  float total = 0.f;
+  e = cudaEventRecord(e1, st);
+  if (!e) e = cudaMemcpyAsync(ns, acc, sizeof ns, cudaMemcpyDeviceToHost, st);
+  if (!e) e = cudaStreamSynchronize(st);
+  if (!e) e = cudaEventElapsedTime(&total, e0, e1);
+  cudaFreeAsync(acc, st);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc) return rc;
+  if (e) return cuda_fail(e, "adattn_b200_forward_timed");
+  // the forward's event-timed duration, split by the CTAs' per-phase time shares
+  const double sum = double(ns[0]) + double(ns[1]) + double(ns[2]) + double(ns[3]);
+  for (int i = 0; i < 4; ++i) phase_ms[i] = sum > 0.0 ? double(total) * double(ns[i]) / sum : 0.0;
   return ADATTN_OK;
 }
 

@@ -23,7 +23,25 @@ struct Geom {
   int in_dtype, out_dtype;
   double alpha, scale, refine_tol;
   double e0;      // 1/(alpha-1)
+  // PhaseTimings (attention.hpp:62-66): when set, one thread per forward CTA adds the
+  // nanoseconds it spends in each reference phase (max, histogram, refinement,
+  // output) to phase_ns[0..3]
+  unsigned long long* phase_ns = nullptr;
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// close phase `i` of this CTA: add the time since `t` and restart the clock
+__device__ __forceinline__ void phase_tick(unsigned long long* acc, int i, unsigned long long& t) {
+  if (acc) {
+    const unsigned long long now = global_ns();
+    atomicAdd(acc + i, now - t);
+    t = now;
+  }
+}
 
 __device__ __forceinline__ double load_elem(const void* base, size_t i, int dtype) {
   if (dtype == ADATTN_BF16)

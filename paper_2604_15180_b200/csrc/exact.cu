@@ -104,6 +104,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const double am1 = g.alpha - 1.0;
   const double e0 = g.e0, e1 = e0 - 1.0, e2 = e0 - 2.0;
 
+  unsigned long long* const pacc = tid == 0 ? g.phase_ns : nullptr;
+  unsigned long long pt = pacc ? global_ns() : 0ull;
   load_rows(sQ, ldq, q, qbase, r0, nr, kTile, g.d, g.in_dtype);
   for (int i = tid; i < kTile; i += kThreads) sRowMax[i] = -CUDART_INF;
   for (int i = tid; i < kTile * g.bins; i += kThreads) sCnt[i] = 0u;
@@ -132,6 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  phase_tick(pacc, 0, pt);
   // Phase 2: histogram counts of z >= 0 (attention.cpp:110-155, 201-210)
   for (int jt = 0; jt <= jlim; ++jt) {
     const int c0 = jt * g.block_c, nc = min(g.block_c, g.m - c0);
@@ -174,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     rs.done = false;
   }
 
+  phase_tick(pacc, 1, pt);
   // Phase 3: refinement passes (attention.cpp:234-332)
   const bool need_sec = g.alpha > 2.0;
   bool first_pass = true;
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int w = tid; w < g.wpr; w += kThreads)
     mask_out[((size_t)bh * g.t_r + it) * g.wpr + w] = sAct[w];
 
+  phase_tick(pacc, 2, pt);
   // Phase 4: O over the set mask bits, ascending (attention.cpp:334-352)
   const int xg = tid & 31, rg = tid >> 5;
   double oacc[8][4];
@@ -304,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (x < g.dv) store_elem(out, obase + (size_t)(r0 + r) * g.dv + x, g.out_dtype, oacc[ii][jj]);
     }
   }
+  phase_tick(pacc, 3, pt);
 }
 
 // ---------------------------------------------------------- compute_delta

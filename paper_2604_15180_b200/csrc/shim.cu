@@ -142,7 +142,6 @@ int tiles(int len, int block) { return (len + block - 1) / block; }
 }  // namespace
 
 AttentionResult forward(const AttentionProblem& p, int threads, PhaseTimings* timings) {
-  (void)threads;
   const adattn_problem a = describe(p);
   const int t_r = tiles(a.n, a.block_r), t_c = tiles(a.m, a.block_c);
   AttentionResult res{Matrix(a.n, a.dv), std::vector<double>(a.n), std::vector<double>(a.n),
@@ -151,20 +150,17 @@ AttentionResult forward(const AttentionProblem& p, int threads, PhaseTimings* ti
       v(p.v.data.data(), p.v.data.size());
   Dev<double> out(res.out.data.size()), tau(a.n), rmax(a.n);
   Dev<uint32_t> mask(res.mask.words().size());
-  cudaEvent_t e0, e1;
-  cuda_check(cudaEventCreate(&e0), "event");
-  cuda_check(cudaEventCreate(&e1), "event");
-  cudaEventRecord(e0, 0);
-  abi_check(adattn_b200_forward(&a, q.p, k.p, v.p, out.p, tau.p, rmax.p, mask.p, nullptr, nullptr,
-                                0, nullptr));
-  cudaEventRecord(e1, 0);
+  if (timings && threads <= 1) {  // filled like the reference (attention.cpp:170)
+    double ph[4];
+    abi_check(adattn_b200_forward_timed(&a, q.p, k.p, v.p, out.p, tau.p, rmax.p, mask.p, nullptr,
+                                        nullptr, 0, nullptr, ph));
+    for (int i = 0; i < 4; ++i) timings->ms[i] += ph[i];
+  } else {
+    abi_check(adattn_b200_forward(&a, q.p, k.p, v.p, out.p, tau.p, rmax.p, mask.p, nullptr,
+                                  nullptr, 0, nullptr));
+  }
   adattn_stats st{};
   abi_check(adattn_b200_stats(&a, mask.p, &st, nullptr));
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (timings) timings->ms[0] += ms;
   out.get(res.out.data.data());
   tau.get(res.tau.data());
   rmax.get(res.row_max.data());

@@ -917,6 +917,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef ADATTN_PIPE_STATS
     long long _pm = clock64();
 #endif
+    // PhaseTimings: epilogue thread 0 attributes its time to the reference phases
+    unsigned long long* const pacc = tid == 0 ? g.phase_ns : nullptr;
+    unsigned long long pt = pacc ? global_ns() : 0ull;
     // ---- pass MAX (attention.cpp:182-195): max of raw dot products, scaled once
     // Also the per-(row group, tile) maximum raw score, for the activity sets
     // of the later sweeps (tiles whose every score is below every row's
@@ -952,6 +955,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bar_sync(bar_rg, 256);
     mraw = fmaxf(sRow[e * 4], sRow[e * 4 + 1]);
     PASS_MARK(0);
+    phase_tick(pacc, 0, pt);
     const float m_f = a.scale_f * mraw;  // == max(scale * s): rounding is monotone
     const double B = 1.0 - (g.alpha - 1.0) * (double)m_f;  // z = A1*acc + B
     const float Bf = (float)B;
@@ -1046,6 +1050,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     PASS_MARK(1);
     solve_counts(cnt, 0);
+    phase_tick(pacc, 1, pt);
     };
 
     const bool need_sec = g.alpha > 2.0;
@@ -1203,6 +1208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // sPart (refinement partials) aliases the count rows of the OTHER row
           // group (sCnt): both groups finish reading counts before any writes them
           bar_sync(3, kEpi);
+          phase_tick(pacc, 1, pt);
         }
         // refinement rounds on the lists (same RowSolve / row_step as the sweeps)
         for (;;) {
@@ -1287,6 +1293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_proxy_async_smem();  // generic writes to the ring before its next TMA loads
         list_ok = true;
+        phase_tick(pacc, 2, pt);
       }
       PASS_MARK(3);
       bar_sync(3, kEpi);
@@ -1360,6 +1367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     PASS_MARK(4);
+    if (!list_ok) phase_tick(pacc, 2, pt);
     // ---- pass OUT (attention.cpp:334-352): P over the active blocks, O = P V
     {
       const float C = sRow[e * 4 + 2];
@@ -1445,6 +1453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     PASS_MARK(6);
+    phase_tick(pacc, 3, pt);
   }
   tc_fence_before();
   if constexpr (PAIR) {

@@ -29,7 +29,7 @@ size_t forward_cand_bytes(const Geom& g);
 bool pv_f16_enabled();
 
 // Power-of-two-scaled fp16 copies of bf16 operands (tc_common.cuh f16_pow2_scale),
-// per head (`heads` consecutive blocks of `elems` values, elems even), so a head's
+// per head (`heads` consecutive blocks of `elems` values, elems % 8 == 0), so a head's
 // results never depend on the other heads of the call (chunked run_host, sharded
 // multi-GPU runs).  f16_absmax: atomicMax of max |x| (float bits) into
 // maxbits[h] (caller zeroes them); f16_convert_scaled: dst = fp16(src * s(maxbits[h])).

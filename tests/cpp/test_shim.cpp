@@ -221,6 +221,19 @@ int main() {
     CHECK(PackedBlockMask::deserialize(want) == mask);
     CHECK(mask.transposed().transposed() == mask);
   }
+  {  // PhaseTimings: filled per phase when threads <= 1, untouched otherwise (attention.cpp:170)
+    Rng rng(8);
+    AttentionProblem p = problem(rng, 256, 32, 1.5, 64, 64, true);
+    PhaseTimings t;
+    const AttentionResult a = forward(p, 1, &t);
+    bool all = true;
+    for (double ms : t.ms) all &= ms > 0.0;
+    CHECK(all);
+    PhaseTimings u;
+    const AttentionResult b = forward(p, 4, &u);
+    CHECK(u.ms[0] == 0.0 && u.ms[1] == 0.0 && u.ms[2] == 0.0 && u.ms[3] == 0.0);
+    CHECK(a.out.data == b.out.data && a.tau == b.tau);
+  }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }
