@@ -180,11 +180,15 @@ def run_reference_arm(args):
     heads = cfg["B"] * cfg["H"]
     budget = float(os.environ.get("ADATTN_REF_BUDGET_S", "1500"))
     t_start = time.perf_counter()
-    # warm-up: one head (a >10 s CPU step needs no more; the rest of the requested
-    # warm-up steps are skipped to keep the arm inside its time limit)
+    # warm-up steps on other heads; if the projected run would overrun the arm's
+    # time budget (ADATTN_REF_BUDGET_S), fewer warm-up / timed steps run and the line
+    # says so (warmup / steps vs *_requested)
     warm = []
-    for w in range(min(args.warmup, 1)):
-        warm.append(cpu_reference_step(head=heads - 1 - w, **kw)["seconds"])
+    for w in range(args.warmup):
+        warm.append(cpu_reference_step(head=heads - 1 - (w % heads), **kw)["seconds"])
+        left = budget - (time.perf_counter() - t_start)
+        if left < (args.steps + 1) * warm[-1]:
+            break
     per = warm[-1] if warm else None
     steps = args.steps
     if per:

@@ -9,6 +9,7 @@
  *   adattn_b200_forward        <- adattn::forward        include/adattn/attention.hpp:72-76
  *                                                         (src/attention.cpp:157-361)
  *   adattn_b200_forward_timed  <- adattn::forward with a PhaseTimings* (attention.hpp:62-76)
+ *   adattn_b200_forward_ex     <- the same, plus the private per-row tau_h (attention.cpp:223)
  *   adattn_b200_compute_delta  <- adattn::compute_delta  attention.hpp:82-85 (attention.cpp:411-446)
  *   adattn_b200_backward       <- adattn::backward       attention.hpp:87-92 (attention.cpp:448-539)
  *   adattn_b200_stats          <- AttentionStats fill + adattn::block_sparsity
@@ -120,6 +121,22 @@ int adattn_b200_forward_timed(const adattn_problem* p, const void* q, const void
                               const void* v, void* out, double* tau, double* row_max,
                               uint32_t* mask, int32_t* row_steps, void* workspace,
                               size_t workspace_bytes, void* stream, double* phase_ms);
+
+/* Optional outputs of adattn_b200_forward_ex (every field nullable):
+ *   phase_ms -- HOST double[4]: PhaseTimings as adattn_b200_forward_timed
+ *               (synchronises `stream` when set);
+ *   tau_h    -- DEVICE double[B][H][n]: each row's histogram solution tau_h
+ *               (solve_histogram, histogram.cpp:73-161), the start of the
+ *               refinement -- kept private by the reference (attention.cpp:223). */
+typedef struct {
+  double* phase_ms;
+  double* tau_h;
+} adattn_forward_extras;
+
+int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k,
+                           const void* v, void* out, double* tau, double* row_max,
+                           uint32_t* mask, int32_t* row_steps, void* workspace,
+                           size_t workspace_bytes, void* stream, const adattn_forward_extras* ex);
 
 int adattn_b200_compute_delta(const adattn_problem* p, const void* q, const void* k,
                               const void* v, const double* tau, const double* row_max,

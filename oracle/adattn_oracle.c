@@ -327,6 +327,8 @@ typedef struct {
   double *out, *tau, *row_max;
   uint32_t* mask;
   int32_t* row_steps;
+  double* tau_h;        /* nullable: per-row solve_histogram result */
+  uint32_t* counts_out; /* nullable: per-row histogram counts [n][bins] */
   int flush_limit_log2; /* bits per bin */
   atomic_ullong flushes;
 } fwd_ctx;
@@ -384,10 +386,13 @@ static void forward_tile(void* vctx, int it) {
     atomic_fetch_add(&C->flushes, (unsigned long long)((J + L - 1) / L));
   }
 
+  if (C->counts_out)
+    memcpy(C->counts_out + (size_t)r0 * bins, counts, sizeof(uint32_t) * (size_t)nr * bins);
   row_solve_t* rows = (row_solve_t*)calloc((size_t)nr, sizeof(row_solve_t));
   for (int r = 0; r < nr; ++r) {
     double lo, hi, th;
     orc_solve_histogram(counts + (size_t)r * bins, bins, p->alpha, &th, NULL, &lo, &hi);
+    if (C->tau_h) C->tau_h[r0 + r] = th;
     rows[r].tau = th;
     rows[r].lo = lo;
     rows[r].hi = hi;
@@ -510,6 +515,13 @@ static void forward_tile(void* vctx, int it) {
 int orc_forward(const orc_params* p, const double* q, const double* k, const double* v,
                 int threads, double* out, double* tau, double* row_max, uint32_t* mask,
                 int32_t* row_steps, orc_stats* stats) {
+  return orc_forward_ex(p, q, k, v, threads, out, tau, row_max, mask, row_steps, stats, NULL,
+                        NULL);
+}
+
+int orc_forward_ex(const orc_params* p, const double* q, const double* k, const double* v,
+                   int threads, double* out, double* tau, double* row_max, uint32_t* mask,
+                   int32_t* row_steps, orc_stats* stats, double* tau_h, uint32_t* counts) {
   geom_t g;
   int rc = validate(p, &g);
   if (rc) return rc;
@@ -528,6 +540,8 @@ int orc_forward(const orc_params* p, const double* q, const double* k, const dou
   C.row_max = row_max;
   C.mask = mask;
   C.row_steps = row_steps;
+  C.tau_h = tau_h;
+  C.counts_out = counts;
   C.flush_limit_log2 = bpb;
   atomic_init(&C.flushes, 0);
   parallel_for(g.t_r, threads, forward_tile, &C);

@@ -55,6 +55,13 @@ int orc_forward(const orc_params* p, const double* q, const double* k, const dou
                 int threads, double* out, double* tau, double* row_max, uint32_t* mask,
                 int32_t* row_steps, orc_stats* stats);
 
+/* forward plus the reference's private per-row histogram state (nullable):
+ * tau_h[n] (solve_histogram, attention.cpp:223-228) and counts[n][bins]
+ * (the streamed histogram, attention.cpp:201-210). */
+int orc_forward_ex(const orc_params* p, const double* q, const double* k, const double* v,
+                   int threads, double* out, double* tau, double* row_max, uint32_t* mask,
+                   int32_t* row_steps, orc_stats* stats, double* tau_h, uint32_t* counts);
+
 /* dense_reference (attention.cpp:363-409). */
 int orc_dense_reference(const orc_params* p, const double* q, const double* k,
                         const double* v, double* out, double* tau, double* row_max,

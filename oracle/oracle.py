@@ -159,6 +159,27 @@ class Oracle:
                     block_sparsity=st.block_sparsity,
                     blocks_visited_fwd=int(st.blocks_visited_fwd), flushes=int(st.flushes))
 
+    def forward_hist(self, pb: Problem, threads: int = 1) -> dict:
+        """forward plus the per-row histogram counts and tau_h (C restatement only:
+        the reference keeps them private)."""
+        if self.kind != "port":
+            raise NotImplementedError("the histogram state is internal to the reference")
+        fn = self.lib.orc_forward_ex
+        fn.argtypes = self._fwd.argtypes + [_DP, _U32P]
+        fn.restype = C.c_int
+        n, dv = pb.q.shape[0], pb.v.shape[1]
+        t_r, t_c = max(pb.t_r, 1), max(pb.t_c, 1)
+        out, tau, rmax = np.zeros((n, dv)), np.zeros(n), np.zeros(n)
+        mask = np.zeros((t_r, (t_c + 31) // 32), dtype=np.uint32)
+        steps = np.zeros(n, dtype=np.int32)
+        tau_h = np.zeros(n)
+        counts = np.zeros((n, pb.bins), dtype=np.uint32)
+        st = OrcStats()
+        self._check(fn(C.byref(pb.params()), self._c(pb.q), self._c(pb.k), self._c(pb.v),
+                       int(threads), out, tau, rmax, mask, steps, C.byref(st), tau_h, counts))
+        return dict(out=out, tau=tau, row_max=rmax, mask=mask, row_steps=steps, tau_h=tau_h,
+                    counts=counts, block_sparsity=st.block_sparsity)
+
     def dense_reference(self, pb: Problem) -> dict:
         n, dv = pb.q.shape[0], pb.v.shape[1]
         wpr = (pb.t_c + 31) // 32

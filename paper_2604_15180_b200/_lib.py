@@ -33,7 +33,7 @@ EXPORTS = (
     "adattn_b200_launch_count", "adattn_b200_profile_enable", "adattn_b200_profile_read",
     "adattn_b200_tensor_save", "adattn_b200_tensor_load", "adattn_b200_io_last_error",
     "adattn_b200_attn_inputs", "adattn_b200_xoshiro", "adattn_b200_entmax_rows",
-    "adattn_b200_block_lists", "adattn_b200_forward_timed",
+    "adattn_b200_block_lists", "adattn_b200_forward_timed", "adattn_b200_forward_ex",
 )
 
 
@@ -47,6 +47,10 @@ class Problem(C.Structure):
         ("in_dtype", C.c_int32), ("out_dtype", C.c_int32), ("path", C.c_int32),
         ("reserved", C.c_int32),
     ]
+
+
+class ForwardExtras(C.Structure):
+    _fields_ = [("phase_ms", C.POINTER(C.c_double)), ("tau_h", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -97,6 +101,8 @@ def load() -> C.CDLL:
         lib.adattn_b200_forward.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
         lib.adattn_b200_forward_timed.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                                   C.c_size_t, vp, C.POINTER(C.c_double)]
+        lib.adattn_b200_forward_ex.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                               C.c_size_t, vp, C.POINTER(ForwardExtras)]
         lib.adattn_b200_compute_delta.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                                   C.c_size_t, vp]
         lib.adattn_b200_backward.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,

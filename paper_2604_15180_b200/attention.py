@@ -237,8 +237,8 @@ def _check_device(*ts):
 _torch_out = {_lib.F32: torch.float32, _lib.F64: torch.float64}
 
 
-def forward(p: AttentionProblem, threads: int = 1,
-            timings: Optional[PhaseTimings] = None) -> AttentionResult:
+def forward(p: AttentionProblem, threads: int = 1, timings: Optional[PhaseTimings] = None,
+            tau_h: Optional[torch.Tensor] = None) -> AttentionResult:
     """Tiled alpha-entmax forward (attention.cpp:157-361).  ``threads`` only
     gates ``timings`` as in the reference (work goes to the current stream)."""
     pb = p.c_problem()
@@ -259,11 +259,20 @@ def forward(p: AttentionProblem, threads: int = 1,
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
     args = (C.byref(pb), _ptr(p.q), _ptr(p.k), _ptr(p.v), _ptr(out), _ptr(tau), _ptr(row_max),
             _ptr(words), _ptr(steps), _ptr(ws), ws_bytes, _stream())
-    if timings is not None and threads <= 1:  # attention.cpp:170
+    timed = timings is not None and threads <= 1  # attention.cpp:170
+    if timed or tau_h is not None:
+        # tau_h (optional, float64 like tau): each row's histogram solution
+        # (solve_histogram, histogram.cpp:73-161), which the reference keeps private
+        if tau_h is not None:
+            if tau_h.shape != tau.shape or tau_h.dtype != torch.float64:
+                raise ValueError("forward: tau_h must be float64 shaped like tau")
+            _check_device(tau_h)
         ph = (C.c_double * 4)()
-        _lib.check(lib.adattn_b200_forward_timed(*args, ph))
-        for i in range(4):
-            timings.ms[i] += ph[i]
+        ex = _lib.ForwardExtras(ph if timed else None, _ptr(tau_h))
+        _lib.check(lib.adattn_b200_forward_ex(*args, C.byref(ex)))
+        if timed:
+            for i in range(4):
+                timings.ms[i] += ph[i]
     else:
         _lib.check(lib.adattn_b200_forward(*args))
     return AttentionResult(out, tau, row_max, PackedBlockMask(words, t_r, t_c), steps, pb)

@@ -96,6 +96,8 @@ int check(const adattn_problem* p, Geom* out) {
   g.bh = p->batch * p->heads;
   g.n = p->n;
   g.m = p->m;
+  g.n_valid = p->n;
+  g.m_valid = p->m;
   g.d = p->d;
   g.dv = p->dv;
   g.block_r = p->block_r;
@@ -193,6 +195,67 @@ HostCtx& host_ctx() {
 
 size_t elem_size(int dtype) { return dtype == ADATTN_BF16 ? 2 : dtype == ADATTN_F32 ? 4 : 8; }
 
+// ---- ragged problems on the tensor-core path ---------------------------------
+// The tensor-core kernels tile 256 query rows x 128 keys.  A problem with
+// n % 256 != 0 or m % 128 != 0 runs on zero-padded copies (padding rows /
+// keys appended to every head); the kernels mask keys >= m_valid like the
+// causal diagonal and keep rows >= n_valid out of the mask, padding rows get
+// zero dO and tau = row_max = 0, so they add exactly nothing to dK / dV, and
+// the results are copied back row by row.  The reference's tiling of the
+// real problem (t_r, t_c, ceil(t_c / 32) mask words) is unchanged: the
+// padded geometry adds at most one key tile (t_c rounds up to even), which
+// never changes the word count.
+bool tc_ragged(const Geom& g) { return g.n % 256 != 0 || g.m % 128 != 0; }
+
+Geom padded_geom(const Geom& g) {
+  Geom p = g;
+  p.n = (g.n + 255) / 256 * 256;
+  p.m = g.causal ? p.n : (g.m + 127) / 128 * 128;
+  p.t_r = p.n / 64;
+  p.t_c = p.m / 64;
+  p.wpr = (p.t_c + 31) / 32;
+  return p;
+}
+
+// stream-ordered scratch, freed (stream-ordered) when the call returns
+class Scratch {
+ public:
+  explicit Scratch(cudaStream_t st) : st_(st) {}
+  ~Scratch() {
+    for (void* p : ptrs_) cudaFreeAsync(p, st_);
+  }
+  // zero-filled device buffer of `bytes` (nullptr with err set on failure)
+  void* zeros(size_t bytes) {
+    void* p = nullptr;
+    if (err_) return nullptr;
+    if ((err_ = cudaMallocAsync(&p, bytes ? bytes : 16, st_))) return nullptr;
+    ptrs_.push_back(p);
+    if ((err_ = cudaMemsetAsync(p, 0, bytes ? bytes : 16, st_))) return nullptr;
+    return p;
+  }
+  // per-head [rows][row_bytes] blocks from a tensor with src_rows rows per head into
+  // one with dst_rows rows per head (the first `rows` rows of each head)
+  void rows(void* dst, size_t dst_rows, const void* src, size_t src_rows, size_t rows,
+            size_t row_bytes, int heads) {
+    if (err_ || !dst || !src) return;
+    err_ = cudaMemcpy2DAsync(dst, dst_rows * row_bytes, src, src_rows * row_bytes,
+                             rows * row_bytes, heads, cudaMemcpyDeviceToDevice, st_);
+  }
+  // a padded copy of a per-head tensor (rows -> prow rows per head, zero padding)
+  void* pad(const void* src, size_t rows, size_t prow, size_t row_bytes, int heads) {
+    if (!src) return nullptr;
+    void* d = zeros(prow * row_bytes * heads);
+    this->rows(d, prow, src, rows, rows, row_bytes, heads);
+    return d;
+  }
+  cudaError_t error() const { return err_; }
+
+ private:
+  cudaStream_t st_;
+  std::vector<void*> ptrs_;
+  cudaError_t err_ = cudaSuccess;
+};
+
 }  // namespace
 
 uint64_t flushes_of(const Geom& g) {
@@ -284,26 +347,48 @@ int adattn_b200_resolved_path(const adattn_problem* p) {
 size_t adattn_b200_forward_workspace(const adattn_problem* p) {
   Geom g;
   if (check(p, &g)) return 0;
-  return resolve(p, g) == ADATTN_PATH_TC ? tc_forward_workspace(g) : 0;
+  return resolve(p, g) == ADATTN_PATH_TC ? tc_forward_workspace(padded_geom(g)) : 0;
 }
 
 size_t adattn_b200_backward_workspace(const adattn_problem* p) {
   Geom g;
   if (check(p, &g)) return 0;
-  return resolve(p, g) == ADATTN_PATH_TC ? tc_backward_workspace(g) : 16;
+  return resolve(p, g) == ADATTN_PATH_TC ? tc_backward_workspace(padded_geom(g)) : 16;
 }
 
 }  // extern "C"
 
 namespace {
+// padded copies of the backward inputs of a ragged problem (padding rows: zero
+// dO, tau = row_max = 0; padding row blocks: empty mask rows)
+struct BwdPadded {
+  const void *q, *k, *v, *dout;
+  const double *tau, *rm;
+  const uint32_t* mask;
+  BwdPadded(Scratch& sc, const Geom& g, const Geom& gp, const void* q0, const void* k0,
+            const void* v0, const double* tau0, const double* rm0, const uint32_t* mask0,
+            const void* dout0) {
+    const size_t ei = elem_size(g.in_dtype);
+    const int H = g.bh;
+    q = sc.pad(q0, g.n, gp.n, g.d * ei, H);
+    k = sc.pad(k0, g.m, gp.m, g.d * ei, H);
+    v = sc.pad(v0, g.m, gp.m, g.dv * ei, H);
+    dout = sc.pad(dout0, g.n, gp.n, g.dv * ei, H);
+    tau = (const double*)sc.pad(tau0, g.n, gp.n, 8, H);
+    rm = (const double*)sc.pad(rm0, g.n, gp.n, 8, H);
+    mask = (const uint32_t*)sc.pad(mask0, g.t_r, gp.t_r, g.wpr * 4, H);
+  }
+};
+
 int forward_impl(const adattn_problem* p, const void* q, const void* k, const void* v,
                  void* out, double* tau, double* row_max, uint32_t* mask, int32_t* row_steps,
                  void* workspace, size_t workspace_bytes, void* stream,
-                 unsigned long long* phase_ns) {
+                 unsigned long long* phase_ns, double* tau_h) {
   Geom g;
   int rc = check(p, &g);
   if (rc) return rc;
   g.phase_ns = phase_ns;
+  g.tau_h_out = tau_h;
   const int path = resolve(p, g);
   if (path < 0) return -path;
   if (!q || !k || !v || !out || !tau || !row_max || !mask)
@@ -311,9 +396,36 @@ int forward_impl(const adattn_problem* p, const void* q, const void* k, const vo
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   if (path == ADATTN_PATH_TC) {
-    if (workspace_bytes < tc_forward_workspace(g))
+    const Geom gp = padded_geom(g);
+    if (workspace_bytes < tc_forward_workspace(gp))
       return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_forward: workspace too small");
-    e = tc_forward(g, q, k, v, out, tau, row_max, mask, row_steps, workspace, st);
+    if (!tc_ragged(g)) {
+      e = tc_forward(g, q, k, v, out, tau, row_max, mask, row_steps, workspace, st);
+    } else {
+      Scratch sc(st);
+      const size_t ei = elem_size(g.in_dtype), eo = elem_size(g.out_dtype);
+      const int H = g.bh;
+      void* qp = sc.pad(q, g.n, gp.n, g.d * ei, H);
+      void* kp = sc.pad(k, g.m, gp.m, g.d * ei, H);
+      void* vp = sc.pad(v, g.m, gp.m, g.dv * ei, H);
+      void* op = sc.zeros((size_t)H * gp.n * g.dv * eo);
+      double* tp = (double*)sc.zeros((size_t)H * gp.n * 8);
+      double* rp = (double*)sc.zeros((size_t)H * gp.n * 8);
+      uint32_t* mp = (uint32_t*)sc.zeros((size_t)H * gp.t_r * gp.wpr * 4);
+      int32_t* sp = row_steps ? (int32_t*)sc.zeros((size_t)H * gp.n * 4) : nullptr;
+      Geom gr = gp;
+      gr.tau_h_out = tau_h ? (double*)sc.zeros((size_t)H * gp.n * 8) : nullptr;
+      if ((e = sc.error())) return cuda_fail(e, "adattn_b200_forward (padding)");
+      if ((e = tc_forward(gr, qp, kp, vp, op, tp, rp, mp, sp, workspace, st)))
+        return cuda_fail(e, "adattn_b200_forward");
+      sc.rows(out, g.n, op, gp.n, g.n, g.dv * eo, H);
+      sc.rows(tau, g.n, tp, gp.n, g.n, 8, H);
+      sc.rows(row_max, g.n, rp, gp.n, g.n, 8, H);
+      sc.rows(mask, g.t_r, mp, gp.t_r, g.t_r, g.wpr * 4, H);
+      sc.rows(row_steps, g.n, sp, gp.n, g.n, 4, H);
+      sc.rows(tau_h, g.n, gr.tau_h_out, gp.n, g.n, 8, H);
+      e = sc.error();
+    }
   } else {
     e = exact_forward(g, q, k, v, out, tau, row_max, mask, row_steps, st);
   }
@@ -329,14 +441,28 @@ int adattn_b200_forward(const adattn_problem* p, const void* q, const void* k, c
                         int32_t* row_steps, void* workspace, size_t workspace_bytes,
                         void* stream) {
   return forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace, workspace_bytes,
-                      stream, nullptr);
+                      stream, nullptr, nullptr);
 }
 
 int adattn_b200_forward_timed(const adattn_problem* p, const void* q, const void* k,
                               const void* v, void* out, double* tau, double* row_max,
                               uint32_t* mask, int32_t* row_steps, void* workspace,
                               size_t workspace_bytes, void* stream, double* phase_ms) {
+  adattn_forward_extras ex{phase_ms, nullptr};
   if (!phase_ms) return fail(ADATTN_ERR_INVALID, "adattn_b200_forward_timed: null phase_ms");
+  return adattn_b200_forward_ex(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
+                                workspace_bytes, stream, &ex);
+}
+
+int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k,
+                           const void* v, void* out, double* tau, double* row_max,
+                           uint32_t* mask, int32_t* row_steps, void* workspace,
+                           size_t workspace_bytes, void* stream, const adattn_forward_extras* ex) {
+  double* const tau_h = ex ? ex->tau_h : nullptr;
+  double* const phase_ms = ex ? ex->phase_ms : nullptr;
+  if (!phase_ms)
+    return forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
+                        workspace_bytes, stream, nullptr, tau_h);
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* acc = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -345,9 +471,9 @@ int adattn_b200_forward_timed(const adattn_problem* p, const void* q, const void
   if (!e) e = cudaEventCreate(&e0);
   if (!e) e = cudaEventCreate(&e1);
   if (!e) e = cudaEventRecord(e0, st);
-  if (e) return cuda_fail(e, "adattn_b200_forward_timed");
+  if (e) return cuda_fail(e, "adattn_b200_forward_ex");
   int rc = forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
-                        workspace_bytes, stream, acc);
+                        workspace_bytes, stream, acc, tau_h);
   unsigned long long ns[4] = {0, 0, 0, 0};
   float total = 0.f;
   e = cudaEventRecord(e1, st);
@@ -358,7 +484,7 @@ int adattn_b200_forward_timed(const adattn_problem* p, const void* q, const void
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (rc) return rc;
-  if (e) return cuda_fail(e, "adattn_b200_forward_timed");
+  if (e) return cuda_fail(e, "adattn_b200_forward_ex");
   // the forward's event-timed duration, split by the CTAs' per-phase time shares
   const double sum = double(ns[0]) + double(ns[1]) + double(ns[2]) + double(ns[3]);
   for (int i = 0; i < 4; ++i) phase_ms[i] = sum > 0.0 ? double(total) * double(ns[i]) / sum : 0.0;
@@ -379,9 +505,21 @@ int adattn_b200_compute_delta(const adattn_problem* p, const void* q, const void
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   if (path == ADATTN_PATH_TC) {
-    if (workspace_bytes < tc_backward_workspace(g))
+    const Geom gp = padded_geom(g);
+    if (workspace_bytes < tc_backward_workspace(gp))
       return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_compute_delta: workspace too small");
-    e = tc_delta(g, q, k, v, tau, row_max, mask, dout, delta, workspace, st);
+    if (!tc_ragged(g)) {
+      e = tc_delta(g, q, k, v, tau, row_max, mask, dout, delta, workspace, st);
+    } else {
+      Scratch sc(st);
+      BwdPadded b(sc, g, gp, q, k, v, tau, row_max, mask, dout);
+      double* dlp = (double*)sc.zeros((size_t)g.bh * gp.n * 8);
+      if ((e = sc.error())) return cuda_fail(e, "adattn_b200_compute_delta (padding)");
+      if ((e = tc_delta(gp, b.q, b.k, b.v, b.tau, b.rm, b.mask, b.dout, dlp, workspace, st)))
+        return cuda_fail(e, "adattn_b200_compute_delta");
+      sc.rows(delta, g.n, dlp, gp.n, g.n, 8, g.bh);
+      e = sc.error();
+    }
   } else {
     e = exact_delta(g, q, k, v, tau, row_max, mask, dout, delta, st);
   }
@@ -404,9 +542,30 @@ int adattn_b200_backward(const adattn_problem* p, const void* q, const void* k,
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   if (path == ADATTN_PATH_TC) {
-    if (workspace_bytes < tc_backward_workspace(g))
+    const Geom gp = padded_geom(g);
+    if (workspace_bytes < tc_backward_workspace(gp))
       return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_backward: workspace too small");
-    e = tc_backward(g, q, k, v, tau, row_max, mask, dout, dq, dk, dv, delta, workspace, st);
+    if (!tc_ragged(g)) {
+      e = tc_backward(g, q, k, v, tau, row_max, mask, dout, dq, dk, dv, delta, workspace, st);
+    } else {
+      Scratch sc(st);
+      BwdPadded b(sc, g, gp, q, k, v, tau, row_max, mask, dout);
+      const size_t eo = elem_size(g.out_dtype);
+      const int H = g.bh;
+      void* dqp = sc.zeros((size_t)H * gp.n * g.d * eo);
+      void* dkp = sc.zeros((size_t)H * gp.m * g.d * eo);
+      void* dvp = sc.zeros((size_t)H * gp.m * g.dv * eo);
+      double* dlp = (double*)sc.zeros((size_t)H * gp.n * 8);
+      if ((e = sc.error())) return cuda_fail(e, "adattn_b200_backward (padding)");
+      if ((e = tc_backward(gp, b.q, b.k, b.v, b.tau, b.rm, b.mask, b.dout, dqp, dkp, dvp, dlp,
+                           workspace, st)))
+        return cuda_fail(e, "adattn_b200_backward");
+      sc.rows(dq, g.n, dqp, gp.n, g.n, g.d * eo, H);
+      sc.rows(dk, g.m, dkp, gp.m, g.m, g.d * eo, H);
+      sc.rows(dv, g.m, dvp, gp.m, g.m, g.dv * eo, H);
+      sc.rows(delta, g.n, dlp, gp.n, g.n, 8, H);
+      e = sc.error();
+    }
   } else {
     if (workspace_bytes < 8 || !workspace)
       return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_backward: workspace too small");

@@ -14,6 +14,9 @@ namespace adattn_b200 {
 struct Geom {
   int bh;         // batch * heads
   int n, m, d, dv;
+  // rows / keys that exist (the tensor-core path runs ragged problems padded to
+  // n % 256 == 0, m % 128 == 0; rows >= n_valid and keys >= m_valid are padding)
+  int n_valid, m_valid;
   int t_r, t_c;   // query / key tile counts
   int wpr;        // mask words per tile row = ceil(t_c / 32)
   int block_r, block_c;
@@ -27,6 +30,9 @@ struct Geom {
   // nanoseconds it spends in each reference phase (max, histogram, refinement,
   // output) to phase_ns[0..3]
   unsigned long long* phase_ns = nullptr;
+  // when set, the forward writes each row's histogram solution tau_h
+  // (solve_histogram, histogram.cpp:73-161) to tau_h_out[bh * n + row]
+  double* tau_h_out = nullptr;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {

@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (own_row) {
     double th, lo, hi;
     solve_histogram_dev(&sCnt[tid * g.bins], g.bins, g.alpha, th, lo, hi);
+    if (g.tau_h_out) g.tau_h_out[(size_t)bh * g.n + r0 + tid] = th;
     rs.tau = th;
     rs.lo = lo;
     rs.hi = hi;

@@ -402,6 +402,8 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
     const int e = rg * 128 + lq * 32 + lane;
     const int rb = e >> 6;
     const int grow = row0 + e;
+    // last key this row sees: the causal diagonal and the problem's real keys
+    const int klim = g.causal ? min(grow, g.m_valid - 1) : g.m_valid - 1;
     const size_t orow = (size_t)bh * g.n + grow;
     const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + rg * 256 + half * 64;
     const float A1 = a.A1;
@@ -430,8 +432,8 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
         if (mine) {
           const int c0 = k0 + 32 * c;
           float n32, d32;
-          if (g.causal && c0 + 31 > grow)
-            delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, grow - c0, n32, d32);
+          if (c0 + 31 > klim)
+            delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, klim - c0, n32, d32);
           else
             delta_chunk<AK, false>(s, dp, A1, C, a.e0f, a.e1f, 0, n32, d32);
           num.add(n32);
@@ -635,6 +637,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
     const int rb = e >> 6;                 // own row block 0..3
     const int pb = 4 * (int)rank + rb;     // pair row block 0..7
     const int grow = row0 + e;
+    // last key this row sees: the causal diagonal and the problem's real keys
+    const int klim = g.causal ? min(grow, g.m_valid - 1) : g.m_valid - 1;
     const size_t orow = (size_t)bh * g.n + grow;
     const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + rg * 256 + half * 64;
     const float A1 = a.A1;
@@ -664,8 +668,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
         if (mine) {
           const int c0 = k0 + 32 * c;
           float n32, d32;
-          if (g.causal && c0 + 31 > grow)
-            delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, grow - c0, n32, d32);
+          if (c0 + 31 > klim)
+            delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, klim - c0, n32, d32);
           else
             delta_chunk<AK, false>(s, dp, A1, C, a.e0f, a.e1f, 0, n32, d32);
           num.add(n32);
@@ -857,6 +861,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
     const int e = lq * 32 + lane;         // local row 0..127
     const int pb = 2 * (int)rank + (e >> 6);  // pair row block 0..3
     const int grow = row0 + e;
+    // last key this row sees: the causal diagonal and the problem's real keys
+    const int klim = g.causal ? min(grow, g.m_valid - 1) : g.m_valid - 1;
     const size_t orow = (size_t)bh * g.n + grow;
     const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16) + cq * 32;
     const float A1 = a.A1;
@@ -880,8 +886,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
       if ((bits2(pb, J) >> (cq >> 1)) & 1u) {  // the reference visits set blocks only
         const int c0 = J * DBN + 32 * cq;
         float n32, d32;
-        if (g.causal && c0 + 31 > grow)
-          delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, grow - c0, n32, d32);
+        if (c0 + 31 > klim)
+          delta_chunk<AK, true>(s, dp, A1, C, a.e0f, a.e1f, klim - c0, n32, d32);
         else
           delta_chunk<AK, false>(s, dp, A1, C, a.e0f, a.e1f, 0, n32, d32);
         num.add(n32);
@@ -1108,6 +1114,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int e = lq * 32 + lane;      // local query row 0..127
     const int rb = e >> 6;
     const int grow = row0 + e;
+    // last key this row sees: the causal diagonal and the problem's real keys
+    const int klim = g.causal ? min(grow, g.m_valid - 1) : g.m_valid - 1;
     const size_t orow = (size_t)bh * g.n + grow;
     const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16);
     const float A1 = a.A1;
@@ -1138,8 +1146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!mine) {
 #pragma unroll
           for (int x = 0; x < 16; ++x) hi[x] = lo[x] = 0u;
-        } else if (g.causal && c0 + 31 > grow) {
-          ds_chunk<AK, true>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, grow - c0, hi, lo);
+        } else if (c0 + 31 > klim) {
+          ds_chunk<AK, true>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, klim - c0, hi, lo);
         } else {
           ds_chunk<AK, false>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, 0, hi, lo);
         }
@@ -1402,6 +1410,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int rb = e >> 6;                // own row block 0/1
     const int prb = (int)rank * 2 + rb;   // row block within the pair
     const int grow = row0 + e;
+    // last key this row sees: the causal diagonal and the problem's real keys
+    const int klim = g.causal ? min(grow, g.m_valid - 1) : g.m_valid - 1;
     const size_t orow = (size_t)bh * g.n + grow;
     const uint32_t tl = tmem + ((uint32_t)(lq * 32) << 16);
     const float A1 = a.A1;
@@ -1434,9 +1444,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (!mine) {
 #pragma unroll
           for (int x = 0; x < 16; ++x) hi[x] = lo[x] = 0u;
-        } else if (g.causal && c0 + 31 > grow) {
-          if (f16s) ds_chunk<AK, true, true>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, grow - c0, hi, lo, sig);
-          else ds_chunk<AK, true>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, grow - c0, hi, lo);
+        } else if (c0 + 31 > klim) {
+          if (f16s) ds_chunk<AK, true, true>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, klim - c0, hi, lo, sig);
+          else ds_chunk<AK, true>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, klim - c0, hi, lo);
         } else {
           if (f16s) ds_chunk<AK, false, true>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, 0, hi, lo, sig);
           else ds_chunk<AK, false>(s, dp, A1, rc.x, rc.y, a.e0f, a.e1f, 0, hi, lo);

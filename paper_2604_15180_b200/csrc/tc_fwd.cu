@@ -858,12 +858,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     float v[32];
     // 32-key chunk c (0/1) of this thread's 64 keys of tile J, from buffer column base
-    auto mask_chunk = [&](float* x, int J, int c) {  // causal: keys beyond the row
+    // keys beyond the row (causal) or beyond the problem (padding of a ragged m)
+    const int klim = g.causal ? min(grow, g.m_valid - 1) : g.m_valid - 1;
+    const bool row_real = grow < g.n_valid;  // padding rows of a ragged n: no mask bits
+    auto mask_chunk = [&](float* x, int J, int c) {
       const int k0 = J * BN + half * 64 + c * 32;
-      if (g.causal && k0 + 31 > grow) {
+      if (k0 + 31 > klim) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          if (k0 + i > grow) x[i] = -CUDART_INF_F;
+          if (k0 + i > klim) x[i] = -CUDART_INF_F;
       }
     };
     auto load_chunk = [&](uint32_t col, int J, int c) {
@@ -1011,6 +1014,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           c32[k] = (k < nb && k >= kmin) ? cnt[k & 15] + row_cnt[k & 15] : 0u;
         double th, lo, hi;
         solve_histogram_dev(c32, nb, g.alpha, th, lo, hi);
+        if (g.tau_h_out) g.tau_h_out[(size_t)bh * g.n + grow] = th;
         rs.tau = th;
         rs.lo = lo;
         rs.hi = hi;
@@ -1115,6 +1119,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // z > lo - eps  <=>  acc > theta (A1 > 0), lowered by a few ulps (superset)
     float theta = -sRow[e * 4 + 0] / A1;
     theta -= 4e-7f * fabsf(theta) + 1e-30f;
+    if (!row_real) theta = 3.0e38f;  // padding rows list nothing
     publish_set(1, theta, true);
 
     if (a.cand) {
@@ -1287,7 +1292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 8; ++j) en[j] = i0 + j < cnt ? lst[i0 + j] : make_uint2(0xFF800000u, 0u);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-              if (fmaf(A1, __uint_as_float(en[j].x), C) > -1e-9f)
+              if (row_real && fmaf(A1, __uint_as_float(en[j].x), C) > -1e-9f)
                 atomicOr(&smask[rb * wpr + (en[j].y >> 5)], 1u << (en[j].y & 31));
           }
         }
@@ -1334,7 +1339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mx_t = fmaxf(mx_t, mx);
         });
         const int jt = 2 * J + half;  // reference key tile of this thread's half
-        if (__any_sync(0xffffffffu, mx_t > -1e-9f) && lane == 0)
+        if (__any_sync(0xffffffffu, row_real && mx_t > -1e-9f) && lane == 0)
           atomicOr(&smask[rb * wpr + (jt >> 5)], 1u << (jt & 31));
       }
       if (half == 1) {

@@ -125,6 +125,18 @@ def test_config1_fp32_four_heads():
     assert steps.mean() <= 2.0
 
 
+def test_exact_tau_h_matches_restatement():
+    """The histogram solution tau_h (private in the reference, attention.cpp:223)
+    of the EXACT path equals the C restatement's bit for bit."""
+    orc = Oracle("port")
+    q, k, v, do = gen_attn_inputs(21, 512, 64, 1.0, orc)
+    prob, res, _ = run_gpu(q, k, v, None, torch.float64, alpha=1.5, causal=True)
+    th = torch.empty(512, dtype=torch.float64, device=DEV)
+    pa.forward(prob, tau_h=th)
+    fp = orc.forward_hist(Problem(q, k, v, alpha=1.5, causal=True), threads=4)
+    assert np.array_equal(np_(th), fp["tau_h"])
+
+
 def test_bf16_inputs_exact_path():
     orc = Oracle("port")
     q, k, v, do = gen_attn_inputs(77, 320, 64, 1.0, orc)

@@ -19,10 +19,12 @@ criterion is acceptance_main.cpp:205-267):
   threshold (the block's max over its rows of z - tau + 1e-9, recomputed here in
   fp64 from the inputs, under the reference's tau or the TC tau of an
   exception row);
-* row_steps: reported against the C restatement (oracle/liboracle.so, pinned
-  bit-for-bit to the reference in tests/test_oracle.py, and checked here to
-  give the reference's tau) where N <= 8192; the agreement fraction must be
-  >= 99%.
+* row_steps and the histogram solution tau_h (both private in the reference):
+  against the C restatement (oracle/liboracle.so, pinned bit-for-bit to the
+  reference in tests/test_oracle.py, and checked here to give the reference's
+  tau) where N <= 8192; steps agree on >= 99% of rows; tau_h is identical on
+  all rows but <= 0.1% (alpha < 1.4, HIST-sweep binning: <= 1%), each of which
+  has a score within 1e-5 of a bin edge.
 
 Set ADATTN_PARITY_OUT=<file> to append one JSON line per case (the committed
 summary is profiles/r2_parity_tc_vs_reference.jsonl).
@@ -120,8 +122,9 @@ def test_tc_vs_reference(case):
     # ---- the product path (AUTO must pick the tensor-core kernels here)
     prob = pa.AttentionProblem(q, k, v, alpha=alpha, causal=causal)
     assert pa.attention.resolved_path(prob.c_problem()) == _lib.PATH_TC
+    tau_h_dev = torch.empty(1, 1, N, dtype=torch.float64, device=DEV)
     t0 = time.perf_counter()
-    res = pa.forward(prob)
+    res = pa.forward(prob, tau_h=tau_h_dev)
     g = pa.backward(prob, res, do)
     torch.cuda.synchronize()
     t_gpu = time.perf_counter() - t0
@@ -182,12 +185,26 @@ def test_tc_vs_reference(case):
     # ---- refinement steps vs the pinned C restatement (same algorithm, exports steps)
     steps_tc = to_np(res.row_steps)
     rec["tc_steps_avg"] = float(steps_tc.mean())
+    hist_unexplained = []
     if N <= 8192:
         port = Oracle("port")
-        fp = port.forward(pb, THREADS)
+        fp = port.forward_hist(pb, THREADS)
         assert np.array_equal(fp["tau"], f["tau"]) and np.array_equal(fp["mask"], f["mask"])
         agree = float((fp["row_steps"] == steps_tc).mean())
         rec.update(ref_steps_avg=float(fp["row_steps"].mean()), steps_agree=agree)
+        # histogram solve (attention.cpp:201-232): the TC tau_h equals the reference
+        # algorithm's except rows where an fp32 z lands on the other side of a bin
+        # edge than the fp64 z (checked per differing row)
+        th_tc = to_np(tau_h_dev)
+        hd = np.nonzero(th_tc != fp["tau_h"])[0]
+        for r in hd[:64]:
+            s_row = scale * (K[: (r + 1 if causal else N)] @ Q[r])
+            z = (alpha - 1.0) * (s_row - f["row_max"][r]) + 1.0
+            z = z[z > -1e-5]  # binned scores (z >= 0) and the ones at the 0 edge
+            edge_gap = np.abs(z * 8 - np.round(z * 8)).min() / 8
+            if edge_gap > 1e-5:
+                hist_unexplained.append((int(r), float(th_tc[r]), float(fp["tau_h"][r]), edge_gap))
+        rec.update(tau_h_rows_differ=int(hd.size), tau_h_unexplained=hist_unexplained[:8])
     print(json.dumps(rec))
     report(rec)
 
@@ -199,3 +216,73 @@ def test_tc_vs_reference(case):
     assert not unexplained, unexplained[:8]
     if "steps_agree" in rec:
         assert rec["steps_agree"] >= STEPS_AGREE, rec["steps_agree"]
+        # list mode (alpha >= 1.4) bins the listed fp32 z exactly as the reference
+        # (min(int(B z), B - 1)); the HIST sweep of the sweep mode (alpha < 1.4, with
+        # thousands of binned scores per row) maps z within ~2e-6 (z + 1) below an
+        # edge one bin low (tc_fwd.cu hist_nib, c = 1 - 2^-20): more rows, same cause
+        frac = TAU_EXC_FRAC if alpha >= 1.4 else 10 * TAU_EXC_FRAC
+        assert rec["tau_h_rows_differ"] <= max(1, int(frac * N))
+        assert not hist_unexplained, hist_unexplained
+
+
+# ragged shapes (n % 256 != 0, m % 128 != 0): the tensor-core path runs them on
+# zero-padded copies with the padding keys masked (capi.cu tc_ragged)
+RAGGED = [
+    # (id, n, m, D, causal, alpha)
+    ("r100-d64-c", 100, 100, 64, True, 1.5),
+    ("r300-a2-c", 300, 300, 128, True, 2.0),
+    ("r1000-a125-c", 1000, 1000, 128, True, 1.25),
+    ("r2500-c", 2500, 2500, 128, True, 1.5),
+    ("r1500x700-nc", 1500, 700, 128, False, 1.5),
+    ("r200x1000-a2-nc-d64", 200, 1000, 64, False, 2.0),
+    ("r333x129-a175-nc", 333, 129, 128, False, 1.75),
+]
+
+
+@pytest.mark.parametrize("case", RAGGED, ids=[c[0] for c in RAGGED])
+def test_tc_ragged_vs_reference(case):
+    name, n, m, D, causal, alpha = case
+    g = torch.Generator(device="cpu").manual_seed(n * 7 + m)
+    mk = lambda rows: torch.randn(1, 2, rows, D, generator=g).to(torch.bfloat16).to(DEV)
+    q, k, v, do = mk(n), mk(m), mk(m), mk(n)
+    prob = pa.AttentionProblem(q, k, v, alpha=alpha, causal=causal)
+    assert pa.attention.resolved_path(prob.c_problem()) == _lib.PATH_TC
+    res = pa.forward(prob)
+    gr = pa.backward(prob, res, do)
+    torch.cuda.synchronize()
+    ref = Oracle("reference")
+    for h in range(2):
+        f64 = lambda t: t[0, h].float().cpu().numpy().astype(np.float64)
+        Q, K, Vv, DO = f64(q), f64(k), f64(v), f64(do)
+        pb = Problem(Q, K, Vv, alpha=alpha, causal=causal)
+        f = ref.forward(pb, THREADS)
+        b = ref.backward(pb, f, DO, THREADS)
+        got = lambda t: t[0, h].double().cpu().numpy()
+        errs = {"tau": float(np.abs(got(res.tau) - f["tau"]).max()),
+                "out": float(np.abs(got(res.out) - f["out"]).max())}
+        for key in ("delta", "dq", "dk", "dv"):
+            errs[key] = float(np.abs(got(getattr(gr, key)) - b[key]).max())
+        t_c = (m + 63) // 64
+        bt = mask_bits(res.mask.words[0, h].cpu().numpy(), t_c)
+        br = mask_bits(f["mask"], t_c)
+        diff = np.argwhere(bt != br)
+        scale = 1.0 / np.sqrt(float(D))
+        bad = []
+        for I, J in diff:
+            r0, c0 = 64 * I, 64 * J
+            s = scale * (Q[r0:r0 + 64] @ K[c0:c0 + 64].T)
+            mrow = f["row_max"][r0:r0 + 64, None]
+            z = np.where(s == mrow, 1.0, (alpha - 1.0) * (s - mrow) + 1.0)
+            if causal:
+                z = np.where(np.arange(c0, c0 + s.shape[1])[None, :] >
+                             np.arange(r0, r0 + s.shape[0])[:, None], -np.inf, z)
+            dec = float((z - f["tau"][r0:r0 + 64, None] + 1e-9).max())
+            if abs(dec) > MASK_SLACK:
+                bad.append((int(I), int(J), dec))
+        print(name, h, {k_: f"{v_:.2e}" for k_, v_ in errs.items()}, "mask diffs", len(diff))
+        assert errs["tau"] <= TAU_TOL, errs
+        for key in ("out", "delta", "dq", "dk", "dv"):
+            assert errs[key] <= GRAD_TOL, (key, errs)
+        assert not bad, bad
+        assert res.mask.words[0, h].cpu().numpy().view(np.uint32)[:, -1].max() >> ((t_c - 1) % 32 + 1) == 0 \
+            if t_c % 32 else True

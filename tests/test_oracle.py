@@ -251,3 +251,19 @@ def test_gen_attn_inputs_order(port):
     q, k, v, do = gen_attn_inputs(5, 3, 2, 2.0, port)
     g = port.gaussian(5, 24)
     assert np.array_equal(q.ravel(), 2.0 * g[:6]) and np.array_equal(do.ravel(), g[18:])
+
+
+def test_port_histogram_state_consistent_with_reference_solver():
+    """orc_forward_ex's private histogram state: solving its counts with the
+    reference's own solve_histogram (oracle/_ref) reproduces its tau_h, and the
+    forward outputs equal the reference's forward bit for bit."""
+    port, ref = Oracle("port"), Oracle("reference")
+    q, k, v, _ = gen_attn_inputs(31, 300, 32, 2.0, port)
+    for alpha, bins in ((1.5, 8), (2.0, 4), (1.25, 16)):
+        pb = Problem(q, k, v, alpha=alpha, causal=True, bins=bins)
+        fh = port.forward_hist(pb, threads=4)
+        fr = ref.forward(pb, threads=4)
+        assert np.array_equal(fh["tau"], fr["tau"]) and np.array_equal(fh["out"], fr["out"])
+        for r in range(0, 300, 7):
+            th, _, _, _ = ref.solve_histogram(fh["counts"][r], alpha)
+            assert th == fh["tau_h"][r]
