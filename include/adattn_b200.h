@@ -12,6 +12,7 @@
  *   adattn_b200_forward_ex     <- the same, plus the private per-row tau_h (attention.cpp:223)
  *   adattn_b200_compute_delta  <- adattn::compute_delta  attention.hpp:82-85 (attention.cpp:411-446)
  *   adattn_b200_backward       <- adattn::backward       attention.hpp:87-92 (attention.cpp:448-539)
+ *   adattn_b200_backward_ex    <- the same, walking the forward's nonzero-block lists
  *   adattn_b200_stats          <- AttentionStats fill + adattn::block_sparsity
  *                                                         attention.hpp:38-43, 94-97 (attention.cpp:355-359, 541-551)
  *   adattn_b200_validate       <- validate() + PackedHistogramAcc ctor checks
@@ -131,6 +132,15 @@ int adattn_b200_forward_timed(const adattn_problem* p, const void* q, const void
 typedef struct {
   double* phase_ms;
   double* tau_h;
+  /* DEVICE nonzero-block lists emitted by the forward (both or neither):
+   *   block_cnt  int32 [B][H][t_r]        active key blocks per row block;
+   *   block_cols uint16 [B][H][t_r][t_c]  their indices, ascending (the first
+   *              block_cnt entries of each row; PackedBlockMask::for_each_set
+   *              order, bitpack.hpp:85-92).
+   * Pass them to adattn_b200_backward_ex: its kernels walk these lists (and
+   * their transpose) to skip zero tiles (attention.cpp:334-352, 462-535). */
+  int32_t* block_cnt;
+  uint16_t* block_cols;
 } adattn_forward_extras;
 
 int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k,
@@ -148,6 +158,20 @@ int adattn_b200_backward(const adattn_problem* p, const void* q, const void* k,
                          const uint32_t* mask, const void* dout, void* dq, void* dk,
                          void* dv, double* delta, void* workspace, size_t workspace_bytes,
                          void* stream);
+
+/* backward with the forward's nonzero-block lists (adattn_forward_extras
+ * block_cnt / block_cols; NULL extras or lists: built from `mask`, as
+ * adattn_b200_backward does). */
+typedef struct {
+  const int32_t* block_cnt;
+  const uint16_t* block_cols;
+} adattn_backward_extras;
+
+int adattn_b200_backward_ex(const adattn_problem* p, const void* q, const void* k,
+                            const void* v, const double* tau, const double* row_max,
+                            const uint32_t* mask, const void* dout, void* dq, void* dk,
+                            void* dv, double* delta, void* workspace, size_t workspace_bytes,
+                            void* stream, const adattn_backward_extras* ex);
 
 /* Mask statistics (synchronises `stream`): popcounts, block sparsity over the
  * addressable blocks, visits (fwd = nnz, bwd = 2 nnz) and the flush count of

@@ -6,11 +6,12 @@ kernels behind a C-ABI (include/adattn_b200.h, libadattn_b200.so), with a
 Python mirror of the reference interface in :mod:`.attention`.
 """
 from .attention import (AttentionGradients, AttentionProblem, AttentionResult, AttentionStats,
-                        BlockLists, PackedBlockMask, PhaseTimings, backward, block_lists,
+                        BlockLists, NonzeroBlockLists, PackedBlockMask, PhaseTimings, backward,
+                        block_lists,
                         block_sparsity, compute_delta, forward)
 
 __all__ = [
     "AttentionProblem", "AttentionResult", "AttentionGradients", "AttentionStats",
     "PackedBlockMask", "PhaseTimings", "forward", "compute_delta", "backward", "block_sparsity",
-    "BlockLists", "block_lists",
+    "BlockLists", "block_lists", "NonzeroBlockLists",
 ]

@@ -34,6 +34,7 @@ EXPORTS = (
     "adattn_b200_tensor_save", "adattn_b200_tensor_load", "adattn_b200_io_last_error",
     "adattn_b200_attn_inputs", "adattn_b200_xoshiro", "adattn_b200_entmax_rows",
     "adattn_b200_block_lists", "adattn_b200_forward_timed", "adattn_b200_forward_ex",
+    "adattn_b200_backward_ex",
 )
 
 
@@ -50,7 +51,12 @@ class Problem(C.Structure):
 
 
 class ForwardExtras(C.Structure):
-    _fields_ = [("phase_ms", C.POINTER(C.c_double)), ("tau_h", C.c_void_p)]
+    _fields_ = [("phase_ms", C.POINTER(C.c_double)), ("tau_h", C.c_void_p),
+                ("block_cnt", C.c_void_p), ("block_cols", C.c_void_p)]
+
+
+class BackwardExtras(C.Structure):
+    _fields_ = [("block_cnt", C.c_void_p), ("block_cols", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -107,6 +113,8 @@ def load() -> C.CDLL:
                                                   C.c_size_t, vp]
         lib.adattn_b200_backward.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                              C.c_size_t, vp]
+        lib.adattn_b200_backward_ex.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                                vp, C.c_size_t, vp, C.POINTER(BackwardExtras)]
         lib.adattn_b200_stats.argtypes = [P, vp, S, vp]
         lib.adattn_b200_mask_sparsity.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                                   S, vp]

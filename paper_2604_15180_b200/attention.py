@@ -177,6 +177,21 @@ class AttentionStats:
 
 
 @dataclass
+class NonzeroBlockLists:
+    """The forward's per-row-block nonzero-block lists (ELL, on the device):
+    ``cnt[..., i]`` active key blocks of row block i, ``cols[..., i, :cnt]`` their
+    indices ascending (PackedBlockMask::for_each_set order, bitpack.hpp:85-92).
+    The backward's kernels walk them (and their transpose)."""
+    cnt: torch.Tensor   # int32 [..., t_r]
+    cols: torch.Tensor  # int16 storage of uint16 [..., t_r, t_c]
+
+    def row(self, i: int, head: int = 0) -> list:
+        c = self.cnt.reshape(-1, self.cnt.shape[-1])[head, i].item()
+        v = self.cols.reshape(-1, *self.cols.shape[-2:])[head, i, :c]
+        return [int(x) & 0xFFFF for x in v.cpu().tolist()]
+
+
+@dataclass
 class AttentionResult:
     """Mirror of AttentionResult (attention.hpp:45-55)."""
     out: torch.Tensor
@@ -184,6 +199,7 @@ class AttentionResult:
     row_max: torch.Tensor
     mask: PackedBlockMask
     row_steps: torch.Tensor
+    lists: Optional[NonzeroBlockLists] = None
     _problem: _lib.Problem = field(repr=False, default=None)
     _stats: Optional[AttentionStats] = field(repr=False, default=None)
     _bwd_done: bool = field(repr=False, default=False)
@@ -260,22 +276,25 @@ def forward(p: AttentionProblem, threads: int = 1, timings: Optional[PhaseTiming
     args = (C.byref(pb), _ptr(p.q), _ptr(p.k), _ptr(p.v), _ptr(out), _ptr(tau), _ptr(row_max),
             _ptr(words), _ptr(steps), _ptr(ws), ws_bytes, _stream())
     timed = timings is not None and threads <= 1  # attention.cpp:170
-    if timed or tau_h is not None:
-        # tau_h (optional, float64 like tau): each row's histogram solution
-        # (solve_histogram, histogram.cpp:73-161), which the reference keeps private
-        if tau_h is not None:
-            if tau_h.shape != tau.shape or tau_h.dtype != torch.float64:
-                raise ValueError("forward: tau_h must be float64 shaped like tau")
-            _check_device(tau_h)
-        ph = (C.c_double * 4)()
-        ex = _lib.ForwardExtras(ph if timed else None, _ptr(tau_h))
-        _lib.check(lib.adattn_b200_forward_ex(*args, C.byref(ex)))
-        if timed:
-            for i in range(4):
-                timings.ms[i] += ph[i]
-    else:
-        _lib.check(lib.adattn_b200_forward(*args))
-    return AttentionResult(out, tau, row_max, PackedBlockMask(words, t_r, t_c), steps, pb)
+    lists = None
+    if t_c <= 65535:  # the nonzero-block lists the backward walks (uint16 indices)
+        lists = NonzeroBlockLists(torch.empty(lead + (t_r,), dtype=torch.int32, device=dev),
+                                  torch.empty(lead + (t_r, t_c), dtype=torch.int16, device=dev))
+    # tau_h (optional, float64 like tau): each row's histogram solution
+    # (solve_histogram, histogram.cpp:73-161), which the reference keeps private
+    if tau_h is not None:
+        if tau_h.shape != tau.shape or tau_h.dtype != torch.float64:
+            raise ValueError("forward: tau_h must be float64 shaped like tau")
+        _check_device(tau_h)
+    ph = (C.c_double * 4)()
+    ex = _lib.ForwardExtras(ph if timed else None, _ptr(tau_h),
+                            _ptr(lists.cnt) if lists else None,
+                            _ptr(lists.cols) if lists else None)
+    _lib.check(lib.adattn_b200_forward_ex(*args, C.byref(ex)))
+    if timed:
+        for i in range(4):
+            timings.ms[i] += ph[i]
+    return AttentionResult(out, tau, row_max, PackedBlockMask(words, t_r, t_c), steps, lists, pb)
 
 
 def _grad_problem(p: AttentionProblem, res: AttentionResult, dout: torch.Tensor) -> _lib.Problem:
@@ -317,10 +336,13 @@ def backward(p: AttentionProblem, res: AttentionResult, dout: torch.Tensor,
     delta = torch.empty_like(res.tau)
     ws_bytes = lib.adattn_b200_backward_workspace(C.byref(pb))
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=p.q.device)
-    _lib.check(lib.adattn_b200_backward(
+    lists = res.lists
+    ex = _lib.BackwardExtras(_ptr(lists.cnt) if lists else None,
+                             _ptr(lists.cols) if lists else None)
+    _lib.check(lib.adattn_b200_backward_ex(
         C.byref(pb), _ptr(p.q), _ptr(p.k), _ptr(p.v), _ptr(res.tau), _ptr(res.row_max),
         _ptr(res.mask.words), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(delta), _ptr(ws),
-        ws_bytes, _stream()))
+        ws_bytes, _stream(), C.byref(ex)))
     res._bwd_done = True  # stats report blocks_visited_bwd = 2 * nnz (attention.cpp:537)
     return AttentionGradients(dq, dk, dv, delta)
 

@@ -20,6 +20,8 @@ cudaError_t entmax_rows(const adattn_rows_problem& p, const void* scores, const 
                         double* tau, double* residual, int32_t* iterations, int32_t* converged,
                         float* probs, double* trace, cudaStream_t st, int* row_err);
 const char* rows_error_message(int code);
+cudaError_t ell_row_lists(const Geom& g, const uint32_t* mask, int32_t* rcnt, uint16_t* rcol,
+                          cudaStream_t st);
 }  // namespace adattn_b200
 
 namespace adattn_b200 {
@@ -383,12 +385,14 @@ struct BwdPadded {
 int forward_impl(const adattn_problem* p, const void* q, const void* k, const void* v,
                  void* out, double* tau, double* row_max, uint32_t* mask, int32_t* row_steps,
                  void* workspace, size_t workspace_bytes, void* stream,
-                 unsigned long long* phase_ns, double* tau_h) {
+                 unsigned long long* phase_ns, double* tau_h, int32_t* lcnt, uint16_t* lcol) {
   Geom g;
   int rc = check(p, &g);
   if (rc) return rc;
   g.phase_ns = phase_ns;
   g.tau_h_out = tau_h;
+  g.rl_cnt_out = lcnt && lcol ? lcnt : nullptr;
+  g.rl_col_out = lcnt && lcol ? lcol : nullptr;
   const int path = resolve(p, g);
   if (path < 0) return -path;
   if (!q || !k || !v || !out || !tau || !row_max || !mask)
@@ -428,6 +432,8 @@ int forward_impl(const adattn_problem* p, const void* q, const void* k, const vo
     }
   } else {
     e = exact_forward(g, q, k, v, out, tau, row_max, mask, row_steps, st);
+    // the EXACT kernels keep no list state: the lists come from the finished mask
+    if (!e && g.rl_cnt_out) e = ell_row_lists(g, mask, g.rl_cnt_out, g.rl_col_out, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "adattn_b200_forward");
   return ADATTN_OK;
@@ -441,14 +447,14 @@ int adattn_b200_forward(const adattn_problem* p, const void* q, const void* k, c
                         int32_t* row_steps, void* workspace, size_t workspace_bytes,
                         void* stream) {
   return forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace, workspace_bytes,
-                      stream, nullptr, nullptr);
+                      stream, nullptr, nullptr, nullptr, nullptr);
 }
 
 int adattn_b200_forward_timed(const adattn_problem* p, const void* q, const void* k,
                               const void* v, void* out, double* tau, double* row_max,
                               uint32_t* mask, int32_t* row_steps, void* workspace,
                               size_t workspace_bytes, void* stream, double* phase_ms) {
-  adattn_forward_extras ex{phase_ms, nullptr};
+  adattn_forward_extras ex{phase_ms, nullptr, nullptr, nullptr};
   if (!phase_ms) return fail(ADATTN_ERR_INVALID, "adattn_b200_forward_timed: null phase_ms");
   return adattn_b200_forward_ex(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
                                 workspace_bytes, stream, &ex);
@@ -460,9 +466,11 @@ int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k
                            size_t workspace_bytes, void* stream, const adattn_forward_extras* ex) {
   double* const tau_h = ex ? ex->tau_h : nullptr;
   double* const phase_ms = ex ? ex->phase_ms : nullptr;
+  int32_t* const lcnt = ex ? ex->block_cnt : nullptr;
+  uint16_t* const lcol = ex ? ex->block_cols : nullptr;
   if (!phase_ms)
     return forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
-                        workspace_bytes, stream, nullptr, tau_h);
+                        workspace_bytes, stream, nullptr, tau_h, lcnt, lcol);
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* acc = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -473,7 +481,7 @@ int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k
   if (!e) e = cudaEventRecord(e0, st);
   if (e) return cuda_fail(e, "adattn_b200_forward_ex");
   int rc = forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
-                        workspace_bytes, stream, acc, tau_h);
+                        workspace_bytes, stream, acc, tau_h, lcnt, lcol);
   unsigned long long ns[4] = {0, 0, 0, 0};
   float total = 0.f;
   e = cudaEventRecord(e1, st);
@@ -532,9 +540,22 @@ int adattn_b200_backward(const adattn_problem* p, const void* q, const void* k,
                          const uint32_t* mask, const void* dout, void* dq, void* dk,
                          void* dv, double* delta, void* workspace, size_t workspace_bytes,
                          void* stream) {
+  return adattn_b200_backward_ex(p, q, k, v, tau, row_max, mask, dout, dq, dk, dv, delta,
+                                 workspace, workspace_bytes, stream, nullptr);
+}
+
+int adattn_b200_backward_ex(const adattn_problem* p, const void* q, const void* k,
+                            const void* v, const double* tau, const double* row_max,
+                            const uint32_t* mask, const void* dout, void* dq, void* dk,
+                            void* dv, double* delta, void* workspace, size_t workspace_bytes,
+                            void* stream, const adattn_backward_extras* ex) {
   Geom g;
   int rc = check(p, &g);
   if (rc) return rc;
+  if (ex && ex->block_cnt && ex->block_cols) {  // the forward's nonzero-block lists
+    g.rl_cnt_in = ex->block_cnt;
+    g.rl_col_in = ex->block_cols;
+  }
   const int path = resolve(p, g);
   if (path < 0) return -path;
   if (!q || !k || !v || !tau || !row_max || !mask || !dout || !dq || !dk || !dv || !delta)
@@ -550,6 +571,9 @@ int adattn_b200_backward(const adattn_problem* p, const void* q, const void* k,
     } else {
       Scratch sc(st);
       BwdPadded b(sc, g, gp, q, k, v, tau, row_max, mask, dout);
+      Geom gq = gp;  // lists of the padded geometry come from the padded mask
+      gq.rl_cnt_in = nullptr;
+      gq.rl_col_in = nullptr;
       const size_t eo = elem_size(g.out_dtype);
       const int H = g.bh;
       void* dqp = sc.zeros((size_t)H * gp.n * g.d * eo);
@@ -557,7 +581,7 @@ int adattn_b200_backward(const adattn_problem* p, const void* q, const void* k,
       void* dvp = sc.zeros((size_t)H * gp.m * g.dv * eo);
       double* dlp = (double*)sc.zeros((size_t)H * gp.n * 8);
       if ((e = sc.error())) return cuda_fail(e, "adattn_b200_backward (padding)");
-      if ((e = tc_backward(gp, b.q, b.k, b.v, b.tau, b.rm, b.mask, b.dout, dqp, dkp, dvp, dlp,
+      if ((e = tc_backward(gq, b.q, b.k, b.v, b.tau, b.rm, b.mask, b.dout, dqp, dkp, dvp, dlp,
                            workspace, st)))
         return cuda_fail(e, "adattn_b200_backward");
       sc.rows(dq, g.n, dqp, gp.n, g.n, g.d * eo, H);

@@ -33,6 +33,13 @@ struct Geom {
   // when set, the forward writes each row's histogram solution tau_h
   // (solve_histogram, histogram.cpp:73-161) to tau_h_out[bh * n + row]
   double* tau_h_out = nullptr;
+  // nonzero-block lists (ELL: per row block the count and the ascending key blocks,
+  // [bh][t_r] / [bh][t_r][t_c] in the caller's geometry): emitted by the forward
+  // when set, consumed by the backward when set (else built from the mask)
+  int32_t* rl_cnt_out = nullptr;
+  uint16_t* rl_col_out = nullptr;
+  const int32_t* rl_cnt_in = nullptr;
+  const uint16_t* rl_col_in = nullptr;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {

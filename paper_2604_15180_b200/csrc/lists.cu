@@ -95,7 +95,75 @@ __global__ void lists_fill_cols(const uint32_t* __restrict__ mask, int cols_tota
     if (m[(size_t)i * wpr] & bit) rows[o++] = i;
 }
 
+// ELL row lists: one thread per (head, row block) writes the ascending active
+// key blocks of its mask row at rcol[row * t_c ..] and their count
+__global__ void ell_rows_kernel(const uint32_t* __restrict__ mask, int rows_total, int t_c, int wpr,
+                                int32_t* __restrict__ rcnt, uint16_t* __restrict__ rcol) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows_total) return;
+  const uint32_t* row = mask + (size_t)r * wpr;
+  uint16_t* out = rcol + (size_t)r * t_c;
+  int n = 0;
+  for (int w = 0; w < wpr; ++w)
+    for (uint32_t bits = row[w]; bits; bits &= bits - 1) {
+      const int j = 32 * w + __ffs(bits) - 1;
+      if (j < t_c) out[n++] = (uint16_t)j;
+    }
+  rcnt[r] = n;
+}
+
+// ELL column lists from the row lists: one warp per (head, key block j); lane l
+// looks j up (binary search) in the lists of row blocks l, l + 32, ..., and a
+// ballot keeps the hits in ascending row order
+__global__ void ell_cols_kernel(const int32_t* __restrict__ rcnt, const uint16_t* __restrict__ rcol,
+                                int cols_total, int t_r, int t_c, int32_t* __restrict__ ccnt,
+                                uint16_t* __restrict__ crow) {
+  const int c = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= cols_total) return;
+  const int h = c / t_c, j = c - h * t_c;
+  uint16_t* out = crow + (size_t)c * t_r;
+  int n = 0;
+  for (int i0 = 0; i0 < t_r; i0 += 32) {
+    const int i = i0 + lane;
+    bool hit = false;
+    if (i < t_r) {
+      const size_t row = (size_t)h * t_r + i;
+      const uint16_t* l = rcol + row * t_c;
+      int lo = 0, hi = rcnt[row];  // first entry >= j
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (l[mid] < j) lo = mid + 1;
+        else hi = mid;
+      }
+      hit = lo < rcnt[row] && l[lo] == j;
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, hit);
+    if (hit) out[n + __popc(b & ((1u << lane) - 1u))] = (uint16_t)i;
+    n += __popc(b);
+  }
+  if (lane == 0) ccnt[c] = n;
+}
+
 }  // namespace
+
+cudaError_t ell_row_lists(const Geom& g, const uint32_t* mask, int32_t* rcnt, uint16_t* rcol,
+                          cudaStream_t st) {
+  const int R = g.bh * g.t_r, T = 128;
+  ell_rows_kernel<<<(R + T - 1) / T, T, 0, st>>>(mask, R, g.t_c, g.wpr, rcnt, rcol);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t ell_col_lists(const Geom& g, const int32_t* rcnt, const uint16_t* rcol, int32_t* ccnt,
+                          uint16_t* crow, cudaStream_t st) {
+  const int Cn = g.bh * g.t_c, T = 256;
+  const size_t threads = (size_t)Cn * 32;
+  ell_cols_kernel<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(rcnt, rcol, Cn, g.t_r, g.t_c,
+                                                                    ccnt, crow);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t block_lists(const Geom& g, const uint32_t* mask, int64_t* rowptr, int32_t* cols,
                         int64_t* colptr, int32_t* rows, cudaStream_t st) {

@@ -55,7 +55,14 @@ struct BwdArgs {
   float e0f, e1f;
   const double* tau;
   const double* row_max;
-  const uint32_t* mask;
+  // the nonzero-block lists the kernels walk (ELL, ascending; ell_row_lists /
+  // ell_col_lists): row block i of head h: rcnt[h t_r + i] key blocks at
+  // rcol[(h t_r + i) t_c ..]; key block j: ccnt[h t_c + j] query blocks at
+  // crow[(h t_c + j) t_r ..]
+  const int32_t* rcnt;
+  const uint16_t* rcol;
+  const int32_t* ccnt;
+  const uint16_t* crow;
   double* delta;
   float2* rowc;  // [bh*n] {C, delta}
   // fp16 operand plan of the pair dQ and dK/dV kernels (device; nullptr: bf16 hi/lo)
@@ -65,6 +72,46 @@ struct BwdArgs {
   void* dv;
   float scale_f;
 };
+
+// Mask words of row blocks rb0 .. rb0 + nrb - 1 of head bh, rebuilt in shared
+// memory from the row lists (all threads of the CTA call this).
+__device__ __forceinline__ void rows_from_lists(uint32_t* dst, int nrb, const BwdArgs& a, int bh,
+                                                int rb0, int tid, int nthreads) {
+  const Geom& g = a.g;
+  for (int i = tid; i < nrb * g.wpr; i += nthreads) dst[i] = 0u;
+  __syncthreads();
+  for (int r = 0; r < nrb; ++r) {
+    const int ib = rb0 + r;
+    if (ib >= g.t_r) break;
+    const size_t row = (size_t)bh * g.t_r + ib;
+    const int cnt = a.rcnt[row];
+    const uint16_t* c = a.rcol + row * g.t_c;
+    for (int k = tid; k < cnt; k += nthreads) {
+      const uint32_t j = c[k];
+      atomicOr(&dst[r * g.wpr + (j >> 5)], 1u << (j & 31));
+    }
+  }
+  __syncthreads();
+}
+
+// ubits[i] = bit kh set iff query block i is active in key block j0 + kh (kh < nkb),
+// from the column lists (all threads of the CTA call this).
+__device__ __forceinline__ void units_from_lists(uint8_t* ubits, int nkb, const BwdArgs& a, int bh,
+                                                 int j0, int tid, int nthreads) {
+  const Geom& g = a.g;
+  for (int i = tid; i < g.t_r; i += nthreads) ubits[i] = 0;
+  __syncthreads();
+  for (int kh = 0; kh < nkb; ++kh) {  // one key block per pass: no two writers per byte
+    const int j = j0 + kh;
+    if (j < g.t_c) {
+      const size_t col = (size_t)bh * g.t_c + j;
+      const int cnt = a.ccnt[col];
+      const uint16_t* r = a.crow + col * g.t_r;
+      for (int k = tid; k < cnt; k += nthreads) ubits[r[k]] |= (uint8_t)(1u << kh);
+    }
+    __syncthreads();
+  }
+}
 
 enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 
@@ -286,10 +333,7 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
   const int nkt = g.m / DBN;
   const int jmax = g.causal ? (row0 + BM - 1) / DBN : nkt - 1;
 
-  for (int i = tid; i < 4 * wpr; i += kDeltaThreads) {
-    const int rbi = i / wpr, w = i - rbi * wpr;
-    smask[i] = a.mask[((size_t)bh * g.t_r + (row0 / 64 + rbi)) * wpr + w];
-  }
+  rows_from_lists(smask, 4, a, bh, row0 / 64, tid, kDeltaThreads);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
       mbar_init(&full[i], 1);
@@ -518,10 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
   const int nkt = g.m / DBN;
   const int jmax = g.causal ? (prow0 + 2 * BM - 1) / DBN : nkt - 1;
 
-  for (int i = tid; i < 8 * wpr; i += kDeltaThreads) {
-    const int rbi = i / wpr, w = i - rbi * wpr;
-    smask[i] = a.mask[((size_t)bh * g.t_r + (prow0 / 64 + rbi)) * wpr + w];
-  }
+  rows_from_lists(smask, 8, a, bh, prow0 / 64, tid, kDeltaThreads);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
       mbar_init(&full[i], 1);
@@ -756,10 +797,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
   const int nkt = g.m / DBN;
   const int jmax = g.causal ? (prow0 + 2 * QR - 1) / DBN : nkt - 1;
 
-  for (int i = tid; i < 4 * wpr; i += kDeltaThreads) {
-    const int rbi = i / wpr, w = i - rbi * wpr;
-    smask[i] = a.mask[((size_t)bh * g.t_r + (prow0 / 64 + rbi)) * wpr + w];
-  }
+  rows_from_lists(smask, 4, a, bh, prow0 / 64, tid, kDeltaThreads);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
       mbar_init(&full[i], 1);
@@ -983,10 +1021,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int jmax = g.causal ? (row0 + QB_DQ - 1) / DBN : nkt - 1;
   const int wpr = g.wpr;
 
-  for (int i = tid; i < 2 * wpr; i += kThreads) {
-    const int rbi = i / wpr, w = i - rbi * wpr;
-    smask[i] = a.mask[((size_t)bh * g.t_r + (row0 / 64 + rbi)) * wpr + w];
-  }
+  rows_from_lists(smask, 2, a, bh, row0 / 64, tid, kThreads);
   if (tid == 0) {
     for (int i = 0; i < NSK; ++i) {
       mbar_init(&kfull[i], 1);
@@ -1270,10 +1305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int jmax = g.causal ? (prow0 + 2 * QB_DQ - 1) / DBN : nkt - 1;
   const int wpr = g.wpr;
 
-  for (int i = tid; i < 4 * wpr; i += kThreads) {
-    const int rbi = i / wpr, w = i - rbi * wpr;
-    smask[i] = a.mask[((size_t)bh * g.t_r + (prow0 / 64 + rbi)) * wpr + w];
-  }
+  rows_from_lists(smask, 4, a, bh, prow0 / 64, tid, kThreads);
   if (tid == 0) {
     for (int i = 0; i < NSK; ++i) {
       mbar_init(&kfull[i], 1);
@@ -1542,14 +1574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int wpr = g.wpr;
   const int i_first = g.causal ? key0 / QT : 0;
 
-  {
-    const int jw = kb * KB / 64;
-    const int bhh = bh;
-    for (int i = threadIdx.x; i < g.t_r; i += kThreads) {
-      const uint32_t w = a.mask[((size_t)bhh * g.t_r + i) * g.wpr + (jw >> 5)];
-      ubits[i] = (uint8_t)((w >> (jw & 31)) & 3u);
-    }
-  }
+  units_from_lists(ubits, 2, a, bh, kb * KB / 64, threadIdx.x, kThreads);
   if (tid == 0) {
     for (int i = 0; i < KST; ++i) {
       mbar_init(&full[i], 1);
@@ -1876,10 +1901,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
   const int pj0 = pkey0 / 64;           // first of the pair's four reference key tiles
   const int i_first = g.causal ? pkey0 / QT : 0;
 
-  for (int i = threadIdx.x; i < g.t_r; i += kKvThreads) {
-    const uint32_t w = a.mask[((size_t)bh * g.t_r + i) * g.wpr + (pj0 >> 5)];
-    ubits[i] = (uint8_t)((w >> (pj0 & 31)) & 15u);
-  }
+  units_from_lists(ubits, 4, a, bh, pj0, threadIdx.x, kKvThreads);
   if (tid == 0) {
     for (int i = 0; i < KS; ++i) {
       mbar_init(&full[i], 1);
@@ -2259,7 +2281,7 @@ static size_t ws_plan(const Geom& g) {
 size_t backward_workspace(const Geom& g) {
   const bool pairs = g.d == 128 && g.dv == 128;
   const bool dvh = pairs && dv_f16_enabled(), dsh = pairs && ds_f16_enabled();
-  return ws_rowc(g) + (dvh || dsh ? ws_h(g, g.dv, g.n) : 0) +
+  return ws_rowc(g) + ell_bytes(g) + (dvh || dsh ? ws_h(g, g.dv, g.n) : 0) +
          (dsh ? ws_h(g, g.d, g.n) + ws_h(g, g.d, g.m) : 0) + ws_plan(g);
 }
 
@@ -2293,7 +2315,30 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   a.e1f = (float)(g.e0 - 1.0);
   a.tau = tau;
   a.row_max = row_max;
-  a.mask = mask;
+  {  // the nonzero-block lists the kernels walk, from the forward's mask
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    uint8_t* w8 = reinterpret_cast<uint8_t*>(workspace) + ws_rowc(g);
+    int32_t* rcnt = reinterpret_cast<int32_t*>(w8);
+    w8 += al((size_t)g.bh * g.t_r * 4);
+    uint16_t* rcol = reinterpret_cast<uint16_t*>(w8);
+    w8 += al((size_t)g.bh * g.t_r * g.t_c * 2);
+    int32_t* ccnt = reinterpret_cast<int32_t*>(w8);
+    w8 += al((size_t)g.bh * g.t_c * 4);
+    uint16_t* crow = reinterpret_cast<uint16_t*>(w8);
+    const int32_t* rc = rcnt;
+    const uint16_t* rl = rcol;
+    if (g.rl_cnt_in && g.rl_col_in) {  // the forward's own lists
+      rc = g.rl_cnt_in;
+      rl = g.rl_col_in;
+    } else if ((e = ell_row_lists(g, mask, rcnt, rcol, st))) {
+      return e;
+    }
+    if (!delta_only && (e = ell_col_lists(g, rc, rl, ccnt, crow, st))) return e;
+    a.rcnt = rc;
+    a.rcol = rl;
+    a.ccnt = ccnt;
+    a.crow = crow;
+  }
   a.delta = delta;
   a.rowc = reinterpret_cast<float2*>(workspace);
   a.f16 = nullptr;
@@ -2305,7 +2350,7 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
     // fp16 operand copies + range maxima, then the per-launch plan (device-side:
     // no host round trip); the pair kernels read it at start
     uint8_t* w8 = reinterpret_cast<uint8_t*>(workspace);
-    size_t off = ws_rowc(g);
+    size_t off = ws_rowc(g) + ell_bytes(g);
     __half2* do16 = reinterpret_cast<__half2*>(w8 + off);
     off += ws_h(g, g.dv, g.n);
     __half2* q16 = nullptr;

@@ -153,6 +153,9 @@ struct FwdArgs {
   int cand_slots;
   // fp16 P V: per head, max |V| (float bits) of the scaled fp16 V copy; nullptr -> bf16 P
   const uint32_t* v16_max;
+  // optional output: per row block its active key blocks (ELL, ascending; ell_bytes layout)
+  int32_t* rcnt;
+  uint16_t* rcol;
 };
 
 template <int D>
@@ -177,7 +180,9 @@ struct FwdSmem {
   __host__ __device__ static int off_actu(int wpr, int nkt) { return off_act(wpr, nkt) + 4 * ((nkt + 31) / 32) * 4; }
   __host__ __device__ static int off_pm(int wpr, int nkt) { return off_actu(wpr, nkt) + 4 * ((nkt + 31) / 32) * 4; }
   __host__ __device__ static int off_xf(int wpr, int nkt) { return off_pm(wpr, nkt) + 4 * wpr * 4; }
-  static size_t bytes(int wpr, int nkt) { return 1024 + off_xf(wpr, nkt) + 16 + 64; }
+  // the output pass's active 128-key tiles (ascending u16), after the exchange flags
+  __host__ __device__ static int off_tiles(int wpr, int nkt) { return off_xf(wpr, nkt) + 16; }
+  static size_t bytes(int wpr, int nkt) { return 1024 + off_tiles(wpr, nkt) + 2 * nkt + 64; }
 };
 
 // Order-preserving float <-> u32 (atomicMax / atomicMin on floats in smem).
@@ -391,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
   volatile uint32_t* s_tmem = misc;  // TMEM base
   volatile uint32_t* s_decision = misc + 1;
+  volatile uint32_t* s_ntiles = misc + 2;  // entries of sTiles
   uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + L::OFF_CNT);
   double* sPart = reinterpret_cast<double*>(smem + L::OFF_PART);
   float* sRow = reinterpret_cast<float*>(smem + L::OFF_ROW);
@@ -404,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* sActU = PAIR ? reinterpret_cast<uint32_t*>(smem + L::off_actu(g.wpr, nkt_)) : sAct;
   uint32_t* sPm = PAIR ? reinterpret_cast<uint32_t*>(smem + L::off_pm(g.wpr, nkt_)) : smask;
   volatile uint32_t* xflag = reinterpret_cast<volatile uint32_t*>(smem + L::off_xf(g.wpr, nkt_));
+  uint16_t* sTiles = reinterpret_cast<uint16_t*>(smem + L::off_tiles(g.wpr, nkt_));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // head-major (the head's K/V stay L2-resident across its CTAs' sweeps),
@@ -490,10 +497,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     return ((m[(2 * rg) * wpr + w] | m[(2 * rg + 1) * wpr + w]) & bits) != 0;
   };
   auto out_active = [&](int rg, int J) -> bool { return out_active_m(sPm, rg, J); };
-  auto next_active = [&](int J) -> int {  // first active key tile >= J, or -1
-    for (; J <= Jmax; ++J)
-      if (out_active(0, J) || out_active(1, J)) return J;
-    return -1;
+  // The output pass walks the CTA's nonzero-tile list: the 128-key tiles that hold an
+  // active block of one of its four row blocks (pairs: of either CTA), ascending --
+  // the union of the row blocks' nonzero-block lists (attention.cpp:334-352).
+  // Built by epilogue warp 0 once the mask is final, before the decision barrier.
+  auto build_tiles = [&]() {
+    uint32_t n = 0;
+    for (int J0 = 0; J0 <= Jmax; J0 += 32) {
+      const int J = J0 + lane;
+      const bool on = J <= Jmax && (out_active(0, J) || out_active(1, J));
+      const uint32_t b = __ballot_sync(0xffffffffu, on);
+      if (on) sTiles[n + __popc(b & ((1u << lane) - 1u))] = (uint16_t)J;
+      n += __popc(b);
+    }
+    if (lane == 0) *s_ntiles = n;
+    __syncwarp();
   };
 
   if (warp == kWarpProd) {
@@ -566,7 +584,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (*s_decision == DEC_OUT) break;
       }
     int prev = -1;
-    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+    for (uint32_t t = 0, nt_ = *s_ntiles; t < nt_; ++t) {
+      const int J = sTiles[t];
       load(false, J);
       if (prev >= 0) load(true, prev);
       prev = J;
@@ -754,7 +773,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     int prev = -1;
     bool prev_act[2] = {false, false};
-    for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+    for (uint32_t t = 0, nt_ = *s_ntiles; t < nt_; ++t) {
+      const int J = sTiles[t];
       const uint32_t kst = wait_ring();  // K(J) is ring item r
       uint32_t vst = 0;
       if (prev >= 0) {
@@ -1303,6 +1323,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       PASS_MARK(3);
       bar_sync(3, kEpi);
       if (PAIR && list_ok) pair_or_words(sPm, smask, 4 * wpr);
+      if (list_ok) {
+        if (warp == 0) build_tiles();
+        bar_sync(3, kEpi);
+      }
       if (tid == 0) {
         *s_decision = list_ok ? DEC_OUT : DEC_REF;
         mbar_arrive(dec_bar);
@@ -1364,6 +1388,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         any = pair_or(any);
         if (!any) pair_or_words(sPm, smask, 4 * wpr);
       }
+      if (!any) {
+        if (warp == 0) build_tiles();
+        bar_sync(3, kEpi);
+      }
       if (tid == 0) {
         *s_decision = any ? DEC_REF : DEC_OUT;
         mbar_arrive(dec_bar);
@@ -1379,7 +1407,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float2 A2 = make_float2(A1, A1), C2 = make_float2(C, C);
       bool any_out = false;
       uint32_t ob = (it + 1) >> 1;  // previous uses of S buffer 0 of this group
-      for (int J = next_active(0); J >= 0; J = next_active(J + 1)) {
+      for (uint32_t t = 0, nt_ = *s_ntiles; t < nt_; ++t) {
+        const int J = sTiles[t];
         if (!out_active(rg, J)) continue;
         any_out = true;
         // pairs: a tile active for the peer's rows only gets P = 0 without reading S
@@ -1455,6 +1484,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = tid; i < 4 * wpr; i += kEpi) {
         const int rbi = i / wpr, w = i - rbi * wpr;
         a.mask[((size_t)bh * g.t_r + (row0 / 64 + rbi)) * wpr + w] = smask[i];
+      }
+      // the nonzero-block lists of the four row blocks (ELL, ascending key blocks),
+      // emitted for the backward; laid out in the caller's (unpadded) geometry
+      if (a.rcnt && warp < 4) {
+        const int t_r_v = (g.n_valid + 63) / 64, t_c_v = (g.m_valid + 63) / 64;
+        const int ib = row0 / 64 + warp;
+        if (ib < t_r_v) {
+          const size_t row = (size_t)bh * t_r_v + ib;
+          uint16_t* out = a.rcol + row * t_c_v;
+          uint32_t n = 0;
+          for (int w0 = 0; w0 < wpr; w0 += 32) {
+            const int w = w0 + lane;
+            uint32_t bits = w < wpr ? smask[warp * wpr + w] : 0u;
+            const int top = t_c_v - 32 * w;  // key blocks >= t_c_v are padding
+            if (top < 32) bits &= top <= 0 ? 0u : ((1u << top) - 1u);
+            const uint32_t c = __popc(bits);
+            uint32_t pre = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t x = __shfl_up_sync(0xffffffffu, pre, o);
+              if (lane >= o) pre += x;
+            }
+            uint32_t k = n + pre - c;
+            for (; bits; bits &= bits - 1) out[k++] = (uint16_t)(32 * w + __ffs(bits) - 1);
+            n += __shfl_sync(0xffffffffu, pre, 31);
+          }
+          if (lane == 0) a.rcnt[row] = (int32_t)n;
+        }
       }
     }
     PASS_MARK(6);
@@ -1555,6 +1612,8 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.row_max = row_max;
   a.mask = mask;
   a.steps = steps;
+  a.rcnt = g.rl_cnt_out;
+  a.rcol = g.rl_col_out;
   const CandPlan cp = cand_plan(g);
   a.cand = (cp.cap > 0 && ws) ? reinterpret_cast<uint2*>(ws) : nullptr;
   a.cand_cap = cp.cap;

@@ -7,6 +7,20 @@
 #include "common.cuh"
 
 namespace adattn_b200 {
+
+// ELL nonzero-block lists (lists.cu): per row block its active key blocks
+// (ascending, capacity t_c), per key block its active query blocks (ascending,
+// capacity t_r) -- the lists the backward kernels walk.
+cudaError_t ell_row_lists(const Geom& g, const uint32_t* mask, int32_t* rcnt, uint16_t* rcol,
+                          cudaStream_t st);
+cudaError_t ell_col_lists(const Geom& g, const int32_t* rcnt, const uint16_t* rcol, int32_t* ccnt,
+                          uint16_t* crow, cudaStream_t st);
+inline size_t ell_bytes(const Geom& g) {
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  return al((size_t)g.bh * g.t_r * 4) + al((size_t)g.bh * g.t_r * g.t_c * 2) +
+         al((size_t)g.bh * g.t_c * 4) + al((size_t)g.bh * g.t_c * g.t_r * 2);
+}
+
 namespace tc {
 
 // 2-D bf16 tensor map over a row-major [rows][cols] matrix, box = 64 columns
