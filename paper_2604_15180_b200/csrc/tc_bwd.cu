@@ -2157,11 +2157,18 @@ bool dv_f16_enabled() {
   const char* s = std::getenv("ADATTN_DV_F16");
   return !(s && *s == '0');
 }
-// opt-in: dQ/dK differ from the hi/lo products by up to ~7e-3 at N = 32K (alpha = 2,
-// max|dK| ~ 35) -- inside the 2e-2 bar but with a 3x margin -- for -2% step time
-bool ds_f16_enabled() {
+// fp16 dS: dQ/dK carry the fp16 rounding of dS (11 significant bits, ~2^-12 of
+// max|grad|).  Measured against the bf16 hi/lo products (themselves within ~1e-4
+// of the reference): alpha = 1.5 -> 3.4e-3 at N = 32K (max|dK| 15), 4.6e-3 at
+// N = 128K (max|dK| 25): a 4-6x margin to the 2e-2 bar, -6% step time.  alpha = 2
+// has ~2x larger gradients (7e-3 .. 9e-3, a 2x margin), so the default
+// ("auto") takes fp16 dS for alpha <= 1.5 only; ADATTN_DS_F16=1 forces it (alpha
+// <= 2, the plan's bound), =0 keeps hi/lo.
+bool ds_f16_enabled(const Geom& g) {
   const char* s = std::getenv("ADATTN_DS_F16");
-  return s && *s == '1';
+  if (s && *s == '1') return true;
+  if (s && *s == '0') return false;
+  return g.alpha <= 1.5;
 }
 
 // CTA-pair dK/dV kernel for d = 128 (ADATTN_KV_PAIRS=0 selects the single-CTA kernel)
@@ -2211,7 +2218,7 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
   }
   if (delta_only) return cudaSuccess;
   if (use_kv_pairs(g)) {
-    auto k2 = ds_f16_enabled() ? tc_dkdv2_kernel<128, AK, true> : tc_dkdv2_kernel<128, AK, false>;
+    auto k2 = ds_f16_enabled(g) ? tc_dkdv2_kernel<128, AK, true> : tc_dkdv2_kernel<128, AK, false>;
     const size_t sm = Kv2Smem<128>::bytes(g.t_r);
     if ((e = set_smem(k2, sm))) return e;
     prof_begin("tc_dkdv", st);
@@ -2231,7 +2238,7 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     if ((e = cudaGetLastError())) return e;
   }
   if (use_dq_pairs(g)) {
-    auto k1 = ds_f16_enabled() ? tc_dq2_kernel<128, AK, true> : tc_dq2_kernel<128, AK, false>;
+    auto k1 = ds_f16_enabled(g) ? tc_dq2_kernel<128, AK, true> : tc_dq2_kernel<128, AK, false>;
     const size_t sm = Dq2Smem<128>::bytes(g.wpr);
     if ((e = set_smem(k1, sm))) return e;
     prof_begin("tc_dq", st);
@@ -2280,7 +2287,7 @@ static size_t ws_plan(const Geom& g) {
 // C-ABI's workspace check fails loudly)
 size_t backward_workspace(const Geom& g) {
   const bool pairs = g.d == 128 && g.dv == 128;
-  const bool dvh = pairs && dv_f16_enabled(), dsh = pairs && ds_f16_enabled();
+  const bool dvh = pairs && dv_f16_enabled(), dsh = pairs && ds_f16_enabled(g);
   return ws_rowc(g) + ell_bytes(g) + (dvh || dsh ? ws_h(g, g.dv, g.n) : 0) +
          (dsh ? ws_h(g, g.d, g.n) + ws_h(g, g.d, g.m) : 0) + ws_plan(g);
 }
@@ -2345,7 +2352,7 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   m[14] = m[7];
   m[15] = m[1];
   m[16] = m[4];
-  const bool want_dv = dv_f16_enabled(), want_ds = ds_f16_enabled();
+  const bool want_dv = dv_f16_enabled(), want_ds = ds_f16_enabled(g);
   if (!delta_only && (use_kv_pairs(g) || use_dq_pairs(g)) && (want_dv || want_ds)) {
     // fp16 operand copies + range maxima, then the per-launch plan (device-side:
     // no host round trip); the pair kernels read it at start

@@ -90,7 +90,7 @@ def flops(D: int, nnz: int, addressable: int, ref_passes: int = 3) -> dict:
     return dict(f_eff=f_eff, f_alg=f_alg, f_fwd=f_fwd)
 
 
-def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None) -> dict:
+def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha: float = 1.5) -> dict:
     """Tensor-core flops each kernel actually issues for one problem (all heads),
     from the 64x64 block mask ([B][H][t_r][wpr] u32) -- the numerator of the
     per-kernel roofline.  Counts every tcgen05 MMA the
@@ -101,7 +101,8 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None) -> dic
     tc_fwd   3 sweeps (MAX, HIST, CAND) of S over the causal 128x128 tiles of
              each 128-row group + OUT (S and P V) over active tiles
     tc_delta S, dP over active (128 rows x 128 keys) tiles
-    tc_dq    S, dP, dQ (fp16 sigma dS and K: one product; bf16 hi/lo otherwise)
+    tc_dq    S, dP, dQ (fp16 sigma dS and K: one product -- default for alpha <= 1.5;
+             bf16 hi/lo otherwise)
              over active (128 x 128) tiles
     tc_dkdv  S^T, dP^T, dV (fp16 P and dO: one product; bf16 hi/lo with
              ADATTN_DV_F16=0 or for d != 128), dK hi/lo over active
@@ -130,7 +131,8 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None) -> dic
     if dv_f16 is None:  # the library's default (csrc/tc_bwd.cu dv_f16_enabled, pair kernel)
         dv_f16 = (d == 128 and os.environ.get("ADATTN_DV_F16", "1") != "0"
                   and os.environ.get("ADATTN_KV_PAIRS", "1") != "0")
-    ds_f16 = d == 128 and os.environ.get("ADATTN_DS_F16", "0") == "1"  # opt-in (alpha <= 2, data in range)
+    ds_env = os.environ.get("ADATTN_DS_F16", "auto")  # the library's rule (tc_bwd.cu ds_f16_enabled)
+    ds_f16 = d == 128 and (ds_env == "1" or (ds_env not in ("0", "1") and alpha <= 1.5))
     kv_pairs = os.environ.get("ADATTN_KV_PAIRS", "1") != "0"
     dq_pairs = os.environ.get("ADATTN_DQ_PAIRS", "1") != "0"
     return {"tc_fwd": (3 * sweep_tiles + 2 * act) * tile,

@@ -221,6 +221,7 @@ def test_tc_long_context_rows_vs_dense(N, D, causal, beta):
 def test_tc_dq_cta_pairs_match_single(monkeypatch):
     """The CTA-pair dQ kernel (cta_group::2, M = 256 across two SMs) gives the
     single-CTA kernel's dQ (same per-tile arithmetic and K order)."""
+    monkeypatch.setenv("ADATTN_DS_F16", "0")  # hi/lo dS: the comparison isolates the dV / pair path
     q, k, v, do = inputs(77, 1, 2, 1024, 128, 1.0)
     prob = pa.AttentionProblem(q, k, v, path="tc", alpha=1.5, causal=True)
     res = pa.forward(prob)
@@ -261,6 +262,7 @@ def test_tc_delta_cta_pairs_match_single(monkeypatch, mode):
     """The CTA-pair delta kernels (mode 1: 256 rows per CTA; mode 2: 128 rows
     per CTA, double-buffered S/dP) give the single-CTA kernel's delta: the same
     fp32 32-key partial sums, combined in a different order in mode 2."""
+    monkeypatch.setenv("ADATTN_DS_F16", "0")  # hi/lo dS: isolates the delta kernels
     for causal in (True, False):
         for alpha in (1.5, 2.0, 1.25):
             q, k, v, do = inputs(79, 1, 2, 1024, 128, 1.0)
@@ -335,6 +337,7 @@ def test_tc_dv_f16_matches_hilo(monkeypatch, alpha):
     K step) against the bf16 hi + lo pair: within 2^-9 of max|dV| (the fp16
     rounding of P), dK and dQ untouched; and against the exact path within the
     bf16 gradient bar (2e-2)."""
+    monkeypatch.setenv("ADATTN_DS_F16", "0")  # hi/lo dS: the comparison isolates the dV / pair path
     q, k, v, do = inputs(81, 1, 2, 4096, 128, 1.0)
     prob = pa.AttentionProblem(q, k, v, path="tc", alpha=alpha, causal=True)
     res = pa.forward(prob)
@@ -358,6 +361,7 @@ def test_tc_dv_f16_scaled_dout(monkeypatch, do_scale):
     [2^14, 2^15)), so small gradients do not underflow fp16 and large ones do not
     overflow: fp16 dV stays within 2^-9 of max|dV| of the bf16 hi/lo product at
     any dO magnitude, and dK / dQ are untouched."""
+    monkeypatch.setenv("ADATTN_DS_F16", "0")  # hi/lo dS: the comparison isolates the dV / pair path
     q, k, v, do = inputs(82, 1, 2, 1024, 128, 1.0)
     do = (do.float() * do_scale).to(torch.bfloat16)
     prob = pa.AttentionProblem(q, k, v, path="tc", alpha=1.5, causal=True)
@@ -398,7 +402,7 @@ def test_tc_f16_plans_are_per_head(monkeypatch):
 
 @pytest.mark.parametrize("alpha", [1.5, 2.0])
 def test_tc_ds_f16_opt_in(monkeypatch, alpha):
-    """Opt-in fp16 dS products (ADATTN_DS_F16=1: dQ = (sigma dS) K, dK = (sigma dS)^T Q
+    """fp16 dS products (ADATTN_DS_F16=1; the default for alpha <= 1.5: dQ = (sigma dS) K, dK = (sigma dS)^T Q
     with a power-of-two sigma from the |dS| bound, fp16 Q/K copies): within 2^-8 of
     max|grad| of the bf16 hi/lo products and within the 2e-2 bar of the exact path;
     alpha > 2 (u = p^(2-alpha) unbounded) keeps hi/lo."""
@@ -487,3 +491,19 @@ def test_tc_pv_f16_scaled_v(monkeypatch, v_scale):
     err = (rf.out - rx.out).abs().max().item()
     print("fp16 P V at V scale", v_scale, err, mag)
     assert mag > 0 and err <= 2e-3 * mag
+
+
+@pytest.mark.parametrize("alpha,forced", [(1.5, "1"), (1.25, "1"), (2.0, "0")])
+def test_tc_ds_f16_default_rule(monkeypatch, alpha, forced):
+    """The default ("auto") takes the fp16 dS products for alpha <= 1.5 (measured margin
+    4-6x to the 2e-2 bar against the reference, tests/test_gpu_oracle_tc.py) and the
+    bf16 hi/lo products above (alpha = 2: ~2x larger gradients)."""
+    q, k, v, do = inputs(88, 1, 2, 2048, 128, 1.0)
+    prob = pa.AttentionProblem(q, k, v, path="tc", alpha=alpha, causal=True)
+    res = pa.forward(prob)
+    monkeypatch.delenv("ADATTN_DS_F16", raising=False)
+    g0 = pa.backward(prob, res, do)
+    monkeypatch.setenv("ADATTN_DS_F16", forced)
+    g1 = pa.backward(prob, res, do)
+    torch.cuda.synchronize()
+    assert torch.equal(g0.dq, g1.dq) and torch.equal(g0.dk, g1.dk)
