@@ -10,8 +10,9 @@
 // reference's operation order (bit-identical results; pow() for alpha outside
 // {1.5, 2} may differ in the last bit).  `threads` is accepted and ignored
 // (work runs on the GPU); PhaseTimings::ms[0..3] receive the forward's
-// per-phase device time when threads <= 1, as in the reference.  A problem outside the GPU envelope (tile > 64, d or dv > 128) throws
-// std::runtime_error -- there is no CPU fallback.
+// per-phase device time when threads <= 1, as in the reference.  Every problem the
+// reference's validate() accepts runs on the GPU (any tile size and width; a CUDA
+// failure throws std::runtime_error) -- there is no CPU fallback.
 #pragma once
 
 #include <cstdint>

@@ -131,8 +131,7 @@ int resolve(const adattn_problem* p, const Geom& g) {
   if (p->path == ADATTN_PATH_AUTO && tc_ok) return ADATTN_PATH_TC;
   if (!exact_supported(g))
     return -fail(ADATTN_ERR_UNSUPPORTED,
-                 "adattn_b200: exact path supports block_r, block_c <= 64, d, dv <= 128 and "
-                 "batch*heads <= 65535");
+                 "adattn_b200: exact path supports batch*heads <= 65535");
   return ADATTN_PATH_EXACT;
 }
 

@@ -594,11 +594,9 @@ cudaError_t prep(K kernel, size_t smem) {
 
 }  // namespace
 
-// (grid.y carries the head index: at most 65535 heads per call)
-bool exact_supported(const Geom& g) {
-  return g.block_r <= kTile && g.block_c <= kTile && g.d <= 128 && g.dv <= 128 &&
-         g.bh <= 65535;
-}
+// (grid.y carries the head index: at most 65535 heads per call).  Blocks > 64 or
+// widths > 128 run on the one-thread-per-row kernels of exact_generic.cu.
+bool exact_supported(const Geom& g) { return g.bh <= 65535; }
 
 static size_t fwd_smem(const Geom& g) {
   const int ldq = odd_ld(g.d), ldk = odd_ld(g.d > g.dv ? g.d : g.dv);
@@ -625,6 +623,8 @@ static size_t dq_smem(const Geom& g) {
 cudaError_t exact_forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                           double* tau, double* row_max, uint32_t* mask, int32_t* steps,
                           cudaStream_t st) {
+  if (exact_generic_needed(g))
+    return exact_generic_forward(g, q, k, v, out, tau, row_max, mask, steps, st);
   const size_t smem = fwd_smem(g);
   const dim3 grid(g.t_r, g.bh);
   cudaError_t e;
@@ -647,6 +647,8 @@ cudaError_t exact_forward(const Geom& g, const void* q, const void* k, const voi
 cudaError_t exact_delta(const Geom& g, const void* q, const void* k, const void* v,
                         const double* tau, const double* row_max, const uint32_t* mask,
                         const void* dout, double* delta, cudaStream_t st) {
+  if (exact_generic_needed(g))
+    return exact_generic_delta(g, q, k, v, tau, row_max, mask, dout, delta, st);
   const size_t smem = delta_smem(g);
   const dim3 grid(g.t_r, g.bh);
   cudaError_t e;
@@ -667,6 +669,9 @@ cudaError_t exact_backward(const Geom& g, const void* q, const void* k, const vo
                            const double* tau, const double* row_max, const uint32_t* mask,
                            const void* dout, void* dq, void* dk, void* dv, double* delta,
                            unsigned long long* visited, cudaStream_t st) {
+  if (exact_generic_needed(g))
+    return exact_generic_backward(g, q, k, v, tau, row_max, mask, dout, dq, dk, dv, delta,
+                                  visited, st);
   cudaError_t e = exact_delta(g, q, k, v, tau, row_max, mask, dout, delta, st);
   if (e) return e;
   const size_t s1 = dkdv_smem(g), s2 = dq_smem(g);

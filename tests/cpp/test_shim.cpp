@@ -110,6 +110,23 @@ int main() {
     bool ok = true;
     try { forward(wide); } catch (...) { ok = false; }
     CHECK(ok);
+    // tiles and widths beyond the tiled kernels' envelope run too (exact_generic.cu)
+    Rng r2(12);
+    AttentionProblem big = problem(r2, 150, 160, 1.5, 128, 96, true);
+    ok = true;
+    try {
+      AttentionResult res = forward(big);
+      const Matrix dout = gauss(r2, 150, 160);
+      const AttentionGradients g = backward(big, res, dout);
+      for (int i = 0; i < big.q.rows; ++i) {
+        double sum = 0.0;
+        for (int j = 0; j < big.k.rows; ++j) sum += prob_at(big, res, i, j);
+        ok &= std::isfinite(sum) && std::abs(sum - 1.0) < 1e-4 && std::isfinite(g.dq.at(i, 0));
+      }
+    } catch (...) {
+      ok = false;
+    }
+    CHECK(ok);
   }
   {  // single query and key reduces to a point mass (107-131)
     AttentionProblem p;

@@ -191,3 +191,45 @@ def test_mask_serialize_layout():
     assert raw[:8] == (7).to_bytes(4, "little") + (7).to_bytes(4, "little")
     assert len(raw) == 8 + 7 * 4
     assert pa.block_sparsity(res.mask, False) == res.stats.block_sparsity
+
+
+GENERIC = [
+    # (n, m, d, dv, alpha, causal, block_r, block_c, bins)
+    (200, 200, 200, 150, 1.5, True, 128, 96, 8),
+    (150, 170, 40, 260, 2.0, False, 80, 70, 8),
+    (130, 130, 130, 64, 2.5, True, 100, 128, 4),
+    (190, 190, 16, 16, 1.25, True, 65, 200, 32),
+    (97, 61, 300, 129, 1.5, False, 256, 32, 16),
+]
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("case", GENERIC, ids=[str(c) for c in GENERIC])
+def test_generic_blocks_and_widths_bitwise(case, dtype):
+    """Blocks larger than 64 and widths above 128 (which the reference's validate
+    accepts, attention.cpp:42-63) run on the one-thread-per-row EXACT kernels
+    (exact_generic.cu) and stay bit-identical to the compiled reference."""
+    n, m, d, dv, alpha, causal, br, bc, bins = case
+    rng = np.random.default_rng(n * 3 + d)
+    cast = (lambda a: a.astype(np.float32).astype(np.float64)) if dtype == torch.float32 else (lambda a: a)
+    q = cast(rng.standard_normal((n, d)) * 1.5)
+    k = cast(rng.standard_normal((m, d)))
+    v = cast(rng.standard_normal((m, dv)))
+    do = cast(rng.standard_normal((n, dv)))
+    kw = dict(alpha=alpha, causal=causal, block_r=br, block_c=bc, bins=bins)
+    prob, res, g = run_gpu(q, k, v, do, dtype, **kw)
+    ref = Oracle("reference")
+    pb = Problem(q, k, v, **kw)
+    f = ref.forward(pb, threads=8)
+    b = ref.backward(pb, f, do, threads=8)
+    assert np.array_equal(np_(res.mask.words), f["mask"])
+    same(np_(res.row_max), f["row_max"], alpha, "row_max")
+    same(np_(res.tau), f["tau"], alpha, "tau")
+    same(np_(res.out), f["out"], alpha, "out")
+    for key in ("delta", "dq", "dk", "dv"):
+        same(np_(getattr(g, key)), b[key], alpha, key)
+    st = res.stats
+    assert st.block_sparsity == f["block_sparsity"]
+    assert st.blocks_visited_fwd == f["blocks_visited_fwd"]
+    assert st.flushes == f["flushes"]
+    assert res.stats.blocks_visited_bwd == b["blocks_visited_bwd"]
