@@ -205,6 +205,12 @@ class AttentionResult:
     _bwd_done: bool = field(repr=False, default=False)
 
     @property
+    def path(self) -> str:
+        """The kernels that ran: "tc" (bf16 tcgen05) or "exact" (fp64 SIMT) --
+        AUTO sends bf16 inputs outside the tensor-core envelope to "exact"."""
+        return "tc" if resolved_path(self._problem) == _lib.PATH_TC else "exact"
+
+    @property
     def stats(self) -> AttentionStats:
         """Lazily computed (one popcount kernel + a stream sync) on first access."""
         if self._stats is None:

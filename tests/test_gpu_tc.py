@@ -180,8 +180,12 @@ def test_tc_bins(bins):
     out_err = (rt.out - rx.out).abs().max().item()
     print(bins, tau_err, out_err)
     assert tau_err <= TAU_TOL and out_err <= 2e-2
+    assert rt.path == "tc" and rx.path == "exact"
     with pytest.raises(Exception):
         run(q, k, v, None, "tc", alpha=1.5, causal=True, bins=32)
+    # AUTO sends the bf16 bins=32 problem to the exact kernels, and says so
+    _, ra, _ = run(q, k, v, None, "auto", alpha=1.5, causal=True, bins=32)
+    assert ra.path == "exact"
 
 
 @pytest.mark.parametrize("N,D,causal,beta", [(131072, 128, True, 1.0), (131072, 128, True, 0.6),
