@@ -451,7 +451,8 @@ def main():
     # per launch of each tensor-core kernel: (a) the tcgen05 MMA flops it executes
     # (roofline numerator, workloads.executed_flops) and (b) the algorithmic count of
     # SURVEY 8(d) (reference algorithm: 2+R dense passes, no hi/lo halves)
-    exe = workloads.executed_flops(res.mask.words, N, D, causal, alpha=alpha)
+    exe = workloads.executed_flops(res.mask.words, N, D, causal, alpha=alpha,
+                                   row_steps=res.row_steps)
     per_alg = {"tc_fwd": fl_rank["f_fwd"], "tc_delta": 4.0 * D * 4096 * nnz_rank,
                "tc_dq": 6.0 * D * 4096 * nnz_rank, "tc_dkdv": 8.0 * D * 4096 * nnz_rank}
     dom = max(kern, key=lambda n: kern[n]["ms_avg"] * kern[n]["launches"]) if kern else None

@@ -90,7 +90,8 @@ def flops(D: int, nnz: int, addressable: int, ref_passes: int = 3) -> dict:
     return dict(f_eff=f_eff, f_alg=f_alg, f_fwd=f_fwd)
 
 
-def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha: float = 1.5) -> dict:
+def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha: float = 1.5,
+                   row_steps=None) -> dict:
     """Tensor-core flops each kernel actually issues for one problem (all heads),
     from the 64x64 block mask ([B][H][t_r][wpr] u32) -- the numerator of the
     per-kernel roofline.  Counts every tcgen05 MMA the
@@ -98,16 +99,21 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha:
     sweeps are counted without tile skipping (exact for inputs where no tile
     is skippable, an upper bound otherwise).
 
-    tc_fwd   3 sweeps (MAX, HIST, CAND) of S over the causal 128x128 tiles of
-             each 128-row group + OUT (S and P V) over active tiles
+    tc_fwd   list mode (alpha >= 1.4, the default): 2 sweeps (MAX, CAND) of S over
+             the causal 128x128 tiles of each 128-row group; sweep mode (alpha < 1.4):
+             MAX + HIST + one REF sweep per refinement pass (the most steps of any
+             row of the 256-row CTA + 1, from row_steps; 3 if not given) -- plus OUT
+             (S and P V) over active tiles
     tc_delta S, dP over active (128 rows x 128 keys) tiles
     tc_dq    S, dP, dQ (fp16 sigma dS and K: one product -- default for alpha <= 1.5;
              bf16 hi/lo otherwise)
              over active (128 x 128) tiles
     tc_dkdv  S^T, dP^T, dV (fp16 P and dO: one product; bf16 hi/lo with
-             ADATTN_DV_F16=0 or for d != 128), dK hi/lo over active
-             (128 keys x 64 queries) units
+             ADATTN_DV_F16=0 or for d != 128), dK (fp16 sigma dS: one product, as
+             for dQ; else hi/lo) over active (128 keys x 64 queries) units
+    (A CTA whose candidate list overflows re-runs HIST + REF sweeps; not counted.)
     """
+    import os
     import torch
     w = mask_words.view(torch.int32)
     Bh = w.shape[0] * w.shape[1]
@@ -127,7 +133,21 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha:
         sweep_tiles = nr * (t_c // 2) * Bh
     act = int(g.sum())
     units = int(u.sum())
-    import os
+    list_mode = alpha >= 1.4 and int(os.environ.get("ADATTN_CAND_CAP", "512")) >= 64
+    if list_mode:
+        sweeps_fwd = 2.0 * sweep_tiles
+    else:  # per 256-row CTA: MAX, HIST, then (max steps + 1) REF sweeps over its tiles
+        if causal:
+            per_rg = (J[None, :] <= rg[:, None]).sum(dim=1).double()  # tiles of each 128-row group
+        else:
+            per_rg = torch.full((nr,), float(t_c // 2), dtype=torch.float64)
+        if row_steps is not None:
+            st = row_steps.reshape(Bh, -1).to(torch.int64).cpu()
+            passes = st.reshape(Bh, -1, 256).amax(dim=2).double() + 1.0  # [Bh, n/256]
+        else:
+            passes = torch.full((Bh, max(1, nr // 2)), 3.0, dtype=torch.float64)
+        rg_pass = passes.repeat_interleave(2, dim=1)[:, :nr]             # [Bh, nr]
+        sweeps_fwd = float(((2.0 + rg_pass) * per_rg[None, :]).sum())
     if dv_f16 is None:  # the library's default (csrc/tc_bwd.cu dv_f16_enabled, pair kernel)
         dv_f16 = (d == 128 and os.environ.get("ADATTN_DV_F16", "1") != "0"
                   and os.environ.get("ADATTN_KV_PAIRS", "1") != "0")
@@ -135,7 +155,7 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha:
     ds_f16 = d == 128 and (ds_env == "1" or (ds_env not in ("0", "1") and alpha <= 1.5))
     kv_pairs = os.environ.get("ADATTN_KV_PAIRS", "1") != "0"
     dq_pairs = os.environ.get("ADATTN_DQ_PAIRS", "1") != "0"
-    return {"tc_fwd": (3 * sweep_tiles + 2 * act) * tile,
+    return {"tc_fwd": (sweeps_fwd + 2 * act) * tile,
             "tc_delta": 2 * act * tile,
             "tc_dq": (3 if ds_f16 and dq_pairs else 4) * act * tile,
             "tc_dkdv": (4 + (0 if dv_f16 else 1) + (0 if ds_f16 and kv_pairs else 1))
