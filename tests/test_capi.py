@@ -59,8 +59,14 @@ def test_valid_and_envelope():
     assert lib.adattn_b200_validate(C.byref(prob(bins=32))) == 0  # 128-bit words
     assert lib.adattn_b200_validate(C.byref(prob(bins=2))) == 0
     assert lib.adattn_b200_resolved_path(C.byref(prob())) == _lib.PATH_EXACT
-    # exact path envelope: d <= 128, tiles <= 64
-    assert lib.adattn_b200_validate(C.byref(prob(d=256))) == _lib.ADATTN_ERR_UNSUPPORTED
-    assert lib.adattn_b200_validate(C.byref(prob(block_r=128))) == _lib.ADATTN_ERR_UNSUPPORTED
+    # every problem the reference accepts has a GPU path: wide and large-tile
+    # problems resolve to the exact kernels (exact_generic.cu)
+    assert lib.adattn_b200_validate(C.byref(prob(d=256))) == 0
+    assert lib.adattn_b200_validate(C.byref(prob(block_r=128))) == 0
+    assert lib.adattn_b200_resolved_path(C.byref(prob(d=256, in_dtype=_lib.BF16))) == _lib.PATH_EXACT
+    # the tensor-core path takes bf16 at d = dv in {64, 128} for any n, m
+    assert lib.adattn_b200_resolved_path(C.byref(prob(d=128, dv=128, n=100, m=100,
+                                                      block_r=64, block_c=64,
+                                                      in_dtype=_lib.BF16))) == _lib.PATH_TC
     # fp32 inputs never take the tensor-core path
     assert lib.adattn_b200_validate(C.byref(prob(path=_lib.PATH_TC))) == _lib.ADATTN_ERR_UNSUPPORTED
