@@ -185,13 +185,13 @@ size_t forward_workspace(const Geom& g) {
 
 // Envelope of the tensor-core kernels: bf16 inputs, 64x64
 // reference tiles, d == dv in {64, 128}, a positive scale (the kernels rank raw
-// scores), bins <= 16.  Any n, m: ragged sizes run padded (capi.cu).
+// scores), bins <= 32.  Any n, m: ragged sizes run padded (capi.cu).
 bool tc_supported(const Geom& g) {
   return g.in_dtype == ADATTN_BF16 && g.block_r == 64 && g.block_c == 64 && g.d == g.dv &&
-         (g.d == 64 || g.d == 128) && g.scale > 0.0 && g.bins <= 16 && g.bins >= 2;
+         (g.d == 64 || g.d == 128) && g.scale > 0.0 && g.bins <= 32 && g.bins >= 2;
 }
 std::string tc_envelope() {
-  return "bf16 inputs, block_r=block_c=64, d=dv in {64,128}, scale>0, 2<=bins<=16";
+  return "bf16 inputs, block_r=block_c=64, d=dv in {64,128}, scale>0, 2<=bins<=32";
 }
 size_t tc_forward_workspace(const Geom& g) { return tc::forward_workspace(g); }
 size_t tc_backward_workspace(const Geom& g) { return tc::backward_workspace(g); }

@@ -364,7 +364,10 @@ __device__ __forceinline__ void hist_sweep(int jl, float2 Aw, float2 Bw, float2 
   drain();
 }
 
-template <int D, int AK, bool PAIR>
+// NB32: bins = 32 (the reference's 128-bit histogram words, attention.cpp:35) -- a
+// separate instantiation, so the 4-word HIST counters' registers do not weigh on
+// the default kernels
+template <int D, int AK, bool PAIR, bool NB32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_v,
@@ -1021,60 +1024,87 @@ __global__ void __launch_bounds__(kThreads, 1)
     rs.lo = rs.hi = 0.0;
     rs.steps = 0;
     rs.done = true;
-    auto solve_counts = [&](const uint32_t* cnt, int kmin) {
-      if (half == 1) {
+    // half 0: the row's solver state from its full counts c32 (solve_histogram +
+    // refine_bracket, histogram.cpp:73-165)
+    auto solve_c32 = [&](const uint32_t* c32) {
+      double th, lo, hi;
+      solve_histogram_dev(c32, nb, g.alpha, th, lo, hi);
+      if (g.tau_h_out) g.tau_h_out[(size_t)bh * g.n + grow] = th;
+      rs.tau = th;
+      rs.lo = lo;
+      rs.hi = hi;
+      rs.f = rs.f1 = rs.f2 = rs.f_hi = 0.0;
+      rs.sec_tau = rs.sec_f = rs.best_tau = 0.0;
+      rs.best_af = CUDART_INF;
+      rs.steps = 0;
+      rs.sec_seeded = false;
+      rs.done = false;
+      sRow[e * 4 + 2] = (float)(B - rs.tau);
+      sRow[e * 4 + 3] = (float)(B - rs.hi);
+    };
+    // the two key halves' HIST counts (cnt[16] per thread, nb <= 16 or the low /
+    // high 16 bins of nb = 32), combined through row_cnt, then solved by half 0
+    auto solve_counts = [&](const uint32_t* cnt, const uint32_t* cnt_hi) {
+      uint32_t c32[32];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) row_cnt[k] = cnt[k];
-      }
-      bar_sync(bar_rg, 256);
-      if (half == 0) {
-        uint32_t c32[32];
+      for (int k = 0; k < 32; ++k) c32[k] = 0u;
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          c32[k] = (k < nb && k >= kmin) ? cnt[k & 15] + row_cnt[k & 15] : 0u;
-        double th, lo, hi;
-        solve_histogram_dev(c32, nb, g.alpha, th, lo, hi);
-        if (g.tau_h_out) g.tau_h_out[(size_t)bh * g.n + grow] = th;
-        rs.tau = th;
-        rs.lo = lo;
-        rs.hi = hi;
-        rs.f = rs.f1 = rs.f2 = rs.f_hi = 0.0;
-        rs.sec_tau = rs.sec_f = rs.best_tau = 0.0;
-        rs.best_af = CUDART_INF;
-        rs.steps = 0;
-        rs.sec_seeded = false;
-        rs.done = false;
-        sRow[e * 4 + 2] = (float)(B - rs.tau);
-        sRow[e * 4 + 3] = (float)(B - rs.hi);
+      for (int part = 0; part < 2; ++part) {
+        const uint32_t* c = part ? cnt_hi : cnt;
+        if (!c) break;
+        if (half == 1) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) row_cnt[k] = c[k];
+        }
+        bar_sync(bar_rg, 256);
+        if (half == 0) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (16 * part + k < nb) c32[16 * part + k] = c[k] + row_cnt[k];
+        }
+        bar_sync(bar_rg, 256);
       }
+      if (half == 0) solve_c32(c32);
     };
 
     // ---- pass HIST (attention.cpp:201-232): counts of min(floor(B z), B-1), z >= 0
     auto hist_solve = [&]() {
-    uint32_t cnt[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) cnt[k] = 0;
-    {
       const float cw = 1.0f - 0x1p-20f;  // keeps z = 1 (the row max) inside bin nb-1
       const float2 Aw = make_float2(A1 * (float)nb * cw, A1 * (float)nb * cw);
       const float bw = (float)((B + 1.0) * (double)nb * (double)cw);
       const float2 Bw = make_float2(bw, bw);
       const float kf = -(0x1p-124f + (float)nb * 0x1p-147f);  // -(2^23 + nb) 2^-147, exact
       const float2 K = make_float2(kf, kf);
-      if (nb <= 8)
-        hist_sweep<1>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
-                      [&](int J, uint32_t* hE, uint32_t* hO) {
-          tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
-        });
-      else
-        hist_sweep<2>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
-                      [&](int J, uint32_t* hE, uint32_t* hO) {
-          tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<2>(v, Aw, Bw, K, hE, hO); });
-        });
-    }
-    PASS_MARK(1);
-    solve_counts(cnt, 0);
-    phase_tick(pacc, 1, pt);
+      if (nb <= 16) {
+        uint32_t cnt[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) cnt[k] = 0;
+        if (nb <= 8)
+          hist_sweep<1>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
+                        [&](int J, uint32_t* hE, uint32_t* hO) {
+            tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
+          });
+        else
+          hist_sweep<2>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
+                        [&](int J, uint32_t* hE, uint32_t* hO) {
+            tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<2>(v, Aw, Bw, K, hE, hO); });
+          });
+        PASS_MARK(1);
+        solve_counts(cnt, nullptr);
+      } else {
+        if constexpr (NB32) {  // bins = 32: four nibble words
+          uint32_t cnt[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) cnt[k] = 0;
+          hist_sweep<4>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
+                        [&](int J, uint32_t* hE, uint32_t* hO) {
+            tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<4>(v, Aw, Bw, K, hE, hO); });
+          });
+          PASS_MARK(1);
+          solve_counts(cnt, cnt + 16);
+        }
+      }
+      phase_tick(pacc, 1, pt);
     };
 
     const bool need_sec = g.alpha > 2.0;
@@ -1209,10 +1239,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* sl = reinterpret_cast<float*>(sRing);
         constexpr int lcap = NST * L::TILE / (kEpi * 4);
         const int ns = cnt < lcap ? cnt : lcap;
-        // the histogram of the listed scores (list mode), read in the same pass
-        uint32_t hc[16];
+        // the histogram of the listed scores (list mode), read in the same pass:
+        // both halves of a row add into its 32 packed 16-bit counters in row_cnt
+        // (a row lists <= 2 x 512 scores)
+        if (half == 0) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) hc[k] = 0u;
+          for (int k = 0; k < 16; ++k) row_cnt[k] = 0u;
+        }
+        bar_sync(bar_rg, 256);
         for (int i0 = 0; i0 < cnt; i0 += 8) {
           uint32_t tmp[8];
 #pragma unroll
@@ -1223,13 +1257,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float z = fmaf(A1, __uint_as_float(tmp[j]), Bf);
             if (z >= 0.f) {
               const int k = min((int)((float)nb * z), nb - 1);
-#pragma unroll
-              for (int q = 0; q < 16; ++q) hc[q] += q == k ? 1u : 0u;
+              atomicAdd(&row_cnt[k >> 1], 1u << (16 * (k & 1)));
             }
           }
         }
         if (list_mode) {
-          solve_counts(hc, half == 0 ? k_s : 0);
+          bar_sync(bar_rg, 256);
+          if (half == 0) {  // bins >= k_s are complete in the lists
+            uint32_t c32[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              c32[k] = (k < nb && k >= k_s) ? (row_cnt[k >> 1] >> (16 * (k & 1))) & 0xFFFFu : 0u;
+            solve_c32(c32);
+          }
           // sPart (refinement partials) aliases the count rows of the OTHER row
           // group (sCnt): both groups finish reading counts before any writes them
           bar_sync(3, kEpi);
@@ -1533,6 +1573,9 @@ cudaError_t launch_fwd(const Geom& g, const CUtensorMap& tq, const CUtensorMap& 
                        const FwdArgs& a, cudaStream_t st) {
   const size_t smem = FwdSmem<D>::bytes(g.wpr, g.m / BN);
   auto kern = tc_fwd_kernel<D, AK, PAIR>;
+  if constexpr (!PAIR) {
+    if (g.bins > 16) kern = tc_fwd_kernel<D, AK, false, true>;
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e) return e;
   const dim3 grid((unsigned)(a.ncta_rows * g.bh));
@@ -1573,7 +1616,7 @@ cudaError_t launch_fwd_d(const Geom& g, int ak, const CUtensorMap& tq, const CUt
 
 // CTA pairs for the forward (ADATTN_FWD_PAIRS=0/1 overrides the default)
 bool use_fwd_pairs(const Geom& g) {
-  if (g.d != 128 || g.dv != 128 || (g.n / BM) % 2 != 0) return false;
+  if (g.d != 128 || g.dv != 128 || (g.n / BM) % 2 != 0 || g.bins > 16) return false;
   const char* s = std::getenv("ADATTN_FWD_PAIRS");
   if (s && *s) return s[0] != '0';
   // With two MMA-issuing warps the single-CTA forward is the faster one at C3

@@ -67,6 +67,8 @@ CASES = [
     ("n4k-d64-a1.5-nc", 4096, 64, False, 1.5, "gauss", None),
     ("n4k-d64-a2-b0.8", 4096, 64, True, 2.0, "anchored", 0.8),
 ]
+# histogram widths other than 8 at the C2 head (bins, alpha)
+BINS = [(32, 1.5), (32, 1.25), (4, 2.0), (16, 1.5)]
 
 TAU_TOL = 1e-5
 TAU_EXC_TOL = 1e-3
@@ -286,3 +288,31 @@ def test_tc_ragged_vs_reference(case):
         assert not bad, bad
         assert res.mask.words[0, h].cpu().numpy().view(np.uint32)[:, -1].max() >> ((t_c - 1) % 32 + 1) == 0 \
             if t_c % 32 else True
+
+
+@pytest.mark.parametrize("bins,alpha", BINS, ids=[f"bins{b}-a{a}" for b, a in BINS])
+def test_tc_bins_vs_reference(bins, alpha):
+    """bins other than 8 (32 = the reference's 128-bit counters, attention.cpp:35)
+    on the tensor-core kernels against the compiled reference at the C2 head."""
+    N, D = 8192, 128
+    q, k, v, do = workloads.gaussian(1, 1, N, D, seed=77 + bins, device=DEV)
+    prob = pa.AttentionProblem(q, k, v, alpha=alpha, causal=True, bins=bins)
+    assert pa.attention.resolved_path(prob.c_problem()) == _lib.PATH_TC
+    res = pa.forward(prob)
+    g = pa.backward(prob, res, do)
+    torch.cuda.synchronize()
+    Q, K, Vv, DO = (to_np(x) for x in (q, k, v, do))
+    pb = Problem(Q, K, Vv, alpha=alpha, causal=True, bins=bins)
+    ref = Oracle("reference")
+    f = ref.forward(pb, THREADS)
+    b = ref.backward(pb, f, DO, THREADS)
+    errs = {"tau": float(np.abs(to_np(res.tau) - f["tau"]).max()),
+            "out": float(np.abs(to_np(res.out) - f["out"]).max())}
+    for key in ("delta", "dq", "dk", "dv"):
+        errs[key] = float(np.abs(to_np(getattr(g, key)) - b[key]).max())
+    nd = int((mask_bits(res.mask.words[0, 0].cpu().numpy(), N // 64) !=
+              mask_bits(f["mask"], N // 64)).sum())
+    print(bins, alpha, errs, "mask diffs", nd)
+    assert errs["tau"] <= TAU_TOL and nd == 0
+    for key in ("out", "delta", "dq", "dk", "dv"):
+        assert errs[key] <= GRAD_TOL, (key, errs)
