@@ -206,7 +206,12 @@ size_t elem_size(int dtype) { return dtype == ADATTN_BF16 ? 2 : dtype == ADATTN_
 // real problem (t_r, t_c, ceil(t_c / 32) mask words) is unchanged: the
 // padded geometry adds at most one key tile (t_c rounds up to even), which
 // never changes the word count.
-bool tc_ragged(const Geom& g) { return g.n % 256 != 0 || g.m % 128 != 0; }
+// Widths work the same way: d, dv <= 128 pad (zero columns) to one D in {64, 128};
+// zero columns add exact zeros to every dot product, the scale stays 1/sqrt(d), and
+// the extra output / gradient columns are dropped.
+bool tc_ragged(const Geom& g) {
+  return g.n % 256 != 0 || g.m % 128 != 0 || g.d != g.dv || (g.d != 64 && g.d != 128);
+}
 
 Geom padded_geom(const Geom& g) {
   Geom p = g;
@@ -215,6 +220,7 @@ Geom padded_geom(const Geom& g) {
   p.t_r = p.n / 64;
   p.t_c = p.m / 64;
   p.wpr = (p.t_c + 31) / 32;
+  p.d = p.dv = (g.d > 64 || g.dv > 64) ? 128 : 64;
   return p;
 }
 
@@ -234,19 +240,30 @@ class Scratch {
     if ((err_ = cudaMemsetAsync(p, 0, bytes ? bytes : 16, st_))) return nullptr;
     return p;
   }
-  // per-head [rows][row_bytes] blocks from a tensor with src_rows rows per head into
-  // one with dst_rows rows per head (the first `rows` rows of each head)
+  // the first `rows` rows x `width` bytes of every head: from a tensor of src_rows
+  // rows of src_pitch bytes per head into one of dst_rows rows of dst_pitch bytes
+  void copy(void* dst, size_t dst_rows, size_t dst_pitch, const void* src, size_t src_rows,
+            size_t src_pitch, size_t rows, size_t width, int heads) {
+    if (err_ || !dst || !src) return;
+    cudaMemcpy3DParms c = {};
+    c.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), src_pitch, width, src_rows);
+    c.dstPtr = make_cudaPitchedPtr(dst, dst_pitch, width, dst_rows);
+    c.extent = make_cudaExtent(width, rows, (size_t)heads);
+    c.kind = cudaMemcpyDeviceToDevice;
+    err_ = cudaMemcpy3DAsync(&c, st_);
+  }
+  // same row width on both sides
   void rows(void* dst, size_t dst_rows, const void* src, size_t src_rows, size_t rows,
             size_t row_bytes, int heads) {
-    if (err_ || !dst || !src) return;
-    err_ = cudaMemcpy2DAsync(dst, dst_rows * row_bytes, src, src_rows * row_bytes,
-                             rows * row_bytes, heads, cudaMemcpyDeviceToDevice, st_);
+    copy(dst, dst_rows, row_bytes, src, src_rows, row_bytes, rows, row_bytes, heads);
   }
-  // a padded copy of a per-head tensor (rows -> prow rows per head, zero padding)
-  void* pad(const void* src, size_t rows, size_t prow, size_t row_bytes, int heads) {
+  // a zero-padded copy of a per-head tensor (rows -> prow rows, row_bytes -> prow_bytes)
+  void* pad(const void* src, size_t rows, size_t prow, size_t row_bytes, int heads,
+            size_t prow_bytes = 0) {
     if (!src) return nullptr;
-    void* d = zeros(prow * row_bytes * heads);
-    this->rows(d, prow, src, rows, rows, row_bytes, heads);
+    if (!prow_bytes) prow_bytes = row_bytes;
+    void* d = zeros(prow * prow_bytes * heads);
+    copy(d, prow, prow_bytes, src, rows, row_bytes, rows, row_bytes, heads);
     return d;
   }
   cudaError_t error() const { return err_; }
@@ -371,10 +388,10 @@ struct BwdPadded {
             const void* dout0) {
     const size_t ei = elem_size(g.in_dtype);
     const int H = g.bh;
-    q = sc.pad(q0, g.n, gp.n, g.d * ei, H);
-    k = sc.pad(k0, g.m, gp.m, g.d * ei, H);
-    v = sc.pad(v0, g.m, gp.m, g.dv * ei, H);
-    dout = sc.pad(dout0, g.n, gp.n, g.dv * ei, H);
+    q = sc.pad(q0, g.n, gp.n, g.d * ei, H, gp.d * ei);
+    k = sc.pad(k0, g.m, gp.m, g.d * ei, H, gp.d * ei);
+    v = sc.pad(v0, g.m, gp.m, g.dv * ei, H, gp.dv * ei);
+    dout = sc.pad(dout0, g.n, gp.n, g.dv * ei, H, gp.dv * ei);
     tau = (const double*)sc.pad(tau0, g.n, gp.n, 8, H);
     rm = (const double*)sc.pad(rm0, g.n, gp.n, 8, H);
     mask = (const uint32_t*)sc.pad(mask0, g.t_r, gp.t_r, g.wpr * 4, H);
@@ -408,10 +425,10 @@ int forward_impl(const adattn_problem* p, const void* q, const void* k, const vo
       Scratch sc(st);
       const size_t ei = elem_size(g.in_dtype), eo = elem_size(g.out_dtype);
       const int H = g.bh;
-      void* qp = sc.pad(q, g.n, gp.n, g.d * ei, H);
-      void* kp = sc.pad(k, g.m, gp.m, g.d * ei, H);
-      void* vp = sc.pad(v, g.m, gp.m, g.dv * ei, H);
-      void* op = sc.zeros((size_t)H * gp.n * g.dv * eo);
+      void* qp = sc.pad(q, g.n, gp.n, g.d * ei, H, gp.d * ei);
+      void* kp = sc.pad(k, g.m, gp.m, g.d * ei, H, gp.d * ei);
+      void* vp = sc.pad(v, g.m, gp.m, g.dv * ei, H, gp.dv * ei);
+      void* op = sc.zeros((size_t)H * gp.n * gp.dv * eo);
       double* tp = (double*)sc.zeros((size_t)H * gp.n * 8);
       double* rp = (double*)sc.zeros((size_t)H * gp.n * 8);
       uint32_t* mp = (uint32_t*)sc.zeros((size_t)H * gp.t_r * gp.wpr * 4);
@@ -421,7 +438,7 @@ int forward_impl(const adattn_problem* p, const void* q, const void* k, const vo
       if ((e = sc.error())) return cuda_fail(e, "adattn_b200_forward (padding)");
       if ((e = tc_forward(gr, qp, kp, vp, op, tp, rp, mp, sp, workspace, st)))
         return cuda_fail(e, "adattn_b200_forward");
-      sc.rows(out, g.n, op, gp.n, g.n, g.dv * eo, H);
+      sc.copy(out, g.n, g.dv * eo, op, gp.n, gp.dv * eo, g.n, g.dv * eo, H);
       sc.rows(tau, g.n, tp, gp.n, g.n, 8, H);
       sc.rows(row_max, g.n, rp, gp.n, g.n, 8, H);
       sc.rows(mask, g.t_r, mp, gp.t_r, g.t_r, g.wpr * 4, H);
@@ -575,17 +592,17 @@ int adattn_b200_backward_ex(const adattn_problem* p, const void* q, const void* 
       gq.rl_col_in = nullptr;
       const size_t eo = elem_size(g.out_dtype);
       const int H = g.bh;
-      void* dqp = sc.zeros((size_t)H * gp.n * g.d * eo);
-      void* dkp = sc.zeros((size_t)H * gp.m * g.d * eo);
-      void* dvp = sc.zeros((size_t)H * gp.m * g.dv * eo);
+      void* dqp = sc.zeros((size_t)H * gp.n * gp.d * eo);
+      void* dkp = sc.zeros((size_t)H * gp.m * gp.d * eo);
+      void* dvp = sc.zeros((size_t)H * gp.m * gp.dv * eo);
       double* dlp = (double*)sc.zeros((size_t)H * gp.n * 8);
       if ((e = sc.error())) return cuda_fail(e, "adattn_b200_backward (padding)");
       if ((e = tc_backward(gq, b.q, b.k, b.v, b.tau, b.rm, b.mask, b.dout, dqp, dkp, dvp, dlp,
                            workspace, st)))
         return cuda_fail(e, "adattn_b200_backward");
-      sc.rows(dq, g.n, dqp, gp.n, g.n, g.d * eo, H);
-      sc.rows(dk, g.m, dkp, gp.m, g.m, g.d * eo, H);
-      sc.rows(dv, g.m, dvp, gp.m, g.m, g.dv * eo, H);
+      sc.copy(dq, g.n, g.d * eo, dqp, gp.n, gp.d * eo, g.n, g.d * eo, H);
+      sc.copy(dk, g.m, g.d * eo, dkp, gp.m, gp.d * eo, g.m, g.d * eo, H);
+      sc.copy(dv, g.m, g.dv * eo, dvp, gp.m, gp.dv * eo, g.m, g.dv * eo, H);
       sc.rows(delta, g.n, dlp, gp.n, g.n, 8, H);
       e = sc.error();
     }

@@ -183,15 +183,16 @@ size_t forward_workspace(const Geom& g) {
 
 }  // namespace tc
 
-// Envelope of the tensor-core kernels: bf16 inputs, 64x64
-// reference tiles, d == dv in {64, 128}, a positive scale (the kernels rank raw
-// scores), bins <= 32.  Any n, m: ragged sizes run padded (capi.cu).
+// Envelope of the tensor-core path: bf16 inputs, 64x64 reference
+// tiles, d, dv <= 128, a positive scale (the kernels rank raw scores), bins <= 32.
+// The kernels run d = dv in {64, 128} with n % 256 == 0, m % 128 == 0; other
+// sizes run on zero-padded copies (capi.cu tc_ragged).
 bool tc_supported(const Geom& g) {
-  return g.in_dtype == ADATTN_BF16 && g.block_r == 64 && g.block_c == 64 && g.d == g.dv &&
-         (g.d == 64 || g.d == 128) && g.scale > 0.0 && g.bins <= 32 && g.bins >= 2;
+  return g.in_dtype == ADATTN_BF16 && g.block_r == 64 && g.block_c == 64 && g.d <= 128 &&
+         g.dv <= 128 && g.scale > 0.0 && g.bins <= 32 && g.bins >= 2;
 }
 std::string tc_envelope() {
-  return "bf16 inputs, block_r=block_c=64, d=dv in {64,128}, scale>0, 2<=bins<=32";
+  return "bf16 inputs, block_r=block_c=64, d, dv <= 128, scale>0, 2<=bins<=32";
 }
 size_t tc_forward_workspace(const Geom& g) { return tc::forward_workspace(g); }
 size_t tc_backward_workspace(const Geom& g) { return tc::backward_workspace(g); }

@@ -230,7 +230,7 @@ def test_tc_vs_reference(case):
 # ragged shapes (n % 256 != 0, m % 128 != 0): the tensor-core path runs them on
 # zero-padded copies with the padding keys masked (capi.cu tc_ragged)
 RAGGED = [
-    # (id, n, m, D, causal, alpha)
+    # (id, n, m, D, causal, alpha[, DV])  -- also widths other than d = dv in {64, 128}
     ("r100-d64-c", 100, 100, 64, True, 1.5),
     ("r300-a2-c", 300, 300, 128, True, 2.0),
     ("r1000-a125-c", 1000, 1000, 128, True, 1.25),
@@ -238,15 +238,20 @@ RAGGED = [
     ("r1500x700-nc", 1500, 700, 128, False, 1.5),
     ("r200x1000-a2-nc-d64", 200, 1000, 64, False, 2.0),
     ("r333x129-a175-nc", 333, 129, 128, False, 1.75),
+    ("w1024-d96-c", 1024, 1024, 96, True, 1.5),
+    ("w700-d32-a2-c", 700, 700, 32, True, 2.0),
+    ("w512x640-d80-dv128-nc", 512, 640, 80, False, 1.5, 128),
+    ("w2048-d128-dv64-c", 2048, 2048, 128, True, 1.5, 64),
 ]
 
 
 @pytest.mark.parametrize("case", RAGGED, ids=[c[0] for c in RAGGED])
 def test_tc_ragged_vs_reference(case):
-    name, n, m, D, causal, alpha = case
+    name, n, m, D, causal, alpha = case[:6]
+    DV = case[6] if len(case) > 6 else D
     g = torch.Generator(device="cpu").manual_seed(n * 7 + m)
-    mk = lambda rows: torch.randn(1, 2, rows, D, generator=g).to(torch.bfloat16).to(DEV)
-    q, k, v, do = mk(n), mk(m), mk(m), mk(n)
+    mk = lambda rows, w: torch.randn(1, 2, rows, w, generator=g).to(torch.bfloat16).to(DEV)
+    q, k, v, do = mk(n, D), mk(m, D), mk(m, DV), mk(n, DV)
     prob = pa.AttentionProblem(q, k, v, alpha=alpha, causal=causal)
     assert pa.attention.resolved_path(prob.c_problem()) == _lib.PATH_TC
     res = pa.forward(prob)
