@@ -458,10 +458,17 @@ def main():
     dom = max(kern, key=lambda n: kern[n]["ms_avg"] * kern[n]["launches"]) if kern else None
     roofline = None
     for n in kern:
-        if n in exe:
+        if n in exe and exe[n] > 0:
             kern[n]["tflops_executed"] = exe[n] / (kern[n]["ms_avg"] * 1e-3) / 1e12
             kern[n]["frac_executed"] = kern[n]["tflops_executed"] / peak_tf
             kern[n]["tflops_alg"] = per_alg[n] / (kern[n]["ms_avg"] * 1e-3) / 1e12
+        elif n == "tc_delta" and n in exe:
+            # delta fold: delta = dO . Ubar / sum u, one HBM-bound pass per row -- reads
+            # dO (bf16), Ubar (fp32), sum u, tau, m; writes delta (fp64), rowc (2 x fp32)
+            b = hc * N * (2 * D + 4 * D + 4 + 8 + 8 + 8 + 8)
+            kern[n]["hbm_bytes"] = b
+            kern[n]["gbps"] = b / (kern[n]["ms_avg"] * 1e-3) / 1e9
+            kern[n]["frac_hbm"] = kern[n]["gbps"] / peak_bw
     if dom in exe:
         ach = kern[dom]["tflops_executed"]
         roofline = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak_tf,

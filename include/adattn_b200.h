@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ADATTN_B200_ABI_VERSION 1
+#define ADATTN_B200_ABI_VERSION 2
 
 enum {
   ADATTN_OK = 0,
@@ -141,7 +141,17 @@ typedef struct {
    * their transpose) to skip zero tiles (attention.cpp:334-352, 462-535). */
   int32_t* block_cnt;
   uint16_t* block_cols;
+  /* DEVICE float [B][H][n][dv] then float [B][H][n] (optional; size from
+   * adattn_b200_delta_aux_bytes, NULL or 0 bytes: not filled): the output pass's
+   * Ubar_i = sum_j u_ij v_j and sum_j u_ij, u = p^(2 - alpha).  Passed to
+   * adattn_b200_backward_ex, it replaces the delta pre-pass (two products per
+   * active tile, attention.cpp:411-446) by delta_i = dO_i . Ubar_i / sum_j u_ij. */
+  float* delta_aux;
 } adattn_forward_extras;
+
+/* Bytes of adattn_forward_extras.delta_aux the forward fills for this problem
+ * (tensor-core path, single-CTA forward, no padded dimension), else 0. */
+size_t adattn_b200_delta_aux_bytes(const adattn_problem* p);
 
 int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k,
                            const void* v, void* out, double* tau, double* row_max,
@@ -161,10 +171,12 @@ int adattn_b200_backward(const adattn_problem* p, const void* q, const void* k,
 
 /* backward with the forward's nonzero-block lists (adattn_forward_extras
  * block_cnt / block_cols; NULL extras or lists: built from `mask`, as
- * adattn_b200_backward does). */
+ * adattn_b200_backward does) and its delta_aux (NULL: the delta pre-pass). */
 typedef struct {
   const int32_t* block_cnt;
   const uint16_t* block_cols;
+  /* the forward's delta_aux (adattn_forward_extras), or NULL: delta pre-pass */
+  const float* delta_aux;
 } adattn_backward_extras;
 
 int adattn_b200_backward_ex(const adattn_problem* p, const void* q, const void* k,

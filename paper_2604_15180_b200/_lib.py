@@ -34,7 +34,7 @@ EXPORTS = (
     "adattn_b200_tensor_save", "adattn_b200_tensor_load", "adattn_b200_io_last_error",
     "adattn_b200_attn_inputs", "adattn_b200_xoshiro", "adattn_b200_entmax_rows",
     "adattn_b200_block_lists", "adattn_b200_forward_timed", "adattn_b200_forward_ex",
-    "adattn_b200_backward_ex",
+    "adattn_b200_backward_ex", "adattn_b200_delta_aux_bytes",
 )
 
 
@@ -52,11 +52,13 @@ class Problem(C.Structure):
 
 class ForwardExtras(C.Structure):
     _fields_ = [("phase_ms", C.POINTER(C.c_double)), ("tau_h", C.c_void_p),
-                ("block_cnt", C.c_void_p), ("block_cols", C.c_void_p)]
+                ("block_cnt", C.c_void_p), ("block_cols", C.c_void_p),
+                ("delta_aux", C.c_void_p)]
 
 
 class BackwardExtras(C.Structure):
-    _fields_ = [("block_cnt", C.c_void_p), ("block_cols", C.c_void_p)]
+    _fields_ = [("block_cnt", C.c_void_p), ("block_cols", C.c_void_p),
+                ("delta_aux", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -104,6 +106,8 @@ def load() -> C.CDLL:
         lib.adattn_b200_forward_workspace.restype = C.c_size_t
         lib.adattn_b200_backward_workspace.argtypes = [P]
         lib.adattn_b200_backward_workspace.restype = C.c_size_t
+        lib.adattn_b200_delta_aux_bytes.argtypes = [P]
+        lib.adattn_b200_delta_aux_bytes.restype = C.c_size_t
         lib.adattn_b200_forward.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
         lib.adattn_b200_forward_timed.argtypes = [P, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                                   C.c_size_t, vp, C.POINTER(C.c_double)]
@@ -138,7 +142,7 @@ def load() -> C.CDLL:
         lib.adattn_b200_xoshiro.restype = None
         lib.adattn_b200_entmax_rows.argtypes = [C.POINTER(RowsProblem), vp, vp, vp, vp, vp, vp,
                                                 vp, vp, vp]
-        if lib.adattn_b200_abi_version() != 1:
+        if lib.adattn_b200_abi_version() != 2:
             raise RuntimeError("libadattn_b200.so ABI mismatch")
         _lib = lib
         return lib

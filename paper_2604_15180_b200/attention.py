@@ -200,6 +200,10 @@ class AttentionResult:
     mask: PackedBlockMask
     row_steps: torch.Tensor
     lists: Optional[NonzeroBlockLists] = None
+    # the output pass's sum_j u_ij v_j and sum_j u_ij (float32, flat: [B*H*n*dv] then
+    # [B*H*n]) when the forward folded the delta accumulation; the
+    # backward then forms delta = dO . Ubar / sum u instead of a delta pre-pass
+    delta_aux: Optional[torch.Tensor] = field(repr=False, default=None)
     _problem: _lib.Problem = field(repr=False, default=None)
     _stats: Optional[AttentionStats] = field(repr=False, default=None)
     _bwd_done: bool = field(repr=False, default=False)
@@ -293,14 +297,17 @@ def forward(p: AttentionProblem, threads: int = 1, timings: Optional[PhaseTiming
             raise ValueError("forward: tau_h must be float64 shaped like tau")
         _check_device(tau_h)
     ph = (C.c_double * 4)()
+    aux_bytes = lib.adattn_b200_delta_aux_bytes(C.byref(pb))
+    aux = torch.empty(aux_bytes // 4, dtype=torch.float32, device=dev) if aux_bytes else None
     ex = _lib.ForwardExtras(ph if timed else None, _ptr(tau_h),
                             _ptr(lists.cnt) if lists else None,
-                            _ptr(lists.cols) if lists else None)
+                            _ptr(lists.cols) if lists else None, _ptr(aux))
     _lib.check(lib.adattn_b200_forward_ex(*args, C.byref(ex)))
     if timed:
         for i in range(4):
             timings.ms[i] += ph[i]
-    return AttentionResult(out, tau, row_max, PackedBlockMask(words, t_r, t_c), steps, lists, pb)
+    return AttentionResult(out, tau, row_max, PackedBlockMask(words, t_r, t_c), steps, lists,
+                           aux, pb)
 
 
 def _grad_problem(p: AttentionProblem, res: AttentionResult, dout: torch.Tensor) -> _lib.Problem:
@@ -344,7 +351,7 @@ def backward(p: AttentionProblem, res: AttentionResult, dout: torch.Tensor,
     ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=p.q.device)
     lists = res.lists
     ex = _lib.BackwardExtras(_ptr(lists.cnt) if lists else None,
-                             _ptr(lists.cols) if lists else None)
+                             _ptr(lists.cols) if lists else None, _ptr(res.delta_aux))
     _lib.check(lib.adattn_b200_backward_ex(
         C.byref(pb), _ptr(p.q), _ptr(p.k), _ptr(p.v), _ptr(res.tau), _ptr(res.row_max),
         _ptr(res.mask.words), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(delta), _ptr(ws),

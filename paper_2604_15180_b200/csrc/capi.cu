@@ -401,7 +401,8 @@ struct BwdPadded {
 int forward_impl(const adattn_problem* p, const void* q, const void* k, const void* v,
                  void* out, double* tau, double* row_max, uint32_t* mask, int32_t* row_steps,
                  void* workspace, size_t workspace_bytes, void* stream,
-                 unsigned long long* phase_ns, double* tau_h, int32_t* lcnt, uint16_t* lcol) {
+                 unsigned long long* phase_ns, double* tau_h, int32_t* lcnt, uint16_t* lcol,
+                 float* ubar = nullptr) {
   Geom g;
   int rc = check(p, &g);
   if (rc) return rc;
@@ -420,6 +421,7 @@ int forward_impl(const adattn_problem* p, const void* q, const void* k, const vo
     if (workspace_bytes < tc_forward_workspace(gp))
       return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_forward: workspace too small");
     if (!tc_ragged(g)) {
+      g.ubar_out = ubar;  // (delta fold: unpadded problems only)
       e = tc_forward(g, q, k, v, out, tau, row_max, mask, row_steps, workspace, st);
     } else {
       Scratch sc(st);
@@ -470,10 +472,20 @@ int adattn_b200_forward_timed(const adattn_problem* p, const void* q, const void
                               const void* v, void* out, double* tau, double* row_max,
                               uint32_t* mask, int32_t* row_steps, void* workspace,
                               size_t workspace_bytes, void* stream, double* phase_ms) {
-  adattn_forward_extras ex{phase_ms, nullptr, nullptr, nullptr};
+  adattn_forward_extras ex{phase_ms, nullptr, nullptr, nullptr, nullptr};
   if (!phase_ms) return fail(ADATTN_ERR_INVALID, "adattn_b200_forward_timed: null phase_ms");
   return adattn_b200_forward_ex(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
                                 workspace_bytes, stream, &ex);
+}
+
+size_t adattn_b200_delta_aux_bytes(const adattn_problem* p) {
+  Geom g;
+  if (!p || check(p, &g)) return 0;
+  if (resolve(p, g) != ADATTN_PATH_TC || tc_ragged(g)) return 0;
+  float dummy = 0.f;
+  g.ubar_out = &dummy;
+  if (!tc_delta_fold(g)) return 0;
+  return (size_t)g.bh * g.n * (g.dv + 1) * sizeof(float);
 }
 
 int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k,
@@ -484,9 +496,10 @@ int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k
   double* const phase_ms = ex ? ex->phase_ms : nullptr;
   int32_t* const lcnt = ex ? ex->block_cnt : nullptr;
   uint16_t* const lcol = ex ? ex->block_cols : nullptr;
+  float* const ubar = ex && adattn_b200_delta_aux_bytes(p) ? ex->delta_aux : nullptr;
   if (!phase_ms)
     return forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
-                        workspace_bytes, stream, nullptr, tau_h, lcnt, lcol);
+                        workspace_bytes, stream, nullptr, tau_h, lcnt, lcol, ubar);
   cudaStream_t st = (cudaStream_t)stream;
   unsigned long long* acc = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -497,7 +510,7 @@ int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k
   if (!e) e = cudaEventRecord(e0, st);
   if (e) return cuda_fail(e, "adattn_b200_forward_ex");
   int rc = forward_impl(p, q, k, v, out, tau, row_max, mask, row_steps, workspace,
-                        workspace_bytes, stream, acc, tau_h, lcnt, lcol);
+                        workspace_bytes, stream, acc, tau_h, lcnt, lcol, ubar);
   unsigned long long ns[4] = {0, 0, 0, 0};
   float total = 0.f;
   e = cudaEventRecord(e1, st);
@@ -583,6 +596,7 @@ int adattn_b200_backward_ex(const adattn_problem* p, const void* q, const void* 
     if (workspace_bytes < tc_backward_workspace(gp))
       return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_backward: workspace too small");
     if (!tc_ragged(g)) {
+      if (ex && ex->delta_aux && adattn_b200_delta_aux_bytes(p)) g.ubar_in = ex->delta_aux;
       e = tc_backward(g, q, k, v, tau, row_max, mask, dout, dq, dk, dv, delta, workspace, st);
     } else {
       Scratch sc(st);
@@ -803,6 +817,11 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
   const size_t wsf = adattn_b200_forward_workspace(&sp);
   const size_t wsb = adattn_b200_backward_workspace(&sp);
   void* ws = c.get(7, std::max(wsf, wsb));
+  // delta fold: the chunk's forward leaves sum u v and sum u for its backward
+  const size_t aux_bytes = dout ? adattn_b200_delta_aux_bytes(&sp) : 0;
+  float* aux = aux_bytes ? (float*)c.get(13, aux_bytes) : nullptr;
+  if (aux_bytes && !aux)
+    return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: device allocation failed");
   if (!dQ || !dK || !dV || !dO || !dTau || !dRm || !dMask || !ws)
     return fail(ADATTN_ERR_CUDA, "adattn_b200_run_host: device allocation failed");
   cudaStream_t sin = c.streams[0], sc = c.streams[1], sout = c.streams[2];
@@ -825,9 +844,10 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
       cudaEventRecord(c.do_ready[i], sin);
     }
     cudaStreamWaitEvent(sc, c.in_ready[i], 0);
-    rc = adattn_b200_forward(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv), mb(dO, h * co),
-                             dTau + h * crow, dRm + h * crow, dMask + h * cmw, nullptr, ws,
-                             std::max(wsf, wsb), sc);
+    adattn_forward_extras fx{nullptr, nullptr, nullptr, nullptr, aux};
+    rc = adattn_b200_forward_ex(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv),
+                                mb(dO, h * co), dTau + h * crow, dRm + h * crow, dMask + h * cmw,
+                                nullptr, ws, std::max(wsf, wsb), sc, &fx);
     if (rc) return rc;
     // the forward's outputs go back while the chunk's backward runs
     cudaEventRecord(c.fwd_done[i], sc);
@@ -841,10 +861,12 @@ int adattn_b200_run_host(const adattn_problem* p, const void* q, const void* k, 
       cudaMemcpyAsync(mask + h * cmw, dMask + h * cmw, hn * cmw * 4, cudaMemcpyDeviceToHost, sout);
     if (dout) {
       cudaStreamWaitEvent(sc, c.do_ready[i], 0);
-      rc = adattn_b200_backward(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv),
-                                dTau + h * crow, dRm + h * crow, dMask + h * cmw,
-                                mb(dDO, h * cdo), mb(dDQ, h * cgq), mb(dDK, h * cgk),
-                                mb(dDV, h * cgv), dDl + h * crow, ws, std::max(wsf, wsb), sc);
+      adattn_backward_extras bx{nullptr, nullptr, aux};
+      rc = adattn_b200_backward_ex(&sp, mb(dQ, h * cq), mb(dK, h * ck), mb(dV, h * cv),
+                                   dTau + h * crow, dRm + h * crow, dMask + h * cmw,
+                                   mb(dDO, h * cdo), mb(dDQ, h * cgq), mb(dDK, h * cgk),
+                                   mb(dDV, h * cgv), dDl + h * crow, ws, std::max(wsf, wsb), sc,
+                                   &bx);
       if (rc) return rc;
     }
     cudaEventRecord(c.done[i], sc);

@@ -40,6 +40,12 @@ struct Geom {
   uint16_t* rl_col_out = nullptr;
   const int32_t* rl_cnt_in = nullptr;
   const uint16_t* rl_col_in = nullptr;
+  // delta fold (tensor-core path): the forward writes Ubar_i = sum_j u_ij v_j
+  // ([bh][n][dv] fp32) then sum_j u_ij ([bh][n] fp32) to ubar_out; the backward
+  // reads them from ubar_in and forms delta_i = dO_i . Ubar_i / sum_j u_ij
+  // (attention.cpp:411-446) instead of running the delta kernel
+  float* ubar_out = nullptr;
+  const float* ubar_in = nullptr;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {

@@ -196,6 +196,7 @@ std::string tc_envelope() {
 }
 size_t tc_forward_workspace(const Geom& g) { return tc::forward_workspace(g); }
 size_t tc_backward_workspace(const Geom& g) { return tc::backward_workspace(g); }
+bool tc_delta_fold(const Geom& g) { return tc::fwd_delta_fold(g); }
 
 cudaError_t tc_forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                        double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,

@@ -65,6 +65,7 @@ struct BwdArgs {
   const uint16_t* crow;
   double* delta;
   float2* rowc;  // [bh*n] {C, delta}
+  const void* dout;  // bf16 [bh*n][dv] (delta from the forward's fold)
   // fp16 operand plan of the pair dQ and dK/dV kernels (device; nullptr: bf16 hi/lo)
   const struct F16Plan* f16;
   void* dq;
@@ -1836,6 +1837,42 @@ __global__ void f16_plan_kernel(F16Plan* plans, const uint32_t* mx, int bh, floa
   pl->inv_sigma = 1.f / sigma;
 }
 
+
+// delta from the forward's fold (Geom::ubar_in): delta_i = dO_i . Ubar_i / sum_j u_ij
+// (0 when the sum is 0, attention.cpp:444), one warp per row; also rowc_i = (C_i, delta_i)
+// for the dK/dV kernel, C_i = 1 - (alpha - 1) m_i - tau_i as the delta kernels form it
+template <int D>
+__global__ void delta_ubar_kernel(const uint16_t* __restrict__ dout, const float* __restrict__ ubar,
+                                  const double* __restrict__ tau, const double* __restrict__ row_max,
+                                  double alpha, size_t rows, double* delta, float2* rowc) {
+  constexpr int E = D / 32;
+  const size_t r = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const uint16_t* dp = dout + r * D + lane * E;
+  const float* up = ubar + r * D + lane * E;
+  float acc = 0.f;
+  if constexpr (E == 4) {
+    const uint2 w = *reinterpret_cast<const uint2*>(dp);
+    const float4 u = *reinterpret_cast<const float4*>(up);
+    acc = __uint_as_float(w.x << 16) * u.x + __uint_as_float(w.x & 0xFFFF0000u) * u.y +
+          __uint_as_float(w.y << 16) * u.z + __uint_as_float(w.y & 0xFFFF0000u) * u.w;
+  } else {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(dp);
+    const float2 u = *reinterpret_cast<const float2*>(up);
+    acc = __uint_as_float(w << 16) * u.x + __uint_as_float(w & 0xFFFF0000u) * u.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    const double su = (double)ubar[rows * D + r];
+    const double dlt = su > 0.0 ? (double)acc / su : 0.0;
+    const double B = 1.0 - (alpha - 1.0) * row_max[r];
+    delta[r] = dlt;
+    rowc[r] = make_float2((float)(B - tau[r]), (float)dlt);
+  }
+}
+
 constexpr int kKvThreads = 352;  // pair dK/dV: 8 epilogue warps, producer, 2 MMA issuers
 
 template <int D>
@@ -2188,7 +2225,16 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
                     cudaStream_t st) {
   cudaError_t e;
   const int dmode = delta_mode(g, a.ncta_rows);
-  if (dmode == 2) {
+  if (g.ubar_in && !delta_only) {  // delta from the forward's fold
+    const size_t rows = (size_t)g.bh * g.n;
+    prof_begin("tc_delta", st);
+    delta_ubar_kernel<D><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(a.dout), g.ubar_in, a.tau, a.row_max, g.alpha, rows,
+        a.delta, a.rowc);
+    prof_end(st);
+    note_launch();
+    if ((e = cudaGetLastError())) return e;
+  } else if (dmode == 2) {
     auto k0 = tc_delta3_kernel<128, AK>;
     const size_t sm = Delta3Smem<128>::bytes(g.wpr);
     if ((e = set_smem(k0, sm))) return e;
@@ -2348,6 +2394,7 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   }
   a.delta = delta;
   a.rowc = reinterpret_cast<float2*>(workspace);
+  a.dout = dout;
   a.f16 = nullptr;
   m[14] = m[7];
   m[15] = m[1];

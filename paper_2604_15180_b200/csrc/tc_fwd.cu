@@ -68,6 +68,10 @@ constexpr int kWarpProd = kEpiWarps, kWarpMma = kEpiWarps + 1;
 constexpr int kThreads = (kEpiWarps + (kDualMma ? 3 : 2)) * 32;
 constexpr int DEC_REF = 0, DEC_OUT = 1;
 constexpr int kTop = 8;  // list mode: largest per-tile maxima kept per thread in the MAX sweep
+// output pass: all 16 epilogue warps write each row group's P in turn (0: 8 warps per group)
+#ifndef ADATTN_OUT_ALL16
+#define ADATTN_OUT_ALL16 1
+#endif
 
 enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 
@@ -77,7 +81,7 @@ enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 // waits on ring-empty, [4] epilogue warp 4 waits on S-full, [6] MMA-warp cycles,
 // [7] ring items.
 #ifdef ADATTN_PIPE_STATS
-__device__ unsigned long long g_pipe_stats[48];
+__device__ unsigned long long g_pipe_stats[64];
 __device__ int g_cur_sweep_dummy;
 #endif
 #ifdef ADATTN_PIPE_TRACE
@@ -123,7 +127,17 @@ namespace {
     atomicAdd(&g_pipe_stats[8 + (k)], (unsigned long long)(_n - _pm));                \
     _pm = _n;                                                                         \
   }
+// list-phase sub-marks (thread 0): [48+k] cycles before mark k since the previous one
+#define LIST_MARK(k)                                                                  \
+  if (tid == 0) {                                                                     \
+    const long long _n = clock64();                                                   \
+    atomicAdd(&g_pipe_stats[48 + (k)], (unsigned long long)(_n - _pm));               \
+    _pm = _n;                                                                         \
+  }
 #else
+#define LIST_MARK(k) \
+  do {               \
+  } while (0)
 #define PASS_MARK(k) \
   do {               \
   } while (0)
@@ -153,6 +167,8 @@ struct FwdArgs {
   int cand_slots;
   // fp16 P V: per head, max |V| (float bits) of the scaled fp16 V copy; nullptr -> bf16 P
   const uint32_t* v16_max;
+  // optional output (delta fold): Ubar [bh][n][dv] fp32, then sum u [bh][n] fp32
+  float* ubar;
   // optional output: per row block its active key blocks (ELL, ascending; ell_bytes layout)
   int32_t* rcnt;
   uint16_t* rcol;
@@ -396,6 +412,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dec_bar = q_full + 1;
   uint64_t* plan_bar = dec_bar + 1;  // activity set published (phase 0: HIST, 1: CAND)
   uint64_t* xbar = plan_bar + 1;     // [2] pair exchanges (the peer arrives)
+  // delta-fold output pass: S full [2], P+U full [2], O / Ubar full, O / Ubar read
+  uint64_t* fs_full = xbar + 2;
+  uint64_t* fp_full = fs_full + 2;
+  uint64_t* fo_full = fp_full + 2;
+  uint64_t* fo_empty = fo_full + 1;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
   volatile uint32_t* s_tmem = misc;  // TMEM base
   volatile uint32_t* s_decision = misc + 1;
@@ -436,6 +457,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // O = P V in fp16 (P in [0, 1], the head's V copied to fp16 scaled by a power of
   // two s, undone on O) unless the head's V holds a non-finite value
   const bool pvf16 = a.v16_max != nullptr && f16_copy_ok(a.v16_max[bh]);
+  // delta fold in the output pass (single-CTA kernel; the C-ABI passes ubar only then)
+  bool fold = false;
+  if constexpr (!PAIR) fold = a.ubar != nullptr;
   const float oinv = pvf16 ? 1.f / f16_pow2_scale(a.v16_max[bh]) : 1.f;
   const int nkt = g.m / BN;                              // 128-key tiles
   const int Jmax = g.causal ? (lim0 + BM - 1) / BN : nkt - 1;
@@ -456,14 +480,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], kArr);
     }
-    mbar_init(&p_full[0], kArr);
-    mbar_init(&p_full[1], kArr);
+    // output pass: all 16 epilogue warps (both CTAs: 32) write each row group's P
+    mbar_init(&p_full[0], ADATTN_OUT_ALL16 ? 2 * kArr : kArr);
+    mbar_init(&p_full[1], ADATTN_OUT_ALL16 ? 2 * kArr : kArr);
     mbar_init(o_full, kDualMma ? 2 : 1);
     mbar_init(q_full, 1);
     mbar_init(dec_bar, 1);
     mbar_init(plan_bar, 1);
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
+    if constexpr (!PAIR) {
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&fs_full[i], 1);
+        mbar_init(&fp_full[i], kEpiWarps);
+      }
+      mbar_init(fo_full, 1);
+      mbar_init(fo_empty, kEpiWarps);
+    }
     fence_barrier_init();
   }
   for (int i = tid; i < 2 * nkt_; i += kThreads) sTmax[i] = 0u;  // < every encoded float
@@ -586,8 +619,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         MBAR_WAIT(dec_bar, (dround + ref) & 1);
         if (*s_decision == DEC_OUT) break;
       }
+    if (fold) {  // output pass, one row group at a time: K(item i), then V(item i - 1)
+      int prevf = -1;
+      for (int g2 = 0; g2 < 2; ++g2)
+        for (uint32_t t = 0, nt_ = *s_ntiles; t < nt_; ++t) {
+          const int J = sTiles[t];
+          if (!out_active(g2, J)) continue;
+          load(false, J);
+          if (prevf >= 0) load(true, prevf);
+          prevf = J;
+        }
+      if (prevf >= 0) load(true, prevf);
+    }
     int prev = -1;
-    for (uint32_t t = 0, nt_ = *s_ntiles; t < nt_; ++t) {
+    for (uint32_t t = 0, nt_ = fold ? 0u : *s_ntiles; t < nt_; ++t) {
       const int J = sTiles[t];
       load(false, J);
       if (prev >= 0) load(true, prev);
@@ -744,6 +789,74 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (*s_decision == DEC_OUT) break;
       }
     sweep_mark(3);  // REF sweeps (fallback) + waiting for the decision
+    if (fold) {
+      // Output pass with the delta fold: one row group at a time;
+      // per active tile (item i) S(i) into buffer i & 1, then -- once the
+      // epilogue has written P(i-1) and U(i-1) over buffer (i-1) & 1 --
+      // O += P V and Ubar += U V.  TMEM: S buffers at 0 / 128, O at 256, Ubar at
+      // 384.  Warp kWarpMma issues everything in order (S(i+1) before the
+      // products of item i, so the epilogue of i+1 overlaps them); the other
+      // MMA warp only releases ring slots.
+      const uint64_t dVf = desc_mnmajor(ring_addr, BN * 128);
+      if (warp != kWarpMma) {
+        for (int g2 = 0; g2 < 2; ++g2)
+          for (uint32_t t = 0, nt_ = *s_ntiles; t < nt_; ++t) {
+            if (!out_active(g2, sTiles[t])) continue;
+            for (int x = 0; x < 2; ++x) {  // K(i), V(i): one release each
+              const uint32_t st = wait_ring();
+              if (elect_one_sync()) mbar_arrive(&empty[st]);
+              __syncwarp();
+              ++r;
+            }
+          }
+      } else {
+        uint32_t fi = 0;        // items issued
+        int pg = -1;            // group of item fi - 1 (-1: none yet)
+        bool p_first = false;   // item fi - 1 is the first of its group
+        bool g0_any = false;    // row group 0 has items (its O / Ubar must be read first)
+        // the products of item fi - 1 (V(item) in ring slot vst)
+        auto products = [&](uint32_t vst, bool last_of_group) {
+          const uint32_t pb = (fi - 1) & 1;
+          MBAR_WAIT(&fp_full[pb], ((fi - 1) >> 1) & 1);
+          // group 1's first products overwrite the accumulators group 0's O / Ubar
+          // were read from
+          if (p_first && pg == 1 && g0_any) MBAR_WAIT(fo_empty, 0);
+          tc_fence_after();
+          const uint64_t bv = dVf + (uint64_t)((vst * ITEM) >> 4);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            // keys 16k..16k+15: P at pb*128 + 32*(k>>1) + 8*(k&1), U 16 columns on
+            const uint32_t acol = pb * 128 + 32 * (k >> 1) + 8 * (k & 1);
+            const uint32_t acc = (!p_first || k > 0) ? 1u : 0u;
+            if (leader) umma_bf16_ts(tmem + 256, tmem + acol, bv + (uint64_t)(128 * k), IDESC_PV, acc);
+            if (leader) umma_bf16_ts(tmem + 384, tmem + acol + 16, bv + (uint64_t)(128 * k), IDESC_PV, acc);
+          }
+          if (last_of_group) commit(fo_full);
+          commit(&empty[vst]);
+          ++r;
+        };
+        for (int g2 = 0; g2 < 2; ++g2) {
+          bool first = true;
+          for (uint32_t t = 0, nt_ = *s_ntiles; t < nt_; ++t) {
+            const int J = sTiles[t];
+            if (!out_active(g2, J)) continue;
+            const uint32_t kst = wait_ring();  // K(J)
+            issue_s(tmem + (fi & 1) * 128, g2, kst);
+            commit(&fs_full[fi & 1]);
+            commit(&empty[kst]);
+            ++r;
+            ++nt;
+            if (pg >= 0) products(wait_ring(), pg != g2);  // V(item fi - 1)
+            if (g2 == 0) g0_any = true;
+            p_first = first;
+            first = false;
+            pg = g2;
+            ++fi;
+          }
+        }
+        if (pg >= 0) products(wait_ring(), true);
+      }
+    } else {
     // output pass: S[g] at g*128 (buffer 0 of each group), O[g] at 256 + g*128.
     // Per active tile J, per group g: PV_g(prev) then S_g(J) -- in tensor-pipe
     // order, so S_g(J) overwrites P_g(prev) only after PV_g(prev) has read it,
@@ -762,9 +875,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t bv = dVmn + (uint64_t)((vst * ITEM) >> 4);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        // keys 16k..16k+15: packed P pairs at TMEM cols rg*128 + 64*(k>>2) + 8*(k&3);
+        // keys 16k..16k+15: packed P pairs at TMEM cols rg*128 + 32*(k>>1) + 8*(k&1)
+        // (each 32-key chunk's P over the first half of its own S columns);
         // a 16-key step of the MN-major V operand is 2048 B = +128
-        const uint32_t acol = rg * 128 + 64 * (k >> 2) + 8 * (k & 3);
+        const uint32_t acol = rg * 128 + 32 * (k >> 1) + 8 * (k & 1);
         const uint32_t acc = (o_init[rg] || k > 0) ? 1u : 0u;
         if constexpr (PAIR) {
           if (leader) umma2_bf16_ts(tmem + 256 + rg * D, tmem + acol, bv + (uint64_t)(128 * k), IDESC_PV, acc);
@@ -821,6 +935,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++r;
     }
     commit(o_full);
+    }  // !fold
     sweep_mark(4);
 #ifdef ADATTN_PIPE_STATS
     if (leader) {
@@ -1230,6 +1345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       PASS_MARK(2);
       bool ovf_any = bar_red_or(4, kEpi, ovf);
+      LIST_MARK(0);  // all warps done with CAND
       if constexpr (PAIR) ovf_any = pair_or(ovf_any);  // both CTAs take the same path
       if (!ovf_any) {
         // The K ring is idle until the decision (producer and MMA warps wait on
@@ -1261,6 +1377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        LIST_MARK(1);  // staging + histogram
         if (list_mode) {
           bar_sync(bar_rg, 256);
           if (half == 0) {  // bins >= k_s are complete in the lists
@@ -1275,6 +1392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           bar_sync(3, kEpi);
           phase_tick(pacc, 1, pt);
         }
+        LIST_MARK(2);  // histogram solve
         // refinement rounds on the lists (same RowSolve / row_step as the sweeps)
         for (;;) {
           bar_sync(bar_rg, 256);  // C / Chi published
@@ -1339,7 +1457,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             sRow[e * 4 + 2] = (float)(B - rs.tau);
           }
           first_pass = false;
-          if (!bar_red_or(4, kEpi, stepped)) break;
+          const bool more = bar_red_or(4, kEpi, stepped);
+          LIST_MARK(3);  // refinement rounds
+          if (!more) break;
         }
         // mask at the final tau: block active iff any z > tau - 1e-9 (attention.cpp:254-266)
         for (int i = tid; i < 4 * wpr; i += kEpi) smask[i] = 0u;
@@ -1359,6 +1479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();  // generic writes to the ring before its next TMA loads
         list_ok = true;
         phase_tick(pacc, 2, pt);
+        LIST_MARK(4);  // mask
       }
       PASS_MARK(3);
       bar_sync(3, kEpi);
@@ -1371,6 +1492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         *s_decision = list_ok ? DEC_OUT : DEC_REF;
         mbar_arrive(dec_bar);
       }
+      LIST_MARK(5);  // tile list + decision
       dround = 1;
       if (!list_ok) hist_solve();  // fallback: the exact histogram by the HIST sweep
     }
@@ -1442,25 +1564,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     PASS_MARK(4);
     if (!list_ok) phase_tick(pacc, 2, pt);
     // ---- pass OUT (attention.cpp:334-352): P over the active blocks, O = P V
+#if ADATTN_OUT_ALL16
     {
-      const float C = sRow[e * 4 + 2];
-      const float2 A2 = make_float2(A1, A1), C2 = make_float2(C, C);
-      bool any_out = false;
-      uint32_t ob = (it + 1) >> 1;  // previous uses of S buffer 0 of this group
-      for (uint32_t t = 0, nt_ = *s_ntiles; t < nt_; ++t) {
-        const int J = sTiles[t];
-        if (!out_active(rg, J)) continue;
-        any_out = true;
-        // pairs: a tile active for the peer's rows only gets P = 0 without reading S
-        const bool own = !PAIR || out_active_m(smask, rg, J);
-        MBAR_WAIT(&s_full[rg], ob & 1);  // output-pass S lives in buffer 0
-        ++ob;
-        tc_fence_after();
+      // All 16 epilogue warps work on each row group's tile in turn (warp w: TMEM
+      // lane quarter w % 4, keys 32 (w / 4) .. +31 of the tile), so a group's P is
+      // ready in half the time one group's 8 warps need: with a single S buffer per
+      // group in this pass, that turnaround is what the other group's MMAs must cover.
+      // P of a 32-key chunk goes over the first 16 of the chunk's own S columns.
+      const int qq = ew >> 2;  // 32-key chunk of the tile
+      if ((ew & 7) == 0 && lane == 0) misc[4 + rg] = it;
+      bar_sync(3, kEpi);
+      uint32_t ob[2], gC[2];
+      int gklim[2];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+      for (int g2 = 0; g2 < 2; ++g2) {
+        ob[g2] = (misc[4 + g2] + 1) >> 1;  // previous uses of S buffer 0 of group g2
+        const int eg = g2 * 128 + lq * 32 + lane;
+        gC[g2] = __float_as_uint(sRow[eg * 4 + 2]);
+        const int gr = row0 + eg;
+        gklim[g2] = g.causal ? min(gr, g.m_valid - 1) : g.m_valid - 1;
+      }
+      bool any_out = false;  // for the O write: tiles of this thread's own group rg
+      const uint32_t tq = tmem + ((uint32_t)(lq * 32) << 16) + 32 * qq;
+      for (uint32_t t = 0, nt_ = fold ? 0u : *s_ntiles; t < nt_; ++t) {
+        const int J = sTiles[t];
+#pragma unroll
+        for (int g2 = 0; g2 < 2; ++g2) {
+          if (!out_active(g2, J)) continue;
+          if (g2 == rg) any_out = true;
+          // pairs: a tile active for the peer's rows only gets P = 0 without reading S
+          const bool own = !PAIR || out_active_m(smask, g2, J);
+          MBAR_WAIT(&s_full[g2], ob[g2] & 1);  // output-pass S lives in buffer 0
+          ++ob[g2];
+          tc_fence_after();
           uint32_t pk[16];
           if (own) {
-            load_chunk(0, J, c);
+            tmem_ld32(tq + g2 * 128, v);
+            tmem_wait_ld();
+            const int k0 = J * BN + 32 * qq;
+            if (k0 + 31 > gklim[g2]) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (k0 + i > gklim[g2]) v[i] = -CUDART_INF_F;
+            }
+            const float C = __uint_as_float(gC[g2]);
+            const float2 A2 = make_float2(A1, A1), C2 = make_float2(C, C);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float2 t = __ffma2_rn(A2, make_float2(v[2 * i], v[2 * i + 1]), C2);
@@ -1482,23 +1630,184 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) pk[i] = 0u;
           }
-          // packed P of keys 64*half + 32c .. +31 -> TMEM cols 64*half + 16c .. +15
-          tmem_st16(tl + c * 16, pk);
+          tmem_st16(tq + g2 * 128, pk);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_mma(&p_full[g2]);
+        }
+      }
+#else
+    {
+      const float C = sRow[e * 4 + 2];
+      const float2 A2 = make_float2(A1, A1), C2 = make_float2(C, C);
+      bool any_out = false;
+      uint32_t ob = (it + 1) >> 1;  // previous uses of S buffer 0 of this group
+      for (uint32_t t = 0, nt_ = fold ? 0u : *s_ntiles; t < nt_; ++t) {
+        const int J = sTiles[t];
+        if (!out_active(rg, J)) continue;
+        any_out = true;
+        const bool own = !PAIR || out_active_m(smask, rg, J);
+        MBAR_WAIT(&s_full[rg], ob & 1);
+        ++ob;
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+          if (own) {
+            load_chunk(0, J, c);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float2 t = __ffma2_rn(A2, make_float2(v[2 * i], v[2 * i + 1]), C2);
+              float2 pp;
+              if constexpr (AK == AK15 || AK == AK125 || AK == AK2) {
+                const float2 tp = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
+                if constexpr (AK == AK2) {
+                  pp = tp;
+                } else {
+                  pp = __fmul2_rn(tp, tp);
+                  if constexpr (AK == AK125) pp = __fmul2_rn(pp, pp);
+                }
+              } else {
+                pp = make_float2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f));
+              }
+              pk[i] = pvf16 ? pack_f16x2(pp.x, pp.y) : pack_bf16x2(pp.x, pp.y);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          }
+          // keys 64*half + 32c .. +31 -> the first 16 of that chunk's own S columns
+          tmem_st16(tl + c * 32, pk);
         }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) arrive_mma(&p_full[rg]);
       }
+#endif
+      if (fold) {
+        // delta fold: P and U = p^(2 - alpha) of item i over the first /
+        // second 16 columns of each 32-key chunk of S buffer i & 1; the MMA warp
+        // accumulates O += P V and Ubar += U V; per row group, O, Ubar and sum u go
+        // to HBM (the backward forms delta = dO . Ubar / sum u, attention.cpp:411-446)
+        const int qq = ew >> 2;  // 32-key chunk of the tile
+        const uint32_t tq = tmem + ((uint32_t)(lq * 32) << 16) + 32 * qq;
+        float* sUs = reinterpret_cast<float*>(sCnt);  // [256][4] partial sums of u
+        uint32_t fi = 0, ndone = 0;
+        for (int g2 = 0; g2 < 2; ++g2) {
+          const int eg = g2 * 128 + lq * 32 + lane;
+          const int gr = row0 + eg;
+          const float Cg = sRow[eg * 4 + 2];
+          const int klg = g.causal ? min(gr, g.m_valid - 1) : g.m_valid - 1;
+          const float2 A2 = make_float2(A1, A1), C2 = make_float2(Cg, Cg);
+          float us = 0.f;
+          bool anyg = false;
+          for (uint32_t t = 0, nt_ = *s_ntiles; t < nt_; ++t) {
+            const int J = sTiles[t];
+            if (!out_active(g2, J)) continue;
+            anyg = true;
+            const uint32_t b = fi & 1;
+            MBAR_WAIT(&fs_full[b], (fi >> 1) & 1);
+            ++fi;
+            tc_fence_after();
+            tmem_ld32(tq + b * 128, v);
+            tmem_wait_ld();
+            const int k0 = J * BN + 32 * qq;
+            if (k0 + 31 > klg) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (k0 + i > klg) v[i] = -CUDART_INF_F;
+            }
+            float2 u2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {  // keys 16 hh .. +15: P -> cols 8 hh, U -> 16 + 8 hh
+              uint32_t pk[8], uk[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int x = 8 * hh + i;
+                const float2 t = __ffma2_rn(A2, make_float2(v[2 * x], v[2 * x + 1]), C2);
+                const float2 tp = make_float2(fmaxf(t.x, 0.f), fmaxf(t.y, 0.f));
+                float2 pp, uu;
+                if constexpr (AK == AK15) {
+                  uu = tp;
+                  pp = __fmul2_rn(tp, tp);
+                } else if constexpr (AK == AK2) {
+                  pp = tp;
+                  uu = make_float2(__saturatef(tp.x * 0x1p126f), __saturatef(tp.y * 0x1p126f));
+                } else if constexpr (AK == AK125) {
+                  const float2 t2 = __fmul2_rn(tp, tp);
+                  uu = __fmul2_rn(t2, tp);
+                  pp = __fmul2_rn(t2, t2);  // (t^2)^2 like the P of the other output passes
+                } else {
+                  uu.x = tp.x > 0.f ? exp2f(a.e1f * __log2f(tp.x)) : 0.f;
+                  uu.y = tp.y > 0.f ? exp2f(a.e1f * __log2f(tp.y)) : 0.f;
+                  pp = make_float2(p_of<AK>(t.x, a.e0f), p_of<AK>(t.y, a.e0f));
+                }
+                u2 = __fadd2_rn(u2, uu);
+                pk[i] = pvf16 ? pack_f16x2(pp.x, pp.y) : pack_bf16x2(pp.x, pp.y);
+                uk[i] = pvf16 ? pack_f16x2(uu.x, uu.y) : pack_bf16x2(uu.x, uu.y);
+              }
+              tmem_st8(tq + b * 128 + 8 * hh, pk);
+              tmem_st8(tq + b * 128 + 16 + 8 * hh, uk);
+            }
+            us += u2.x + u2.y;
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&fp_full[b]);
+          }
+          // O and Ubar of this row group: lane quarter lq, columns 32 qq .. +31
+          const bool rd = 32 * qq < D;
+          const size_t orow_g = (size_t)bh * g.n + gr;
+          if (anyg) {
+            MBAR_WAIT(fo_full, ndone & 1);
+            ++ndone;
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int which = 0; which < 2; ++which) {  // 0: O, 1: Ubar
+            float o[32];
+            if (anyg && rd) {
+              tmem_ld32(tmem + ((uint32_t)(lq * 32) << 16) + 256 + 128 * which + 32 * qq, o);
+              tmem_wait_ld();
+            }
+            if (which == 1 && anyg) {  // both read: group 1's products may overwrite them
+              tc_fence_before();
+              __syncwarp();
+              if (g2 == 0 && lane == 0) mbar_arrive(fo_empty);
+            }
+            if (!rd) continue;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = anyg ? o[i] * oinv : 0.f;
+            if (which == 0 && g.out_dtype == ADATTN_F64) {
+              double* dst = reinterpret_cast<double*>(a.out) + orow_g * D + 32 * qq;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) dst[i] = (double)o[i];
+            } else {
+              float* base = which == 0 ? reinterpret_cast<float*>(a.out) : a.ubar;
+              float4* dst = reinterpret_cast<float4*>(base + orow_g * D + 32 * qq);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+            }
+          }
+          sUs[eg * 4 + qq] = us;
+        }
+        bar_sync(3, kEpi);
+        if (tid < BM) {
+          const float* su = sUs + tid * 4;
+          a.ubar[(size_t)g.bh * g.n * D + (size_t)bh * g.n + row0 + tid] = (su[0] + su[1]) + (su[2] + su[3]);
+        }
+      }
       // write O (fp32 or fp64): this thread's half of the row's dv columns
       const size_t orow = (size_t)bh * g.n + grow;
-      MBAR_WAIT(o_full, 0);
+      if (!fold) MBAR_WAIT(o_full, 0);
       PASS_MARK(5);
       tc_fence_after();
       const bool written = __any_sync(0xffffffffu, any_out);
       const uint32_t to = tmem + ((uint32_t)(lq * 32) << 16) + 256 + rg * D + half * (D / 2);
 #pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
+      for (int c = 0; c < (fold ? 0 : D / 64); ++c) {
         float o[32];
         tmem_ld32(to + c * 32, o);
         tmem_wait_ld();
@@ -1626,6 +1935,20 @@ bool use_fwd_pairs(const Geom& g) {
 
 }  // namespace
 
+// The output pass folds the delta accumulation (single-CTA kernel only).  U goes
+// through the tensor cores as fp16, so Ubar carries u's 2^-11 relative rounding:
+// exact for alpha = 2 (u in {0, 1}), but at alpha = 1.5 delta moves by ~5e-3 on
+// rows with small supports (a coherent per-row shift of dS), which exceeds the
+// gradient bar on peaked inputs -- so the fold is on by default for alpha = 2 only
+// (ADATTN_DELTA_FOLD=1 forces it on, 0 off).
+bool fwd_delta_fold(const Geom& g) {
+  if (!g.ubar_out || g.d != g.dv) return false;
+  if (g.d == 128 && use_fwd_pairs(g)) return false;
+  const char* s = std::getenv("ADATTN_DELTA_FOLD");
+  if (s && *s) return *s != '0';
+  return g.alpha == 2.0;
+}
+
 int alpha_kind(double alpha) {
   if (alpha == 1.5) return AK15;
   if (alpha == 2.0) return AK2;
@@ -1655,6 +1978,7 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.row_max = row_max;
   a.mask = mask;
   a.steps = steps;
+  a.ubar = fwd_delta_fold(g) ? g.ubar_out : nullptr;
   a.rcnt = g.rl_cnt_out;
   a.rcol = g.rl_col_out;
   const CandPlan cp = cand_plan(g);
@@ -1694,9 +2018,9 @@ extern "C" unsigned adattn_b200_trace_read(unsigned long long* out, int reset) {
 #endif
 #ifdef ADATTN_PIPE_STATS
 extern "C" void adattn_b200_pipe_stats(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, adattn_b200::tc::g_pipe_stats, sizeof(unsigned long long) * 48);
+  cudaMemcpyFromSymbol(out, adattn_b200::tc::g_pipe_stats, sizeof(unsigned long long) * 64);
   if (reset) {
-    unsigned long long z[48] = {};
+    unsigned long long z[64] = {};
     cudaMemcpyToSymbol(adattn_b200::tc::g_pipe_stats, z, sizeof z);
   }
 }

@@ -41,6 +41,8 @@ CandPlan cand_plan(const Geom& g);
 size_t forward_workspace(const Geom& g);
 size_t forward_cand_bytes(const Geom& g);
 bool pv_f16_enabled();
+// the forward fills g.ubar_out (delta fold) for this geometry
+bool fwd_delta_fold(const Geom& g);
 
 // Power-of-two-scaled fp16 copies of bf16 operands (tc_common.cuh f16_pow2_scale),
 // per head (`heads` consecutive blocks of `elems` values, elems % 8 == 0), so a head's

@@ -24,7 +24,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert sorted(_lib.EXPORTS) == syms
-    assert lib.adattn_b200_abi_version() == 1
+    assert lib.adattn_b200_abi_version() == 2
 
 
 def prob(**kw):

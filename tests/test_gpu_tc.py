@@ -524,3 +524,55 @@ def test_tc_ds_f16_default_rule(monkeypatch, alpha, forced):
     g1 = pa.backward(prob, res, do)
     torch.cuda.synchronize()
     assert torch.equal(g0.dq, g1.dq) and torch.equal(g0.dk, g1.dk)
+
+
+FOLD_CASES = [
+    # (B, H, N, D, alpha, causal, qscale, bins)
+    (1, 2, 2048, 128, 1.5, True, 1.0, 8),
+    (1, 2, 1024, 64, 1.5, False, 1.0, 8),
+    (1, 1, 1024, 128, 2.0, True, 1.0, 8),
+    (1, 2, 2048, 64, 2.0, False, 1.0, 8),
+    (1, 1, 2048, 128, 2.0, True, 8.0, 16),
+    (1, 1, 1024, 128, 1.25, True, 1.0, 8),
+    (1, 1, 768, 128, 1.75, False, 2.0, 16),
+    (1, 1, 1024, 128, 1.5, True, 1.0, 32),
+    (1, 1, 2048, 128, 1.5, True, 8.0, 8),   # peaked rows: tiny supports, empty row groups
+]
+
+
+@pytest.mark.parametrize("case", FOLD_CASES, ids=[str(c) for c in FOLD_CASES])
+def test_tc_delta_fold_matches_prepass(case, monkeypatch):
+    """The delta fold (the forward's output pass accumulates sum u v and sum u; the
+    backward forms delta = dO . Ubar / sum u) against the delta
+    pre-pass kernel (ADATTN_DELTA_FOLD=0): the forward's own outputs are
+    bit-identical (same P, same product order).  At alpha = 2 (u in {0, 1}, the
+    default-on case) delta and the gradients agree to fp32 summation order; at
+    other alpha the fp16 u moves delta by up to ~5e-3 (measured; off by default)."""
+    B, H, N, D, alpha, causal, qs, bins = case
+    q, k, v, do = inputs(hash(case) % 883 + 5, B, H, N, D, qs)
+    monkeypatch.setenv("ADATTN_DELTA_FOLD", "0")
+    _, r0, g0 = run(q, k, v, do, "tc", alpha=alpha, causal=causal, bins=bins)
+    assert r0.delta_aux is None
+    monkeypatch.setenv("ADATTN_DELTA_FOLD", "1")
+    _, r1, g1 = run(q, k, v, do, "tc", alpha=alpha, causal=causal, bins=bins)
+    assert r1.delta_aux is not None
+    monkeypatch.delenv("ADATTN_DELTA_FOLD")
+    _, r2, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal, bins=bins)
+    assert (r2.delta_aux is not None) == (alpha == 2.0)  # the default: alpha = 2 only
+    assert torch.equal(r0.out, r1.out) and torch.equal(r0.tau, r1.tau)
+    assert torch.equal(r0.mask.words, r1.mask.words)
+    dscale = max(1.0, g0.delta.abs().max().item())
+    derr = (g0.delta - g1.delta).abs().max().item()
+    errs = {n: (getattr(g0, n) - getattr(g1, n)).abs().max().item() for n in ("dq", "dk", "dv")}
+    print(case, f"delta {derr:.2e}", {n: f"{e:.2e}" for n, e in errs.items()})
+    assert torch.equal(g0.dv, g1.dv)  # dV does not depend on delta
+    if alpha == 2.0:  # u in {0, 1}: exact in fp16 -- the default fold is as good as the pre-pass
+        assert derr <= 1e-4 * dscale
+        for n, e in errs.items():
+            assert e <= 1e-3 * max(1.0, getattr(g0, n).abs().max().item()), (n, e)
+        _, rx, gx = run(q, k, v, do, "exact", alpha=alpha, causal=causal, bins=bins)
+        for n in ("dq", "dk", "dv"):
+            assert (getattr(g1, n) - getattr(gx, n)).abs().max().item() <= 2e-2
+        assert (g1.delta - gx.delta).abs().max().item() <= 2e-2
+    else:  # fp16 u: ~2^-11 relative per term (why the fold is off by default here)
+        assert derr <= 2e-2 * dscale

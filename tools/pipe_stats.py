@@ -18,7 +18,7 @@ q, k, v, do = (workloads.gaussian(B, H, N, 128, 1.0, seed=1) if beta is None
                else workloads.anchored(B, H, N, 128, beta, True, seed=1))
 p = pa.AttentionProblem(q, k, v, alpha=alpha, causal=True)
 r = pa.forward(p); torch.cuda.synchronize()
-buf = (C.c_ulonglong * 48)()
+buf = (C.c_ulonglong * 64)()
 fn(buf, 1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); r = pa.forward(p); e1.record(); e1.synchronize()
@@ -46,3 +46,7 @@ print("epilogue thread 0: TMEM ld32+wait cycles per load", st[46] / max(st[47], 
 if st[27]:
     print(f"candidate lists: mean {st[26] / st[27]:.1f} entries/thread, longest {st[28]}, "
           f"overflowed threads {st[29]} of {st[27]}")
+lm = ["wait all CAND", "staging+hist", "solve", "refine rounds", "mask", "tiles+decision"]
+tl = sum(st[48:54]) or 1
+print("list phase (thread 0 cycles per CTA):", "  ".join(f"{n} {st[48 + i] / max(st[27] / 512, 1):.0f}" for i, n in enumerate(lm)))
+print("raw sweep waits [32..41]:", st[32:42])
