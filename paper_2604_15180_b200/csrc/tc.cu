@@ -175,10 +175,16 @@ size_t forward_cand_bytes(const Geom& g) {
   const CandPlan p = cand_plan(g);
   return p.cap > 0 ? ((size_t)p.slots * 512 * (size_t)p.cap * 8 + 255) / 256 * 256 : 0;
 }
-size_t forward_workspace(const Geom& g) {
+// then per resident CTA slot and epilogue warp the warp's tile maxima (activity sets)
+size_t forward_wtm_offset(const Geom& g) {
   return forward_cand_bytes(g) +
          (pv_f16_enabled() ? ((size_t)g.bh * g.m * g.dv * 2 + 255) / 256 * 256 +
                                  ((size_t)g.bh * 4 + 255) / 256 * 256 : 0);
+}
+int forward_wtm_slots() { return std::max(0, nsmid_slots()); }
+size_t forward_workspace(const Geom& g) {
+  return forward_wtm_offset(g) +
+         ((size_t)forward_wtm_slots() * 16 * (size_t)(g.m / 128) * 4 + 255) / 256 * 256;
 }
 
 }  // namespace tc

@@ -114,6 +114,35 @@ __device__ __forceinline__ void units_from_lists(uint8_t* ubits, int nkb, const 
   }
 }
 
+
+// Nonzero tiles / units of a CTA, compacted once (one warp, ascending) so every role
+// walks a list instead of scanning all tile indices with mask lookups (at 99% block
+// sparsity those scans were most of the backward's time).
+template <typename P>
+__device__ __forceinline__ void compact_active(uint16_t* list, volatile uint32_t* cnt, int last,
+                                               int lane, P&& pred) {
+  uint32_t n = 0;
+  for (int b = 0; b <= last; b += 32) {
+    const int J = b + lane;
+    const bool on = J <= last && pred(J);
+    const uint32_t m = __ballot_sync(0xffffffffu, on);
+    if (on) list[n + __popc(m & ((1u << lane) - 1u))] = (uint16_t)J;
+    n += __popc(m);
+  }
+  if (lane == 0) *cnt = n;
+}
+// next(J): the first listed index >= J (-1: none); consecutive calls with increasing J
+// advance a cursor, a call with J <= the previous result starts a new walk
+struct ActiveList {
+  const uint16_t* l;
+  int n, cur;
+  __device__ __forceinline__ int next(int J) {
+    if (cur > 0 && (int)l[cur - 1] >= J) cur = 0;
+    while (cur < n && (int)l[cur] < J) ++cur;
+    return cur < n ? (int)l[cur++] : -1;
+  }
+};
+
 enum AlphaKind { AK15 = 0, AK2 = 1, AK125 = 2, AKGEN = 3 };
 
 // fp16 operands for the gradient products (decided on the device, per launch):
@@ -295,7 +324,9 @@ struct DeltaSmem {
   static constexpr int OFF_MISC = OFF_BAR + 32 * 8;
   static constexpr int OFF_RED = OFF_RING;  // [256] x 2 f64 half-1 partials (ring drained)
   static constexpr int OFF_MASK = OFF_MISC + 64;
-  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
+  __host__ __device__ static int off_list(int wpr) { return OFF_MASK + 4 * wpr * 4; }
+  // + the compacted nonzero-tile list (<= 16 wpr u16)
+  static size_t bytes(int wpr) { return 1024 + off_list(wpr) + 32 * wpr + 64; }
 };
 
 constexpr int kDeltaThreads = 512 + 64;  // 16 epilogue warps, producer, MMA issuer
@@ -358,11 +389,14 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
     return (smask[rb * wpr + ((2 * J) >> 5)] >> ((2 * J) & 31)) & 3u;
   };
   auto rg_active = [&](int rg, int J) -> bool { return (bits2(2 * rg, J) | bits2(2 * rg + 1, J)) != 0; };
-  auto next_active = [&](int J) -> int {
-    for (; J <= jmax; ++J)
-      if (rg_active(0, J) || rg_active(1, J)) return J;
-    return -1;
-  };
+  // the CTA's nonzero 128-key tiles, compacted once
+  uint16_t* sList = reinterpret_cast<uint16_t*>(smem + L::off_list(wpr));
+  volatile uint32_t* sListN = reinterpret_cast<volatile uint32_t*>(smem + L::OFF_MISC) + 2;
+  if (warp == 0)
+    compact_active(sList, sListN, jmax, lane, [&](int J) -> bool { return rg_active(0, J) || rg_active(1, J); });
+  __syncthreads();
+  ActiveList walk{sList, (int)*sListN, 0};
+  auto next_active = [&](int J) -> int { return walk.next(J); };
 
   if (warp == 16) {  // TMA producer
     const bool leader = elect_one_sync();
@@ -524,7 +558,9 @@ struct Delta2Smem {
   static constexpr int OFF_MISC = OFF_BAR + 32 * 8;
   static constexpr int OFF_RED = OFF_RING;  // [256] x 2 f64 half-1 partials (ring drained)
   static constexpr int OFF_MASK = OFF_MISC + 64;
-  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 8 * wpr * 4 + 64; }
+  __host__ __device__ static int off_list(int wpr) { return OFF_MASK + 8 * wpr * 4; }
+  // + the compacted nonzero-tile list (<= 16 wpr u16)
+  static size_t bytes(int wpr) { return 1024 + off_list(wpr) + 32 * wpr + 64; }
 };
 
 template <int D, int AK>
@@ -589,11 +625,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
   auto rg_active = [&](int rg, int J) -> bool {  // row group rg of either CTA
     return (bits2(2 * rg, J) | bits2(2 * rg + 1, J) | bits2(4 + 2 * rg, J) | bits2(5 + 2 * rg, J)) != 0;
   };
-  auto next_active = [&](int J) -> int {
-    for (; J <= jmax; ++J)
-      if (rg_active(0, J) || rg_active(1, J)) return J;
-    return -1;
-  };
+  // the CTA's nonzero 128-key tiles, compacted once
+  uint16_t* sList = reinterpret_cast<uint16_t*>(smem + L::off_list(wpr));
+  volatile uint32_t* sListN = reinterpret_cast<volatile uint32_t*>(smem + L::OFF_MISC) + 2;
+  if (warp == 0)
+    compact_active(sList, sListN, jmax, lane, [&](int J) -> bool { return rg_active(0, J) || rg_active(1, J); });
+  __syncthreads();
+  ActiveList walk{sList, (int)*sListN, 0};
+  auto next_active = [&](int J) -> int { return walk.next(J); };
 
   if (warp == 16) {  // TMA producer (both CTAs)
     const bool leader = elect_one_sync();
@@ -758,7 +797,9 @@ struct Delta3Smem {
   static constexpr int OFF_MISC = OFF_BAR + 32 * 8;
   static constexpr int OFF_RED = OFF_RING;  // [4][128] x 2 f64 partials (ring drained)
   static constexpr int OFF_MASK = OFF_MISC + 64;
-  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
+  __host__ __device__ static int off_list(int wpr) { return OFF_MASK + 4 * wpr * 4; }
+  // + the compacted nonzero-tile list (<= 16 wpr u16)
+  static size_t bytes(int wpr) { return 1024 + off_list(wpr) + 32 * wpr + 64; }
 };
 
 template <int D, int AK>
@@ -821,11 +862,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
   auto bits2 = [&](int pb, int J) -> uint32_t {
     return (smask[pb * wpr + ((2 * J) >> 5)] >> ((2 * J) & 31)) & 3u;
   };
-  auto next_active = [&](int J) -> int {
-    for (; J <= jmax; ++J)
-      if (bits2(0, J) | bits2(1, J) | bits2(2, J) | bits2(3, J)) return J;
-    return -1;
-  };
+  // the CTA's nonzero 128-key tiles, compacted once
+  uint16_t* sList = reinterpret_cast<uint16_t*>(smem + L::off_list(wpr));
+  volatile uint32_t* sListN = reinterpret_cast<volatile uint32_t*>(smem + L::OFF_MISC) + 2;
+  if (warp == 0)
+    compact_active(sList, sListN, jmax, lane, [&](int J) -> bool { return bits2(0, J) | bits2(1, J) | bits2(2, J) | bits2(3, J); });
+  __syncthreads();
+  ActiveList walk{sList, (int)*sListN, 0};
+  auto next_active = [&](int J) -> int { return walk.next(J); };
 
   if (warp == 16) {  // TMA producer (both CTAs)
     const bool leader = elect_one_sync();
@@ -981,7 +1025,9 @@ struct DqSmem {
   static constexpr int OFF_BAR = OFF_VR + NSV * TILE;
   static constexpr int OFF_MISC = OFF_BAR + 40 * 8;
   static constexpr int OFF_MASK = OFF_MISC + 64;
-  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 2 * wpr * 4 + 64; }
+  __host__ __device__ static int off_list(int wpr) { return OFF_MASK + 2 * wpr * 4; }
+  // + the compacted nonzero-tile list (<= 16 wpr u16)
+  static size_t bytes(int wpr) { return 1024 + off_list(wpr) + 32 * wpr + 64; }
 };
 
 template <int D, int AK>
@@ -1050,11 +1096,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto bits2 = [&](int rb, int J) -> uint32_t {
     return (smask[rb * wpr + ((2 * J) >> 5)] >> ((2 * J) & 31)) & 3u;
   };
-  auto next_active = [&](int J) -> int {
-    for (; J <= jmax; ++J)
-      if (bits2(0, J) | bits2(1, J)) return J;
-    return -1;
-  };
+  // the CTA's nonzero 128-key tiles, compacted once
+  uint16_t* sList = reinterpret_cast<uint16_t*>(smem + L::off_list(wpr));
+  volatile uint32_t* sListN = reinterpret_cast<volatile uint32_t*>(smem + L::OFF_MISC) + 2;
+  if (warp == 0)
+    compact_active(sList, sListN, jmax, lane, [&](int J) -> bool { return bits2(0, J) | bits2(1, J); });
+  __syncthreads();
+  ActiveList walk{sList, (int)*sListN, 0};
+  auto next_active = [&](int J) -> int { return walk.next(J); };
 
   if (warp == 8) {  // TMA producer
     const bool leader = elect_one_sync();
@@ -1256,7 +1305,9 @@ struct Dq2Smem {
   static constexpr int OFF_BAR = OFF_VS + NSV * HB;
   static constexpr int OFF_MISC = OFF_BAR + 40 * 8;
   static constexpr int OFF_MASK = OFF_MISC + 64;
-  static size_t bytes(int wpr) { return 1024 + OFF_MASK + 4 * wpr * 4 + 64; }
+  __host__ __device__ static int off_list(int wpr) { return OFF_MASK + 4 * wpr * 4; }
+  // + the compacted nonzero-tile list (<= 16 wpr u16)
+  static size_t bytes(int wpr) { return 1024 + off_list(wpr) + 32 * wpr + 64; }
 };
 
 template <int D, int AK, bool DSF16>
@@ -1334,11 +1385,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   auto bits2 = [&](int rb, int J) -> uint32_t {  // rb: 0..3 over the pair's 256 rows
     return (smask[rb * wpr + ((2 * J) >> 5)] >> ((2 * J) & 31)) & 3u;
   };
-  auto next_active = [&](int J) -> int {  // union over both CTAs' rows
-    for (; J <= jmax; ++J)
-      if (bits2(0, J) | bits2(1, J) | bits2(2, J) | bits2(3, J)) return J;
-    return -1;
-  };
+  // the CTA's nonzero 128-key tiles, compacted once (union over both CTAs' rows)
+  uint16_t* sList = reinterpret_cast<uint16_t*>(smem + L::off_list(wpr));
+  volatile uint32_t* sListN = reinterpret_cast<volatile uint32_t*>(smem + L::OFF_MISC) + 2;
+  if (warp == 0)
+    compact_active(sList, sListN, jmax, lane, [&](int J) -> bool { return bits2(0, J) | bits2(1, J) | bits2(2, J) | bits2(3, J); });
+  __syncthreads();
+  ActiveList walk{sList, (int)*sListN, 0};
+  auto next_active = [&](int J) -> int { return walk.next(J); };
 
   if (warp == 8) {  // TMA producer (both CTAs load their own halves)
     const bool leader = elect_one_sync();
@@ -1538,7 +1592,9 @@ struct KvSmem {
   static constexpr int OFF_BAR = OFF_ST + KST * STAGE;
   static constexpr int OFF_MISC = OFF_BAR + 32 * 8;
   static constexpr int OFF_UB = OFF_MISC + 64;
-  static size_t bytes(int t_r) { return 1024 + OFF_UB + t_r + 64; }
+  __host__ __device__ static int off_list(int t_r) { return OFF_UB + (t_r + 15) / 16 * 16; }
+  // + the compacted active-unit list (t_r u16)
+  static size_t bytes(int t_r) { return 1024 + off_list(t_r) + 2 * t_r + 64; }
 };
 
 template <int D, int AK>
@@ -1600,11 +1656,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto unit_bits = [&](int i) -> uint32_t { return ubits[i]; };
   (void)wpr;
   (void)j0;
-  auto next_unit = [&](int i) -> int {
-    for (; i < g.t_r; ++i)
-      if (unit_bits(i)) return i;
-    return -1;
-  };
+  // the CTA's active query units, compacted once
+  uint16_t* sList = reinterpret_cast<uint16_t*>(smem + L::off_list(g.t_r));
+  volatile uint32_t* sListN = reinterpret_cast<volatile uint32_t*>(smem + L::OFF_MISC) + 2;
+  if (warp == 0)
+    compact_active(sList, sListN, g.t_r - 1, lane, [&](int i) -> bool { return unit_bits(i) != 0; });
+  __syncthreads();
+  ActiveList walk{sList, (int)*sListN, 0};
+  auto next_unit = [&](int i) -> int { return walk.next(i); };
 
   if (warp == 8) {  // TMA producer
     {
@@ -1889,7 +1948,9 @@ struct Kv2Smem {
   static constexpr int OFF_BAR = OFF_ST + KST2 * STAGE;
   static constexpr int OFF_MISC = OFF_BAR + 40 * 8;
   static constexpr int OFF_UB = OFF_MISC + 64;
-  static size_t bytes(int t_r) { return 1024 + OFF_UB + t_r + 64; }
+  __host__ __device__ static int off_list(int t_r) { return OFF_UB + (t_r + 15) / 16 * 16; }
+  // + the compacted active-unit list (t_r u16)
+  static size_t bytes(int t_r) { return 1024 + off_list(t_r) + 2 * t_r + 64; }
 };
 
 template <int D, int AK, bool DSF16>
@@ -1961,11 +2022,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
-  auto next_unit = [&](int i) -> int {
-    for (; i < g.t_r; ++i)
-      if (ubits[i]) return i;
-    return -1;
-  };
+  // the CTA's active query units, compacted once
+  uint16_t* sList = reinterpret_cast<uint16_t*>(smem + L::off_list(g.t_r));
+  volatile uint32_t* sListN = reinterpret_cast<volatile uint32_t*>(smem + L::OFF_MISC) + 2;
+  if (warp == 0)
+    compact_active(sList, sListN, g.t_r - 1, lane, [&](int i) -> bool { return ubits[i] != 0; });
+  __syncthreads();
+  ActiveList walk{sList, (int)*sListN, 0};
+  auto next_unit = [&](int i) -> int { return walk.next(i); };
 
   if (warp == 8) {  // TMA producer (both CTAs)
     const bool leader = elect_one_sync();

@@ -169,6 +169,10 @@ struct FwdArgs {
   const uint32_t* v16_max;
   // optional output (delta fold): Ubar [bh][n][dv] fp32, then sum u [bh][n] fp32
   float* ubar;
+  // per resident CTA slot (%smid) and epilogue warp: the warp's maximum raw score of
+  // every 128-key tile (its 32 rows x its 64 keys), nkt floats; nullptr: no skipping
+  float* wtm;
+  int wtm_slots;
   // optional output: per row block its active key blocks (ELL, ascending; ell_bytes layout)
   int32_t* rcnt;
   uint16_t* rcol;
@@ -187,10 +191,10 @@ struct FwdSmem {
   static constexpr int OFF_MISC = OFF_BAR + NBAR * 8;
   static constexpr int OFF_ROW = OFF_MISC + 64;  // [256][4] f32 per-row scratch
   static constexpr int OFF_MASK = OFF_ROW + BM * 4 * 4;
-  // after the mask ([4][wpr] u32): tile maxima [2][nkt] u32 (ordered encoding),
+  // after the mask ([4][wpr] u32): per-warp activity words [2 sets][16 warps][aw] u32,
   // thresholds [4] u32, activity sets [2 sets][2 row groups][aw] u32
-  __host__ __device__ static int off_tmax(int wpr) { return OFF_MASK + 4 * wpr * 4; }
-  __host__ __device__ static int off_thr(int wpr, int nkt) { return off_tmax(wpr) + 2 * nkt * 4; }
+  __host__ __device__ static int off_wact(int wpr) { return OFF_MASK + 4 * wpr * 4; }
+  __host__ __device__ static int off_thr(int wpr, int nkt) { return off_wact(wpr) + 2 * kEpiWarps * ((nkt + 31) / 32) * 4; }
   __host__ __device__ static int off_act(int wpr, int nkt) { return off_thr(wpr, nkt) + 16; }
   // CTA pairs: union activity sets [2][2][aw], union mask [4][wpr], exchange flags [2]
   __host__ __device__ static int off_actu(int wpr, int nkt) { return off_act(wpr, nkt) + 4 * ((nkt + 31) / 32) * 4; }
@@ -426,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sRow = reinterpret_cast<float*>(smem + L::OFF_ROW);
   uint32_t* smask = reinterpret_cast<uint32_t*>(smem + L::OFF_MASK);  // [4][wpr]
   const int nkt_ = g.m / BN, aw = (nkt_ + 31) / 32;
-  uint32_t* sTmax = reinterpret_cast<uint32_t*>(smem + L::off_tmax(g.wpr));   // [2][nkt]
+  uint32_t* sWAct = reinterpret_cast<uint32_t*>(smem + L::off_wact(g.wpr));   // [2][16][aw]
   uint32_t* sThr = reinterpret_cast<uint32_t*>(smem + L::off_thr(g.wpr, nkt_));  // [2 sets][2 rg]
   uint32_t* sAct = reinterpret_cast<uint32_t*>(smem + L::off_act(g.wpr, nkt_));  // [2][2][aw]
   // pairs: the MMAs are joint, so sweeps and the output pass run over the union
@@ -499,7 +503,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_barrier_init();
   }
-  for (int i = tid; i < 2 * nkt_; i += kThreads) sTmax[i] = 0u;  // < every encoded float
   if (tid < 4) sThr[tid] = 0xFFFFFFFFu;
   if (warp == kWarpProd) {
     if constexpr (PAIR) tmem_alloc_2sm(const_cast<uint32_t*>(s_tmem), 512);
@@ -519,9 +522,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   // threshold-sweep activity: set s (0: HIST, 1: CAND / REF), row group rg, tile J
   auto act = [&](int s, int rg, int J) -> bool {  // union (pairs) -- the tiles issued
     return (sActU[(s * 2 + rg) * aw + (J >> 5)] >> (J & 31)) & 1u;
-  };
-  auto act_own = [&](int s, int rg, int J) -> bool {
-    return !PAIR || ((sAct[(s * 2 + rg) * aw + (J >> 5)] >> (J & 31)) & 1u);
   };
   auto act_any = [&](int s, int J) -> bool { return act(s, 0, J) || act(s, 1, J); };
 
@@ -956,6 +956,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int jl = rg_jlim[rg];       // tiles the MMA warp issues to this row group
     const int own_jl = own_jlim[rg];  // ... of which this CTA's rows can see (causal)
     const int bar_rg = 1 + rg;        // named barrier of this row group (256 threads)
+    uint32_t smid_e;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_e));
+    float* const wt = (a.wtm && (int)smid_e < a.wtm_slots)
+                          ? a.wtm + ((size_t)smid_e * kEpiWarps + ew) * (size_t)nkt_ : nullptr;
+    // this warp's activity for set s, tile J (publish_set)
+    auto wact = [&](int s, int J) -> bool {
+      return (sWAct[(s * kEpiWarps + ew) * aw + (J >> 5)] >> (J & 31)) & 1u;
+    };
     // S-buffer / P handshakes go to the pair leader's barriers (its MMA warp waits on them)
     auto arrive_mma = [&](uint64_t* bar) {
       if (PAIR && !lead_cta) mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
@@ -1025,7 +1033,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (own == false: a tile issued for the peer CTA's rows only -- release it unread)
     auto tau_tile = [&](int J, bool own, auto&& body) {
       const uint32_t b = it & 1;
-      if (PAIR && !own) {
+      if (!own) {  // not this warp's tile (no candidate rows; pairs: the peer's rows only)
         MBAR_WAIT(&s_full[b * 2 + rg], (it >> 1) & 1);
         ++it;
         __syncwarp();
@@ -1090,7 +1098,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mraw = fmaxf(mraw, tmx);
       tmx = warp_max(tmx);
-      if (lane == 0) atomicMax(&sTmax[rg * nkt_ + J], f2ord(tmx));
+      if (lane == 0 && wt) wt[J] = tmx;  // the warp's tile maximum (its rows x its 64 keys)
     }
     sRow[e * 4 + half] = mraw;
     bar_sync(bar_rg, 256);
@@ -1101,22 +1109,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const double B = 1.0 - (g.alpha - 1.0) * (double)m_f;  // z = A1*acc + B
     const float Bf = (float)B;
 
-    // activity set 0 (HIST): tile J of row group rg can hold a binned score
-    // (z >= 0 <=> acc >= -B/A1) only if its max reaches the group's lowest
-    // row threshold (lowered by a few ulps: a superset)
+    // activity sets: tile J matters to epilogue warp w only if w's tile maximum (its
+    // 32 rows x its 64 keys, from the MAX sweep) reaches the lowest threshold of its
+    // rows (lowered by a few ulps: a superset); set 0 (HIST): z >= 0 <=>
+    // acc >= -B/A1; set 1 (CAND / REF): z > lo - eps.  A warp skips the epilogue work
+    // of the tiles outside its set (it only releases the S buffer), and the MMAs of a
+    // row group skip the tiles outside the union of its 8 warps' sets.
     auto publish_set = [&](int s, float thr, bool arrive) {
       thr = warp_min(thr);
-      if (lane == 0) atomicMin(&sThr[s * 2 + rg], f2ord(thr));
+      for (int i = tid; i < 2 * aw; i += kEpi) sAct[s * 2 * aw + i] = 0u;
       bar_sync(3, kEpi);
-      for (int i = tid; i < 2 * aw; i += kEpi) {
-        const int r = i / aw, w = i - r * aw;
-        const uint32_t th = sThr[s * 2 + r];
-        uint32_t bits = 0;
-        for (int b = 0; b < 32; ++b) {
-          const int J = 32 * w + b;
-          if (J <= own_jlim[r] && sTmax[r * nkt_ + J] >= th) bits |= 1u << b;
+      for (int w0 = 0; w0 < aw; ++w0) {
+        const int J = 32 * w0 + lane;
+        const bool on = J <= own_jl && (!wt || wt[J] >= thr);
+        const uint32_t bits = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) {
+          sWAct[(s * kEpiWarps + ew) * aw + w0] = bits;
+          if (bits) atomicOr(&sAct[(s * 2 + rg) * aw + w0], bits);
         }
-        sAct[(s * 2 + r) * aw + w] = bits;
       }
       bar_sync(3, kEpi);
       if constexpr (PAIR) pair_or_words(sActU + s * 2 * aw, sAct + s * 2 * aw, 2 * aw);
@@ -1197,12 +1207,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (nb <= 8)
           hist_sweep<1>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
                         [&](int J, uint32_t* hE, uint32_t* hO) {
-            tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
+            tau_tile(J, wact(0, J), [&](const float* v) { hist_nib<1>(v, Aw, Bw, K, hE, hO); });
           });
         else
           hist_sweep<2>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
                         [&](int J, uint32_t* hE, uint32_t* hO) {
-            tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<2>(v, Aw, Bw, K, hE, hO); });
+            tau_tile(J, wact(0, J), [&](const float* v) { hist_nib<2>(v, Aw, Bw, K, hE, hO); });
           });
         PASS_MARK(1);
         solve_counts(cnt, nullptr);
@@ -1213,7 +1223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 32; ++k) cnt[k] = 0;
           hist_sweep<4>(jl, Aw, Bw, K, cnt, [&](int J) { return act(0, rg, J); },
                         [&](int J, uint32_t* hE, uint32_t* hO) {
-            tau_tile(J, act_own(0, rg, J), [&](const float* v) { hist_nib<4>(v, Aw, Bw, K, hE, hO); });
+            tau_tile(J, wact(0, J), [&](const float* v) { hist_nib<4>(v, Aw, Bw, K, hE, hO); });
           });
           PASS_MARK(1);
           solve_counts(cnt, cnt + 16);
@@ -1301,7 +1311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t blk = (uint32_t)(2 * J + half);
           // a tile appends <= 64 entries; warp-uniform (the append votes are warp-collective)
           ovf = __any_sync(0xffffffffu, ovf || (int)(wp - lst) > cap - 64);
-          tau_tile(J, act_own(1, rg, J), [&](const float* v) {
+          tau_tile(J, wact(1, J), [&](const float* v) {
             if (ovf) return;
             // candidates are rare (~0.3% of scores): one 3-input max + warp vote per
             // 4 scores keeps the common path at 2 FMNMX + compare + vote + branch
@@ -1507,7 +1517,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int J = 0; J <= jl; ++J) {
         if (!act(1, rg, J)) continue;
         float mx_t = -CUDART_INF_F;
-        tau_tile(J, act_own(1, rg, J), [&](const float* v) {
+        tau_tile(J, wact(1, J), [&](const float* v) {
           float s0, s1, s2, mx;
           ref_slice<AK>(v, A1, C, a.e0f, a.e1f, a.e2f, s0, s1, s2, mx);
           if (first_pass && need_sec) {
@@ -1979,6 +1989,8 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.mask = mask;
   a.steps = steps;
   a.ubar = fwd_delta_fold(g) ? g.ubar_out : nullptr;
+  a.wtm = ws ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + forward_wtm_offset(g)) : nullptr;
+  a.wtm_slots = a.wtm ? forward_wtm_slots() : 0;
   a.rcnt = g.rl_cnt_out;
   a.rcol = g.rl_col_out;
   const CandPlan cp = cand_plan(g);

@@ -40,6 +40,8 @@ struct CandPlan {
 CandPlan cand_plan(const Geom& g);
 size_t forward_workspace(const Geom& g);
 size_t forward_cand_bytes(const Geom& g);
+size_t forward_wtm_offset(const Geom& g);
+int forward_wtm_slots();
 bool pv_f16_enabled();
 // the forward fills g.ubar_out (delta fold) for this geometry
 bool fwd_delta_fold(const Geom& g);
