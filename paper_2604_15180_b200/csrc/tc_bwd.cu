@@ -2239,11 +2239,10 @@ bool use_dq_pairs(const Geom& g) {
   return env != 0 && g.d == 128 && g.dv == 128 && g.n % (2 * QB_DQ) == 0;
 }
 
-// CTA-pair delta kernel for d = 128, opt-in (ADATTN_DELTA_PAIRS=1): bit-identical but
-// not faster than the single-CTA kernel at C3 (16.8 vs 15.9 ms; the per-group S/dP
-// buffers are released only when both CTAs' epilogues have read them).
-// delta kernel: 0 single-CTA (256 rows), 1 pair (256 rows per CTA), 2 pair with
-// 128 rows per CTA and double-buffered S/dP (ADATTN_DELTA_PAIRS overrides)
+// delta kernel: 0 single-CTA (256 rows), 1 CTA pair with 256 rows per CTA (the default:
+// compensated fp32 sums, C3 11.4 ms vs 15.1 single), 2 pair with 128 rows per CTA and
+// double-buffered S/dP (12.6 ms); ADATTN_DELTA_PAIRS overrides.  (Not launched when
+// the forward folded the delta accumulation: delta_ubar_kernel instead.)
 int delta_mode(const Geom& g, int ncta_rows) {
   if (g.d != 128 || g.dv != 128 || ncta_rows % 2 != 0) return 0;
   const char* s = std::getenv("ADATTN_DELTA_PAIRS");
@@ -2251,9 +2250,12 @@ int delta_mode(const Geom& g, int ncta_rows) {
 }
 
 // fp16 gradient products in the pair kernels: dV = P^T dO (default; ADATTN_DV_F16=0:
-// bf16 hi + lo) and dQ = dS K, dK = dS^T Q with a power-of-two dS scale (opt-in,
-// ADATTN_DS_F16=1); each also falls back on the device when the data do not fit
-// fp16 (F16Plan)
+// bf16 hi + lo) and dQ = dS K, dK = dS^T Q with a power-of-two dS scale (default for
+// alpha <= 1.5, ADATTN_DS_F16=0/1 overrides); each also falls back on the device when
+// the data do not fit fp16 (F16Plan).  The d = 64 single-CTA kernels keep bf16 hi + lo:
+// fp16 copies there added per-unit TMA boxes (TMA-bound at d = 64) and, in dK/dV, a
+// stage size that no longer lets a second CTA's prologue overlap (C4: dK/dV 57.8 ->
+// 58.0 ms, dQ 29.7 -> 33.1 ms; tried in round 2)
 bool dv_f16_enabled() {
   const char* s = std::getenv("ADATTN_DV_F16");
   return !(s && *s == '0');
