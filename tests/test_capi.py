@@ -70,3 +70,26 @@ def test_valid_and_envelope():
                                                       in_dtype=_lib.BF16))) == _lib.PATH_TC
     # fp32 inputs never take the tensor-core path
     assert lib.adattn_b200_validate(C.byref(prob(path=_lib.PATH_TC))) == _lib.ADATTN_ERR_UNSUPPORTED
+
+
+def test_delta_aux_size_query():
+    """adattn_b200_delta_aux_bytes (a pure host query, no GPU): the forward folds the
+    delta accumulation (sum u V and sum u per row, [B][H][n][dv] then [B][H][n] float)
+    only on the tensor-core path of unpadded problems, by default for alpha = 2."""
+    lib = _lib.load()
+    tc = dict(batch=2, heads=3, n=512, m=512, d=128, dv=128, causal=1, block_r=64, block_c=64,
+              in_dtype=_lib.BF16, out_dtype=_lib.F32)
+    old = os.environ.pop("ADATTN_DELTA_FOLD", None)
+    try:
+        assert lib.adattn_b200_delta_aux_bytes(C.byref(prob(alpha=2.0, **tc))) == 2 * 3 * 512 * 129 * 4
+        assert lib.adattn_b200_delta_aux_bytes(C.byref(prob(alpha=1.5, **tc))) == 0
+        assert lib.adattn_b200_delta_aux_bytes(C.byref(prob(alpha=2.0, **dict(tc, n=500, m=500)))) == 0
+        assert lib.adattn_b200_delta_aux_bytes(C.byref(prob(alpha=2.0, **dict(tc, in_dtype=_lib.F32)))) == 0
+        os.environ["ADATTN_DELTA_FOLD"] = "1"
+        assert lib.adattn_b200_delta_aux_bytes(C.byref(prob(alpha=1.5, **tc))) == 2 * 3 * 512 * 129 * 4
+        os.environ["ADATTN_DELTA_FOLD"] = "0"
+        assert lib.adattn_b200_delta_aux_bytes(C.byref(prob(alpha=2.0, **tc))) == 0
+    finally:
+        os.environ.pop("ADATTN_DELTA_FOLD", None)
+        if old is not None:
+            os.environ["ADATTN_DELTA_FOLD"] = old
