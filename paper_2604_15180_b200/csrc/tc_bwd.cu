@@ -29,6 +29,10 @@ namespace tc {
 // dK/dV kernel: [0] MMA waits on Q/dO stage, [1] MMA waits on p_full, [2]
 // epilogue warp 4 waits on s_full, [3] MMA-warp cycles, [4] units
 __device__ unsigned long long g_bwd_stats[8];
+// event trace of the pair dK/dV kernel's first cluster (leader CTA): [role][unit][event]
+__device__ long long g_btrace[3][512][4];
+#define BTRACE(role, uu, ev) \
+  if (blockIdx.x == 0 && (uu) < 512) g_btrace[role][uu][ev] = clock64()
 #define BSTAT_T0() const long long _t0 = clock64()
 #define BSTAT_ADD(i, cond) \
   if (cond) atomicAdd(&g_bwd_stats[i], (unsigned long long)(clock64() - _t0))
@@ -38,6 +42,9 @@ __device__ unsigned long long g_bwd_stats[8];
   } while (0)
 #define BSTAT_ADD(i, cond) \
   do {                     \
+  } while (0)
+#define BTRACE(role, uu, ev) \
+  do {                       \
   } while (0)
 #endif
 namespace {
@@ -66,6 +73,7 @@ struct BwdArgs {
   double* delta;
   float2* rowc;  // [bh*n] {C, delta}
   const void* dout;  // bf16 [bh*n][dv] (delta from the forward's fold)
+  int skip_f16;      // pair dK/dV two-buffer kernel: skip heads the SLOT3 kernel takes
   // fp16 operand plan of the pair dQ and dK/dV kernels (device; nullptr: bf16 hi/lo)
   const struct F16Plan* f16;
   void* dq;
@@ -1953,7 +1961,15 @@ struct Kv2Smem {
   static size_t bytes(int t_r) { return 1024 + off_list(t_r) + 2 * t_r + 64; }
 };
 
-template <int D, int AK, bool DSF16>
+// SLOT3 (fp16 P and fp16 dS heads only): TMEM holds three 64-column S^T slots and one
+// dP^T slot instead of two S^T + dP^T buffers.  The epilogue reads S^T(u) and dP^T(u),
+// releases the dP^T slot at once, and writes the packed P^T and dS^T (16 columns per
+// 32-query half each) over S^T(u)'s own slot; so dP^T(u+1) needs only the epilogue's
+// loads of unit u, and S^T(u+3) the gradient products of unit u -- the S^T -> epilogue
+// -> gradients -> S^T(u+2) chain that left the two-buffer pipe ~40% idle (trace:
+// 1880 cycles per unit against 1152 of MMA work) is broken.  Heads whose fp16 plan
+// fails run in a second launch of the two-buffer kernel (skip_f16 = the other heads).
+template <int D, int AK, bool DSF16, bool SLOT3 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
     tc_dkdv2_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_qd,
                     const __grid_constant__ CUtensorMap tm_kb, const __grid_constant__ CUtensorMap tm_vb,
@@ -1980,6 +1996,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
   uint64_t* kv_full = p_full + 2;    // leader
   uint64_t* acc_full = kv_full + 1;  // each CTA
   uint64_t* grad_done = acc_full + 1;  // [2] leader: gradient MMAs of the unit in S buffer b done
+  // SLOT3: s3_full / p3_full / g3_done per S^T slot [3], dp_free (leader, 16 warps)
+  uint64_t* s3_full = grad_done + 2;
+  uint64_t* p3_full = s3_full + 3;
+  uint64_t* g3_done = p3_full + 3;
+  uint64_t* dp_free = g3_done + 3;
   volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
   uint8_t* ubits = smem + L::OFF_UB;  // [t_r]: bit 2r+kh = block (i, key tile kh of CTA r)
 
@@ -1993,6 +2014,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
   const bool f16 = pl && pl->dv_ok;
   const bool f16s = DSF16 && f16 && pl->ds_ok;  // (fp16 dS only with fp16 P: 3 epilogue variants)
   const float sig = f16s ? pl->sigma : 1.f;
+  // (uniform per cluster: both CTAs belong to head bh)
+  if constexpr (SLOT3) {
+    if (!f16s) return;
+  } else {
+    if (a.skip_f16 && f16s) return;
+  }
   const int kp = pair % npair;          // low key pairs (most query units) first
   const int pkey0 = kp * 2 * KB;
   const int key0 = pkey0 + (int)rank * KB;
@@ -2014,6 +2041,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
     mbar_init(acc_full, 1);
     mbar_init(&grad_done[0], 1);
     mbar_init(&grad_done[1], 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&s3_full[i], 1);
+      mbar_init(&p3_full[i], 16);
+      mbar_init(&g3_done[i], 1);
+    }
+    mbar_init(dp_free, 16);
     fence_barrier_init();
   }
   if (warp == 8) tmem_alloc_2sm(const_cast<uint32_t*>(s_tmem), 512);
@@ -2074,17 +2107,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
       const long long t_m0 = clock64();
 #endif
       uint32_t u = 0;
-      if (warp == 9) {
+      if (warp == 9 && SLOT3) {
+        const uint64_t dK0 = desc_kmajor(k_addr), dV0 = desc_kmajor(v_addr);
+        const uint64_t dQS0 = desc_kmajor(st_addr), dDS0 = desc_kmajor(st_addr + L::HB);
+        for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
+          const uint32_t st = u % KS, x = u % 3;
+          mbar_wait(&full[st], (u / KS) & 1);
+          mbar_wait(&g3_done[x], ((u / 3) & 1) ^ 1);  // slot x: unit u-3's gradients done
+          tc_fence_after();
+          const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
+          if (leader)
+            umma_ss_d128<2, ((KB * 128) >> 4), ((32 * 128) >> 4)>(tmem + x * 64, dK0, dQS0 + so, IDESC_S, 0u);
+          if (u > 0) mbar_wait(dp_free, (u - 1) & 1);  // unit u-1's dP^T loaded by every warp
+          tc_fence_after();
+          if (leader)
+            umma_ss_d128<2, ((KB * 128) >> 4), ((32 * 128) >> 4)>(tmem + 192, dV0, dDS0 + so, IDESC_S, 0u);
+          if (leader) umma2_commit_mc(&s3_full[x]);
+          if (leader) umma2_commit_mc(&empty[st]);
+        }
+      } else if (warp == 9) {
         const uint64_t dK0 = desc_kmajor(k_addr), dV0 = desc_kmajor(v_addr);
         const uint64_t dQS0 = desc_kmajor(st_addr), dDS0 = desc_kmajor(st_addr + L::HB);
         for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
           const uint32_t st = u % KS, b = u & 1;
+          if (leader) BTRACE(0, u, 0);
           {
             BSTAT_T0();
             mbar_wait(&full[st], (u / KS) & 1);
             BSTAT_ADD(0, leader);
           }
-          mbar_wait(&grad_done[b], ((u >> 1) & 1) ^ 1);
+          if (leader) BTRACE(0, u, 1);
+          {
+            BSTAT_T0();
+            mbar_wait(&grad_done[b], ((u >> 1) & 1) ^ 1);
+            BSTAT_ADD(7, leader);
+          }
+          if (leader) BTRACE(0, u, 2);
           tc_fence_after();
           BSTAT_T0();
           const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
@@ -2096,18 +2154,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
           if (leader) umma2_commit_mc(&s_full[b]);
           if (leader) umma2_commit_mc(&empty[st]);
           BSTAT_ADD(5, leader);
+          if (leader) BTRACE(0, u, 3);
         }
       } else {
         const uint64_t dQD = desc_mnmajor(st_addr + 2 * L::HB, QT * 128);
         const uint64_t dDD = desc_mnmajor(st_addr + 2 * L::HB + L::DB, QT * 128);
         bool init = false;
+        if constexpr (SLOT3) {
+          for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
+            const uint32_t st = u % KS, x = u % 3;
+            mbar_wait(&p3_full[x], (u / 3) & 1);
+            tc_fence_after();
+            const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              // queries 16k..16k+15: half k>>1's packed P^T at x*64 + 16(k>>1) + 8(k&1), dS^T +32
+              const uint32_t pa = x * 64 + 16 * (k >> 1) + 8 * (k & 1);
+              const uint32_t acc = (init || k > 0) ? 1u : 0u;
+              if (leader) umma2_bf16_ts(tmem + 256, tmem + pa, dDD + so + (uint64_t)(128 * k), IDESC_G16, acc);
+              if (leader)
+                umma2_bf16_ts(tmem + 256 + D, tmem + pa + 32, dQD + so + (uint64_t)(128 * k), IDESC_G16, acc);
+            }
+            init = true;
+            if (leader) umma2_commit_mc(&g3_done[x]);
+            if (leader) umma2_commit_mc(&empty[st]);
+          }
+        } else
         for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
           const uint32_t st = u % KS, b = u & 1;
+          if (leader) BTRACE(1, u, 0);
           {
             BSTAT_T0();
             mbar_wait(&p_full[b], (u >> 1) & 1);
             BSTAT_ADD(1, leader);
           }
+          if (leader) BTRACE(1, u, 1);
           tc_fence_after();
           BSTAT_T0();
           const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
@@ -2134,6 +2215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
           if (leader) umma2_commit_mc(&grad_done[b]);
           if (leader) umma2_commit_mc(&empty[st]);
           BSTAT_ADD(6, leader);
+          if (leader) BTRACE(1, u, 2);
         }
         if (leader) umma2_commit_mc(acc_full);
       }
@@ -2156,15 +2238,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
     const uint32_t p_full_c1 = mapa_shared(smem_u32(&p_full[1]), 0);
     uint32_t u = 0;
     bool any = false;
+    if constexpr (SLOT3) {
+      const uint32_t dp_free_c = mapa_shared(smem_u32(dp_free), 0);
+      for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
+        const uint32_t st = u % KS, x = u % 3;
+        const bool mine = (ubits[i] >> kbit) & 1u;
+        any |= mine;
+        mbar_wait(&s3_full[x], (u / 3) & 1);
+        mbar_wait(&rfull[st], (u / KS) & 1);
+        tc_fence_after();
+        float s[32], dp[32];
+        tmem_ld32(tl + x * 64 + half * 32, s);
+        tmem_ld32(tl + 192 + half * 32, dp);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(dp_free_c);  // dP^T slot read
+        bar_sync(1, 256);  // every warp of this CTA has read S^T(u): slot x may be overwritten
+        tc_fence_after();
+        const float2* rc = reinterpret_cast<const float2*>(sSt + st * L::STAGE + 2 * L::HB + 2 * L::DB);
+        uint32_t ph[16], pl[16], dh[16], dl[16];
+        const int q0 = i * QT + half * 32;
+        if (!mine) {
+#pragma unroll
+          for (int y = 0; y < 16; ++y) ph[y] = dh[y] = 0u;
+        } else {
+          const bool msk = g.causal && q0 < key0 + lq * 32 + 31;
+          const int lim = msk ? gkey - q0 : 0;
+          if (msk) pds_chunk<AK, true, true, true>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, lim, ph, pl, dh, dl, sig);
+          else pds_chunk<AK, false, true, true>(s, dp, rc + half * 32, A1, a.e0f, a.e1f, 0, ph, pl, dh, dl, sig);
+        }
+        tmem_st16(tl + x * 64 + half * 16, ph);
+        tmem_st16(tl + x * 64 + 32 + half * 16, dh);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&p3_full[x]), 0));
+      }
+    } else
     for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1), ++u) {
       const uint32_t st = u % KS, b = u & 1;
       const bool mine = (ubits[i] >> kbit) & 1u;
       any |= mine;
+      if (warp == 0 && lane == 0 && lead_cta) BTRACE(2, u, 0);
       {
         BSTAT_T0();
         mbar_wait(&s_full[b], (u >> 1) & 1);
         BSTAT_ADD(2, warp == 0 && lane == 0);
       }
+      if (warp == 0 && lane == 0 && lead_cta) BTRACE(2, u, 1);
       mbar_wait(&rfull[st], (u / KS) & 1);
       tc_fence_after();
       float s[32], dp[32];
@@ -2194,6 +2316,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
+      if (warp == 0 && lane == 0 && lead_cta) BTRACE(2, u, 2);
       if (lane == 0) mbar_arrive_cluster(b ? p_full_c1 : p_full_c0);
     }
     mbar_wait(acc_full, 0);
@@ -2274,6 +2397,12 @@ bool ds_f16_enabled(const Geom& g) {
   return g.alpha <= 1.5;
 }
 
+// three-slot pair dK/dV kernel for the fp16 P / dS heads (ADATTN_KV_SLOT3=0: two buffers)
+bool kv_slot3_enabled(const Geom& g) {
+  const char* s = std::getenv("ADATTN_KV_SLOT3");
+  return !(s && *s == '0') && ds_f16_enabled(g) && dv_f16_enabled();
+}
+
 // CTA-pair dK/dV kernel for d = 128 (ADATTN_KV_PAIRS=0 selects the single-CTA kernel)
 bool use_kv_pairs(const Geom& g) {
   const char* s = std::getenv("ADATTN_KV_PAIRS");
@@ -2330,12 +2459,25 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
   }
   if (delta_only) return cudaSuccess;
   if (use_kv_pairs(g)) {
+    const bool slot3 = kv_slot3_enabled(g) && a.f16;
     auto k2 = ds_f16_enabled(g) ? tc_dkdv2_kernel<128, AK, true> : tc_dkdv2_kernel<128, AK, false>;
     const size_t sm = Kv2Smem<128>::bytes(g.t_r);
     if ((e = set_smem(k2, sm))) return e;
     prof_begin("tc_dkdv", st);
-    k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kKvThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
-                                                                   m[7], m[14], m[16], a);
+    if (slot3) {  // fp16 P / dS heads, then (skip_f16) the rest with the two-buffer layout
+      auto k3 = tc_dkdv2_kernel<128, AK, true, true>;
+      if ((e = set_smem(k3, sm))) return e;
+      k3<<<dim3((unsigned)((g.m / KB) * g.bh)), kKvThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
+                                                                     m[7], m[14], m[16], a);
+      note_launch();
+      BwdArgs a2 = a;
+      a2.skip_f16 = 1;
+      k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kKvThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
+                                                                     m[7], m[14], m[16], a2);
+    } else {
+      k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kKvThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
+                                                                     m[7], m[14], m[16], a);
+    }
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
@@ -2461,6 +2603,7 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   a.delta = delta;
   a.rowc = reinterpret_cast<float2*>(workspace);
   a.dout = dout;
+  a.skip_f16 = 0;
   a.f16 = nullptr;
   m[14] = m[7];
   m[15] = m[1];
@@ -2523,6 +2666,9 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
 }  // namespace adattn_b200
 
 #ifdef ADATTN_PIPE_STATS
+extern "C" void adattn_b200_bwd_trace(long long* out) {
+  cudaMemcpyFromSymbol(out, adattn_b200::tc::g_btrace, sizeof(long long) * 3 * 512 * 4);
+}
 extern "C" void adattn_b200_bwd_stats(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, adattn_b200::tc::g_bwd_stats, sizeof(unsigned long long) * 8);
   if (reset) {

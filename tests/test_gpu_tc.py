@@ -576,3 +576,19 @@ def test_tc_delta_fold_matches_prepass(case, monkeypatch):
         assert (g1.delta - gx.delta).abs().max().item() <= 2e-2
     else:  # fp16 u: ~2^-11 relative per term (why the fold is off by default here)
         assert derr <= 2e-2 * dscale
+
+
+@pytest.mark.parametrize("case", [(1, 2, 2048, 1.5, True, 1.0), (1, 2, 2048, 1.5, False, 1.0),
+                                  (2, 1, 4096, 1.25, True, 1.0), (1, 1, 4096, 1.5, True, 8.0)],
+                         ids=str)
+def test_tc_dkdv_slot3_matches_two_buffers(case, monkeypatch):
+    """The three-slot pair dK/dV kernel (fp16 P / dS heads) issues the same products
+    in the same order as the two-buffer kernel: dK and dV are bit-identical."""
+    B, H, N, alpha, causal, qs = case
+    q, k, v, do = inputs(hash(case) % 907 + 11, B, H, N, 128, qs)
+    monkeypatch.setenv("ADATTN_DS_F16", "1")
+    monkeypatch.setenv("ADATTN_KV_SLOT3", "0")
+    _, r0, g0 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_KV_SLOT3", "1")
+    _, r1, g1 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    assert torch.equal(g0.dv, g1.dv) and torch.equal(g0.dk, g1.dk) and torch.equal(g0.dq, g1.dq)
