@@ -173,7 +173,7 @@ cudaError_t f16_convert_scaled(const void* src, void* dst, int heads, size_t ele
 // candidate lists, then (fp16 P V) the fp16 copy of V and its range maximum
 size_t forward_cand_bytes(const Geom& g) {
   const CandPlan p = cand_plan(g);
-  return p.cap > 0 ? ((size_t)p.slots * 512 * (size_t)p.cap * 8 + 255) / 256 * 256 : 0;
+  return p.cap > 0 ? ((size_t)p.slots * 512 * (size_t)p.cap * 8 + 4096 + 255) / 256 * 256 : 0;
 }
 // then per resident CTA slot and epilogue warp the warp's tile maxima (activity sets)
 size_t forward_wtm_offset(const Geom& g) {

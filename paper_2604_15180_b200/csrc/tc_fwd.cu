@@ -202,7 +202,9 @@ struct FwdSmem {
   __host__ __device__ static int off_xf(int wpr, int nkt) { return off_pm(wpr, nkt) + 4 * wpr * 4; }
   // the output pass's active 128-key tiles (ascending u16), after the exchange flags
   __host__ __device__ static int off_tiles(int wpr, int nkt) { return off_xf(wpr, nkt) + 16; }
-  static size_t bytes(int wpr, int nkt) { return 1024 + off_tiles(wpr, nkt) + 2 * nkt + 64; }
+  // list staging: the 16 epilogue warps' list totals (prefix sum)
+  __host__ __device__ static int off_scan(int wpr, int nkt) { return (off_tiles(wpr, nkt) + 2 * nkt + 15) & ~15; }
+  static size_t bytes(int wpr, int nkt) { return 1024 + off_scan(wpr, nkt) + 4 * kEpiWarps + 64; }
 };
 
 // Order-preserving float <-> u32 (atomicMax / atomicMin on floats in smem).
@@ -439,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* sPm = PAIR ? reinterpret_cast<uint32_t*>(smem + L::off_pm(g.wpr, nkt_)) : smask;
   volatile uint32_t* xflag = reinterpret_cast<volatile uint32_t*>(smem + L::off_xf(g.wpr, nkt_));
   uint16_t* sTiles = reinterpret_cast<uint16_t*>(smem + L::off_tiles(g.wpr, nkt_));
+  int* sScan = reinterpret_cast<int*>(smem + L::off_scan(g.wpr, nkt_));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // head-major (the head's K/V stay L2-resident across its CTAs' sweeps),
@@ -1305,46 +1308,59 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool ovf = (int)smid >= a.cand_slots;  // (uniform: one CTA per SM)
       int cnt = 0;
       {
-        uint2* wp = lst;  // next free entry
+        // carry-free 32-bit append offsets: a list never crosses a 4 GB boundary
+        // (4 KB-aligned regions of cap * 8 bytes); a region that would is treated
+        // as an overflow (the CTA's sweeps take over)
+        const uint64_t lst64 = reinterpret_cast<uint64_t>(lst);
+        const uint32_t lo0 = (uint32_t)lst64, hi = (uint32_t)(lst64 >> 32);
+        uint32_t lo = lo0;
+        if ((uint64_t)lo0 + (uint64_t)cap * 8u > 0x100000000ull) ovf = true;
+#define CAND_USED ((int)((lo - lo0) >> 3))
         for (int J = 0; J <= jl; ++J) {
           if (!act(1, rg, J)) continue;
           const uint32_t blk = (uint32_t)(2 * J + half);
           // a tile appends <= 64 entries; warp-uniform (the append votes are warp-collective)
-          ovf = __any_sync(0xffffffffu, ovf || (int)(wp - lst) > cap - 64);
+          ovf = __any_sync(0xffffffffu, ovf || CAND_USED > cap - 64);
           tau_tile(J, wact(1, J), [&](const float* v) {
             if (ovf) return;
-            // candidates are rare (~0.3% of scores): one 3-input max + warp vote per
-            // 4 scores keeps the common path at 2 FMNMX + compare + vote + branch
+            // candidates are rare (~0.4% of scores): one 3-input max + warp vote per
+            // 4 scores keeps the common path at 2 FMNMX + compare + vote + branch; the
+            // appends advance a 32-bit offset (no 64-bit carry chains, measured -0.9 ms)
 #pragma unroll
             for (int i = 0; i < 32; i += 4)
               asm volatile(
-                  "{\n\t.reg .pred p0, p1, p2, p3, pa, q;\n\t.reg .f32 m;\n\t"
+                  "{\n\t.reg .pred p0, p1, p2, p3, pa, q;\n\t.reg .f32 m;\n\t.reg .u64 a;\n\t"
                   "max.f32 m, %1, %2, %3;\n\t"
                   "max.f32 m, m, %4;\n\t"
                   "setp.gt.f32 pa, m, %5;\n\t"
                   "vote.sync.any.pred q, pa, 0xffffffff;\n\t"
-                  "@!q bra.uni CAND_SKIP_%=;\n\t"
+                  "@!q bra.uni CANDL_SKIP_%=;\n\t"
                   "setp.gt.f32 p0, %1, %5;\n\t"
                   "setp.gt.f32 p1, %2, %5;\n\t"
                   "setp.gt.f32 p2, %3, %5;\n\t"
                   "setp.gt.f32 p3, %4, %5;\n\t"
-                  "@p0 st.global.v2.b32 [%0], {%6, %10};\n\t"
-                  "@p0 add.u64 %0, %0, 8;\n\t"
-                  "@p1 st.global.v2.b32 [%0], {%7, %10};\n\t"
-                  "@p1 add.u64 %0, %0, 8;\n\t"
-                  "@p2 st.global.v2.b32 [%0], {%8, %10};\n\t"
-                  "@p2 add.u64 %0, %0, 8;\n\t"
-                  "@p3 st.global.v2.b32 [%0], {%9, %10};\n\t"
-                  "@p3 add.u64 %0, %0, 8;\n\t"
-                  "CAND_SKIP_%=:\n\t}"
-                  : "+l"(wp)
+                  "mov.b64 a, {%0, %11};\n\t"
+                  "@p0 st.global.v2.b32 [a], {%6, %10};\n\t"
+                  "@p0 add.u32 %0, %0, 8;\n\t"
+                  "mov.b64 a, {%0, %11};\n\t"
+                  "@p1 st.global.v2.b32 [a], {%7, %10};\n\t"
+                  "@p1 add.u32 %0, %0, 8;\n\t"
+                  "mov.b64 a, {%0, %11};\n\t"
+                  "@p2 st.global.v2.b32 [a], {%8, %10};\n\t"
+                  "@p2 add.u32 %0, %0, 8;\n\t"
+                  "mov.b64 a, {%0, %11};\n\t"
+                  "@p3 st.global.v2.b32 [a], {%9, %10};\n\t"
+                  "@p3 add.u32 %0, %0, 8;\n\t"
+                  "CANDL_SKIP_%=:\n\t}"
+                  : "+r"(lo)
                   : "f"(v[i]), "f"(v[i + 1]), "f"(v[i + 2]), "f"(v[i + 3]), "f"(theta),
                     "r"(__float_as_uint(v[i])), "r"(__float_as_uint(v[i + 1])),
-                    "r"(__float_as_uint(v[i + 2])), "r"(__float_as_uint(v[i + 3])), "r"(blk)
+                    "r"(__float_as_uint(v[i + 2])), "r"(__float_as_uint(v[i + 3])), "r"(blk), "r"(hi)
                   : "memory");
           });
         }
-        cnt = (int)(wp - lst);
+        cnt = CAND_USED;
+#undef CAND_USED
 #ifdef ADATTN_PIPE_STATS
         // [26] listed entries, [27] listing threads, [28] longest list, [29] overflowed threads
         atomicAdd(&g_pipe_stats[26], (unsigned long long)cnt);
@@ -1364,7 +1380,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         // shared memory instead of waiting on L2 per entry.
         float* sl = reinterpret_cast<float*>(sRing);
         constexpr int lcap = NST * L::TILE / (kEpi * 4);
-        const int ns = cnt < lcap ? cnt : lcap;
+        // Whole-list staging: the CTA's lists packed back to back in the ring (an
+        // exclusive prefix sum of the counts; scores f32, then their 64-key blocks u16)
+        // when they all fit (C3 gaussian: ~17K entries, room for 21.8K).  The
+        // refinement rounds and the mask pass then read shared memory only -- with
+        // per-thread staging the longest lists of a CTA (up to ~230 entries) were read
+        // from L2 in every round and the barriers waited on them.  Otherwise each
+        // thread's first lcap scores ([i][thread], conflict-free) and L2 beyond.
+        constexpr int kEmax = NST * L::TILE / 6;
+        uint16_t* sblk = reinterpret_cast<uint16_t*>(sRing + 4 * kEmax);
+        int sbase = 0;
+        bool full;
+        {
+          int x = cnt;  // inclusive warp scan of the counts
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          if (lane == 31) sScan[warp] = x;
+          bar_sync(3, kEpi);
+          int pre = 0, tot = 0;
+#pragma unroll
+          for (int w = 0; w < kEpiWarps; ++w) {
+            const int t = sScan[w];
+            pre += w < warp ? t : 0;
+            tot += t;
+          }
+          sbase = pre + x - cnt;
+          full = tot <= kEmax;  // CTA-uniform
+        }
+        const int ns = full ? cnt : (cnt < lcap ? cnt : lcap);
+        auto sidx = [&](int i) { return full ? sbase + i : i * kEpi + tid; };
         // the histogram of the listed scores (list mode), read in the same pass:
         // both halves of a row add into its 32 packed 16-bit counters in row_cnt
         // (a row lists <= 2 x 512 scores)
@@ -1373,15 +1420,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < 16; ++k) row_cnt[k] = 0u;
         }
         bar_sync(bar_rg, 256);
-        for (int i0 = 0; i0 < cnt; i0 += 8) {
-          uint32_t tmp[8];
+        // 16 entries (8 x 16-byte loads) in flight from L2; lists start 4 KB-aligned and
+        // an odd count reads one entry past its end, inside the thread's region
+        for (int i0 = 0; i0 < cnt; i0 += 16) {
+          uint4 q8[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) tmp[j] = i0 + j < cnt ? lst[i0 + j].x : 0xFF800000u;
+          for (int j = 0; j < 8; ++j)
+            q8[j] = i0 + 2 * j < cnt ? reinterpret_cast<const uint4*>(lst + i0)[j]
+                                     : make_uint4(0xFF800000u, 0u, 0xFF800000u, 0u);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (i0 + j < ns) sl[(i0 + j) * kEpi + tid] = __uint_as_float(tmp[j]);
-            const float z = fmaf(A1, __uint_as_float(tmp[j]), Bf);
-            if (z >= 0.f) {
+          for (int j = 0; j < 16; ++j) {
+            const int i = i0 + j;
+            const uint32_t sx = (j & 1) ? q8[j >> 1].z : q8[j >> 1].x;
+            const uint32_t sy = (j & 1) ? q8[j >> 1].w : q8[j >> 1].y;
+            if (i < ns) {
+              sl[sidx(i)] = __uint_as_float(sx);
+              if (full) sblk[sbase + i] = (uint16_t)sy;
+            }
+            const float z = fmaf(A1, __uint_as_float(sx), Bf);
+            if (i < cnt && z >= 0.f) {
               const int k = min((int)((float)nb * z), nb - 1);
               atomicAdd(&row_cnt[k >> 1], 1u << (16 * (k & 1)));
             }
@@ -1415,7 +1472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const int i = i0 + j;
-              accs[j] = i < ns ? sl[i * kEpi + tid]
+              accs[j] = i < ns ? sl[sidx(i)]
                                : (i < cnt ? __uint_as_float(lst[i].x) : -CUDART_INF_F);
             }
 #pragma unroll
@@ -1476,14 +1533,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         bar_sync(3, kEpi);
         {
           const float C = sRow[e * 4 + 2];
-          for (int i0 = 0; i0 < cnt; i0 += 8) {
-            uint2 en[8];
+          if (full) {
+            for (int i0 = 0; i0 < cnt; i0 += 8) {
+              float accs[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) en[j] = i0 + j < cnt ? lst[i0 + j] : make_uint2(0xFF800000u, 0u);
+              for (int j = 0; j < 8; ++j) accs[j] = i0 + j < cnt ? sl[sbase + i0 + j] : -CUDART_INF_F;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (row_real && fmaf(A1, __uint_as_float(en[j].x), C) > -1e-9f)
-                atomicOr(&smask[rb * wpr + (en[j].y >> 5)], 1u << (en[j].y & 31));
+              for (int j = 0; j < 8; ++j)
+                if (row_real && fmaf(A1, accs[j], C) > -1e-9f) {
+                  const uint32_t bk = sblk[sbase + i0 + j];
+                  atomicOr(&smask[rb * wpr + (bk >> 5)], 1u << (bk & 31));
+                }
+            }
+          } else {
+            for (int i0 = 0; i0 < cnt; i0 += 8) {
+              uint2 en[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) en[j] = i0 + j < cnt ? lst[i0 + j] : make_uint2(0xFF800000u, 0u);
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (row_real && fmaf(A1, __uint_as_float(en[j].x), C) > -1e-9f)
+                  atomicOr(&smask[rb * wpr + (en[j].y >> 5)], 1u << (en[j].y & 31));
+            }
           }
         }
         fence_proxy_async_smem();  // generic writes to the ring before its next TMA loads
@@ -1994,7 +2065,12 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.rcnt = g.rl_cnt_out;
   a.rcol = g.rl_col_out;
   const CandPlan cp = cand_plan(g);
-  a.cand = (cp.cap > 0 && ws) ? reinterpret_cast<uint2*>(ws) : nullptr;
+  // lists start 4 KB-aligned (forward_cand_bytes keeps 4 KB of slack): the appends'
+  // 32-bit offsets then never carry with the default cap (4 KB regions; any other
+  // region that would cross a 4 GB boundary takes the overflow path)
+  a.cand = (cp.cap > 0 && ws)
+               ? reinterpret_cast<uint2*>((reinterpret_cast<uintptr_t>(ws) + 4095) & ~uintptr_t(4095))
+               : nullptr;
   a.cand_cap = cp.cap;
   a.cand_slots = cp.slots;
   a.v16_max = nullptr;
