@@ -1612,6 +1612,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const BwdArgs a) {
   using L = KvSmem<D>;
   constexpr int NCH = D / 64;
+  // S^T / dP^T buffers in TMEM (128 columns each) ahead of the dV, dK accumulators: d = 64
+  // leaves room for three, so the gradients of unit u are issued after S^T(u + 2) and
+  // the epilogue of unit u has two units of MMA work to hide behind (two buffers: the
+  // S^T -> epilogue -> gradients -> S^T(u + 2) chain idled the pipe ~45% at C4)
+  constexpr int NB = D == 64 ? 3 : 2;
+  constexpr uint32_t ACC = NB * 128;
   const Geom& g = a.g;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned base that stays in the shared address space (LDS/STS, not
@@ -1623,9 +1629,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   uint64_t* full = bars;             // [KST]
   uint64_t* empty = bars + KST;      // [KST]
-  uint64_t* s_full = bars + 2 * KST; // [2]
-  uint64_t* p_full = s_full + 2;     // [2]
-  uint64_t* kv_full = p_full + 2;
+  uint64_t* s_full = bars + 2 * KST; // [NB]
+  uint64_t* p_full = s_full + NB;    // [NB]
+  uint64_t* kv_full = p_full + NB;
   uint64_t* acc_full = kv_full + 1;
   volatile uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::OFF_MISC);
   uint8_t* ubits = smem + L::OFF_UB;  // [t_r] 2-bit activity of (i, j0), (i, j0+1)
@@ -1645,7 +1651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NB; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 8);
     }
@@ -1721,13 +1727,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       uint32_t u = 0;
       bool init = false;
-      int prev = -1;
-      uint32_t prev_st = 0;
-      auto grad_mma = [&](uint32_t uu, uint32_t st) {
-        const uint32_t b = uu & 1;
+      auto grad_mma = [&](uint32_t uu) {
+        const uint32_t b = uu % NB, st = uu % KST;
         {
           BSTAT_T0();
-          mbar_wait(&p_full[b], (uu >> 1) & 1);
+          mbar_wait(&p_full[b], (uu / NB) & 1);
           BSTAT_ADD(1, leader);
         }
         tc_fence_after();
@@ -1742,10 +1746,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t bdo = dDOmn + so + (uint64_t)(128 * k);
           const uint64_t bq = dQmn + so + (uint64_t)(128 * k);
           const uint32_t acc = (init || k > 0) ? 1u : 0u;
-          if (leader) umma_bf16_ts(tmem + 256, tmem + b * 128 + acol, bdo, IDESC_G, acc);
-          if (leader) umma_bf16_ts(tmem + 256, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
-          if (leader) umma_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol, bq, IDESC_G, acc);
-          if (leader) umma_bf16_ts(tmem + 256 + D, tmem + b * 128 + 64 + acol + 16, bq, IDESC_G, 1u);
+          if (leader) umma_bf16_ts(tmem + ACC, tmem + b * 128 + acol, bdo, IDESC_G, acc);
+          if (leader) umma_bf16_ts(tmem + ACC, tmem + b * 128 + acol + 16, bdo, IDESC_G, 1u);
+          if (leader) umma_bf16_ts(tmem + ACC + D, tmem + b * 128 + 64 + acol, bq, IDESC_G, acc);
+          if (leader) umma_bf16_ts(tmem + ACC + D, tmem + b * 128 + 64 + acol + 16, bq, IDESC_G, 1u);
         }
         init = true;
         if (leader) umma_commit(&empty[st]);
@@ -1759,7 +1763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           BSTAT_ADD(0, leader);
         }
         tc_fence_after();
-        const uint32_t b = u & 1;
+        const uint32_t b = u % NB;
         const uint64_t so = (uint64_t)((st * (uint32_t)L::STAGE) >> 4);
         BSTAT_T0();
 #pragma unroll
@@ -1773,12 +1777,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         if (leader) umma_commit(&s_full[b]);
         BSTAT_ADD(5, leader);
-        if (prev >= 0) grad_mma(u - 1, prev_st);
-        prev = i;
-        prev_st = st;
+        // in pipe order after grad(u - NB), which read buffer b
+        if (u >= NB - 1) grad_mma(u - (NB - 1));
         ++u;
       }
-      if (prev >= 0) grad_mma(u - 1, prev_st);
+      for (uint32_t uu = u > NB - 1 ? u - (NB - 1) : 0; uu < u; ++uu) grad_mma(uu);
       if (leader) umma_commit(acc_full);
 #ifdef ADATTN_PIPE_STATS
       if (leader) {
@@ -1799,12 +1802,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t u = 0;
     bool any = false;
     for (int i = next_unit(i_first); i >= 0; i = next_unit(i + 1)) {
-      const uint32_t st = u % KST, b = u & 1;
+      const uint32_t st = u % KST, b = u % NB;
       const bool mine = (unit_bits(i) >> ksub) & 1u;
       any |= mine;
       {
         BSTAT_T0();
-        mbar_wait(&s_full[b], (u >> 1) & 1);
+        mbar_wait(&s_full[b], (u / NB) & 1);
         BSTAT_ADD(2, warp == 0 && lane == 0);
       }
       tc_fence_after();
@@ -1846,7 +1849,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
         float o[32];
-        tmem_ld32(tl + 256 + which * D + half * (D / 2) + c * 32, o);
+        tmem_ld32(tl + ACC + which * D + half * (D / 2) + c * 32, o);
         tmem_wait_ld();
         const int x0 = half * (D / 2) + c * 32;
         if (g.out_dtype == ADATTN_F64) {

@@ -1,6 +1,6 @@
 """A/B timing of library variants / env settings, interleaved (dev tool).
     python tools/ab.py VARIANT [VARIANT ...]   VARIANT = path/to/lib.so[:ENV=VAL[,ENV=VAL]]
-Runs the C3 forward (+backward with BWD=1) of each variant in turn, REPS rounds,
+Runs the C3 forward (+backward with BWD=1; SHAPE=B,H,N D=.. CAUSAL=0/1 for other shapes) of each variant in turn, REPS rounds,
 and prints the median ms per variant: interleaving cancels clock drift."""
 import os, sys, statistics
 sys.path.insert(0, ".")
@@ -14,6 +14,8 @@ alpha = float(os.environ.get("ALPHA", "1.5"))
 beta = os.environ.get("BETA")
 reps = int(os.environ.get("REPS", "7"))
 bwd = os.environ.get("BWD", "0") == "1"
+D = int(os.environ.get("D", "128"))
+causal = os.environ.get("CAUSAL", "1") == "1"
 vars_ = []
 for a in sys.argv[1:]:
     path, _, envs = a.partition(":")
@@ -21,9 +23,9 @@ for a in sys.argv[1:]:
     L.LIB_PATH = os.path.abspath(path)
     L._lib = None
     vars_.append((a, L.load(), env))
-q, k, v, do = (workloads.gaussian(B, H, N, 128, 1.0, seed=1) if beta is None
-               else workloads.anchored(B, H, N, 128, float(beta), True, seed=1))
-p = pa.AttentionProblem(q, k, v, alpha=alpha, causal=True)
+q, k, v, do = (workloads.gaussian(B, H, N, D, 1.0, seed=1) if beta is None
+               else workloads.anchored(B, H, N, D, float(beta), causal, seed=1))
+p = pa.AttentionProblem(q, k, v, alpha=alpha, causal=causal)
 ts = {a: [] for a, _, _ in vars_}
 kts = {a: {} for a, _, _ in vars_}
 for rep in range(reps + 1):

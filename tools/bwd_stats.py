@@ -1,4 +1,4 @@
-"""dK/dV kernel wait fractions (ADATTN_PIPE_STATS build).  python tools/bwd_stats.py B H N"""
+"""dK/dV kernel wait fractions (ADATTN_PIPE_STATS build).  python tools/bwd_stats.py B H N  (env D=64 CAUSAL=0 for other shapes)"""
 import ctypes as C, os, sys
 sys.path.insert(0, ".")
 import paper_2604_15180_b200._lib as L
@@ -11,8 +11,10 @@ fn = lib.adattn_b200_bwd_stats
 fn.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 B, H, N = (int(x) for x in sys.argv[1:4])
 os.environ.setdefault("ADATTN_DELTA_FOLD", "0")
-q, k, v, do = workloads.gaussian(B, H, N, 128, 1.0, seed=1)
-p = pa.AttentionProblem(q, k, v, alpha=1.5, causal=True)
+D = int(os.environ.get("D", "128"))
+causal = os.environ.get("CAUSAL", "1") == "1"
+q, k, v, do = workloads.gaussian(B, H, N, D, 1.0, seed=1)
+p = pa.AttentionProblem(q, k, v, alpha=1.5, causal=causal)
 r = pa.forward(p); g = pa.backward(p, r, do); torch.cuda.synchronize()
 buf = (C.c_ulonglong * 8)()
 fn(buf, 1)
