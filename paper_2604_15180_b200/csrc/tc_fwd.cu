@@ -165,6 +165,7 @@ struct FwdArgs {
   uint2* cand;
   int cand_cap;
   int cand_slots;
+  int list_stage;  // 1: whole lists staged in the ring when they fit (ADATTN_LIST_STAGE=0: off)
   // fp16 P V: per head, max |V| (float bits) of the scaled fp16 V copy; nullptr -> bf16 P
   const uint32_t* v16_max;
   // optional output (delta fold): Ubar [bh][n][dv] fp32, then sum u [bh][n] fp32
@@ -1408,7 +1409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tot += t;
           }
           sbase = pre + x - cnt;
-          full = tot <= kEmax;  // CTA-uniform
+          full = a.list_stage != 0 && tot <= kEmax;  // CTA-uniform
         }
         const int ns = full ? cnt : (cnt < lcap ? cnt : lcap);
         auto sidx = [&](int i) { return full ? sbase + i : i * kEpi + tid; };
@@ -2073,6 +2074,10 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
                : nullptr;
   a.cand_cap = cp.cap;
   a.cand_slots = cp.slots;
+  {
+    const char* ls = std::getenv("ADATTN_LIST_STAGE");
+    a.list_stage = (ls && *ls == '0') ? 0 : 1;
+  }
   a.v16_max = nullptr;
   tv16 = tv;
   if (pv_f16_enabled() && ws) {

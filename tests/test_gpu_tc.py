@@ -592,3 +592,21 @@ def test_tc_dkdv_slot3_matches_two_buffers(case, monkeypatch):
     monkeypatch.setenv("ADATTN_KV_SLOT3", "1")
     _, r1, g1 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
     assert torch.equal(g0.dv, g1.dv) and torch.equal(g0.dk, g1.dk) and torch.equal(g0.dq, g1.dq)
+
+
+@pytest.mark.parametrize("case", [(1, 2, 4096, 128, 1.5, True, 1.0), (1, 2, 2048, 64, 1.5, False, 1.0),
+                                  (1, 1, 4096, 128, 2.0, True, 2.0), (2, 1, 2304, 128, 1.75, True, 1.0)],
+                         ids=str)
+def test_tc_list_staging_whole_vs_per_thread(case, monkeypatch):
+    """Whole-list staging in the ring (prefix-sum packed lists, the default when the
+    CTA's lists fit) and per-thread staging with L2 reads beyond 64 entries
+    (ADATTN_LIST_STAGE=0) read the same entries in the same order: identical
+    thresholds, steps, masks and outputs."""
+    B, H, N, D, alpha, causal, qs = case
+    q, k, v, do = inputs(hash(case) % 883 + 5, B, H, N, D, qs)
+    monkeypatch.setenv("ADATTN_LIST_STAGE", "0")
+    _, r0, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_LIST_STAGE", "1")
+    _, r1, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
+    assert torch.equal(r0.tau, r1.tau) and torch.equal(r0.row_steps, r1.row_steps)
+    assert torch.equal(r0.mask.words, r1.mask.words) and torch.equal(r0.out, r1.out)
