@@ -462,10 +462,18 @@ def main():
             kern[n]["tflops_executed"] = exe[n] / (kern[n]["ms_avg"] * 1e-3) / 1e12
             kern[n]["frac_executed"] = kern[n]["tflops_executed"] / peak_tf
             kern[n]["tflops_alg"] = per_alg[n] / (kern[n]["ms_avg"] * 1e-3) / 1e12
-        elif n == "tc_delta" and n in exe:
-            # delta fold: delta = dO . Ubar / sum u, one HBM-bound pass per row -- reads
-            # dO (bf16), Ubar (fp32), sum u, tau, m; writes delta (fp64), rowc (2 x fp32)
-            b = hc * N * (2 * D + 4 * D + 4 + 8 + 8 + 8 + 8)
+        elif n == "tc_delta" and n in exe and res.delta_aux is not None:
+            if alpha == 2.0 and os.environ.get("ADATTN_DELTA_SUPP", "1") == "0":
+                # delta fold: delta = dO . Ubar / sum u, one HBM-bound pass per row -- reads
+                # dO (bf16), Ubar (fp32), sum u, tau, m; writes delta (fp64), rowc (2 x fp32)
+                b = hc * N * (2 * D + 4 * D + 4 + 8 + 8 + 8 + 8)
+                kern[n]["kind"] = "delta fold row kernel (HBM)"
+            else:
+                # support lists: per row dO (bf16), 2 (count, offset), ~30 (key, u) entries,
+                # tau, m in; delta (fp64), rowc (2 x fp32) out; the V rows it gathers stay
+                # L2-resident (one head's V at a time) and are not counted
+                b = hc * N * (2 * D + 16 + 30 * 8 + 8 + 8 + 8 + 8)
+                kern[n]["kind"] = "delta from support lists (SIMT gather, no MMA)"
             kern[n]["hbm_bytes"] = b
             kern[n]["gbps"] = b / (kern[n]["ms_avg"] * 1e-3) / 1e9
             kern[n]["frac_hbm"] = kern[n]["gbps"] / peak_bw

@@ -421,7 +421,8 @@ int forward_impl(const adattn_problem* p, const void* q, const void* k, const vo
     if (workspace_bytes < tc_forward_workspace(gp))
       return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_forward: workspace too small");
     if (!tc_ragged(g)) {
-      g.ubar_out = ubar;  // (delta fold: unpadded problems only)
+      g.ubar_out = ubar;  // (delta fold / support lists: unpadded problems only)
+      g.supp_out = ubar;
       e = tc_forward(g, q, k, v, out, tau, row_max, mask, row_steps, workspace, st);
     } else {
       Scratch sc(st);
@@ -484,8 +485,8 @@ size_t adattn_b200_delta_aux_bytes(const adattn_problem* p) {
   if (resolve(p, g) != ADATTN_PATH_TC || tc_ragged(g)) return 0;
   float dummy = 0.f;
   g.ubar_out = &dummy;
-  if (!tc_delta_fold(g)) return 0;
-  return (size_t)g.bh * g.n * (g.dv + 1) * sizeof(float);
+  if (tc_delta_fold(g)) return (size_t)g.bh * g.n * (g.dv + 1) * sizeof(float);
+  return tc_delta_supp_bytes(g);  // support lists (list mode), else 0
 }
 
 int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k,
@@ -596,7 +597,13 @@ int adattn_b200_backward_ex(const adattn_problem* p, const void* q, const void* 
     if (workspace_bytes < tc_backward_workspace(gp))
       return fail(ADATTN_ERR_WORKSPACE, "adattn_b200_backward: workspace too small");
     if (!tc_ragged(g)) {
-      if (ex && ex->delta_aux && adattn_b200_delta_aux_bytes(p)) g.ubar_in = ex->delta_aux;
+      if (ex && ex->delta_aux && adattn_b200_delta_aux_bytes(p)) {
+        Geom gf = g;
+        float dummy = 0.f;
+        gf.ubar_out = &dummy;
+        if (tc_delta_fold(gf)) g.ubar_in = ex->delta_aux;
+        else g.supp_in = ex->delta_aux;
+      }
       e = tc_backward(g, q, k, v, tau, row_max, mask, dout, dq, dk, dv, delta, workspace, st);
     } else {
       Scratch sc(st);

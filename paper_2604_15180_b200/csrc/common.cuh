@@ -46,6 +46,12 @@ struct Geom {
   // (attention.cpp:411-446) instead of running the delta kernel
   float* ubar_out = nullptr;
   const float* ubar_in = nullptr;
+  // delta from the support lists (tensor-core list mode, tc.cu supp_layout): the forward
+  // writes each row's keys and u with t > 0 at the final tau to supp_out; the backward
+  // forms delta_i = sum u_ij (dO_i . v_j) / sum u_ij from supp_in (the delta kernel takes
+  // the heads flagged as overflowed)
+  void* supp_out = nullptr;
+  const void* supp_in = nullptr;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {

@@ -171,6 +171,46 @@ cudaError_t f16_convert_scaled(const void* src, void* dst, int heads, size_t ele
 }
 
 // candidate lists, then (fp16 P V) the fp16 copy of V and its range maximum
+// delta from the support lists: list mode only (every score with t > 0
+// at the final tau is in the candidate lists), and not when the forward folds delta
+bool delta_supp_possible(const Geom& g) {
+  const char* s = std::getenv("ADATTN_DELTA_SUPP");
+  if (s && *s == '0') return false;
+  return cand_plan(g).cap > 0 && (g.dv == 64 || g.dv == 128);
+}
+bool delta_supp_enabled(const Geom& g) {
+  if (!delta_supp_possible(g)) return false;
+  Geom gf = g;
+  float dummy = 0.f;
+  gf.ubar_out = &dummy;
+  return !fwd_delta_fold(gf);
+}
+static int supp_cap_of() {
+  // support entries per row, pooled per 256-row block (C3 gaussian: ~30 per row; a block
+  // whose rows need more than 256 * cap in total falls back to the delta kernel)
+  int cap = 48;
+  if (const char* s = std::getenv("ADATTN_SUPP_CAP")) cap = std::max(1, std::atoi(s));
+  return cap;
+}
+size_t supp_bytes(const Geom& g) {
+  if (!delta_supp_enabled(g)) return 0;
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t rows = (size_t)g.bh * g.n, nblk = (rows + 255) / 256;
+  return al(nblk * 4) + al(rows * 2 * 8) + nblk * 256 * (size_t)supp_cap_of() * 8;
+}
+SuppLayout supp_layout(const Geom& g, void* base) {
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t rows = (size_t)g.bh * g.n, nblk = (rows + 255) / 256;
+  uint8_t* p = reinterpret_cast<uint8_t*>(base);
+  SuppLayout l;
+  l.flag = reinterpret_cast<uint32_t*>(p);
+  l.cnt = reinterpret_cast<int2*>(p + al(nblk * 4));
+  l.ent = reinterpret_cast<uint2*>(p + al(nblk * 4) + al(rows * 2 * 8));
+  l.cap = supp_cap_of();
+  l.nblk = nblk;
+  return l;
+}
+
 size_t forward_cand_bytes(const Geom& g) {
   const CandPlan p = cand_plan(g);
   return p.cap > 0 ? ((size_t)p.slots * 512 * (size_t)p.cap * 8 + 4096 + 255) / 256 * 256 : 0;
@@ -203,6 +243,7 @@ std::string tc_envelope() {
 size_t tc_forward_workspace(const Geom& g) { return tc::forward_workspace(g); }
 size_t tc_backward_workspace(const Geom& g) { return tc::backward_workspace(g); }
 bool tc_delta_fold(const Geom& g) { return tc::fwd_delta_fold(g); }
+size_t tc_delta_supp_bytes(const Geom& g) { return tc::supp_bytes(g); }
 
 cudaError_t tc_forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                        double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,

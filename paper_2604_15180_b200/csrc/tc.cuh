@@ -12,6 +12,8 @@ size_t tc_forward_workspace(const Geom& g);
 size_t tc_backward_workspace(const Geom& g);
 // the forward fills g.ubar_out (delta fold) for this (unpadded) geometry
 bool tc_delta_fold(const Geom& g);
+// bytes of the support-list buffer the forward fills for the backward's delta (0: off)
+size_t tc_delta_supp_bytes(const Geom& g);
 
 cudaError_t tc_forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                        double* tau, double* row_max, uint32_t* mask, int32_t* steps,

@@ -73,6 +73,10 @@ struct BwdArgs {
   double* delta;
   float2* rowc;  // [bh*n] {C, delta}
   const void* dout;  // bf16 [bh*n][dv] (delta from the forward's fold)
+  const void* v;     // bf16 [bh*m][dv] (delta from the support lists)
+  // delta kernels: 256-row blocks (global row / 256) whose delta the support kernel
+  // formed are skipped (supp_skip[block] == 0); nullptr: every block
+  const uint32_t* supp_skip;
   int skip_f16;      // pair dK/dV two-buffer kernel: skip heads the SLOT3 kernel takes
   // fp16 operand plan of the pair dQ and dK/dV kernels (device; nullptr: bf16 hi/lo)
   const struct F16Plan* f16;
@@ -373,6 +377,8 @@ __global__ void __launch_bounds__(kDeltaThreads, 1)
   const int nkt = g.m / DBN;
   const int jmax = g.causal ? (row0 + BM - 1) / DBN : nkt - 1;
 
+  // delta from the support lists: only the 256-row blocks the forward flagged run here
+  if (a.supp_skip && a.supp_skip[((size_t)bh * g.n + row0) / BM] == 0u) return;
   rows_from_lists(smask, 4, a, bh, row0 / 64, tid, kDeltaThreads);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
@@ -607,6 +613,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
   const int nkt = g.m / DBN;
   const int jmax = g.causal ? (prow0 + 2 * BM - 1) / DBN : nkt - 1;
 
+  if (a.supp_skip) {  // the pair's two 256-row blocks (both CTAs decide alike)
+    const size_t b0 = ((size_t)bh * g.n + prow0) / BM;
+    if (a.supp_skip[b0] == 0u && a.supp_skip[b0 + 1] == 0u) return;
+  }
   rows_from_lists(smask, 8, a, bh, prow0 / 64, tid, kDeltaThreads);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
@@ -847,6 +857,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDeltaThreads, 1)
   const int nkt = g.m / DBN;
   const int jmax = g.causal ? (prow0 + 2 * QR - 1) / DBN : nkt - 1;
 
+  // the pair's 256 rows: one forward block (both CTAs decide alike)
+  if (a.supp_skip && a.supp_skip[((size_t)bh * g.n + prow0) / 256] == 0u) return;
   rows_from_lists(smask, 4, a, bh, prow0 / 64, tid, kDeltaThreads);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
@@ -1943,6 +1955,84 @@ __global__ void delta_ubar_kernel(const uint16_t* __restrict__ dout, const float
   }
 }
 
+// delta from the support lists (Geom::supp_in, written by the forward's list phase):
+// delta_i = sum_e u_e (dO_i . v_{j_e}) / sum_e u_e over the row's entries (key half 0,
+// then half 1, list order; 0 when the sum is 0, attention.cpp:444) -- the terms the delta
+// kernel sums (u = 0 outside the support), without recomputing S and dP for every active
+// block: ~30 entries per row at C3 against 16K keys.  One warp per row, lane l holds d
+// elements l*E..; the head's V rows stay L2-resident.  Heads the forward flagged (a row
+// half over the cap, or a CTA that fell back to the sweeps) are left to the delta kernel.
+// Also rowc_i = (C_i, delta_i) for the dK/dV kernel, as the delta kernels form it.
+template <int D>
+__global__ void __launch_bounds__(256) delta_supp_kernel(
+    const uint16_t* __restrict__ dout, const uint16_t* __restrict__ vv, const uint2* __restrict__ pool,
+    const int2* __restrict__ cnt, const uint32_t* __restrict__ flag, int cap, int unit,
+    const double* __restrict__ tau, const double* __restrict__ row_max, double alpha, size_t rows,
+    int n, int m, double* delta, float2* rowc) {
+  constexpr int E = D / 32;
+  const size_t r = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const size_t bh = r / (size_t)n;
+  // the delta kernel's unit of `unit` rows (head-aligned) runs when any of its 256-row
+  // blocks is flagged; its rows are left to it (one writer per row)
+  const size_t u0 = (bh * n + (r - bh * n) / unit * unit) / 256;
+  for (int b = 0; b < unit / 256; ++b)
+    if (flag[u0 + b]) return;
+  const int2 h0 = cnt[r * 2], h1 = cnt[r * 2 + 1];
+  const int c0 = h0.x, tot = h0.x + h1.x;
+  const uint2* base = pool + (r / 256) * (size_t)(256 * cap);
+  const uint16_t* vb = vv + bh * (size_t)m * D + lane * E;
+  float acc[E];
+#pragma unroll
+  for (int x = 0; x < E; ++x) acc[x] = 0.f;
+  double su = 0.0;
+  auto add = [&](uint32_t key, float u) {
+    if constexpr (E == 4) {
+      const uint2 w = *reinterpret_cast<const uint2*>(vb + (size_t)key * D);
+      acc[0] = fmaf(u, __uint_as_float(w.x << 16), acc[0]);
+      acc[1] = fmaf(u, __uint_as_float(w.x & 0xFFFF0000u), acc[1]);
+      acc[2] = fmaf(u, __uint_as_float(w.y << 16), acc[2]);
+      acc[3] = fmaf(u, __uint_as_float(w.y & 0xFFFF0000u), acc[3]);
+    } else {
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(vb + (size_t)key * D);
+      acc[0] = fmaf(u, __uint_as_float(w << 16), acc[0]);
+      acc[1] = fmaf(u, __uint_as_float(w & 0xFFFF0000u), acc[1]);
+    }
+  };
+  for (int b = 0; b < tot; b += 32) {
+    const int idx = b + lane;  // lane l fetches entry b + l (half 0's, then half 1's)
+    uint2 my = make_uint2(0u, 0u);
+    if (idx < tot) my = idx < c0 ? base[h0.y + idx] : base[h1.y + idx - c0];
+    const int nk = min(32, tot - b);
+#pragma unroll 4
+    for (int k = 0; k < nk; ++k) {
+      const uint32_t key = __shfl_sync(0xffffffffu, my.x, k);
+      const float u = __uint_as_float(__shfl_sync(0xffffffffu, my.y, k));
+      su += (double)u;
+      add(key, u);
+    }
+  }
+  const uint16_t* dp = dout + r * D + lane * E;
+  float dot = 0.f;
+  if constexpr (E == 4) {
+    const uint2 w = *reinterpret_cast<const uint2*>(dp);
+    dot = __uint_as_float(w.x << 16) * acc[0] + __uint_as_float(w.x & 0xFFFF0000u) * acc[1] +
+          __uint_as_float(w.y << 16) * acc[2] + __uint_as_float(w.y & 0xFFFF0000u) * acc[3];
+  } else {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(dp);
+    dot = __uint_as_float(w << 16) * acc[0] + __uint_as_float(w & 0xFFFF0000u) * acc[1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  if (lane == 0) {
+    const double dlt = su > 0.0 ? (double)dot / su : 0.0;
+    const double B = 1.0 - (alpha - 1.0) * row_max[r];
+    delta[r] = dlt;
+    rowc[r] = make_float2((float)(B - tau[r]), (float)dlt);
+  }
+}
+
 constexpr int kKvThreads = 352;  // pair dK/dV: 8 epilogue warps, producer, 2 MMA issuers
 
 template <int D>
@@ -2423,6 +2513,22 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
                     cudaStream_t st) {
   cudaError_t e;
   const int dmode = delta_mode(g, a.ncta_rows);
+  BwdArgs ad = a;  // the delta kernels' arguments (support mode: flagged heads only)
+  const char* dname = "tc_delta";
+  if (g.supp_in && !delta_only) {  // delta from the forward's support lists
+    const SuppLayout sl = supp_layout(g, const_cast<void*>(g.supp_in));
+    const size_t rows = (size_t)g.bh * g.n;
+    prof_begin("tc_delta", st);
+    delta_supp_kernel<D><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(a.dout), reinterpret_cast<const uint16_t*>(a.v), sl.ent,
+        sl.cnt, sl.flag, sl.cap, dmode == 1 ? 512 : 256, a.tau, a.row_max, g.alpha, rows, g.n, g.m,
+        a.delta, a.rowc);
+    prof_end(st);
+    note_launch();
+    if ((e = cudaGetLastError())) return e;
+    ad.supp_skip = sl.flag;
+    dname = "tc_delta_fb";
+  }
   if (g.ubar_in && !delta_only) {  // delta from the forward's fold
     const size_t rows = (size_t)g.bh * g.n;
     prof_begin("tc_delta", st);
@@ -2436,8 +2542,8 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     auto k0 = tc_delta3_kernel<128, AK>;
     const size_t sm = Delta3Smem<128>::bytes(g.wpr);
     if ((e = set_smem(k0, sm))) return e;
-    prof_begin("tc_delta", st);
-    k0<<<dim3((unsigned)((g.n / 128) * g.bh)), kDeltaThreads, sm, st>>>(m[8], m[10], m[11], m[9], a);
+    prof_begin(dname, st);
+    k0<<<dim3((unsigned)((g.n / 128) * g.bh)), kDeltaThreads, sm, st>>>(m[8], m[10], m[11], m[9], ad);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
@@ -2445,8 +2551,8 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     auto k0 = tc_delta2_kernel<128, AK>;
     const size_t sm = Delta2Smem<128>::bytes(g.wpr);
     if ((e = set_smem(k0, sm))) return e;
-    prof_begin("tc_delta", st);
-    k0<<<dim3((unsigned)(a.ncta_rows * g.bh)), kDeltaThreads, sm, st>>>(m[0], m[10], m[11], m[3], a);
+    prof_begin(dname, st);
+    k0<<<dim3((unsigned)(a.ncta_rows * g.bh)), kDeltaThreads, sm, st>>>(m[0], m[10], m[11], m[3], ad);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
@@ -2454,8 +2560,8 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     auto k0 = tc_delta_kernel<D, AK>;
     const size_t sm = DeltaSmem<D>::bytes(g.wpr);
     if ((e = set_smem(k0, sm))) return e;
-    prof_begin("tc_delta", st);
-    k0<<<dim3((unsigned)(a.ncta_rows * g.bh)), kDeltaThreads, sm, st>>>(m[0], m[1], m[2], m[3], a);
+    prof_begin(dname, st);
+    k0<<<dim3((unsigned)(a.ncta_rows * g.bh)), kDeltaThreads, sm, st>>>(m[0], m[1], m[2], m[3], ad);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
@@ -2606,6 +2712,8 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   a.delta = delta;
   a.rowc = reinterpret_cast<float2*>(workspace);
   a.dout = dout;
+  a.v = v;
+  a.supp_skip = nullptr;
   a.skip_f16 = 0;
   a.f16 = nullptr;
   m[14] = m[7];

@@ -166,6 +166,14 @@ struct FwdArgs {
   int cand_cap;
   int cand_slots;
   int list_stage;  // 1: whole lists staged in the ring when they fit (ADATTN_LIST_STAGE=0: off)
+  // support lists (list mode, delta from the support): the keys and u = p^(2 - alpha) of
+  // the scores with t > 0 at the final tau, per 256-row CTA block in a pool of
+  // 256 * supp_cap entries; per row and key half (count, pool offset); supp_flag[block] = 1
+  // when the block's pool overflowed or the CTA fell back to the sweeps; nullptr: off
+  uint2* supp;
+  int2* supp_cnt;
+  uint32_t* supp_flag;
+  int supp_cap;
   // fp16 P V: per head, max |V| (float bits) of the scaled fp16 V copy; nullptr -> bf16 P
   const uint32_t* v16_max;
   // optional output (delta fold): Ubar [bh][n][dv] fp32, then sum u [bh][n] fp32
@@ -242,6 +250,23 @@ __device__ __forceinline__ float p_of(float t, float e0f) {
 
 // Partial sums of one 32-element slice for the refinement pass: two
 // independent accumulator sets of packed f32x2 for ILP.
+// u = p^(2 - alpha) = t^(e0 - 1) for t > 0 (the backward's pu_of, tc_bwd.cu: the same
+// operations, so the support lists carry the u the delta kernel would form)
+template <int AK>
+__device__ __forceinline__ float u_of(float t, float e1f) {
+  const float tp = fmaxf(t, 0.f);
+  if constexpr (AK == AK15) {
+    return tp;
+  } else if constexpr (AK == AK2) {
+    return __saturatef(tp * 0x1p126f);
+  } else if constexpr (AK == AK125) {
+    const float t2 = tp * tp;
+    return t2 * tp;
+  } else {
+    return tp > 0.f ? exp2f(e1f * __log2f(tp)) : 0.f;
+  }
+}
+
 template <int AK>
 __device__ __forceinline__ void ref_slice(const float* v, float A1, float C, float e0f, float e1f,
                                           float e2f, float& s0o, float& s1o, float& s2o,
@@ -390,6 +415,55 @@ __device__ __forceinline__ void hist_sweep(int jl, float2 Aw, float2 Bw, float2 
 // NB32: bins = 32 (the reference's 128-bit histogram words, attention.cpp:35) -- a
 // separate instantiation, so the 4-word HIST counters' registers do not weigh on
 // the default kernels
+// CAND appends of one 32-key chunk, unrolled at compile time (the key offset of each
+// 4-score group is an immediate of the append path, so the vote path carries no key math)
+template <int I>
+struct CandGroups {
+  static __device__ __forceinline__ void run(uint32_t& lo, const float* v, float theta, uint32_t kc,
+                                             uint32_t hi) {
+    asm volatile(
+        "{\n\t.reg .pred p0, p1, p2, p3, pa, q;\n\t.reg .f32 m;\n\t.reg .u64 a;\n\t"
+        ".reg .b32 k0, k1, k2, k3;\n\t"
+        "max.f32 m, %1, %2, %3;\n\t"
+        "max.f32 m, m, %4;\n\t"
+        "setp.gt.f32 pa, m, %5;\n\t"
+        "vote.sync.any.pred q, pa, 0xffffffff;\n\t"
+        "@!q bra.uni CANDL_SKIP_%=;\n\t"
+        "setp.gt.f32 p0, %1, %5;\n\t"
+        "setp.gt.f32 p1, %2, %5;\n\t"
+        "setp.gt.f32 p2, %3, %5;\n\t"
+        "setp.gt.f32 p3, %4, %5;\n\t"
+        "add.u32 k0, %10, %11;\n\t"
+        "add.u32 k1, k0, 1;\n\t"
+        "add.u32 k2, k0, 2;\n\t"
+        "add.u32 k3, k0, 3;\n\t"
+        "mov.b64 a, {%0, %12};\n\t"
+        "@p0 st.global.v2.b32 [a], {%6, k0};\n\t"
+        "@p0 add.u32 %0, %0, 8;\n\t"
+        "mov.b64 a, {%0, %12};\n\t"
+        "@p1 st.global.v2.b32 [a], {%7, k1};\n\t"
+        "@p1 add.u32 %0, %0, 8;\n\t"
+        "mov.b64 a, {%0, %12};\n\t"
+        "@p2 st.global.v2.b32 [a], {%8, k2};\n\t"
+        "@p2 add.u32 %0, %0, 8;\n\t"
+        "mov.b64 a, {%0, %12};\n\t"
+        "@p3 st.global.v2.b32 [a], {%9, k3};\n\t"
+        "@p3 add.u32 %0, %0, 8;\n\t"
+        "CANDL_SKIP_%=:\n\t}"
+        : "+r"(lo)
+        : "f"(v[I]), "f"(v[I + 1]), "f"(v[I + 2]), "f"(v[I + 3]), "f"(theta),
+          "r"(__float_as_uint(v[I])), "r"(__float_as_uint(v[I + 1])),
+          "r"(__float_as_uint(v[I + 2])), "r"(__float_as_uint(v[I + 3])), "r"(kc), "n"(I),
+          "r"(hi)
+        : "memory");
+    CandGroups<I + 4>::run(lo, v, theta, kc, hi);
+  }
+};
+template <>
+struct CandGroups<32> {
+  static __device__ __forceinline__ void run(uint32_t&, const float*, float, uint32_t, uint32_t) {}
+};
+
 template <int D, int AK, bool PAIR, bool NB32 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -1319,45 +1393,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #define CAND_USED ((int)((lo - lo0) >> 3))
         for (int J = 0; J <= jl; ++J) {
           if (!act(1, rg, J)) continue;
-          const uint32_t blk = (uint32_t)(2 * J + half);
+          // entries carry the key index (its 64-key block is key >> 6)
+          const uint32_t key0 = (uint32_t)(J * BN + half * 64);
+          int ck = 0;  // 32-key chunk of the tile the body is called for
           // a tile appends <= 64 entries; warp-uniform (the append votes are warp-collective)
           ovf = __any_sync(0xffffffffu, ovf || CAND_USED > cap - 64);
           tau_tile(J, wact(1, J), [&](const float* v) {
+            const uint32_t kc = key0 + 32u * (uint32_t)(ck++);
             if (ovf) return;
             // candidates are rare (~0.4% of scores): one 3-input max + warp vote per
             // 4 scores keeps the common path at 2 FMNMX + compare + vote + branch; the
             // appends advance a 32-bit offset (no 64-bit carry chains, measured -0.9 ms)
-#pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              asm volatile(
-                  "{\n\t.reg .pred p0, p1, p2, p3, pa, q;\n\t.reg .f32 m;\n\t.reg .u64 a;\n\t"
-                  "max.f32 m, %1, %2, %3;\n\t"
-                  "max.f32 m, m, %4;\n\t"
-                  "setp.gt.f32 pa, m, %5;\n\t"
-                  "vote.sync.any.pred q, pa, 0xffffffff;\n\t"
-                  "@!q bra.uni CANDL_SKIP_%=;\n\t"
-                  "setp.gt.f32 p0, %1, %5;\n\t"
-                  "setp.gt.f32 p1, %2, %5;\n\t"
-                  "setp.gt.f32 p2, %3, %5;\n\t"
-                  "setp.gt.f32 p3, %4, %5;\n\t"
-                  "mov.b64 a, {%0, %11};\n\t"
-                  "@p0 st.global.v2.b32 [a], {%6, %10};\n\t"
-                  "@p0 add.u32 %0, %0, 8;\n\t"
-                  "mov.b64 a, {%0, %11};\n\t"
-                  "@p1 st.global.v2.b32 [a], {%7, %10};\n\t"
-                  "@p1 add.u32 %0, %0, 8;\n\t"
-                  "mov.b64 a, {%0, %11};\n\t"
-                  "@p2 st.global.v2.b32 [a], {%8, %10};\n\t"
-                  "@p2 add.u32 %0, %0, 8;\n\t"
-                  "mov.b64 a, {%0, %11};\n\t"
-                  "@p3 st.global.v2.b32 [a], {%9, %10};\n\t"
-                  "@p3 add.u32 %0, %0, 8;\n\t"
-                  "CANDL_SKIP_%=:\n\t}"
-                  : "+r"(lo)
-                  : "f"(v[i]), "f"(v[i + 1]), "f"(v[i + 2]), "f"(v[i + 3]), "f"(theta),
-                    "r"(__float_as_uint(v[i])), "r"(__float_as_uint(v[i + 1])),
-                    "r"(__float_as_uint(v[i + 2])), "r"(__float_as_uint(v[i + 3])), "r"(blk), "r"(hi)
-                  : "memory");
+            CandGroups<0>::run(lo, v, theta, kc, hi);
           });
         }
         cnt = CAND_USED;
@@ -1388,8 +1435,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // per-thread staging the longest lists of a CTA (up to ~230 entries) were read
         // from L2 in every round and the barriers waited on them.  Otherwise each
         // thread's first lcap scores ([i][thread], conflict-free) and L2 beyond.
-        constexpr int kEmax = NST * L::TILE / 6;
-        uint16_t* sblk = reinterpret_cast<uint16_t*>(sRing + 4 * kEmax);
+        constexpr int kEmax = NST * L::TILE / 7;
+        uint16_t* sblk = reinterpret_cast<uint16_t*>(sRing + 4 * kEmax);  // key >> 6
+        uint8_t* sko = sRing + 6 * kEmax;                                   // key & 63
         int sbase = 0;
         bool full;
         {
@@ -1436,7 +1484,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t sy = (j & 1) ? q8[j >> 1].w : q8[j >> 1].y;
             if (i < ns) {
               sl[sidx(i)] = __uint_as_float(sx);
-              if (full) sblk[sbase + i] = (uint16_t)sy;
+              if (full) {
+                sblk[sbase + i] = (uint16_t)(sy >> 6);
+                sko[sbase + i] = (uint8_t)(sy & 63u);
+              }
             }
             const float z = fmaf(A1, __uint_as_float(sx), Bf);
             if (i < cnt && z >= 0.f) {
@@ -1534,17 +1585,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         bar_sync(3, kEpi);
         {
           const float C = sRow[e * 4 + 2];
+          // support lists (delta from the support in the backward): the entries with
+          // t > 0 at the final tau, in list order, packed per CTA (256 rows) in a pool of
+          // supp_cap entries per row: counted in the mask pass, placed by a prefix sum over
+          // the CTA's threads, written by a second pass over the staged list
+          const bool sup = a.supp != nullptr;
+          int ns_ = 0;
           if (full) {
             for (int i0 = 0; i0 < cnt; i0 += 8) {
               float accs[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) accs[j] = i0 + j < cnt ? sl[sbase + i0 + j] : -CUDART_INF_F;
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (row_real && fmaf(A1, accs[j], C) > -1e-9f) {
+              for (int j = 0; j < 8; ++j) {
+                const float t = fmaf(A1, accs[j], C);
+                if (row_real && t > -1e-9f) {
                   const uint32_t bk = sblk[sbase + i0 + j];
                   atomicOr(&smask[rb * wpr + (bk >> 5)], 1u << (bk & 31));
+                  ns_ += t > 0.f;
                 }
+              }
             }
           } else {
             for (int i0 = 0; i0 < cnt; i0 += 8) {
@@ -1552,9 +1612,57 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int j = 0; j < 8; ++j) en[j] = i0 + j < cnt ? lst[i0 + j] : make_uint2(0xFF800000u, 0u);
 #pragma unroll
-              for (int j = 0; j < 8; ++j)
-                if (row_real && fmaf(A1, __uint_as_float(en[j].x), C) > -1e-9f)
-                  atomicOr(&smask[rb * wpr + (en[j].y >> 5)], 1u << (en[j].y & 31));
+              for (int j = 0; j < 8; ++j) {
+                const float t = fmaf(A1, __uint_as_float(en[j].x), C);
+                if (row_real && t > -1e-9f) {
+                  const uint32_t bk = en[j].y >> 6;
+                  atomicOr(&smask[rb * wpr + (bk >> 5)], 1u << (bk & 31));
+                  ns_ += t > 0.f;
+                }
+              }
+            }
+          }
+          if (sup) {
+            int x = ns_;  // inclusive warp scan, then the 16 warp totals
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(0xffffffffu, x, o);
+              if (lane >= o) x += y;
+            }
+            bar_sync(3, kEpi);  // (sScan of the staging scan consumed)
+            if (lane == 31) sScan[warp] = x;
+            bar_sync(3, kEpi);
+            int pre = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kEpiWarps; ++w) {
+              const int tw = sScan[w];
+              pre += w < warp ? tw : 0;
+              tot += tw;
+            }
+            const int pc = BM * a.supp_cap;  // the CTA's pool
+            const size_t blk256 = ((size_t)bh * g.n + row0) / BM;
+            const size_t srow = (size_t)bh * g.n + grow;
+            if (tot > pc) {
+              if (tid == 0) a.supp_flag[blk256] = 1u;  // the delta kernel takes these rows
+            } else {
+              int off = pre + x - ns_;
+              a.supp_cnt[srow * 2 + half] = make_int2(ns_, off);
+              uint2* pool = a.supp + blk256 * (size_t)pc;
+              for (int i = 0; i < cnt; ++i) {
+                float acc;
+                uint32_t key;
+                if (full) {
+                  acc = sl[sbase + i];
+                  key = ((uint32_t)sblk[sbase + i] << 6) | sko[sbase + i];
+                } else {
+                  const uint2 en = lst[i];
+                  acc = __uint_as_float(en.x);
+                  key = en.y;
+                }
+                const float t = fmaf(A1, acc, C);
+                if (row_real && t > 0.f)
+                  pool[off++] = make_uint2(key, __float_as_uint(u_of<AK>(t, a.e1f)));
+              }
             }
           }
         }
@@ -1576,7 +1684,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       LIST_MARK(5);  // tile list + decision
       dround = 1;
-      if (!list_ok) hist_solve();  // fallback: the exact histogram by the HIST sweep
+      if (!list_ok) {
+        // no support lists for this CTA's rows: the backward's delta kernel takes the head
+        if (tid == 0 && a.supp) a.supp_flag[((size_t)bh * g.n + row0) / BM] = 1u;
+        hist_solve();  // fallback: the exact histogram by the HIST sweep
+      }
     }
 
     // ---- passes REF (attention.cpp:234-332): sweeps (no lists, or a list overflowed)
@@ -2021,14 +2133,15 @@ bool use_fwd_pairs(const Geom& g) {
 // through the tensor cores as fp16, so Ubar carries u's 2^-11 relative rounding:
 // exact for alpha = 2 (u in {0, 1}), but at alpha = 1.5 delta moves by ~5e-3 on
 // rows with small supports (a coherent per-row shift of dS), which exceeds the
-// gradient bar on peaked inputs -- so the fold is on by default for alpha = 2 only
-// (ADATTN_DELTA_FOLD=1 forces it on, 0 off).
+// gradient bar on peaked inputs.  The support lists (list mode) are cheaper still
+// (C3 alpha = 2: 83.6 vs 89.5 ms per step), so the fold is the default only for
+// alpha = 2 without them (ADATTN_DELTA_FOLD=1 forces it on, 0 off).
 bool fwd_delta_fold(const Geom& g) {
   if (!g.ubar_out || g.d != g.dv) return false;
   if (g.d == 128 && use_fwd_pairs(g)) return false;
   const char* s = std::getenv("ADATTN_DELTA_FOLD");
   if (s && *s) return *s != '0';
-  return g.alpha == 2.0;
+  return g.alpha == 2.0 && !delta_supp_possible(g);
 }
 
 int alpha_kind(double alpha) {
@@ -2074,6 +2187,21 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
                : nullptr;
   a.cand_cap = cp.cap;
   a.cand_slots = cp.slots;
+  a.supp = nullptr;
+  a.supp_cnt = nullptr;
+  a.supp_flag = nullptr;
+  a.supp_cap = 0;
+  if (!a.ubar && a.cand && g.supp_out && delta_supp_enabled(g)) {  // (list mode only)
+    const SuppLayout sl = supp_layout(g, g.supp_out);
+    if ((e = cudaMemsetAsync(sl.flag, 0, 4 * sl.nblk, st))) return e;
+    a.supp = sl.ent;
+    a.supp_cnt = sl.cnt;
+    a.supp_flag = sl.flag;
+    a.supp_cap = sl.cap;
+  } else if (g.supp_out && delta_supp_enabled(g)) {  // no lists written: every head flagged
+    const SuppLayout sl = supp_layout(g, g.supp_out);
+    if ((e = cudaMemsetAsync(sl.flag, 1, 4 * sl.nblk, st))) return e;
+  }
   {
     const char* ls = std::getenv("ADATTN_LIST_STAGE");
     a.list_stage = (ls && *ls == '0') ? 0 : 1;

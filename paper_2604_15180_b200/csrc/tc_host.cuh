@@ -45,6 +45,20 @@ int forward_wtm_slots();
 bool pv_f16_enabled();
 // the forward fills g.ubar_out (delta fold) for this geometry
 bool fwd_delta_fold(const Geom& g);
+// delta from support lists: layout of the forward -> backward buffer (delta_aux) --
+// per 256-row block (a forward CTA's rows, global row index / 256) a fallback flag and a
+// pool of 256 * cap (key, u bits) entries; per row and key half (count, pool offset)
+struct SuppLayout {
+  uint32_t* flag;
+  int2* cnt;
+  uint2* ent;
+  int cap;
+  size_t nblk;
+};
+bool delta_supp_possible(const Geom& g);  // list mode, ADATTN_DELTA_SUPP != 0
+bool delta_supp_enabled(const Geom& g);   // ... and the forward does not fold delta
+size_t supp_bytes(const Geom& g);
+SuppLayout supp_layout(const Geom& g, void* base);
 
 // Power-of-two-scaled fp16 copies of bf16 operands (tc_common.cuh f16_pow2_scale),
 // per head (`heads` consecutive blocks of `elems` values, elems % 8 == 0), so a head's

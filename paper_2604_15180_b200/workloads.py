@@ -104,10 +104,11 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha:
              MAX + HIST + one REF sweep per refinement pass (the most steps of any
              row of the 256-row CTA + 1, from row_steps; 3 if not given) -- plus OUT
              (S and P V) over active tiles
-             + with the delta fold (default for alpha = 2; ADATTN_DELTA_FOLD=1/0;
+             + with the delta fold (alpha = 2 without support lists; ADATTN_DELTA_FOLD=1/0;
              single-CTA forward, n % 256 == 0, m % 128 == 0) U V over active tiles
-    tc_delta S, dP over active (128 rows x 128 keys) tiles; 0 with the delta fold
-             (delta = dO . Ubar / sum u: an HBM-bound row kernel)
+    tc_delta S, dP over active (128 rows x 128 keys) tiles; 0 with the support lists
+             (list mode: delta = sum u (dO . v) / sum u over each row's support, a
+             SIMT gather kernel) or the delta fold (delta = dO . Ubar / sum u)
     tc_dq    S, dP, dQ (fp16 sigma dS and K: one product -- default for alpha <= 1.5;
              bf16 hi/lo otherwise)
              over active (128 x 128) tiles
@@ -158,11 +159,16 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha:
     ds_f16 = d == 128 and (ds_env == "1" or (ds_env not in ("0", "1") and alpha <= 1.5))
     kv_pairs = os.environ.get("ADATTN_KV_PAIRS", "1") != "0"
     dq_pairs = os.environ.get("ADATTN_DQ_PAIRS", "1") != "0"
+    # delta source (tc.cu delta_supp_possible / tc_fwd.cu fwd_delta_fold): the forward's
+    # support lists in list mode (a SIMT gather kernel, no MMA), else the fold (alpha = 2,
+    # or ADATTN_DELTA_FOLD=1), else the S, dP pre-pass
+    supp = list_mode and os.environ.get("ADATTN_DELTA_SUPP", "1") != "0"
     fold_env = os.environ.get("ADATTN_DELTA_FOLD", "")
-    fold = ((fold_env == "1" or (fold_env in ("", "auto") and alpha == 2.0)) and n % 256 == 0
+    fold = ((fold_env == "1" or (fold_env in ("", "auto") and alpha == 2.0 and not supp))
+            and n % 256 == 0
             and (d != 128 or os.environ.get("ADATTN_FWD_PAIRS", "0") in ("", "0")))
     return {"tc_fwd": (sweeps_fwd + (3 if fold else 2) * act) * tile,
-            "tc_delta": (0 if fold else 2) * act * tile,
+            "tc_delta": (0 if (fold or supp) else 2) * act * tile,
             "tc_dq": (3 if ds_f16 and dq_pairs else 4) * act * tile,
             "tc_dkdv": (4 + (0 if dv_f16 else 1) + (0 if ds_f16 and kv_pairs else 1))
             * units * (2.0 * 128 * 64 * d)}

@@ -546,10 +546,12 @@ def test_tc_delta_fold_matches_prepass(case, monkeypatch):
     backward forms delta = dO . Ubar / sum u) against the delta
     pre-pass kernel (ADATTN_DELTA_FOLD=0): the forward's own outputs are
     bit-identical (same P, same product order).  At alpha = 2 (u in {0, 1}, the
-    default-on case) delta and the gradients agree to fp32 summation order; at
-    other alpha the fp16 u moves delta by up to ~5e-3 (measured; off by default)."""
+    default-on case without support lists) delta and the gradients agree to fp32
+    summation order; at other alpha the fp16 u moves delta by up to ~5e-3 (measured;
+    off by default)."""
     B, H, N, D, alpha, causal, qs, bins = case
     q, k, v, do = inputs(hash(case) % 883 + 5, B, H, N, D, qs)
+    monkeypatch.setenv("ADATTN_DELTA_SUPP", "0")  # fold vs the pre-pass (support lists off)
     monkeypatch.setenv("ADATTN_DELTA_FOLD", "0")
     _, r0, g0 = run(q, k, v, do, "tc", alpha=alpha, causal=causal, bins=bins)
     assert r0.delta_aux is None
@@ -610,3 +612,33 @@ def test_tc_list_staging_whole_vs_per_thread(case, monkeypatch):
     _, r1, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
     assert torch.equal(r0.tau, r1.tau) and torch.equal(r0.row_steps, r1.row_steps)
     assert torch.equal(r0.mask.words, r1.mask.words) and torch.equal(r0.out, r1.out)
+
+
+@pytest.mark.parametrize("case", [(1, 2, 4096, 128, 1.5, True, 1.0), (1, 2, 2048, 64, 1.5, False, 1.0),
+                                  (1, 2, 4096, 128, 1.75, True, 2.0), (2, 1, 2048, 128, 2.0, True, 1.0),
+                                  (1, 1, 8192, 128, 1.5, True, 8.0)],
+                         ids=str)
+@pytest.mark.parametrize("cap", [None, "2"], ids=["cap48", "cap2-overflow"])
+def test_tc_delta_support_lists_match_prepass(case, cap, monkeypatch):
+    """delta from the forward's support lists (keys and u of the scores with t > 0 at the
+    final tau; the backward sums u (dO . v) over them) equals the delta pre-pass, which
+    sums u dp over every active block (u = 0 off the support): within fp32 summation
+    order, and the gradients within the same margin.  A pool of 2 entries per row overflows
+    on every 256-row block: those blocks fall back to the pre-pass kernel."""
+    B, H, N, D, alpha, causal, qs = case
+    q, k, v, do = inputs(hash(case) % 877 + 3, B, H, N, D, qs)
+    monkeypatch.setenv("ADATTN_DELTA_FOLD", "0")
+    monkeypatch.setenv("ADATTN_DELTA_SUPP", "0")
+    _, r0, g0 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_DELTA_SUPP", "1")
+    if cap:
+        monkeypatch.setenv("ADATTN_SUPP_CAP", cap)
+    _, r1, g1 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    assert torch.equal(r0.tau, r1.tau) and torch.equal(r0.out, r1.out)
+    dscale = g0.delta.abs().max().item() + 1e-30
+    derr = (g1.delta - g0.delta).abs().max().item()
+    errs = {n: (getattr(g1, n) - getattr(g0, n)).abs().max().item() for n in ("dq", "dk", "dv")}
+    print(case, cap, f"delta {derr:.2e} (max |delta| {dscale:.2f})", errs)
+    assert derr <= 1e-5 * max(dscale, 1.0)
+    for n, e in errs.items():  # fp32 summation order of delta, through dS = u (dp - delta)
+        assert e <= 1e-4 * max(getattr(g0, n).abs().max().item(), 1.0) + 1e-4, n
