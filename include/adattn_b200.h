@@ -141,16 +141,22 @@ typedef struct {
    * their transpose) to skip zero tiles (attention.cpp:334-352, 462-535). */
   int32_t* block_cnt;
   uint16_t* block_cols;
-  /* DEVICE float [B][H][n][dv] then float [B][H][n] (optional; size from
-   * adattn_b200_delta_aux_bytes, NULL or 0 bytes: not filled): the output pass's
-   * Ubar_i = sum_j u_ij v_j and sum_j u_ij, u = p^(2 - alpha).  Passed to
-   * adattn_b200_backward_ex, it replaces the delta pre-pass (two products per
-   * active tile, attention.cpp:411-446) by delta_i = dO_i . Ubar_i / sum_j u_ij. */
+  /* DEVICE buffer (optional; size from adattn_b200_delta_aux_bytes, NULL or 0
+   * bytes: not filled) the forward leaves for the backward's delta
+   * (attention.cpp:411-446), which it then forms without the delta pre-pass (two
+   * products per active tile).  Default (candidate-list mode, alpha >= 1.4): the
+   * support lists -- for every row the keys j and u_ij = p_ij^(2 - alpha) of its
+   * scores with t > 0 at the final tau, pooled per 256-row block; the backward
+   * sums delta_i = sum_j u_ij (dO_i . v_j) / sum_j u_ij (blocks whose pool
+   * overflowed fall back to the pre-pass).  With the delta fold
+   * (ADATTN_DELTA_FOLD=1): float Ubar_i = sum_j u_ij v_j [B][H][n][dv], then
+   * sum_j u_ij [B][H][n], and delta_i = dO_i . Ubar_i / sum_j u_ij. */
   float* delta_aux;
 } adattn_forward_extras;
 
 /* Bytes of adattn_forward_extras.delta_aux the forward fills for this problem
- * (tensor-core path, single-CTA forward, no padded dimension), else 0. */
+ * (tensor-core path, no padded dimension; support lists in candidate-list mode,
+ * else the fold where it applies), else 0. */
 size_t adattn_b200_delta_aux_bytes(const adattn_problem* p);
 
 int adattn_b200_forward_ex(const adattn_problem* p, const void* q, const void* k,
