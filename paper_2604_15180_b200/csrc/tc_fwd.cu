@@ -1435,9 +1435,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // per-thread staging the longest lists of a CTA (up to ~230 entries) were read
         // from L2 in every round and the barriers waited on them.  Otherwise each
         // thread's first lcap scores ([i][thread], conflict-free) and L2 beyond.
-        constexpr int kEmax = NST * L::TILE / 7;
-        uint16_t* sblk = reinterpret_cast<uint16_t*>(sRing + 4 * kEmax);  // key >> 6
-        uint8_t* sko = sRing + 6 * kEmax;                                   // key & 63
+        // entries: f32 score + u16 key (m <= 65536: 21.8K entries at d = 128), else
+        // f32 score + u16 key >> 6 + u8 key & 63 (18.7K)
+        const bool k16 = g.m <= 65536;
+        const int kEmax = k16 ? NST * L::TILE / 6 : NST * L::TILE / 7;
+        uint16_t* sblk = reinterpret_cast<uint16_t*>(sRing + 4 * kEmax);  // key (k16) or key >> 6
+        uint8_t* sko = sRing + 6 * kEmax;                                   // key & 63 (!k16)
         int sbase = 0;
         bool full;
         {
@@ -1485,8 +1488,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (i < ns) {
               sl[sidx(i)] = __uint_as_float(sx);
               if (full) {
-                sblk[sbase + i] = (uint16_t)(sy >> 6);
-                sko[sbase + i] = (uint8_t)(sy & 63u);
+                if (k16) {
+                  sblk[sbase + i] = (uint16_t)sy;
+                } else {
+                  sblk[sbase + i] = (uint16_t)(sy >> 6);
+                  sko[sbase + i] = (uint8_t)(sy & 63u);
+                }
               }
             }
             const float z = fmaf(A1, __uint_as_float(sx), Bf);
@@ -1600,7 +1607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int j = 0; j < 8; ++j) {
                 const float t = fmaf(A1, accs[j], C);
                 if (row_real && t > -1e-9f) {
-                  const uint32_t bk = sblk[sbase + i0 + j];
+                  const uint32_t bk = k16 ? (uint32_t)sblk[sbase + i0 + j] >> 6 : sblk[sbase + i0 + j];
                   atomicOr(&smask[rb * wpr + (bk >> 5)], 1u << (bk & 31));
                   ns_ += t > 0.f;
                 }
@@ -1648,20 +1655,31 @@ __global__ void __launch_bounds__(kThreads, 1)
               int off = pre + x - ns_;
               a.supp_cnt[srow * 2 + half] = make_int2(ns_, off);
               uint2* pool = a.supp + blk256 * (size_t)pc;
-              for (int i = 0; i < cnt; ++i) {
-                float acc;
-                uint32_t key;
-                if (full) {
-                  acc = sl[sbase + i];
-                  key = ((uint32_t)sblk[sbase + i] << 6) | sko[sbase + i];
-                } else {
-                  const uint2 en = lst[i];
-                  acc = __uint_as_float(en.x);
-                  key = en.y;
+              for (int i0 = 0; i0 < cnt; i0 += 8) {  // 8 entries in flight
+                float accs[8];
+                uint32_t keys[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const int i = i0 + j;
+                  if (i >= cnt) {
+                    accs[j] = -CUDART_INF_F;
+                    keys[j] = 0u;
+                  } else if (full) {
+                    accs[j] = sl[sbase + i];
+                    keys[j] = k16 ? (uint32_t)sblk[sbase + i]
+                                  : ((uint32_t)sblk[sbase + i] << 6) | sko[sbase + i];
+                  } else {
+                    const uint2 en = lst[i];
+                    accs[j] = __uint_as_float(en.x);
+                    keys[j] = en.y;
+                  }
                 }
-                const float t = fmaf(A1, acc, C);
-                if (row_real && t > 0.f)
-                  pool[off++] = make_uint2(key, __float_as_uint(u_of<AK>(t, a.e1f)));
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const float t = fmaf(A1, accs[j], C);
+                  if (row_real && t > 0.f)
+                    pool[off++] = make_uint2(keys[j], __float_as_uint(u_of<AK>(t, a.e1f)));
+                }
               }
             }
           }

@@ -642,3 +642,19 @@ def test_tc_delta_support_lists_match_prepass(case, cap, monkeypatch):
     assert derr <= 1e-5 * max(dscale, 1.0)
     for n, e in errs.items():  # fp32 summation order of delta, through dS = u (dp - delta)
         assert e <= 1e-4 * max(getattr(g0, n).abs().max().item(), 1.0) + 1e-4, n
+
+
+@pytest.mark.parametrize("case", [(1, 2, 4096, 1.5, True, 1.0), (1, 1, 2048, 2.0, False, 2.0)], ids=str)
+def test_tc_delta_support_lists_pair_forward(case, monkeypatch):
+    """The CTA-pair forward (ADATTN_FWD_PAIRS=1) writes the same support lists as the
+    single-CTA forward (each CTA its own 256 rows): identical delta and gradients."""
+    B, H, N, alpha, causal, qs = case
+    q, k, v, do = inputs(hash(case) % 701 + 9, B, H, N, 128, qs)
+    monkeypatch.setenv("ADATTN_FWD_PAIRS", "0")
+    _, r0, g0 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_FWD_PAIRS", "1")
+    _, r1, g1 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    assert r0.delta_aux is not None and r1.delta_aux is not None
+    assert torch.equal(r0.tau, r1.tau) and torch.equal(r0.out, r1.out)
+    for n in ("delta", "dq", "dk", "dv"):
+        assert torch.equal(getattr(g0, n), getattr(g1, n)), n
