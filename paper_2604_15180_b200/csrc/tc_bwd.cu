@@ -2005,7 +2005,7 @@ __global__ void __launch_bounds__(256) delta_supp_kernel(
     uint2 my = make_uint2(0u, 0u);
     if (idx < tot) my = idx < c0 ? base[h0.y + idx] : base[h1.y + idx - c0];
     const int nk = min(32, tot - b);
-#pragma unroll 4
+#pragma unroll 16
     for (int k = 0; k < nk; ++k) {
       const uint32_t key = __shfl_sync(0xffffffffu, my.x, k);
       const float u = __uint_as_float(__shfl_sync(0xffffffffu, my.y, k));
