@@ -192,22 +192,42 @@ static int supp_cap_of() {
   if (const char* s = std::getenv("ADATTN_SUPP_CAP")) cap = std::max(1, std::atoi(s));
   return cap;
 }
+// layout (tc_host.cuh SuppLayout), 256-byte aligned sections
+static size_t supp_sections(const Geom& g, size_t off[9]) {
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t rows = (size_t)g.bh * g.n, nblk = (rows + 255) / 256;
+  const size_t ent = nblk * 256 * (size_t)supp_cap_of();
+  const size_t sz[9] = {nblk * 4, (size_t)g.bh * 4, rows * 2 * 8, ent * 8,
+                        (size_t)g.bh * g.m * 4, (size_t)g.bh * (g.m + 1) * 4,
+                        (size_t)g.bh * g.m * 4, ent * 4, ent * 8};
+  size_t o = 0;
+  for (int i = 0; i < 9; ++i) {
+    off[i] = o;
+    o += al(sz[i]);
+  }
+  return o;
+}
 size_t supp_bytes(const Geom& g) {
   if (!delta_supp_enabled(g)) return 0;
-  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-  const size_t rows = (size_t)g.bh * g.n, nblk = (rows + 255) / 256;
-  return al(nblk * 4) + al(rows * 2 * 8) + nblk * 256 * (size_t)supp_cap_of() * 8;
+  size_t off[9];
+  return supp_sections(g, off);
 }
 SuppLayout supp_layout(const Geom& g, void* base) {
-  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-  const size_t rows = (size_t)g.bh * g.n, nblk = (rows + 255) / 256;
+  size_t off[9];
+  supp_sections(g, off);
   uint8_t* p = reinterpret_cast<uint8_t*>(base);
   SuppLayout l;
-  l.flag = reinterpret_cast<uint32_t*>(p);
-  l.cnt = reinterpret_cast<int2*>(p + al(nblk * 4));
-  l.ent = reinterpret_cast<uint2*>(p + al(nblk * 4) + al(rows * 2 * 8));
+  l.flag = reinterpret_cast<uint32_t*>(p + off[0]);
+  l.hflag = reinterpret_cast<uint32_t*>(p + off[1]);
+  l.cnt = reinterpret_cast<int2*>(p + off[2]);
+  l.ent = reinterpret_cast<uint2*>(p + off[3]);
+  l.kcnt = reinterpret_cast<int32_t*>(p + off[4]);
+  l.koff = reinterpret_cast<int32_t*>(p + off[5]);
+  l.kcur = reinterpret_cast<int32_t*>(p + off[6]);
+  l.krow = reinterpret_cast<int32_t*>(p + off[7]);
+  l.kpd = reinterpret_cast<float2*>(p + off[8]);
   l.cap = supp_cap_of();
-  l.nblk = nblk;
+  l.nblk = ((size_t)g.bh * g.n + 255) / 256;
   return l;
 }
 

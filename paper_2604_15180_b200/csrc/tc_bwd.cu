@@ -77,6 +77,9 @@ struct BwdArgs {
   // delta kernels: 256-row blocks (global row / 256) whose delta the support kernel
   // formed are skipped (supp_skip[block] == 0); nullptr: every block
   const uint32_t* supp_skip;
+  // dQ kernels: heads whose dQ the support-list rows kernel formed (dq_skip[bh] == 0)
+  const uint32_t* dq_skip;
+  const void* kp;  // bf16 [bh*m][d] (dQ from the support lists)
   int skip_f16;      // pair dK/dV two-buffer kernel: skip heads the SLOT3 kernel takes
   // fp16 operand plan of the pair dQ and dK/dV kernels (device; nullptr: bf16 hi/lo)
   const struct F16Plan* f16;
@@ -1088,6 +1091,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int jmax = g.causal ? (row0 + QB_DQ - 1) / DBN : nkt - 1;
   const int wpr = g.wpr;
 
+  if (a.dq_skip && a.dq_skip[bh] == 0u) return;  // dQ from the support lists
   rows_from_lists(smask, 2, a, bh, row0 / 64, tid, kThreads);
   if (tid == 0) {
     for (int i = 0; i < NSK; ++i) {
@@ -1377,6 +1381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int jmax = g.causal ? (prow0 + 2 * QB_DQ - 1) / DBN : nkt - 1;
   const int wpr = g.wpr;
 
+  if (a.dq_skip && a.dq_skip[bh] == 0u) return;  // dQ from the support lists (both CTAs)
   rows_from_lists(smask, 4, a, bh, prow0 / 64, tid, kThreads);
   if (tid == 0) {
     for (int i = 0; i < NSK; ++i) {
@@ -1955,27 +1960,33 @@ __global__ void delta_ubar_kernel(const uint16_t* __restrict__ dout, const float
   }
 }
 
-// delta from the support lists (Geom::supp_in, written by the forward's list phase):
-// delta_i = sum_e u_e (dO_i . v_{j_e}) / sum_e u_e over the row's entries (key half 0,
-// then half 1, list order; 0 when the sum is 0, attention.cpp:444) -- the terms the delta
-// kernel sums (u = 0 outside the support), without recomputing S and dP for every active
-// block: ~30 entries per row at C3 against 16K keys.  One warp per row, lane l holds d
-// elements l*E..; the head's V rows stay L2-resident.  Heads the forward flagged (a row
-// half over the cap, or a CTA that fell back to the sweeps) are left to the delta kernel.
+// delta and dQ from the support lists (Geom::supp_in, written by the forward's list
+// phase: per row its keys j and t_ij > 0 at the final tau).  The backward's terms vanish
+// off the support (u = p = 0 for t <= 0, attention.cpp:411-446, 508-535), so per row:
+//   dp_j = dO_i . v_j,  delta_i = sum u_j dp_j / sum u_j  (0 when the sum is 0),
+//   dQ_i = scale * sum_j u_j (dp_j - delta_i) k_j
+// over ~30 entries at C3 instead of S and dP over every active block (the delta
+// pre-pass: two products per tile, the dQ kernel: three).  One warp per row, lane l holds
+// d elements l*E..; the head's K / V rows stay L2-resident (rows run head by head).
+// Entries go in list order (key half 0, then half 1), sums in fp64: deterministic.
+// Rows of a 256-row block the forward flagged are left to the delta kernel (its unit
+// of `unit` rows runs when any of its blocks is flagged); dQ only for heads without a
+// flagged block (hflag; the tensor-core dQ kernel takes the others) -- a row with more
+// than 96 entries flags its head here (the dQ kernel runs after this one).
 // Also rowc_i = (C_i, delta_i) for the dK/dV kernel, as the delta kernels form it.
-template <int D>
-__global__ void __launch_bounds__(256) delta_supp_kernel(
-    const uint16_t* __restrict__ dout, const uint16_t* __restrict__ vv, const uint2* __restrict__ pool,
-    const int2* __restrict__ cnt, const uint32_t* __restrict__ flag, int cap, int unit,
-    const double* __restrict__ tau, const double* __restrict__ row_max, double alpha, size_t rows,
-    int n, int m, double* delta, float2* rowc) {
+template <int D, int AK>
+__global__ void __launch_bounds__(256) sparse_rows_kernel(
+    const uint16_t* __restrict__ dout, const uint16_t* __restrict__ vv, const uint16_t* __restrict__ kk,
+    const uint2* __restrict__ pool, const int2* __restrict__ cnt, const uint32_t* __restrict__ flag,
+    uint32_t* hflag, int cap, int unit, const double* __restrict__ tau,
+    const double* __restrict__ row_max, double alpha, float e0f, float e1f, float scale,
+    size_t rows, int n, int m, int out_f64, bool want_dq, void* dq, double* delta, float2* rowc) {
   constexpr int E = D / 32;
+  constexpr int NCH = 3;  // entries kept in registers: 3 x 32 per row (C3: ~30)
   const size_t r = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
   const size_t bh = r / (size_t)n;
-  // the delta kernel's unit of `unit` rows (head-aligned) runs when any of its 256-row
-  // blocks is flagged; its rows are left to it (one writer per row)
   const size_t u0 = (bh * n + (r - bh * n) / unit * unit) / 256;
   for (int b = 0; b < unit / 256; ++b)
     if (flag[u0 + b]) return;
@@ -1983,53 +1994,101 @@ __global__ void __launch_bounds__(256) delta_supp_kernel(
   const int c0 = h0.x, tot = h0.x + h1.x;
   const uint2* base = pool + (r / 256) * (size_t)(256 * cap);
   const uint16_t* vb = vv + bh * (size_t)m * D + lane * E;
-  float acc[E];
-#pragma unroll
-  for (int x = 0; x < E; ++x) acc[x] = 0.f;
-  double su = 0.0;
-  auto add = [&](uint32_t key, float u) {
+  const uint16_t* kb = kk + bh * (size_t)m * D + lane * E;
+  auto ld_row = [&](const uint16_t* p, float* x) {  // E bf16 of a row -> fp32
     if constexpr (E == 4) {
-      const uint2 w = *reinterpret_cast<const uint2*>(vb + (size_t)key * D);
-      acc[0] = fmaf(u, __uint_as_float(w.x << 16), acc[0]);
-      acc[1] = fmaf(u, __uint_as_float(w.x & 0xFFFF0000u), acc[1]);
-      acc[2] = fmaf(u, __uint_as_float(w.y << 16), acc[2]);
-      acc[3] = fmaf(u, __uint_as_float(w.y & 0xFFFF0000u), acc[3]);
+      const uint2 w = *reinterpret_cast<const uint2*>(p);
+      x[0] = __uint_as_float(w.x << 16);
+      x[1] = __uint_as_float(w.x & 0xFFFF0000u);
+      x[2] = __uint_as_float(w.y << 16);
+      x[3] = __uint_as_float(w.y & 0xFFFF0000u);
     } else {
-      const uint32_t w = *reinterpret_cast<const uint32_t*>(vb + (size_t)key * D);
-      acc[0] = fmaf(u, __uint_as_float(w << 16), acc[0]);
-      acc[1] = fmaf(u, __uint_as_float(w & 0xFFFF0000u), acc[1]);
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+      x[0] = __uint_as_float(w << 16);
+      x[1] = __uint_as_float(w & 0xFFFF0000u);
     }
   };
-  for (int b = 0; b < tot; b += 32) {
-    const int idx = b + lane;  // lane l fetches entry b + l (half 0's, then half 1's)
+  float dov[E];
+  ld_row(dout + r * D + lane * E, dov);
+  // phase 1: dp of every entry (warp dot products), delta
+  uint32_t keyr[NCH];
+  float ur[NCH], dpr[NCH];
+  double num = 0.0, den = 0.0;
+  for (int b = 0, ch = 0; b < tot; b += 32, ++ch) {
+    const int idx = b + lane;
     uint2 my = make_uint2(0u, 0u);
     if (idx < tot) my = idx < c0 ? base[h0.y + idx] : base[h1.y + idx - c0];
+    float p_, u_;
+    pu_of<AK>(__uint_as_float(my.y), e0f, e1f, p_, u_);
+    if (idx >= tot) u_ = 0.f;
     const int nk = min(32, tot - b);
-#pragma unroll 16
+    float dpk = 0.f;
+#pragma unroll 8
     for (int k = 0; k < nk; ++k) {
       const uint32_t key = __shfl_sync(0xffffffffu, my.x, k);
-      const float u = __uint_as_float(__shfl_sync(0xffffffffu, my.y, k));
-      su += (double)u;
-      add(key, u);
-    }
-  }
-  const uint16_t* dp = dout + r * D + lane * E;
-  float dot = 0.f;
-  if constexpr (E == 4) {
-    const uint2 w = *reinterpret_cast<const uint2*>(dp);
-    dot = __uint_as_float(w.x << 16) * acc[0] + __uint_as_float(w.x & 0xFFFF0000u) * acc[1] +
-          __uint_as_float(w.y << 16) * acc[2] + __uint_as_float(w.y & 0xFFFF0000u) * acc[3];
-  } else {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(dp);
-    dot = __uint_as_float(w << 16) * acc[0] + __uint_as_float(w & 0xFFFF0000u) * acc[1];
-  }
+      float x[E];
+      ld_row(vb + (size_t)key * D, x);
+      float s = 0.f;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      for (int e = 0; e < E; ++e) s = fmaf(dov[e], x[e], s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      const float uk = __shfl_sync(0xffffffffu, u_, k);
+      num += (double)uk * (double)s;
+      den += (double)uk;
+      if (lane == k) dpk = s;
+    }
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+      if (c == ch) {
+        keyr[c] = my.x;
+        ur[c] = u_;
+        dpr[c] = dpk;
+      }
+  }
+  const double dlt = den > 0.0 ? num / den : 0.0;
   if (lane == 0) {
-    const double dlt = su > 0.0 ? (double)dot / su : 0.0;
     const double B = 1.0 - (alpha - 1.0) * row_max[r];
     delta[r] = dlt;
     rowc[r] = make_float2((float)(B - tau[r]), (float)dlt);
+  }
+  if (!want_dq || hflag[bh]) return;
+  if (tot > NCH * 32) {  // the tensor-core dQ kernel (launched after this one) takes the head
+    if (lane == 0) atomicOr(&hflag[bh], 1u);
+    return;
+  }
+  // phase 2: dQ_i = scale * sum_j dS_j k_j, dS_j = u_j (dp_j - delta_i)
+  const float dl = (float)dlt;
+  float acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int b = c * 32;
+    if (b >= tot) break;
+    const float dsc = ur[c] * (dpr[c] - dl);
+    const int nk = min(32, tot - b);
+#pragma unroll 8
+    for (int k = 0; k < nk; ++k) {
+      const uint32_t key = __shfl_sync(0xffffffffu, keyr[c], k);
+      const float ds = __shfl_sync(0xffffffffu, dsc, k);
+      float x[E];
+      ld_row(kb + (size_t)key * D, x);
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = fmaf(ds, x[e], acc[e]);
+    }
+  }
+  if (out_f64) {
+    double* dst = reinterpret_cast<double*>(dq) + r * D + lane * E;
+#pragma unroll
+    for (int e = 0; e < E; ++e) dst[e] = (double)(scale * acc[e]);
+  } else {
+    float* dst = reinterpret_cast<float*>(dq) + r * D + lane * E;
+    if constexpr (E == 4) {
+      *reinterpret_cast<float4*>(dst) = make_float4(scale * acc[0], scale * acc[1], scale * acc[2], scale * acc[3]);
+    } else {
+      *reinterpret_cast<float2*>(dst) = make_float2(scale * acc[0], scale * acc[1]);
+    }
   }
 }
 
@@ -2490,6 +2549,13 @@ bool ds_f16_enabled(const Geom& g) {
   return g.alpha <= 1.5;
 }
 
+// dQ from the support lists with delta (sparse_rows_kernel; ADATTN_SPARSE_DQ=0: the
+// tensor-core dQ kernel)
+bool sparse_dq_enabled() {
+  const char* s = std::getenv("ADATTN_SPARSE_DQ");
+  return !(s && *s == '0');
+}
+
 // three-slot pair dK/dV kernel for the fp16 P / dS heads (ADATTN_KV_SLOT3=0: two buffers)
 bool kv_slot3_enabled(const Geom& g) {
   const char* s = std::getenv("ADATTN_KV_SLOT3");
@@ -2515,19 +2581,23 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
   const int dmode = delta_mode(g, a.ncta_rows);
   BwdArgs ad = a;  // the delta kernels' arguments (support mode: flagged heads only)
   const char* dname = "tc_delta";
-  if (g.supp_in && !delta_only) {  // delta from the forward's support lists
+  BwdArgs aq = a;  // the dQ kernels' arguments (support lists: flagged heads only)
+  if (g.supp_in && !delta_only) {  // delta (and dQ) from the forward's support lists
     const SuppLayout sl = supp_layout(g, const_cast<void*>(g.supp_in));
     const size_t rows = (size_t)g.bh * g.n;
+    const bool want_dq = sparse_dq_enabled() && g.d == g.dv;
     prof_begin("tc_delta", st);
-    delta_supp_kernel<D><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(
-        reinterpret_cast<const uint16_t*>(a.dout), reinterpret_cast<const uint16_t*>(a.v), sl.ent,
-        sl.cnt, sl.flag, sl.cap, dmode == 1 ? 512 : 256, a.tau, a.row_max, g.alpha, rows, g.n, g.m,
-        a.delta, a.rowc);
+    sparse_rows_kernel<D, AK><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(a.dout), reinterpret_cast<const uint16_t*>(a.v),
+        reinterpret_cast<const uint16_t*>(a.kp), sl.ent, sl.cnt, sl.flag, sl.hflag, sl.cap,
+        dmode == 1 ? 512 : 256, a.tau, a.row_max, g.alpha, a.e0f, a.e1f, (float)g.scale, rows,
+        g.n, g.m, g.out_dtype == ADATTN_F64 ? 1 : 0, want_dq, a.dq, a.delta, a.rowc);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
     ad.supp_skip = sl.flag;
     dname = "tc_delta_fb";
+    if (want_dq) aq.dq_skip = sl.hflag;
   }
   if (g.ubar_in && !delta_only) {  // delta from the forward's fold
     const size_t rows = (size_t)g.bh * g.n;
@@ -2604,9 +2674,9 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     auto k1 = ds_f16_enabled(g) ? tc_dq2_kernel<128, AK, true> : tc_dq2_kernel<128, AK, false>;
     const size_t sm = Dq2Smem<128>::bytes(g.wpr);
     if ((e = set_smem(k1, sm))) return e;
-    prof_begin("tc_dq", st);
+    prof_begin(aq.dq_skip ? "tc_dq_fb" : "tc_dq", st);
     k1<<<dim3((unsigned)((g.n / QB_DQ) * g.bh)), kThreads, sm, st>>>(m[8], m[10], m[1], m[11], m[9],
-                                                                      m[15], a);
+                                                                      m[15], aq);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
@@ -2614,8 +2684,8 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     auto k1 = tc_dq_kernel<D, AK>;
     const size_t sm = DqSmem<D>::bytes(g.wpr);
     if ((e = set_smem(k1, sm))) return e;
-    prof_begin("tc_dq", st);
-    k1<<<dim3((unsigned)((g.n / QB_DQ) * g.bh)), kThreads, sm, st>>>(m[8], m[1], m[2], m[9], a);
+    prof_begin(aq.dq_skip ? "tc_dq_fb" : "tc_dq", st);
+    k1<<<dim3((unsigned)((g.n / QB_DQ) * g.bh)), kThreads, sm, st>>>(m[8], m[1], m[2], m[9], aq);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
@@ -2713,7 +2783,9 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   a.rowc = reinterpret_cast<float2*>(workspace);
   a.dout = dout;
   a.v = v;
+  a.kp = k;
   a.supp_skip = nullptr;
+  a.dq_skip = nullptr;
   a.skip_f16 = 0;
   a.f16 = nullptr;
   m[14] = m[7];

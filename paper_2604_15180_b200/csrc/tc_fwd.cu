@@ -170,9 +170,11 @@ struct FwdArgs {
   // the scores with t > 0 at the final tau, per 256-row CTA block in a pool of
   // 256 * supp_cap entries; per row and key half (count, pool offset); supp_flag[block] = 1
   // when the block's pool overflowed or the CTA fell back to the sweeps; nullptr: off
-  uint2* supp;
+  uint2* supp;           // entries (key, t bits): t > 0 at the final tau
   int2* supp_cnt;
-  uint32_t* supp_flag;
+  uint32_t* supp_flag;   // per 256-row block
+  uint32_t* supp_hflag;  // per head: any of its blocks flagged
+  int32_t* supp_kcnt;    // per key of every head: support entries (the backward's transpose)
   int supp_cap;
   // fp16 P V: per head, max |V| (float bits) of the scaled fp16 V copy; nullptr -> bf16 P
   const uint32_t* v16_max;
@@ -250,23 +252,6 @@ __device__ __forceinline__ float p_of(float t, float e0f) {
 
 // Partial sums of one 32-element slice for the refinement pass: two
 // independent accumulator sets of packed f32x2 for ILP.
-// u = p^(2 - alpha) = t^(e0 - 1) for t > 0 (the backward's pu_of, tc_bwd.cu: the same
-// operations, so the support lists carry the u the delta kernel would form)
-template <int AK>
-__device__ __forceinline__ float u_of(float t, float e1f) {
-  const float tp = fmaxf(t, 0.f);
-  if constexpr (AK == AK15) {
-    return tp;
-  } else if constexpr (AK == AK2) {
-    return __saturatef(tp * 0x1p126f);
-  } else if constexpr (AK == AK125) {
-    const float t2 = tp * tp;
-    return t2 * tp;
-  } else {
-    return tp > 0.f ? exp2f(e1f * __log2f(tp)) : 0.f;
-  }
-}
-
 template <int AK>
 __device__ __forceinline__ void ref_slice(const float* v, float A1, float C, float e0f, float e1f,
                                           float e2f, float& s0o, float& s1o, float& s2o,
@@ -1650,7 +1635,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const size_t blk256 = ((size_t)bh * g.n + row0) / BM;
             const size_t srow = (size_t)bh * g.n + grow;
             if (tot > pc) {
-              if (tid == 0) a.supp_flag[blk256] = 1u;  // the delta kernel takes these rows
+              if (tid == 0) {  // the delta kernel (and the tensor-core backward) take these rows
+                a.supp_flag[blk256] = 1u;
+                a.supp_hflag[bh] = 1u;
+              }
             } else {
               int off = pre + x - ns_;
               a.supp_cnt[srow * 2 + half] = make_int2(ns_, off);
@@ -1677,8 +1665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                   const float t = fmaf(A1, accs[j], C);
-                  if (row_real && t > 0.f)
-                    pool[off++] = make_uint2(keys[j], __float_as_uint(u_of<AK>(t, a.e1f)));
+                  if (row_real && t > 0.f) pool[off++] = make_uint2(keys[j], __float_as_uint(t));
                 }
               }
             }
@@ -1704,7 +1691,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       dround = 1;
       if (!list_ok) {
         // no support lists for this CTA's rows: the backward's delta kernel takes the head
-        if (tid == 0 && a.supp) a.supp_flag[((size_t)bh * g.n + row0) / BM] = 1u;
+        if (tid == 0 && a.supp) {
+          a.supp_flag[((size_t)bh * g.n + row0) / BM] = 1u;
+          a.supp_hflag[bh] = 1u;
+        }
         hist_solve();  // fallback: the exact histogram by the HIST sweep
       }
     }
@@ -2208,6 +2198,8 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.supp = nullptr;
   a.supp_cnt = nullptr;
   a.supp_flag = nullptr;
+  a.supp_hflag = nullptr;
+  a.supp_kcnt = nullptr;
   a.supp_cap = 0;
   if (!a.ubar && a.cand && g.supp_out && delta_supp_enabled(g)) {  // (list mode only)
     const SuppLayout sl = supp_layout(g, g.supp_out);
@@ -2215,10 +2207,14 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
     a.supp = sl.ent;
     a.supp_cnt = sl.cnt;
     a.supp_flag = sl.flag;
+    a.supp_hflag = sl.hflag;
+    a.supp_kcnt = sl.kcnt;
     a.supp_cap = sl.cap;
+    if ((e = cudaMemsetAsync(sl.hflag, 0, 4 * (size_t)g.bh, st))) return e;
   } else if (g.supp_out && delta_supp_enabled(g)) {  // no lists written: every head flagged
     const SuppLayout sl = supp_layout(g, g.supp_out);
     if ((e = cudaMemsetAsync(sl.flag, 1, 4 * sl.nblk, st))) return e;
+    if ((e = cudaMemsetAsync(sl.hflag, 1, 4 * (size_t)g.bh, st))) return e;
   }
   {
     const char* ls = std::getenv("ADATTN_LIST_STAGE");

@@ -49,9 +49,15 @@ bool fwd_delta_fold(const Geom& g);
 // per 256-row block (a forward CTA's rows, global row index / 256) a fallback flag and a
 // pool of 256 * cap (key, u bits) entries; per row and key half (count, pool offset)
 struct SuppLayout {
-  uint32_t* flag;
-  int2* cnt;
-  uint2* ent;
+  uint32_t* flag;   // [nblk] 256-row blocks whose rows the tensor-core kernels handle
+  uint32_t* hflag;  // [bh] heads with a flagged block (sparse backward: whole head)
+  int2* cnt;        // [rows][2] (count, pool offset)
+  uint2* ent;       // [nblk][256 cap] (key, t bits)
+  int32_t* kcnt;    // [bh][m] support entries per key (forward atomics)
+  int32_t* koff;    // [bh][m + 1] their exclusive prefix (backward)
+  int32_t* kcur;    // [bh][m] scatter cursors (backward)
+  int32_t* krow;    // [nblk 256 cap] key-major lists: query row ...
+  float2* kpd;      // ... and (p, dS)
   int cap;
   size_t nblk;
 };
