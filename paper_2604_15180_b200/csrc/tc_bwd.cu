@@ -79,7 +79,10 @@ struct BwdArgs {
   const uint32_t* supp_skip;
   // dQ kernels: heads whose dQ the support-list rows kernel formed (dq_skip[bh] == 0)
   const uint32_t* dq_skip;
+  // dK/dV kernels: heads whose dK/dV the support-list keys kernel formed (kv_skip[bh] == 0)
+  const uint32_t* kv_skip;
   const void* kp;  // bf16 [bh*m][d] (dQ from the support lists)
+  const void* qp;  // bf16 [bh*n][d] (dK from the support lists)
   int skip_f16;      // pair dK/dV two-buffer kernel: skip heads the SLOT3 kernel takes
   // fp16 operand plan of the pair dQ and dK/dV kernels (device; nullptr: bf16 hi/lo)
   const struct F16Plan* f16;
@@ -1662,6 +1665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int wpr = g.wpr;
   const int i_first = g.causal ? key0 / QT : 0;
 
+  if (a.kv_skip && a.kv_skip[bh] == 0u) return;  // dK/dV from the support lists
   units_from_lists(ubits, 2, a, bh, kb * KB / 64, threadIdx.x, kThreads);
   if (tid == 0) {
     for (int i = 0; i < KST; ++i) {
@@ -1978,7 +1982,8 @@ template <int D, int AK>
 __global__ void __launch_bounds__(256) sparse_rows_kernel(
     const uint16_t* __restrict__ dout, const uint16_t* __restrict__ vv, const uint16_t* __restrict__ kk,
     const uint2* __restrict__ pool, const int2* __restrict__ cnt, const uint32_t* __restrict__ flag,
-    uint32_t* hflag, int cap, int unit, const double* __restrict__ tau,
+    uint32_t* hflag, int cap, int unit, const int32_t* __restrict__ koff, int32_t* kcur,
+    int32_t* krow, float2* kpd, const double* __restrict__ tau,
     const double* __restrict__ row_max, double alpha, float e0f, float e1f, float scale,
     size_t rows, int n, int m, int out_f64, bool want_dq, void* dq, double* delta, float2* rowc) {
   constexpr int E = D / 32;
@@ -2012,7 +2017,7 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
   ld_row(dout + r * D + lane * E, dov);
   // phase 1: dp of every entry (warp dot products), delta
   uint32_t keyr[NCH];
-  float ur[NCH], dpr[NCH];
+  float ur[NCH], dpr[NCH], pr[NCH];
   double num = 0.0, den = 0.0;
   for (int b = 0, ch = 0; b < tot; b += 32, ++ch) {
     const int idx = b + lane;
@@ -2043,6 +2048,7 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
       if (c == ch) {
         keyr[c] = my.x;
         ur[c] = u_;
+        pr[c] = p_;
         dpr[c] = dpk;
       }
   }
@@ -2068,6 +2074,13 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
     if (b >= tot) break;
     const float dsc = ur[c] * (dpr[c] - dl);
     const int nk = min(32, tot - b);
+    if (koff && lane < nk) {  // this entry into its key's list (sorted by row in the keys kernel)
+      const size_t kj = bh * (size_t)m + keyr[c];
+      // head bh's lists live in its own n * cap entries
+      const size_t slot = bh * (size_t)n * cap + (size_t)(koff[kj + bh] + atomicAdd(&kcur[kj], 1));
+      krow[slot] = (int)(r - bh * n);
+      kpd[slot] = make_float2(pr[c], dsc);
+    }
 #pragma unroll 8
     for (int k = 0; k < nk; ++k) {
       const uint32_t key = __shfl_sync(0xffffffffu, keyr[c], k);
@@ -2088,6 +2101,140 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
       *reinterpret_cast<float4*>(dst) = make_float4(scale * acc[0], scale * acc[1], scale * acc[2], scale * acc[3]);
     } else {
       *reinterpret_cast<float2*>(dst) = make_float2(scale * acc[0], scale * acc[1]);
+    }
+  }
+}
+
+// exclusive prefix of the per-key support counts (the forward's atomics), one CTA per head
+// (koff[h (m + 1) + j]; heads with a flagged block are skipped)
+__global__ void __launch_bounds__(1024) supp_scan_kernel(const int32_t* __restrict__ kcnt,
+                                                         int32_t* koff, const uint32_t* hflag, int m) {
+  const int h = blockIdx.x;
+  if (hflag[h]) return;
+  __shared__ int ws[32];
+  const int32_t* c = kcnt + (size_t)h * m;
+  int32_t* o = koff + (size_t)h * (m + 1);
+  const int T = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int per = (m + T - 1) / T;
+  const int b0 = min(m, t * per), b1 = min(m, b0 + per);
+  int sum = 0;
+  for (int i = b0; i < b1; ++i) sum += c[i];
+  int x = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) ws[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int y = lane < T / 32 ? ws[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int z = __shfl_up_sync(0xffffffffu, y, d);
+      if (lane >= d) y += z;
+    }
+    ws[lane] = y;
+  }
+  __syncthreads();
+  int pre = (w ? ws[w - 1] : 0) + x - sum;
+  for (int i = b0; i < b1; ++i) {
+    o[i] = pre;
+    pre += c[i];
+  }
+  if (t == T - 1) o[m] = pre;
+}
+
+// dK and dV from the support lists, key-major: key j's entries (query row i, p_ij,
+// dS_ij) -- scattered by the rows kernel in arbitrary order -- are sorted by row (a
+// bitonic sort in shared memory: the summation order, and so every bit of the result,
+// is fixed), then dV_j = sum_i p_ij dO_i and dK_j = scale sum_i dS_ij q_i over gathered
+// dO / Q rows (attention.cpp:464-506: the terms vanish off the support).  One warp per
+// key; a key with more than kMaxKey entries flags its head (the tensor-core dK/dV
+// kernel, launched after this one, then takes the whole head).
+constexpr int kMaxKey = 1024;
+template <int D>
+__global__ void __launch_bounds__(128) sparse_keys_kernel(
+    const uint16_t* __restrict__ dout, const uint16_t* __restrict__ qq,
+    const int32_t* __restrict__ koff, const int32_t* __restrict__ krow,
+    const float2* __restrict__ kpd, uint32_t* hflag, int cap, float scale, size_t keys, int n,
+    int m, int out_f64, void* dk, void* dv) {
+  constexpr int E = D / 32;
+  __shared__ unsigned long long sk[4][kMaxKey];
+  const size_t kr = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  if (kr >= keys) return;
+  const size_t bh = kr / (size_t)m;
+  if (hflag[bh]) return;
+  const size_t j = kr - bh * m;
+  const int cntk = koff[bh * (m + 1) + j + 1] - koff[bh * (m + 1) + j];
+  const size_t s0 = bh * (size_t)n * cap + (size_t)koff[bh * (m + 1) + j];
+  if (cntk > kMaxKey) {
+    if (lane == 0) atomicOr(&hflag[bh], 1u);
+    return;
+  }
+  unsigned long long* sm = sk[wi];
+  int np = 32;
+  while (np < cntk) np <<= 1;
+  for (int i = lane; i < np; i += 32)
+    sm[i] = i < cntk ? ((unsigned long long)(uint32_t)krow[s0 + i] << 32) | (uint32_t)i : ~0ull;
+  __syncwarp();
+  for (int k = 2; k <= np; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = lane; i < np; i += 32) {
+        const int ixj = i ^ jj;
+        if (ixj > i) {
+          const unsigned long long x = sm[i], y = sm[ixj];
+          if ((x > y) == ((i & k) == 0)) {
+            sm[i] = y;
+            sm[ixj] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  const uint16_t* db = dout + bh * (size_t)n * D + lane * E;
+  const uint16_t* qb = qq + bh * (size_t)n * D + lane * E;
+  float av[E], ak[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) av[e] = ak[e] = 0.f;
+#pragma unroll 8
+  for (int i = 0; i < cntk; ++i) {
+    const unsigned long long x = sm[i];
+    const uint32_t row = (uint32_t)(x >> 32), sl = (uint32_t)x;
+    const float2 pd = kpd[s0 + sl];
+    float od[E], oq[E];
+    if constexpr (E == 4) {
+      const uint2 w0 = *reinterpret_cast<const uint2*>(db + (size_t)row * D);
+      const uint2 w1 = *reinterpret_cast<const uint2*>(qb + (size_t)row * D);
+      od[0] = __uint_as_float(w0.x << 16); od[1] = __uint_as_float(w0.x & 0xFFFF0000u);
+      od[2] = __uint_as_float(w0.y << 16); od[3] = __uint_as_float(w0.y & 0xFFFF0000u);
+      oq[0] = __uint_as_float(w1.x << 16); oq[1] = __uint_as_float(w1.x & 0xFFFF0000u);
+      oq[2] = __uint_as_float(w1.y << 16); oq[3] = __uint_as_float(w1.y & 0xFFFF0000u);
+    } else {
+      const uint32_t w0 = *reinterpret_cast<const uint32_t*>(db + (size_t)row * D);
+      const uint32_t w1 = *reinterpret_cast<const uint32_t*>(qb + (size_t)row * D);
+      od[0] = __uint_as_float(w0 << 16); od[1] = __uint_as_float(w0 & 0xFFFF0000u);
+      oq[0] = __uint_as_float(w1 << 16); oq[1] = __uint_as_float(w1 & 0xFFFF0000u);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      av[e] = fmaf(pd.x, od[e], av[e]);
+      ak[e] = fmaf(pd.y, oq[e], ak[e]);
+    }
+  }
+  const size_t orow = kr * D + lane * E;
+  if (out_f64) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      reinterpret_cast<double*>(dv)[orow + e] = (double)av[e];
+      reinterpret_cast<double*>(dk)[orow + e] = (double)(scale * ak[e]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      reinterpret_cast<float*>(dv)[orow + e] = av[e];
+      reinterpret_cast<float*>(dk)[orow + e] = scale * ak[e];
     }
   }
 }
@@ -2178,6 +2325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kKvThreads, 1)
   const int pj0 = pkey0 / 64;           // first of the pair's four reference key tiles
   const int i_first = g.causal ? pkey0 / QT : 0;
 
+  if (a.kv_skip && a.kv_skip[bh] == 0u) return;  // dK/dV from the support lists (both CTAs)
   units_from_lists(ubits, 4, a, bh, pj0, threadIdx.x, kKvThreads);
   if (tid == 0) {
     for (int i = 0; i < KS; ++i) {
@@ -2555,6 +2703,12 @@ bool sparse_dq_enabled() {
   const char* s = std::getenv("ADATTN_SPARSE_DQ");
   return !(s && *s == '0');
 }
+// dK/dV from the support lists (sparse_keys_kernel; ADATTN_SPARSE_KV=0: the tensor-core
+// dK/dV kernel); needs the sparse dQ pass, which scatters the key lists
+bool sparse_kv_enabled() {
+  const char* s = std::getenv("ADATTN_SPARSE_KV");
+  return !(s && *s == '0');
+}
 
 // three-slot pair dK/dV kernel for the fp16 P / dS heads (ADATTN_KV_SLOT3=0: two buffers)
 bool kv_slot3_enabled(const Geom& g) {
@@ -2581,16 +2735,26 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
   const int dmode = delta_mode(g, a.ncta_rows);
   BwdArgs ad = a;  // the delta kernels' arguments (support mode: flagged heads only)
   const char* dname = "tc_delta";
-  BwdArgs aq = a;  // the dQ kernels' arguments (support lists: flagged heads only)
-  if (g.supp_in && !delta_only) {  // delta (and dQ) from the forward's support lists
-    const SuppLayout sl = supp_layout(g, const_cast<void*>(g.supp_in));
+  BwdArgs aq = a;   // the dQ kernels' arguments (support lists: flagged heads only)
+  BwdArgs akv = a;  // the dK/dV kernels' arguments (likewise)
+  bool want_kv = false;
+  SuppLayout sl{};
+  if (g.supp_in && !delta_only) {  // delta, dQ (and dK, dV) from the forward's support lists
+    sl = supp_layout(g, const_cast<void*>(g.supp_in));
     const size_t rows = (size_t)g.bh * g.n;
     const bool want_dq = sparse_dq_enabled() && g.d == g.dv;
+    want_kv = want_dq && sparse_kv_enabled();
+    if (want_kv) {  // key-list offsets and cursors for the rows kernel's scatter
+      if ((e = cudaMemsetAsync(sl.kcur, 0, 4 * (size_t)g.bh * g.m, st))) return e;
+      supp_scan_kernel<<<(unsigned)g.bh, 1024, 0, st>>>(sl.kcnt, sl.koff, sl.hflag, g.m);
+      note_launch();
+      if ((e = cudaGetLastError())) return e;
+    }
     prof_begin("tc_delta", st);
     sparse_rows_kernel<D, AK><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(
         reinterpret_cast<const uint16_t*>(a.dout), reinterpret_cast<const uint16_t*>(a.v),
         reinterpret_cast<const uint16_t*>(a.kp), sl.ent, sl.cnt, sl.flag, sl.hflag, sl.cap,
-        dmode == 1 ? 512 : 256, a.tau, a.row_max, g.alpha, a.e0f, a.e1f, (float)g.scale, rows,
+        dmode == 1 ? 512 : 256, want_kv ? sl.koff : nullptr, sl.kcur, sl.krow, sl.kpd, a.tau, a.row_max, g.alpha, a.e0f, a.e1f, (float)g.scale, rows,
         g.n, g.m, g.out_dtype == ADATTN_F64 ? 1 : 0, want_dq, a.dq, a.delta, a.rowc);
     prof_end(st);
     note_launch();
@@ -2598,6 +2762,7 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     ad.supp_skip = sl.flag;
     dname = "tc_delta_fb";
     if (want_dq) aq.dq_skip = sl.hflag;
+    if (want_kv) akv.kv_skip = sl.hflag;
   }
   if (g.ubar_in && !delta_only) {  // delta from the forward's fold
     const size_t rows = (size_t)g.bh * g.n;
@@ -2637,25 +2802,36 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     if ((e = cudaGetLastError())) return e;
   }
   if (delta_only) return cudaSuccess;
+  if (want_kv) {  // dK, dV from the support lists (heads without a flagged block)
+    const size_t keys = (size_t)g.bh * g.m;
+    prof_begin("tc_dkdv", st);
+    sparse_keys_kernel<D><<<(unsigned)((keys * 32 + 127) / 128), 128, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(a.dout), reinterpret_cast<const uint16_t*>(a.qp),
+        sl.koff, sl.krow, sl.kpd, sl.hflag, sl.cap, (float)g.scale, keys, g.n, g.m,
+        g.out_dtype == ADATTN_F64 ? 1 : 0, a.dk, a.dv);
+    prof_end(st);
+    note_launch();
+    if ((e = cudaGetLastError())) return e;
+  }
   if (use_kv_pairs(g)) {
     const bool slot3 = kv_slot3_enabled(g) && a.f16;
     auto k2 = ds_f16_enabled(g) ? tc_dkdv2_kernel<128, AK, true> : tc_dkdv2_kernel<128, AK, false>;
     const size_t sm = Kv2Smem<128>::bytes(g.t_r);
     if ((e = set_smem(k2, sm))) return e;
-    prof_begin("tc_dkdv", st);
+    prof_begin(akv.kv_skip ? "tc_dkdv_fb" : "tc_dkdv", st);
     if (slot3) {  // fp16 P / dS heads, then (skip_f16) the rest with the two-buffer layout
       auto k3 = tc_dkdv2_kernel<128, AK, true, true>;
       if ((e = set_smem(k3, sm))) return e;
       k3<<<dim3((unsigned)((g.m / KB) * g.bh)), kKvThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
-                                                                     m[7], m[14], m[16], a);
+                                                                     m[7], m[14], m[16], akv);
       note_launch();
-      BwdArgs a2 = a;
+      BwdArgs a2 = akv;
       a2.skip_f16 = 1;
       k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kKvThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
                                                                      m[7], m[14], m[16], a2);
     } else {
       k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kKvThreads, sm, st>>>(m[12], m[4], m[5], m[6], m[13],
-                                                                     m[7], m[14], m[16], a);
+                                                                     m[7], m[14], m[16], akv);
     }
     prof_end(st);
     note_launch();
@@ -2664,8 +2840,8 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     auto k2 = tc_dkdv_kernel<D, AK>;
     const size_t sm = KvSmem<D>::bytes(g.t_r);
     if ((e = set_smem(k2, sm))) return e;
-    prof_begin("tc_dkdv", st);
-    k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kThreads, sm, st>>>(m[4], m[5], m[6], m[7], a);
+    prof_begin(akv.kv_skip ? "tc_dkdv_fb" : "tc_dkdv", st);
+    k2<<<dim3((unsigned)((g.m / KB) * g.bh)), kThreads, sm, st>>>(m[4], m[5], m[6], m[7], akv);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;
@@ -2784,8 +2960,10 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
   a.dout = dout;
   a.v = v;
   a.kp = k;
+  a.qp = q;
   a.supp_skip = nullptr;
   a.dq_skip = nullptr;
+  a.kv_skip = nullptr;
   a.skip_f16 = 0;
   a.f16 = nullptr;
   m[14] = m[7];

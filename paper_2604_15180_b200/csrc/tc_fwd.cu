@@ -1665,7 +1665,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                   const float t = fmaf(A1, accs[j], C);
-                  if (row_real && t > 0.f) pool[off++] = make_uint2(keys[j], __float_as_uint(t));
+                  if (row_real && t > 0.f) {
+                    pool[off++] = make_uint2(keys[j], __float_as_uint(t));
+                    atomicAdd(&a.supp_kcnt[(size_t)bh * g.m + keys[j]], 1);  // (the transpose)
+                  }
                 }
               }
             }
@@ -2211,6 +2214,7 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
     a.supp_kcnt = sl.kcnt;
     a.supp_cap = sl.cap;
     if ((e = cudaMemsetAsync(sl.hflag, 0, 4 * (size_t)g.bh, st))) return e;
+    if ((e = cudaMemsetAsync(sl.kcnt, 0, 4 * (size_t)g.bh * g.m, st))) return e;
   } else if (g.supp_out && delta_supp_enabled(g)) {  // no lists written: every head flagged
     const SuppLayout sl = supp_layout(g, g.supp_out);
     if ((e = cudaMemsetAsync(sl.flag, 1, 4 * sl.nblk, st))) return e;

@@ -623,7 +623,8 @@ def test_tc_delta_support_lists_match_prepass(case, cap, monkeypatch):
     """delta from the forward's support lists (keys and u of the scores with t > 0 at the
     final tau; the backward sums u (dO . v) over them) equals the delta pre-pass, which
     sums u dp over every active block (u = 0 off the support): within fp32 summation
-    order, and the gradients within the same margin.  A pool of 2 entries per row overflows
+    order; the gradients (from the support lists too, against the tensor-core kernels'
+    fp16 products) within their fp16 rounding.  A pool of 2 entries per row overflows
     on every 256-row block: those blocks fall back to the pre-pass kernel."""
     B, H, N, D, alpha, causal, qs = case
     q, k, v, do = inputs(hash(case) % 877 + 3, B, H, N, D, qs)
@@ -641,8 +642,9 @@ def test_tc_delta_support_lists_match_prepass(case, cap, monkeypatch):
     print(case, cap, f"delta {derr:.2e} (max |delta| {dscale:.2f})", errs)
     assert derr <= 1e-5 * max(dscale, 1.0)
     for n, e in errs.items():  # fp32 summation order of delta, through dS = u (dp - delta);
-        # dQ from the support lists is exact-product fp32 against the fp16 sigma dS product
-        tol = (3e-3 if n == "dq" else 1e-4) * max(getattr(g0, n).abs().max().item(), 1.0) + 1e-4
+        # dQ / dK / dV from the support lists are exact-product fp32 sums against the
+        # tensor-core kernels' fp16 sigma dS and fp16 P products (~2^-12 of max |grad|)
+        tol = 3e-3 * max(getattr(g0, n).abs().max().item(), 1.0) + 1e-4
         assert e <= tol, n
 
 
@@ -674,6 +676,7 @@ def test_tc_sparse_dq_matches_tensor_core(case, monkeypatch):
     B, H, N, D, alpha, causal, qs = case
     q, k, v, do = inputs(hash(case) % 661 + 13, B, H, N, D, qs)
     monkeypatch.setenv("ADATTN_DS_F16", "0")
+    monkeypatch.setenv("ADATTN_SPARSE_KV", "0")  # isolates dQ (dK/dV from the tensor cores)
     monkeypatch.setenv("ADATTN_SPARSE_DQ", "0")
     _, r0, g0 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
     monkeypatch.setenv("ADATTN_SPARSE_DQ", "1")
@@ -687,3 +690,30 @@ def test_tc_sparse_dq_matches_tensor_core(case, monkeypatch):
     assert err <= 1e-4 * scale
     _, rx, gx = run(q, k, v, do, "exact", alpha=alpha, causal=causal)
     assert (g1.dq - gx.dq).abs().max().item() <= 2e-2
+
+
+@pytest.mark.parametrize("case", [(1, 2, 4096, 128, 1.5, True, 1.0), (1, 2, 2048, 64, 1.5, False, 1.0),
+                                  (1, 2, 4096, 128, 2.0, True, 2.0), (1, 1, 8192, 128, 1.5, True, 8.0),
+                                  (2, 1, 2048, 128, 1.75, False, 1.0)],
+                         ids=str)
+def test_tc_sparse_dkdv_matches_tensor_core(case, monkeypatch):
+    """dK / dV from the support lists (the rows kernel scatters (row, p, dS) into key
+    lists; sparse_keys_kernel sorts each key's list by row and sums p dO_i, dS q_i) against
+    the tensor-core dK/dV kernel with bf16 hi/lo products (ADATTN_SPARSE_KV=0,
+    ADATTN_DV_F16=0, ADATTN_DS_F16=0): within 1e-4 relative; bitwise reproducible."""
+    B, H, N, D, alpha, causal, qs = case
+    q, k, v, do = inputs(hash(case) % 653 + 17, B, H, N, D, qs)
+    monkeypatch.setenv("ADATTN_DS_F16", "0")
+    monkeypatch.setenv("ADATTN_DV_F16", "0")
+    monkeypatch.setenv("ADATTN_SPARSE_KV", "0")
+    _, r0, g0 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_SPARSE_KV", "1")
+    _, r1, g1 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    _, r2, g2 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    for n in ("dk", "dv"):
+        scale = max(getattr(g0, n).abs().max().item(), 1.0)
+        err = (getattr(g1, n) - getattr(g0, n)).abs().max().item()
+        print(case, n, f"{err:.2e} (max {scale:.2f})")
+        assert err <= 1e-4 * scale, n
+        assert torch.equal(getattr(g1, n), getattr(g2, n)), n  # deterministic order
+    assert torch.equal(g0.delta, g1.delta) and torch.equal(g0.dq, g1.dq)
