@@ -469,11 +469,20 @@ def main():
                 b = hc * N * (2 * D + 4 * D + 4 + 8 + 8 + 8 + 8)
                 kern[n]["kind"] = "delta fold row kernel (HBM)"
             else:
-                # support lists: per row dO (bf16), 2 (count, offset), ~30 (key, u) entries,
-                # tau, m in; delta (fp64), rowc (2 x fp32) out; the V rows it gathers stay
-                # L2-resident (one head's V at a time) and are not counted
-                b = hc * N * (2 * D + 16 + 30 * 8 + 8 + 8 + 8 + 8)
-                kern[n]["kind"] = "delta from support lists (SIMT gather, no MMA)"
+                # support lists (sparse_rows_kernel: delta and dQ): per row dO (bf16),
+                # (count, offset), ~30 (key, t) entries, tau, m in; delta (fp64), rowc, dQ
+                # (fp32) and ~30 scattered (row, p, dS) out; the V and K rows it gathers
+                # (2 x 256 B per entry) stay L2-resident (one head at a time), not counted
+                b = hc * N * (2 * D + 16 + 30 * 8 + 8 + 8 + 8 + 8 + 4 * D + 30 * 12)
+                kern[n]["kind"] = "delta and dQ from support lists (SIMT gather, no MMA)"
+            kern[n]["hbm_bytes"] = b
+            kern[n]["gbps"] = b / (kern[n]["ms_avg"] * 1e-3) / 1e9
+            kern[n]["frac_hbm"] = kern[n]["gbps"] / peak_bw
+        elif n == "tc_dkdv" and n in exe and exe[n] == 0:
+            # sparse_keys_kernel: per key its (row, p, dS) list (~30 x 12 B) and offsets
+            # in, dK and dV (fp32) out; the dO / Q rows it gathers stay L2-resident
+            b = hc * N * (30 * 12 + 8 + 2 * 4 * D)
+            kern[n]["kind"] = "dK and dV from support lists (SIMT gather, no MMA)"
             kern[n]["hbm_bytes"] = b
             kern[n]["gbps"] = b / (kern[n]["ms_avg"] * 1e-3) / 1e9
             kern[n]["frac_hbm"] = kern[n]["gbps"] / peak_bw

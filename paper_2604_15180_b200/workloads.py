@@ -112,6 +112,9 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha:
     tc_dq    S, dP, dQ (fp16 sigma dS and K: one product -- default for alpha <= 1.5;
              bf16 hi/lo otherwise)
              over active (128 x 128) tiles
+    (support lists, the default in list mode: tc_delta, tc_dq and tc_dkdv are 0 -- delta
+    and dQ come from sparse_rows_kernel, dK and dV from sparse_keys_kernel, gathers over
+    each row's / key's support entries)
     tc_dkdv  S^T, dP^T, dV (fp16 P and dO: one product; bf16 hi/lo with
              ADATTN_DV_F16=0 or for d != 128), dK (fp16 sigma dS: one product, as
              for dQ; else hi/lo) over active (128 keys x 64 queries) units
@@ -167,8 +170,13 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha:
     fold = ((fold_env == "1" or (fold_env in ("", "auto") and alpha == 2.0 and not supp))
             and n % 256 == 0
             and (d != 128 or os.environ.get("ADATTN_FWD_PAIRS", "0") in ("", "0")))
+    # with the support lists the gradients come from gather kernels too (no MMA):
+    # sparse_rows_kernel (delta, dQ; reported as tc_delta) and sparse_keys_kernel (dK, dV;
+    # reported as tc_dkdv) unless ADATTN_SPARSE_DQ / ADATTN_SPARSE_KV = 0
+    sp_dq = supp and os.environ.get("ADATTN_SPARSE_DQ", "1") != "0"
+    sp_kv = sp_dq and os.environ.get("ADATTN_SPARSE_KV", "1") != "0"
     return {"tc_fwd": (sweeps_fwd + (3 if fold else 2) * act) * tile,
             "tc_delta": (0 if (fold or supp) else 2) * act * tile,
-            "tc_dq": (3 if ds_f16 and dq_pairs else 4) * act * tile,
-            "tc_dkdv": (4 + (0 if dv_f16 else 1) + (0 if ds_f16 and kv_pairs else 1))
+            "tc_dq": 0 if sp_dq else (3 if ds_f16 and dq_pairs else 4) * act * tile,
+            "tc_dkdv": 0 if sp_kv else (4 + (0 if dv_f16 else 1) + (0 if ds_f16 and kv_pairs else 1))
             * units * (2.0 * 128 * 64 * d)}
