@@ -186,22 +186,22 @@ bool delta_supp_enabled(const Geom& g) {
   return !fwd_delta_fold(gf);
 }
 static int supp_cap_of() {
-  // support entries per row, pooled per 256-row block (C3 gaussian: ~30 per row; a block
-  // whose rows need more than 256 * cap in total falls back to the delta kernel)
-  int cap = 48;
+  // support entries per row, pooled per 256-row block (C3 gaussian: ~30 per row, C5 ~40; a
+  // block whose rows need more than 256 * cap in total falls back to the tensor cores)
+  int cap = 64;
   if (const char* s = std::getenv("ADATTN_SUPP_CAP")) cap = std::max(1, std::atoi(s));
   return cap;
 }
 // layout (tc_host.cuh SuppLayout), 256-byte aligned sections
-static size_t supp_sections(const Geom& g, size_t off[9]) {
+static size_t supp_sections(const Geom& g, size_t off[10]) {
   auto al = [](size_t b) { return (b + 255) / 256 * 256; };
   const size_t rows = (size_t)g.bh * g.n, nblk = (rows + 255) / 256;
   const size_t ent = nblk * 256 * (size_t)supp_cap_of();
-  const size_t sz[9] = {nblk * 4, (size_t)g.bh * 4, rows * 2 * 8, ent * 8,
+  const size_t sz[10] = {nblk * 4, (size_t)g.bh * 4, rows * 2 * 8, ent * 8,
                         (size_t)g.bh * g.m * 4, (size_t)g.bh * (g.m + 1) * 4,
-                        (size_t)g.bh * g.m * 4, ent * 4, ent * 8};
+                        (size_t)g.bh * g.m * 4, ent * 4, ent * 8, ((size_t)g.bh * g.m + 1) * 4};
   size_t o = 0;
-  for (int i = 0; i < 9; ++i) {
+  for (int i = 0; i < 10; ++i) {
     off[i] = o;
     o += al(sz[i]);
   }
@@ -209,11 +209,11 @@ static size_t supp_sections(const Geom& g, size_t off[9]) {
 }
 size_t supp_bytes(const Geom& g) {
   if (!delta_supp_enabled(g)) return 0;
-  size_t off[9];
+  size_t off[10];
   return supp_sections(g, off);
 }
 SuppLayout supp_layout(const Geom& g, void* base) {
-  size_t off[9];
+  size_t off[10];
   supp_sections(g, off);
   uint8_t* p = reinterpret_cast<uint8_t*>(base);
   SuppLayout l;
@@ -226,6 +226,7 @@ SuppLayout supp_layout(const Geom& g, void* base) {
   l.kcur = reinterpret_cast<int32_t*>(p + off[6]);
   l.krow = reinterpret_cast<int32_t*>(p + off[7]);
   l.kpd = reinterpret_cast<float2*>(p + off[8]);
+  l.klong = reinterpret_cast<int32_t*>(p + off[9]);
   l.cap = supp_cap_of();
   l.nblk = ((size_t)g.bh * g.n + 255) / 256;
   return l;

@@ -1976,7 +1976,7 @@ __global__ void delta_ubar_kernel(const uint16_t* __restrict__ dout, const float
 // Rows of a 256-row block the forward flagged are left to the delta kernel (its unit
 // of `unit` rows runs when any of its blocks is flagged); dQ only for heads without a
 // flagged block (hflag; the tensor-core dQ kernel takes the others) -- a row with more
-// than 96 entries flags its head here (the dQ kernel runs after this one).
+// than 192 entries flags its head here (the tensor-core kernels run after this one).
 // Also rowc_i = (C_i, delta_i) for the dK/dV kernel, as the delta kernels form it.
 template <int D, int AK>
 __global__ void __launch_bounds__(256) sparse_rows_kernel(
@@ -1987,7 +1987,8 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
     const double* __restrict__ row_max, double alpha, float e0f, float e1f, float scale,
     size_t rows, int n, int m, int out_f64, bool want_dq, void* dq, double* delta, float2* rowc) {
   constexpr int E = D / 32;
-  constexpr int NCH = 3;  // entries kept in registers: 3 x 32 per row (C3: ~30)
+  constexpr int NCH = 3;  // entries kept in registers: 3 x 32 per row (C3: ~30, C5: ~40);
+                          // longer rows recompute dp for the rest in phase 2
   const size_t r = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -2059,37 +2060,57 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
     rowc[r] = make_float2((float)(B - tau[r]), (float)dlt);
   }
   if (!want_dq || hflag[bh]) return;
-  if (tot > NCH * 32) {  // the tensor-core dQ kernel (launched after this one) takes the head
-    if (lane == 0) atomicOr(&hflag[bh], 1u);
-    return;
-  }
   // phase 2: dQ_i = scale * sum_j dS_j k_j, dS_j = u_j (dp_j - delta_i)
   const float dl = (float)dlt;
   float acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    const int b = c * 32;
-    if (b >= tot) break;
-    const float dsc = ur[c] * (dpr[c] - dl);
+  // one chunk of up to 32 entries: scatter into the key lists, accumulate dS k_j
+  auto dq_chunk = [&](int b, uint32_t keyc, float pc, float dsc) {
     const int nk = min(32, tot - b);
     if (koff && lane < nk) {  // this entry into its key's list (sorted by row in the keys kernel)
-      const size_t kj = bh * (size_t)m + keyr[c];
+      const size_t kj = bh * (size_t)m + keyc;
       // head bh's lists live in its own n * cap entries
       const size_t slot = bh * (size_t)n * cap + (size_t)(koff[kj + bh] + atomicAdd(&kcur[kj], 1));
       krow[slot] = (int)(r - bh * n);
-      kpd[slot] = make_float2(pr[c], dsc);
+      kpd[slot] = make_float2(pc, dsc);
     }
 #pragma unroll 8
     for (int k = 0; k < nk; ++k) {
-      const uint32_t key = __shfl_sync(0xffffffffu, keyr[c], k);
+      const uint32_t key = __shfl_sync(0xffffffffu, keyc, k);
       const float ds = __shfl_sync(0xffffffffu, dsc, k);
       float x[E];
       ld_row(kb + (size_t)key * D, x);
 #pragma unroll
       for (int e = 0; e < E; ++e) acc[e] = fmaf(ds, x[e], acc[e]);
     }
+  };
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    if (c * 32 >= tot) break;
+    dq_chunk(c * 32, keyr[c], pr[c], ur[c] * (dpr[c] - dl));
+  }
+  for (int b = NCH * 32; b < tot; b += 32) {  // beyond the registers: entries and dp again
+    const int idx = b + lane;
+    uint2 my = make_uint2(0u, 0u);
+    if (idx < tot) my = idx < c0 ? base[h0.y + idx] : base[h1.y + idx - c0];
+    float pc, uc;
+    pu_of<AK>(__uint_as_float(my.y), e0f, e1f, pc, uc);
+    if (idx >= tot) uc = 0.f;
+    float dpc = 0.f;
+    const int nk = min(32, tot - b);
+    for (int k = 0; k < nk; ++k) {
+      const uint32_t key = __shfl_sync(0xffffffffu, my.x, k);
+      float x[E];
+      ld_row(vb + (size_t)key * D, x);
+      float sd = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) sd = fmaf(dov[e], x[e], sd);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
+      if (lane == k) dpc = sd;
+    }
+    dq_chunk(b, my.x, pc, uc * (dpc - dl));
   }
   if (out_f64) {
     double* dst = reinterpret_cast<double*>(dq) + r * D + lane * E;
@@ -2152,26 +2173,41 @@ __global__ void __launch_bounds__(1024) supp_scan_kernel(const int32_t* __restri
 // dO / Q rows (attention.cpp:464-506: the terms vanish off the support).  One warp per
 // key; a key with more than kMaxKey entries flags its head (the tensor-core dK/dV
 // kernel, launched after this one, then takes the whole head).
-constexpr int kMaxKey = 1024;
-template <int D>
-__global__ void __launch_bounds__(128) sparse_keys_kernel(
+// Two launches: keys with <= 256 entries, one warp each and 8 warps per CTA (16 KB of
+// shared memory: high occupancy for the latency-bound gathers), which queue the longer
+// lists (the first keys of a causal head: ~30 ln(n / j) entries) in klong; then a
+// persistent launch whose warps take the queued keys (<= 4096 entries, 32 KB per warp).
+template <int D, int KMAX, int WARPS, bool LONG>
+__global__ void __launch_bounds__(WARPS * 32) sparse_keys_kernel(
     const uint16_t* __restrict__ dout, const uint16_t* __restrict__ qq,
     const int32_t* __restrict__ koff, const int32_t* __restrict__ krow,
-    const float2* __restrict__ kpd, uint32_t* hflag, int cap, float scale, size_t keys, int n,
-    int m, int out_f64, void* dk, void* dv) {
+    const float2* __restrict__ kpd, uint32_t* hflag, int32_t* klong, int cap, float scale,
+    size_t keys, int n, int m, int out_f64, void* dk, void* dv) {
   constexpr int E = D / 32;
-  __shared__ unsigned long long sk[4][kMaxKey];
-  const size_t kr = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  __shared__ unsigned long long sk[WARPS][KMAX];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  if (kr >= keys) return;
+  size_t kr = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nwarps = (size_t)gridDim.x * WARPS;
+  const size_t nlong = LONG ? (size_t)klong[0] : 0;
+  for (size_t it = kr;; it += nwarps) {  // (short lists: one key per warp, no loop)
+  if (LONG) {
+    if (it >= nlong) return;
+    kr = (size_t)klong[1 + it];
+  } else {
+    if (it != kr || kr >= keys) return;
+  }
   const size_t bh = kr / (size_t)m;
-  if (hflag[bh]) return;
+  if (hflag[bh]) continue;
   const size_t j = kr - bh * m;
   const int cntk = koff[bh * (m + 1) + j + 1] - koff[bh * (m + 1) + j];
   const size_t s0 = bh * (size_t)n * cap + (size_t)koff[bh * (m + 1) + j];
-  if (cntk > kMaxKey) {
-    if (lane == 0) atomicOr(&hflag[bh], 1u);
+  if (!LONG && cntk > KMAX) {  // queued for the long-list launch
+    if (lane == 0) klong[1 + atomicAdd(&klong[0], 1)] = (int32_t)kr;
     return;
+  }
+  if (cntk > KMAX) {  // the tensor-core dK/dV kernel (launched after this one) takes the head
+    if (lane == 0) atomicOr(&hflag[bh], 1u);
+    continue;
   }
   unsigned long long* sm = sk[wi];
   int np = 32;
@@ -2236,6 +2272,8 @@ __global__ void __launch_bounds__(128) sparse_keys_kernel(
       reinterpret_cast<float*>(dv)[orow + e] = av[e];
       reinterpret_cast<float*>(dk)[orow + e] = scale * ak[e];
     }
+  }
+  __syncwarp();  // (the shared-memory list is reused by the warp's next key)
   }
 }
 
@@ -2805,9 +2843,15 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
   if (want_kv) {  // dK, dV from the support lists (heads without a flagged block)
     const size_t keys = (size_t)g.bh * g.m;
     prof_begin("tc_dkdv", st);
-    sparse_keys_kernel<D><<<(unsigned)((keys * 32 + 127) / 128), 128, 0, st>>>(
+    if ((e = cudaMemsetAsync(sl.klong, 0, 4, st))) return e;
+    sparse_keys_kernel<D, 256, 8, false><<<(unsigned)((keys + 7) / 8), 8 * 32, 0, st>>>(
         reinterpret_cast<const uint16_t*>(a.dout), reinterpret_cast<const uint16_t*>(a.qp),
-        sl.koff, sl.krow, sl.kpd, sl.hflag, sl.cap, (float)g.scale, keys, g.n, g.m,
+        sl.koff, sl.krow, sl.kpd, sl.hflag, sl.klong, sl.cap, (float)g.scale, keys, g.n, g.m,
+        g.out_dtype == ADATTN_F64 ? 1 : 0, a.dk, a.dv);
+    note_launch();
+    sparse_keys_kernel<D, 4096, 1, true><<<148 * 6, 32, 0, st>>>(
+        reinterpret_cast<const uint16_t*>(a.dout), reinterpret_cast<const uint16_t*>(a.qp),
+        sl.koff, sl.krow, sl.kpd, sl.hflag, sl.klong, sl.cap, (float)g.scale, keys, g.n, g.m,
         g.out_dtype == ADATTN_F64 ? 1 : 0, a.dk, a.dv);
     prof_end(st);
     note_launch();

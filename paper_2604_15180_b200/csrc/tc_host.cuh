@@ -58,6 +58,7 @@ struct SuppLayout {
   int32_t* kcur;    // [bh][m] scatter cursors (backward)
   int32_t* krow;    // [nblk 256 cap] key-major lists: query row ...
   float2* kpd;      // ... and (p, dS)
+  int32_t* klong;   // [1 + bh m]: count, then the keys with long lists (keys kernel)
   int cap;
   size_t nblk;
 };
