@@ -2016,7 +2016,19 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
   };
   float dov[E];
   ld_row(dout + r * D + lane * E, dov);
-  // phase 1: dp of every entry (warp dot products), delta
+  // phase 1: dp of every entry -- lane k takes entry k whole (its V row, 16-byte loads,
+  // against dO staged in shared memory as fp32), no per-entry warp reduction -- and delta
+  __shared__ float4 sdo[8][D / 4];  // (8 warps per CTA)
+  const int wi = (threadIdx.x >> 5) & 7;
+  {  // the warp's dO row, fp32, d-ordered
+    const uint16_t* dr = dout + r * D;
+    for (int x = lane; x < D / 4; x += 32) {
+      const uint2 w = *reinterpret_cast<const uint2*>(dr + 4 * x);
+      sdo[wi][x] = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                               __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+    }
+  }
+  __syncwarp();
   uint32_t keyr[NCH];
   float ur[NCH], dpr[NCH], pr[NCH];
   double num = 0.0, den = 0.0;
@@ -2026,24 +2038,38 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
     if (idx < tot) my = idx < c0 ? base[h0.y + idx] : base[h1.y + idx - c0];
     float p_, u_;
     pu_of<AK>(__uint_as_float(my.y), e0f, e1f, p_, u_);
-    if (idx >= tot) u_ = 0.f;
-    const int nk = min(32, tot - b);
     float dpk = 0.f;
-#pragma unroll 8
-    for (int k = 0; k < nk; ++k) {
-      const uint32_t key = __shfl_sync(0xffffffffu, my.x, k);
-      float x[E];
-      ld_row(vb + (size_t)key * D, x);
-      float s = 0.f;
+    if (idx < tot) {
+      const uint4* vr = reinterpret_cast<const uint4*>(vv + (bh * (size_t)m + my.x) * D);
+      uint4 w[D / 8];
 #pragma unroll
-      for (int e = 0; e < E; ++e) s = fmaf(dov[e], x[e], s);
+      for (int x = 0; x < D / 8; ++x) w[x] = vr[x];
+      float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      const float uk = __shfl_sync(0xffffffffu, u_, k);
-      num += (double)uk * (double)s;
-      den += (double)uk;
-      if (lane == k) dpk = s;
+      for (int x = 0; x < D / 8; ++x) {
+        const float4 o0 = sdo[wi][2 * x], o1 = sdo[wi][2 * x + 1];
+        s0 = fmaf(o0.x, __uint_as_float(w[x].x << 16), s0);
+        s1 = fmaf(o0.y, __uint_as_float(w[x].x & 0xFFFF0000u), s1);
+        s0 = fmaf(o0.z, __uint_as_float(w[x].y << 16), s0);
+        s1 = fmaf(o0.w, __uint_as_float(w[x].y & 0xFFFF0000u), s1);
+        s0 = fmaf(o1.x, __uint_as_float(w[x].z << 16), s0);
+        s1 = fmaf(o1.y, __uint_as_float(w[x].z & 0xFFFF0000u), s1);
+        s0 = fmaf(o1.z, __uint_as_float(w[x].w << 16), s0);
+        s1 = fmaf(o1.w, __uint_as_float(w[x].w & 0xFFFF0000u), s1);
+      }
+      dpk = s0 + s1;
+    } else {
+      u_ = 0.f;
     }
+    // sum u dp, sum u over the chunk: a fixed fp64 tree
+    double tn = (double)u_ * (double)dpk, td = (double)u_;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tn += __shfl_xor_sync(0xffffffffu, tn, o);
+      td += __shfl_xor_sync(0xffffffffu, td, o);
+    }
+    num += tn;
+    den += td;
 #pragma unroll
     for (int c = 0; c < NCH; ++c)
       if (c == ch) {
@@ -2098,17 +2124,23 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
     pu_of<AK>(__uint_as_float(my.y), e0f, e1f, pc, uc);
     if (idx >= tot) uc = 0.f;
     float dpc = 0.f;
-    const int nk = min(32, tot - b);
-    for (int k = 0; k < nk; ++k) {
-      const uint32_t key = __shfl_sync(0xffffffffu, my.x, k);
-      float x[E];
-      ld_row(vb + (size_t)key * D, x);
-      float sd = 0.f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) sd = fmaf(dov[e], x[e], sd);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sd += __shfl_xor_sync(0xffffffffu, sd, o);
-      if (lane == k) dpc = sd;
+    if (idx < tot) {
+      const uint4* vr = reinterpret_cast<const uint4*>(vv + (bh * (size_t)m + my.x) * D);
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll 4
+      for (int x = 0; x < D / 8; ++x) {
+        const uint4 w = vr[x];
+        const float4 o0 = sdo[wi][2 * x], o1 = sdo[wi][2 * x + 1];
+        s0 = fmaf(o0.x, __uint_as_float(w.x << 16), s0);
+        s1 = fmaf(o0.y, __uint_as_float(w.x & 0xFFFF0000u), s1);
+        s0 = fmaf(o0.z, __uint_as_float(w.y << 16), s0);
+        s1 = fmaf(o0.w, __uint_as_float(w.y & 0xFFFF0000u), s1);
+        s0 = fmaf(o1.x, __uint_as_float(w.z << 16), s0);
+        s1 = fmaf(o1.y, __uint_as_float(w.z & 0xFFFF0000u), s1);
+        s0 = fmaf(o1.z, __uint_as_float(w.w << 16), s0);
+        s1 = fmaf(o1.w, __uint_as_float(w.w & 0xFFFF0000u), s1);
+      }
+      dpc = s0 + s1;
     }
     dq_chunk(b, my.x, pc, uc * (dpc - dl));
   }
