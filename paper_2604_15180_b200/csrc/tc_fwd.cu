@@ -176,6 +176,9 @@ struct FwdArgs {
   uint32_t* supp_hflag;  // per head: any of its blocks flagged
   int32_t* supp_kcnt;    // per key of every head: support entries (the backward's transpose)
   int supp_cap;
+  // O from the support lists (sparse_out_kernel after this kernel): CTAs whose lists went
+  // into the pool skip the output pass and the O store
+  int supp_o;
   // fp16 P V: per head, max |V| (float bits) of the scaled fp16 V copy; nullptr -> bf16 P
   const uint32_t* v16_max;
   // optional output (delta fold): Ubar [bh][n][dv] fp32, then sum u [bh][n] fp32
@@ -1300,6 +1303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bool first_pass = true;
     uint32_t dround = 0;
     bool list_ok = false;
+    bool so = false;  // O from the support lists (this CTA's rows all in the pool)
 
     // ---- pass CAND: every score that can matter for the histogram solve, for
     // tau in [lo, hi] or for the mask is appended to a per-thread list as (raw
@@ -1634,6 +1638,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int pc = BM * a.supp_cap;  // the CTA's pool
             const size_t blk256 = ((size_t)bh * g.n + row0) / BM;
             const size_t srow = (size_t)bh * g.n + grow;
+            so = a.supp_o != 0 && tot <= pc;  // (CTA-uniform)
             if (tot > pc) {
               if (tid == 0) {  // the delta kernel (and the tensor-core backward) take these rows
                 a.supp_flag[blk256] = 1u;
@@ -1683,7 +1688,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       bar_sync(3, kEpi);
       if (PAIR && list_ok) pair_or_words(sPm, smask, 4 * wpr);
       if (list_ok) {
-        if (warp == 0) build_tiles();
+        if (so) {  // no output pass: sparse_out_kernel forms O from the support lists
+          if (tid == 0) *s_ntiles = 0u;
+        } else if (warp == 0) {
+          build_tiles();
+        }
         bar_sync(3, kEpi);
       }
       if (tid == 0) {
@@ -2012,7 +2021,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool written = __any_sync(0xffffffffu, any_out);
       const uint32_t to = tmem + ((uint32_t)(lq * 32) << 16) + 256 + rg * D + half * (D / 2);
 #pragma unroll
-      for (int c = 0; c < (fold ? 0 : D / 64); ++c) {
+      for (int c = 0; c < (fold || so ? 0 : D / 64); ++c) {
         float o[32];
         tmem_ld32(to + c * 32, o);
         tmem_wait_ld();
@@ -2162,6 +2171,90 @@ int alpha_kind(double alpha) {
   return AKGEN;
 }
 
+// O from the support lists: O_i = sum_j p_ij v_j over the row's entries (key, t_ij > 0 at
+// the final tau) -- the output pass's P V without the zero terms (attention.cpp:334-352),
+// exact bf16 products summed in fp32 in list order.  One warp per row, lane l holds dv
+// elements l*E..; rows of blocks the forward flagged (their CTA ran the output pass) are
+// left alone.
+template <int D, int AK>
+__global__ void __launch_bounds__(256) sparse_out_kernel(
+    const uint16_t* __restrict__ vv, const uint2* __restrict__ pool, const int2* __restrict__ cnt,
+    const uint32_t* __restrict__ flag, int cap, float e0f, size_t rows, int n, int m, int out_f64,
+    void* out) {
+  constexpr int E = D / 32;
+  const size_t r = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows || flag[r / 256]) return;
+  const size_t bh = r / (size_t)n;
+  const int2 h0 = cnt[r * 2], h1 = cnt[r * 2 + 1];
+  const int c0 = h0.x, tot = h0.x + h1.x;
+  const uint2* base = pool + (r / 256) * (size_t)(256 * cap);
+  const uint16_t* vb = vv + bh * (size_t)m * D + lane * E;
+  float acc[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  for (int b = 0; b < tot; b += 32) {
+    const int idx = b + lane;
+    uint2 my = make_uint2(0u, 0u);
+    if (idx < tot) my = idx < c0 ? base[h0.y + idx] : base[h1.y + idx - c0];
+    const float pl = idx < tot ? p_of<AK>(__uint_as_float(my.y), e0f) : 0.f;
+    const int nk = min(32, tot - b);
+#pragma unroll 8
+    for (int k = 0; k < nk; ++k) {
+      const uint32_t key = __shfl_sync(0xffffffffu, my.x, k);
+      const float p = __shfl_sync(0xffffffffu, pl, k);
+      const uint16_t* vr = vb + (size_t)key * D;
+      if constexpr (E == 4) {
+        const uint2 w = *reinterpret_cast<const uint2*>(vr);
+        acc[0] = fmaf(p, __uint_as_float(w.x << 16), acc[0]);
+        acc[1] = fmaf(p, __uint_as_float(w.x & 0xFFFF0000u), acc[1]);
+        acc[2] = fmaf(p, __uint_as_float(w.y << 16), acc[2]);
+        acc[3] = fmaf(p, __uint_as_float(w.y & 0xFFFF0000u), acc[3]);
+      } else {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(vr);
+        acc[0] = fmaf(p, __uint_as_float(w << 16), acc[0]);
+        acc[1] = fmaf(p, __uint_as_float(w & 0xFFFF0000u), acc[1]);
+      }
+    }
+  }
+  if (out_f64) {
+    double* dst = reinterpret_cast<double*>(out) + r * D + lane * E;
+#pragma unroll
+    for (int e = 0; e < E; ++e) dst[e] = (double)acc[e];
+  } else {
+    float* dst = reinterpret_cast<float*>(out) + r * D + lane * E;
+#pragma unroll
+    for (int e = 0; e < E; ++e) dst[e] = acc[e];
+  }
+}
+
+template <int D>
+cudaError_t launch_sparse_out(const Geom& g, int ak, const FwdArgs& a, const void* v,
+                              cudaStream_t st) {
+  const SuppLayout sl = supp_layout(g, g.supp_out);
+  const size_t rows = (size_t)g.bh * g.n;
+  const unsigned grid = (unsigned)((rows * 32 + 255) / 256);
+  const int f64 = g.out_dtype == ADATTN_F64 ? 1 : 0;
+  const uint16_t* vb = reinterpret_cast<const uint16_t*>(v);
+  prof_begin("tc_fwd_out", st);
+  switch (ak) {
+    case AK15: sparse_out_kernel<D, AK15><<<grid, 256, 0, st>>>(vb, sl.ent, sl.cnt, sl.flag, sl.cap, a.e0f, rows, g.n, g.m, f64, a.out); break;
+    case AK2: sparse_out_kernel<D, AK2><<<grid, 256, 0, st>>>(vb, sl.ent, sl.cnt, sl.flag, sl.cap, a.e0f, rows, g.n, g.m, f64, a.out); break;
+    case AK125: sparse_out_kernel<D, AK125><<<grid, 256, 0, st>>>(vb, sl.ent, sl.cnt, sl.flag, sl.cap, a.e0f, rows, g.n, g.m, f64, a.out); break;
+    default: sparse_out_kernel<D, AKGEN><<<grid, 256, 0, st>>>(vb, sl.ent, sl.cnt, sl.flag, sl.cap, a.e0f, rows, g.n, g.m, f64, a.out); break;
+  }
+  prof_end(st);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// O from the support lists (ADATTN_SPARSE_OUT=0: the output pass on the tensor cores);
+// needs the support lists and the single-CTA forward
+bool sparse_out_enabled() {
+  const char* s = std::getenv("ADATTN_SPARSE_OUT");
+  return !(s && *s == '0');
+}
+
 cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, void* out,
                     double* tau, double* row_max, uint32_t* mask, int32_t* steps, void* ws,
                     cudaStream_t st) {
@@ -2204,6 +2297,7 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   a.supp_hflag = nullptr;
   a.supp_kcnt = nullptr;
   a.supp_cap = 0;
+  a.supp_o = 0;
   if (!a.ubar && a.cand && g.supp_out && delta_supp_enabled(g)) {  // (list mode only)
     const SuppLayout sl = supp_layout(g, g.supp_out);
     if ((e = cudaMemsetAsync(sl.flag, 0, 4 * sl.nblk, st))) return e;
@@ -2239,9 +2333,13 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   }
 
   const int ak = alpha_kind(g.alpha);
-  if (g.d == 64) return launch_fwd_d<64, false>(g, ak, tq, tk, tkh, tv, tv16, a, st);
-  if (use_fwd_pairs(g)) return launch_fwd_d<128, true>(g, ak, tq, tk, tkh, tv, tv16, a, st);
-  return launch_fwd_d<128, false>(g, ak, tq, tk, tkh, tv, tv16, a, st);
+  const bool pairs = g.d == 128 && use_fwd_pairs(g);
+  a.supp_o = a.supp && !pairs && g.d == g.dv && sparse_out_enabled() ? 1 : 0;
+  if (g.d == 64) e = launch_fwd_d<64, false>(g, ak, tq, tk, tkh, tv, tv16, a, st);
+  else if (pairs) e = launch_fwd_d<128, true>(g, ak, tq, tk, tkh, tv, tv16, a, st);
+  else e = launch_fwd_d<128, false>(g, ak, tq, tk, tkh, tv, tv16, a, st);
+  if (e || !a.supp_o) return e;
+  return g.dv == 64 ? launch_sparse_out<64>(g, ak, a, v, st) : launch_sparse_out<128>(g, ak, a, v, st);
 }
 
 }  // namespace tc

@@ -175,7 +175,11 @@ def executed_flops(mask_words, n: int, d: int, causal: bool, dv_f16=None, alpha:
     # reported as tc_dkdv) unless ADATTN_SPARSE_DQ / ADATTN_SPARSE_KV = 0
     sp_dq = supp and os.environ.get("ADATTN_SPARSE_DQ", "1") != "0"
     sp_kv = sp_dq and os.environ.get("ADATTN_SPARSE_KV", "1") != "0"
-    return {"tc_fwd": (sweeps_fwd + (3 if fold else 2) * act) * tile,
+    # O from the support lists (sparse_out_kernel) replaces the output pass (S, P V) in
+    # list mode with the support lists (single-CTA forward)
+    sp_out = (supp and os.environ.get("ADATTN_SPARSE_OUT", "1") != "0"
+              and not (d == 128 and os.environ.get("ADATTN_FWD_PAIRS", "0") not in ("", "0")))
+    return {"tc_fwd": (sweeps_fwd + (0 if sp_out else (3 if fold else 2) * act)) * tile,
             "tc_delta": (0 if (fold or supp) else 2) * act * tile,
             "tc_dq": 0 if sp_dq else (3 if ds_f16 and dq_pairs else 4) * act * tile,
             "tc_dkdv": 0 if sp_kv else (4 + (0 if dv_f16 else 1) + (0 if ds_f16 and kv_pairs else 1))

@@ -323,6 +323,7 @@ def test_tc_fwd_cta_pairs_match_single(case, monkeypatch):
     union of the two CTAs' activity sets, which only adds exact zeros; when one
     CTA of a pair overflows its candidate list both take the sweep refinement,
     which agrees with the list refinement to fp32 summation order."""
+    monkeypatch.setenv("ADATTN_SPARSE_OUT", "0")  # the tensor-core output pass under test
     B, H, N, alpha, causal, qs, cap = case
     q, k, v, _ = inputs(hash(case) % 977 + 3, B, H, N, 128, qs)
     if cap is None:
@@ -481,6 +482,7 @@ def test_tc_pv_f16_vs_bf16(monkeypatch):
     """O = P V with fp16 P (default; V copied to fp16) is closer to the exact path than
     bf16 P (ADATTN_PV_F16=0), and both stay within the 2e-2 bar; tau and masks are
     untouched (the output pass only)."""
+    monkeypatch.setenv("ADATTN_SPARSE_OUT", "0")  # the tensor-core output pass under test
     q, k, v, _ = inputs(85, 1, 2, 4096, 128, 1.0)
     _, rx, _ = run(q, k, v, None, "exact", alpha=1.5, causal=True)
     monkeypatch.setenv("ADATTN_PV_F16", "0")
@@ -499,6 +501,7 @@ def test_tc_pv_f16_scaled_v(monkeypatch, v_scale):
     """O = P V with the per-head power-of-two-scaled fp16 V copy stays within the
     bf16 bar (relative to max|O|) of the exact path at any V magnitude: 1e-6 (an
     unscaled fp16 copy would underflow) and 1e5 (it would overflow)."""
+    monkeypatch.setenv("ADATTN_SPARSE_OUT", "0")  # the tensor-core output pass under test
     q, k, v, _ = inputs(86, 1, 1, 1024, 128, 1.0)
     v = (v.float() * v_scale).to(torch.bfloat16)
     _, rx, _ = run(q, k, v, None, "exact", alpha=1.5, causal=True)
@@ -635,7 +638,9 @@ def test_tc_delta_support_lists_match_prepass(case, cap, monkeypatch):
     if cap:
         monkeypatch.setenv("ADATTN_SUPP_CAP", cap)
     _, r1, g1 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
-    assert torch.equal(r0.tau, r1.tau) and torch.equal(r0.out, r1.out)
+    assert torch.equal(r0.tau, r1.tau) and torch.equal(r0.mask.words, r1.mask.words)
+    # O from the support lists (exact products) against the fp16 P V output pass
+    assert (r1.out - r0.out).abs().max().item() <= 3e-3 * max(r0.out.abs().max().item(), 1.0)
     dscale = g0.delta.abs().max().item() + 1e-30
     derr = (g1.delta - g0.delta).abs().max().item()
     errs = {n: (getattr(g1, n) - getattr(g0, n)).abs().max().item() for n in ("dq", "dk", "dv")}
@@ -652,6 +657,7 @@ def test_tc_delta_support_lists_match_prepass(case, cap, monkeypatch):
 def test_tc_delta_support_lists_pair_forward(case, monkeypatch):
     """The CTA-pair forward (ADATTN_FWD_PAIRS=1) writes the same support lists as the
     single-CTA forward (each CTA its own 256 rows): identical delta and gradients."""
+    monkeypatch.setenv("ADATTN_SPARSE_OUT", "0")  # the tensor-core output pass under test
     B, H, N, alpha, causal, qs = case
     q, k, v, do = inputs(hash(case) % 701 + 9, B, H, N, 128, qs)
     monkeypatch.setenv("ADATTN_FWD_PAIRS", "0")
@@ -717,3 +723,29 @@ def test_tc_sparse_dkdv_matches_tensor_core(case, monkeypatch):
         assert err <= 1e-4 * scale, n
         assert torch.equal(getattr(g1, n), getattr(g2, n)), n  # deterministic order
     assert torch.equal(g0.delta, g1.delta) and torch.equal(g0.dq, g1.dq)
+
+
+@pytest.mark.parametrize("case", [(1, 2, 4096, 128, 1.5, True, 1.0), (1, 2, 2048, 64, 1.5, False, 1.0),
+                                  (1, 2, 4096, 128, 2.0, True, 2.0), (1, 1, 8192, 128, 1.5, True, 8.0),
+                                  (2, 1, 2304, 128, 1.75, True, 1.0)],
+                         ids=str)
+def test_tc_sparse_out_matches_output_pass(case, monkeypatch):
+    """O from the support lists (sparse_out_kernel: O_i = sum_j p_ij v_j over the row's
+    support, exact bf16 products in fp32) against the tensor-core output pass with bf16 P
+    (ADATTN_SPARSE_OUT=0, ADATTN_PV_F16=0): within 1e-2 of max |O| (bf16 P rounding), and
+    the compiled-reference-pinned exact path within 2e-2; tau, masks, steps identical."""
+    B, H, N, D, alpha, causal, qs = case
+    q, k, v, do = inputs(hash(case) % 641 + 19, B, H, N, D, qs)
+    monkeypatch.setenv("ADATTN_SPARSE_OUT", "0")
+    _, r0, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_SPARSE_OUT", "1")
+    _, r1, _ = run(q, k, v, None, "tc", alpha=alpha, causal=causal)
+    assert torch.equal(r0.tau, r1.tau) and torch.equal(r0.mask.words, r1.mask.words)
+    assert torch.equal(r0.row_steps, r1.row_steps)
+    err = (r1.out - r0.out).abs().max().item()
+    print(case, f"out {err:.2e}")
+    assert err <= 1e-2 * max(r0.out.abs().max().item(), 1.0)
+    _, rx, _ = run(q, k, v, None, "exact", alpha=alpha, causal=causal)
+    ex = (r1.out - rx.out).abs().max().item()
+    print(case, f"out vs exact {ex:.2e}")
+    assert ex <= 2e-2
