@@ -111,8 +111,12 @@ bool pv_f16_enabled() {
 // blocks [h * bpp, (h + 1) * bpp) cover head h's n8 groups of 8 bf16 (16-byte
 // loads: 4-byte accesses left these HBM-bound passes at ~1.2 TB/s)
 __global__ void absmax_bf16_kernel(const uint4* __restrict__ src, size_t n8, int bpp,
-                                   uint32_t* maxbits) {
+                                   uint32_t* maxbits, const uint32_t* need) {
   const int h = blockIdx.x / bpp, b = blockIdx.x - h * bpp;
+  if (need && need[h] == 0u) {  // no tensor-core kernel reads this head: no copy (a
+    if (b == 0 && threadIdx.x == 0) maxbits[h] = 0xFFFFFFFFu;  // non-finite: bf16 plan)
+    return;
+  }
   src += (size_t)h * n8;
   uint32_t m = 0;
   for (size_t i = b * (size_t)blockDim.x + threadIdx.x; i < n8; i += (size_t)bpp * blockDim.x) {
@@ -152,10 +156,10 @@ __global__ void f16_scaled_kernel(const uint4* __restrict__ src, uint4* __restri
 static int blocks_per_head(int heads) { return std::max(2, std::min(128, 8 * 148 / heads)); }
 
 cudaError_t f16_absmax(const void* src, int heads, size_t elems, uint32_t* maxbits,
-                       cudaStream_t st) {
+                       cudaStream_t st, const uint32_t* need) {
   const int bpp = blocks_per_head(heads);
   absmax_bf16_kernel<<<heads * bpp, 256, 0, st>>>(reinterpret_cast<const uint4*>(src),
-                                                  elems / 8, bpp, maxbits);
+                                                  elems / 8, bpp, maxbits, need);
   note_launch();
   return cudaGetLastError();
 }

@@ -3068,11 +3068,16 @@ cudaError_t backward(const Geom& g, const void* q, const void* k, const void* v,
     // per head: dO [n][dv], V [m][dv], Q [n][d], K [m][d]
     const size_t eo = (size_t)g.n * g.dv, ev = (size_t)g.m * g.dv;
     const size_t eq = (size_t)g.n * g.d, ek = (size_t)g.m * g.d;
-    if ((e = f16_absmax(dout, H, eo, mx, st))) return e;
+    // support-list backward: only heads the forward flagged reach the tensor-core
+    // dQ / dK-dV kernels, so only they get fp16 copies
+    const uint32_t* need = g.supp_in && sparse_dq_enabled() && sparse_kv_enabled() && g.d == g.dv
+                               ? supp_layout(g, const_cast<void*>(g.supp_in)).hflag
+                               : nullptr;
+    if ((e = f16_absmax(dout, H, eo, mx, st, need))) return e;
     if (want_ds) {
-      if ((e = f16_absmax(v, H, ev, mx + H, st))) return e;
-      if ((e = f16_absmax(q, H, eq, mx + 2 * H, st))) return e;
-      if ((e = f16_absmax(k, H, ek, mx + 3 * H, st))) return e;
+      if ((e = f16_absmax(v, H, ev, mx + H, st, need))) return e;
+      if ((e = f16_absmax(q, H, eq, mx + 2 * H, st, need))) return e;
+      if ((e = f16_absmax(k, H, ek, mx + 3 * H, st, need))) return e;
     }
     f16_plan_kernel<<<(H + 127) / 128, 128, 0, st>>>(plan, mx, H, (float)g.alpha, g.d,
                                                      want_dv ? 1 : 0, want_ds ? 1 : 0);

@@ -2320,7 +2320,11 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   }
   a.v16_max = nullptr;
   tv16 = tv;
-  if (pv_f16_enabled() && ws) {
+  // O from the support lists: the output pass runs only in flagged CTAs, which then take
+  // bf16 P and V (no fp16 V copy for them)
+  const bool pairs = g.d == 128 && use_fwd_pairs(g);
+  const bool supp_o = a.supp && !pairs && g.d == g.dv && sparse_out_enabled();
+  if (pv_f16_enabled() && ws && !supp_o) {
     uint8_t* w8 = reinterpret_cast<uint8_t*>(ws) + forward_cand_bytes(g);
     __half2* v16 = reinterpret_cast<__half2*>(w8);
     uint32_t* vmax = reinterpret_cast<uint32_t*>(w8 + ((size_t)g.bh * g.m * g.dv * 2 + 255) / 256 * 256);
@@ -2333,8 +2337,7 @@ cudaError_t forward(const Geom& g, const void* q, const void* k, const void* v, 
   }
 
   const int ak = alpha_kind(g.alpha);
-  const bool pairs = g.d == 128 && use_fwd_pairs(g);
-  a.supp_o = a.supp && !pairs && g.d == g.dv && sparse_out_enabled() ? 1 : 0;
+  a.supp_o = supp_o ? 1 : 0;
   if (g.d == 64) e = launch_fwd_d<64, false>(g, ak, tq, tk, tkh, tv, tv16, a, st);
   else if (pairs) e = launch_fwd_d<128, true>(g, ak, tq, tk, tkh, tv, tv16, a, st);
   else e = launch_fwd_d<128, false>(g, ak, tq, tk, tkh, tv, tv16, a, st);

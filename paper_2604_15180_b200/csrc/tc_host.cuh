@@ -72,8 +72,10 @@ SuppLayout supp_layout(const Geom& g, void* base);
 // results never depend on the other heads of the call (chunked run_host, sharded
 // multi-GPU runs).  f16_absmax: atomicMax of max |x| (float bits) into
 // maxbits[h] (caller zeroes them); f16_convert_scaled: dst = fp16(src * s(maxbits[h])).
+// need (optional): heads with need[h] == 0 get a non-finite maximum -- no copy, and a
+// bf16 plan should a tensor-core kernel still take the head.
 cudaError_t f16_absmax(const void* src, int heads, size_t elems, uint32_t* maxbits,
-                       cudaStream_t st);
+                       cudaStream_t st, const uint32_t* need = nullptr);
 cudaError_t f16_convert_scaled(const void* src, void* dst, int heads, size_t elems,
                                const uint32_t* maxbits, cudaStream_t st);
 

@@ -147,6 +147,7 @@ def test_tc_candidate_lists_and_sweep_fallback(case, monkeypatch):
     list capacity too small to hold the candidates -> per-CTA overflow ->
     fallback) give the same thresholds, masks and outputs, and both match the
     exact path."""
+    monkeypatch.setenv("ADATTN_SPARSE_OUT", "0")  # one output pass (fp16 P V) for all three
     B, H, N, D, alpha, causal, qs = case
     q, k, v, do = inputs(hash(case) % 991 + 7, B, H, N, D, qs)
     _, rx, _ = run(q, k, v, None, "exact", alpha=alpha, causal=causal)
