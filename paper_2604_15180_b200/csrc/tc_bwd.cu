@@ -1978,8 +1978,13 @@ __global__ void delta_ubar_kernel(const uint16_t* __restrict__ dout, const float
 // flagged block (hflag; the tensor-core dQ kernel takes the others) -- a row with more
 // than 192 entries flags its head here (the tensor-core kernels run after this one).
 // Also rowc_i = (C_i, delta_i) for the dK/dV kernel, as the delta kernels form it.
+// (d = 64: a 64-register bound -- 4 CTAs of 256 per SM -- makes ptxas schedule more gathers
+// ahead: C4 rows kernel 12.4 -> 9.9 ms; d = 128 keeps the unhinted bound, the hint cost 0.3 ms)
+#ifndef ADATTN_ROWS_MINB128
+#define ADATTN_ROWS_MINB128 0
+#endif
 template <int D, int AK>
-__global__ void __launch_bounds__(256) sparse_rows_kernel(
+__global__ void __launch_bounds__(256, D == 64 ? 4 : ADATTN_ROWS_MINB128) sparse_rows_kernel(
     const uint16_t* __restrict__ dout, const uint16_t* __restrict__ vv, const uint16_t* __restrict__ kk,
     const uint2* __restrict__ pool, const int2* __restrict__ cnt, const uint32_t* __restrict__ flag,
     uint32_t* hflag, int cap, int unit, const int32_t* __restrict__ koff, int32_t* kcur,
@@ -1994,9 +1999,9 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
   if (r >= rows) return;
   const size_t bh = r / (size_t)n;
   const size_t u0 = (bh * n + (r - bh * n) / unit * unit) / 256;
+  const int2 h0 = cnt[r * 2], h1 = cnt[r * 2 + 1];  // (read beside the flags)
   for (int b = 0; b < unit / 256; ++b)
     if (flag[u0 + b]) return;
-  const int2 h0 = cnt[r * 2], h1 = cnt[r * 2 + 1];
   const int c0 = h0.x, tot = h0.x + h1.x;
   const uint2* base = pool + (r / 256) * (size_t)(256 * cap);
   const uint16_t* vb = vv + bh * (size_t)m * D + lane * E;
@@ -2101,7 +2106,7 @@ __global__ void __launch_bounds__(256) sparse_rows_kernel(
       krow[slot] = (int)(r - bh * n);
       kpd[slot] = make_float2(pc, dsc);
     }
-#pragma unroll 8
+#pragma unroll kGatherUnroll
     for (int k = 0; k < nk; ++k) {
       const uint32_t key = __shfl_sync(0xffffffffu, keyc, k);
       const float ds = __shfl_sync(0xffffffffu, dsc, k);
@@ -2214,7 +2219,7 @@ __global__ void __launch_bounds__(WARPS * 32) sparse_keys_kernel(
     const uint16_t* __restrict__ dout, const uint16_t* __restrict__ qq,
     const int32_t* __restrict__ koff, const int32_t* __restrict__ krow,
     const float2* __restrict__ kpd, uint32_t* hflag, int32_t* klong, int cap, float scale,
-    size_t keys, int n, int m, int out_f64, void* dk, void* dv) {
+    size_t keys, int n, int m, int out_f64, void* dk, void* dv, int shfl_sort) {
   constexpr int E = D / 32;
   __shared__ unsigned long long sk[WARPS][KMAX];
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
@@ -2229,10 +2234,11 @@ __global__ void __launch_bounds__(WARPS * 32) sparse_keys_kernel(
     if (it != kr || kr >= keys) return;
   }
   const size_t bh = kr / (size_t)m;
-  if (hflag[bh]) continue;
   const size_t j = kr - bh * m;
-  const int cntk = koff[bh * (m + 1) + j + 1] - koff[bh * (m + 1) + j];
-  const size_t s0 = bh * (size_t)n * cap + (size_t)koff[bh * (m + 1) + j];
+  const int o0 = koff[bh * (m + 1) + j], o1 = koff[bh * (m + 1) + j + 1];  // (beside hflag)
+  if (hflag[bh]) continue;
+  const int cntk = o1 - o0;
+  const size_t s0 = bh * (size_t)n * cap + (size_t)o0;
   if (!LONG && cntk > KMAX) {  // queued for the long-list launch
     if (lane == 0) klong[1 + atomicAdd(&klong[0], 1)] = (int32_t)kr;
     return;
@@ -2244,6 +2250,19 @@ __global__ void __launch_bounds__(WARPS * 32) sparse_keys_kernel(
   unsigned long long* sm = sk[wi];
   int np = 32;
   while (np < cntk) np <<= 1;
+  if (shfl_sort && np == 32) {  // one entry per lane: the same bitonic network in registers
+    unsigned long long x = lane < cntk ? ((unsigned long long)(uint32_t)krow[s0 + lane] << 32) | (uint32_t)lane : ~0ull;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, jj);
+        const bool take_min = ((lane & jj) == 0) == ((lane & k) == 0);
+        x = take_min ? (x < y ? x : y) : (x < y ? y : x);
+      }
+    sm[lane] = x;
+    __syncwarp();
+  } else {
   for (int i = lane; i < np; i += 32)
     sm[i] = i < cntk ? ((unsigned long long)(uint32_t)krow[s0 + i] << 32) | (uint32_t)i : ~0ull;
   __syncwarp();
@@ -2261,12 +2280,13 @@ __global__ void __launch_bounds__(WARPS * 32) sparse_keys_kernel(
       }
       __syncwarp();
     }
+  }
   const uint16_t* db = dout + bh * (size_t)n * D + lane * E;
   const uint16_t* qb = qq + bh * (size_t)n * D + lane * E;
   float av[E], ak[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) av[e] = ak[e] = 0.f;
-#pragma unroll 8
+#pragma unroll kGatherUnroll
   for (int i = 0; i < cntk; ++i) {
     const unsigned long long x = sm[i];
     const uint32_t row = (uint32_t)(x >> 32), sl = (uint32_t)x;
@@ -2773,6 +2793,12 @@ bool sparse_dq_enabled() {
   const char* s = std::getenv("ADATTN_SPARSE_DQ");
   return !(s && *s == '0');
 }
+// key lists of <= 32 entries sorted with warp shuffles (ADATTN_KEYS_SHFL=0: in shared
+// memory; the same network, bit-identical results)
+bool keys_shfl_enabled() {
+  const char* s = std::getenv("ADATTN_KEYS_SHFL");
+  return !(s && *s == '0');
+}
 // dK/dV from the support lists (sparse_keys_kernel; ADATTN_SPARSE_KV=0: the tensor-core
 // dK/dV kernel); needs the sparse dQ pass, which scatters the key lists
 bool sparse_kv_enabled() {
@@ -2879,12 +2905,12 @@ cudaError_t run_bwd(const Geom& g, const CUtensorMap* m, const BwdArgs& a, bool 
     sparse_keys_kernel<D, 256, 8, false><<<(unsigned)((keys + 7) / 8), 8 * 32, 0, st>>>(
         reinterpret_cast<const uint16_t*>(a.dout), reinterpret_cast<const uint16_t*>(a.qp),
         sl.koff, sl.krow, sl.kpd, sl.hflag, sl.klong, sl.cap, (float)g.scale, keys, g.n, g.m,
-        g.out_dtype == ADATTN_F64 ? 1 : 0, a.dk, a.dv);
+        g.out_dtype == ADATTN_F64 ? 1 : 0, a.dk, a.dv, keys_shfl_enabled() ? 1 : 0);
     note_launch();
     sparse_keys_kernel<D, 4096, 1, true><<<148 * 6, 32, 0, st>>>(
         reinterpret_cast<const uint16_t*>(a.dout), reinterpret_cast<const uint16_t*>(a.qp),
         sl.koff, sl.krow, sl.kpd, sl.hflag, sl.klong, sl.cap, (float)g.scale, keys, g.n, g.m,
-        g.out_dtype == ADATTN_F64 ? 1 : 0, a.dk, a.dv);
+        g.out_dtype == ADATTN_F64 ? 1 : 0, a.dk, a.dv, 0);
     prof_end(st);
     note_launch();
     if ((e = cudaGetLastError())) return e;

@@ -19,6 +19,13 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+
+// entries in flight per warp in the support-list gather loops (sparse_out / sparse_rows /
+// sparse_keys kernels)
+#ifndef ADATTN_GATHER_UNROLL
+#define ADATTN_GATHER_UNROLL 8
+#endif
+constexpr int kGatherUnroll = ADATTN_GATHER_UNROLL;
 #include <cuda_runtime.h>
 #include <stdint.h>
 

@@ -2184,9 +2184,10 @@ __global__ void __launch_bounds__(256) sparse_out_kernel(
   constexpr int E = D / 32;
   const size_t r = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (r >= rows || flag[r / 256]) return;
+  if (r >= rows) return;
+  const int2 h0 = cnt[r * 2], h1 = cnt[r * 2 + 1];  // (read beside the flag: one L2 trip)
+  if (flag[r / 256]) return;
   const size_t bh = r / (size_t)n;
-  const int2 h0 = cnt[r * 2], h1 = cnt[r * 2 + 1];
   const int c0 = h0.x, tot = h0.x + h1.x;
   const uint2* base = pool + (r / 256) * (size_t)(256 * cap);
   const uint16_t* vb = vv + bh * (size_t)m * D + lane * E;
@@ -2199,7 +2200,7 @@ __global__ void __launch_bounds__(256) sparse_out_kernel(
     if (idx < tot) my = idx < c0 ? base[h0.y + idx] : base[h1.y + idx - c0];
     const float pl = idx < tot ? p_of<AK>(__uint_as_float(my.y), e0f) : 0.f;
     const int nk = min(32, tot - b);
-#pragma unroll 8
+#pragma unroll kGatherUnroll
     for (int k = 0; k < nk; ++k) {
       const uint32_t key = __shfl_sync(0xffffffffu, my.x, k);
       const float p = __shfl_sync(0xffffffffu, pl, k);

@@ -727,6 +727,23 @@ def test_tc_sparse_dkdv_matches_tensor_core(case, monkeypatch):
 
 
 @pytest.mark.parametrize("case", [(1, 2, 4096, 128, 1.5, True, 1.0), (1, 2, 2048, 64, 1.5, False, 1.0),
+                                  (1, 2, 4096, 128, 2.0, True, 2.0), (1, 1, 8192, 128, 1.5, True, 8.0)],
+                         ids=str)
+def test_tc_sparse_keys_shuffle_sort_bitwise(case, monkeypatch):
+    """Key lists of <= 32 entries sorted with warp shuffles (the default) and in shared
+    memory (ADATTN_KEYS_SHFL=0) run the same bitonic network on unique (row, slot) keys, so
+    the summation order and every bit of dK / dV agree."""
+    B, H, N, D, alpha, causal, qs = case
+    q, k, v, do = inputs(hash(case) % 541 + 29, B, H, N, D, qs)
+    monkeypatch.setenv("ADATTN_KEYS_SHFL", "0")
+    _, _, g0 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    monkeypatch.setenv("ADATTN_KEYS_SHFL", "1")
+    _, _, g1 = run(q, k, v, do, "tc", alpha=alpha, causal=causal)
+    for n in ("dq", "dk", "dv", "delta"):
+        assert torch.equal(getattr(g0, n), getattr(g1, n)), n
+
+
+@pytest.mark.parametrize("case", [(1, 2, 4096, 128, 1.5, True, 1.0), (1, 2, 2048, 64, 1.5, False, 1.0),
                                   (1, 2, 4096, 128, 2.0, True, 2.0), (1, 1, 8192, 128, 1.5, True, 8.0),
                                   (2, 1, 2304, 128, 1.75, True, 1.0)],
                          ids=str)
