@@ -1980,11 +1980,8 @@ __global__ void delta_ubar_kernel(const uint16_t* __restrict__ dout, const float
 // Also rowc_i = (C_i, delta_i) for the dK/dV kernel, as the delta kernels form it.
 // (d = 64: a 64-register bound -- 4 CTAs of 256 per SM -- makes ptxas schedule more gathers
 // ahead: C4 rows kernel 12.4 -> 9.9 ms; d = 128 keeps the unhinted bound, the hint cost 0.3 ms)
-#ifndef ADATTN_ROWS_MINB128
-#define ADATTN_ROWS_MINB128 0
-#endif
 template <int D, int AK>
-__global__ void __launch_bounds__(256, D == 64 ? 4 : ADATTN_ROWS_MINB128) sparse_rows_kernel(
+__global__ void __launch_bounds__(256, D == 64 ? 4 : 0) sparse_rows_kernel(
     const uint16_t* __restrict__ dout, const uint16_t* __restrict__ vv, const uint16_t* __restrict__ kk,
     const uint2* __restrict__ pool, const int2* __restrict__ cnt, const uint32_t* __restrict__ flag,
     uint32_t* hflag, int cap, int unit, const int32_t* __restrict__ koff, int32_t* kcur,
