@@ -2278,6 +2278,49 @@ __global__ void __launch_bounds__(WARPS * 32) sparse_keys_kernel(
       __syncwarp();
     }
   }
+  if constexpr (D == 64) {  // half-warps take alternate entries, 4 elements (8 bytes) a lane
+    const int hf = lane >> 4, hl = lane & 15;
+    const uint16_t* db4 = dout + bh * (size_t)n * D + hl * 4;
+    const uint16_t* qb4 = qq + bh * (size_t)n * D + hl * 4;
+    float av[4] = {0.f, 0.f, 0.f, 0.f}, ak[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll kGatherUnroll
+    for (int i = hf; i < cntk; i += 2) {
+      const unsigned long long x = sm[i];
+      const uint32_t row = (uint32_t)(x >> 32), sl = (uint32_t)x;
+      const float2 pd = kpd[s0 + sl];
+      const uint2 w0 = *reinterpret_cast<const uint2*>(db4 + (size_t)row * D);
+      const uint2 w1 = *reinterpret_cast<const uint2*>(qb4 + (size_t)row * D);
+      av[0] = fmaf(pd.x, __uint_as_float(w0.x << 16), av[0]);
+      av[1] = fmaf(pd.x, __uint_as_float(w0.x & 0xFFFF0000u), av[1]);
+      av[2] = fmaf(pd.x, __uint_as_float(w0.y << 16), av[2]);
+      av[3] = fmaf(pd.x, __uint_as_float(w0.y & 0xFFFF0000u), av[3]);
+      ak[0] = fmaf(pd.y, __uint_as_float(w1.x << 16), ak[0]);
+      ak[1] = fmaf(pd.y, __uint_as_float(w1.x & 0xFFFF0000u), ak[1]);
+      ak[2] = fmaf(pd.y, __uint_as_float(w1.y << 16), ak[2]);
+      ak[3] = fmaf(pd.y, __uint_as_float(w1.y & 0xFFFF0000u), ak[3]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {  // even entries + odd entries (the same sum on both halves)
+      av[e] += __shfl_xor_sync(0xffffffffu, av[e], 16);
+      ak[e] += __shfl_xor_sync(0xffffffffu, ak[e], 16);
+    }
+    if (hf == 0) {
+      const size_t orow = kr * D + hl * 4;
+      if (out_f64) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          reinterpret_cast<double*>(dv)[orow + e] = (double)av[e];
+          reinterpret_cast<double*>(dk)[orow + e] = (double)(scale * ak[e]);
+        }
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(dv) + orow) = make_float4(av[0], av[1], av[2], av[3]);
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(dk) + orow) =
+            make_float4(scale * ak[0], scale * ak[1], scale * ak[2], scale * ak[3]);
+      }
+    }
+    __syncwarp();
+    continue;
+  }
   const uint16_t* db = dout + bh * (size_t)n * D + lane * E;
   const uint16_t* qb = qq + bh * (size_t)n * D + lane * E;
   float av[E], ak[E];
