@@ -2093,6 +2093,10 @@ __global__ void __launch_bounds__(256, D == 64 ? 4 : 0) sparse_rows_kernel(
   float acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
+  // d = 64: half-warps take alternate entries, 4 elements (8 bytes) a lane
+  const int hf = lane >> 4, hl = lane & 15;
+  const uint16_t* kb4 = kk + bh * (size_t)m * D + hl * 4;
+  float a4[4] = {0.f, 0.f, 0.f, 0.f};
   // one chunk of up to 32 entries: scatter into the key lists, accumulate dS k_j
   auto dq_chunk = [&](int b, uint32_t keyc, float pc, float dsc) {
     const int nk = min(32, tot - b);
@@ -2102,6 +2106,22 @@ __global__ void __launch_bounds__(256, D == 64 ? 4 : 0) sparse_rows_kernel(
       const size_t slot = bh * (size_t)n * cap + (size_t)(koff[kj + bh] + atomicAdd(&kcur[kj], 1));
       krow[slot] = (int)(r - bh * n);
       kpd[slot] = make_float2(pc, dsc);
+    }
+    if constexpr (D == 64) {
+#pragma unroll kGatherUnroll
+      for (int k2 = 0; k2 < (nk + 1) / 2; ++k2) {
+        const int k = 2 * k2 + hf;
+        const uint32_t key = __shfl_sync(0xffffffffu, keyc, k & 31);
+        const float ds = __shfl_sync(0xffffffffu, dsc, k & 31);
+        if (k < nk) {
+          const uint2 w = *reinterpret_cast<const uint2*>(kb4 + (size_t)key * D);
+          a4[0] = fmaf(ds, __uint_as_float(w.x << 16), a4[0]);
+          a4[1] = fmaf(ds, __uint_as_float(w.x & 0xFFFF0000u), a4[1]);
+          a4[2] = fmaf(ds, __uint_as_float(w.y << 16), a4[2]);
+          a4[3] = fmaf(ds, __uint_as_float(w.y & 0xFFFF0000u), a4[3]);
+        }
+      }
+      return;
     }
 #pragma unroll kGatherUnroll
     for (int k = 0; k < nk; ++k) {
@@ -2145,6 +2165,20 @@ __global__ void __launch_bounds__(256, D == 64 ? 4 : 0) sparse_rows_kernel(
       dpc = s0 + s1;
     }
     dq_chunk(b, my.x, pc, uc * (dpc - dl));
+  }
+  if constexpr (D == 64) {  // (even entries) + (odd entries); the first half-warp writes
+#pragma unroll
+    for (int e = 0; e < 4; ++e) a4[e] += __shfl_xor_sync(0xffffffffu, a4[e], 16);
+    if (hf) return;
+    if (out_f64) {
+      double* dst = reinterpret_cast<double*>(dq) + r * D + hl * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = (double)(scale * a4[e]);
+    } else {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(dq) + r * D + hl * 4) =
+          make_float4(scale * a4[0], scale * a4[1], scale * a4[2], scale * a4[3]);
+    }
+    return;
   }
   if (out_f64) {
     double* dst = reinterpret_cast<double*>(dq) + r * D + lane * E;

@@ -2191,6 +2191,44 @@ __global__ void __launch_bounds__(256) sparse_out_kernel(
   const int c0 = h0.x, tot = h0.x + h1.x;
   const uint2* base = pool + (r / 256) * (size_t)(256 * cap);
   const uint16_t* vb = vv + bh * (size_t)m * D + lane * E;
+  if constexpr (D == 64) {  // half-warps take alternate entries, 4 elements (8 bytes) a lane
+    const int hf = lane >> 4, hl = lane & 15;
+    const uint16_t* vb4 = vv + bh * (size_t)m * D + hl * 4;
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int b = 0; b < tot; b += 32) {
+      const int idx = b + lane;
+      uint2 my = make_uint2(0u, 0u);
+      if (idx < tot) my = idx < c0 ? base[h0.y + idx] : base[h1.y + idx - c0];
+      const float pl = idx < tot ? p_of<AK>(__uint_as_float(my.y), e0f) : 0.f;
+      const int nk = min(32, tot - b);
+#pragma unroll kGatherUnroll
+      for (int k2 = 0; k2 < (nk + 1) / 2; ++k2) {
+        const int k = 2 * k2 + hf;
+        const uint32_t key = __shfl_sync(0xffffffffu, my.x, k & 31);
+        const float p = __shfl_sync(0xffffffffu, pl, k & 31);
+        if (k < nk) {
+          const uint2 w = *reinterpret_cast<const uint2*>(vb4 + (size_t)key * D);
+          a4[0] = fmaf(p, __uint_as_float(w.x << 16), a4[0]);
+          a4[1] = fmaf(p, __uint_as_float(w.x & 0xFFFF0000u), a4[1]);
+          a4[2] = fmaf(p, __uint_as_float(w.y << 16), a4[2]);
+          a4[3] = fmaf(p, __uint_as_float(w.y & 0xFFFF0000u), a4[3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) a4[e] += __shfl_xor_sync(0xffffffffu, a4[e], 16);
+    if (hf == 0) {
+      if (out_f64) {
+        double* dst = reinterpret_cast<double*>(out) + r * D + hl * 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dst[e] = (double)a4[e];
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + r * D + hl * 4) =
+            make_float4(a4[0], a4[1], a4[2], a4[3]);
+      }
+    }
+    return;
+  }
   float acc[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
